@@ -1,0 +1,126 @@
+// common.cuh — internal helpers of libconvpart (B200, sm_100a).
+// Nothing here is shared with the oracle (oracle/ is a separate C program).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/convpart.h"
+
+namespace cp {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+std::atomic<int64_t>& launch_counter();
+
+#define CP_FAIL(code, msg)         \
+  do {                             \
+    ::cp::set_error(msg);          \
+    return (code);                 \
+  } while (0)
+
+#define CP_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e__ = (call);                                                              \
+    if (e__ != cudaSuccess) {                                                              \
+      ::cp::set_error(std::string(#call) + ": " + cudaGetErrorString(e__));                \
+      return CP_ERR_CUDA;                                                                  \
+    }                                                                                      \
+  } while (0)
+
+// after a kernel launch: count it and surface launch errors
+#define CP_LAUNCHED()                                                                      \
+  do {                                                                                     \
+    ::cp::launch_counter().fetch_add(1, std::memory_order_relaxed);                        \
+    cudaError_t e__ = cudaGetLastError();                                                  \
+    if (e__ != cudaSuccess) {                                                              \
+      ::cp::set_error(std::string("kernel launch (") + __FILE__ + ":" +                   \
+                      std::to_string(__LINE__) + "): " + cudaGetErrorString(e__));         \
+      return CP_ERR_CUDA;                                                                  \
+    }                                                                                      \
+  } while (0)
+
+#define CP_TRY(expr)                 \
+  do {                               \
+    int rc__ = (expr);               \
+    if (rc__ != CP_OK) return rc__;  \
+  } while (0)
+
+static inline int roundup(int a, int b) { return (a + b - 1) / b * b; }
+static inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- gather geometry
+// A tensor in the rank-blocked gather layout: blocks [H][W][Bp][kw[r]] in rank order.
+struct Blocks {
+  int n;                     // number of rank blocks
+  int H, W, Bp;              // spatial extent of every block, padded batch
+  int kb[CP_MAX_RANKS];      // first logical channel of block r
+  int kc[CP_MAX_RANKS];      // real channels in block r
+  int kw[CP_MAX_RANKS];      // slots in block r (multiple of 8)
+  int coff[CP_MAX_RANKS];    // slot offset of block r in the concatenated slot space
+  int64_t start[CP_MAX_RANKS + 1];  // element offset of block r (start[n] = total)
+  int Cg;                    // total slots = sum kw
+};
+
+static inline Blocks make_blocks(const cp_partition& p, int H, int W, int Bp) {
+  Blocks g{};
+  g.n = p.n_ranks;
+  g.H = H;
+  g.W = W;
+  g.Bp = Bp;
+  int64_t s = 0;
+  int c = 0;
+  for (int r = 0; r < p.n_ranks; ++r) {
+    g.kb[r] = p.k_begin[r];
+    g.kc[r] = p.k_count[r];
+    g.kw[r] = p.k_width[r];
+    g.coff[r] = c;
+    g.start[r] = s;
+    c += p.k_width[r];
+    s += (int64_t)H * W * Bp * p.k_width[r];
+  }
+  g.start[p.n_ranks] = s;
+  g.Cg = c;
+  return g;
+}
+
+// block owning concatenated slot c' (device side; n <= 16, linear scan)
+__host__ __device__ inline int block_of_slot(const Blocks& g, int cslot) {
+  int r = 0;
+  while (r + 1 < g.n && cslot >= g.coff[r + 1]) ++r;
+  return r;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// ---------------------------------------------------------------- layer state
+struct Layer {
+  cp_conv_desc d;
+  cp_comm comm;
+  // derived geometry
+  int B, Bp;
+  int C, H, W, R, S;      // input
+  int Ho, Wo, Hp, Wp;     // conv output and pooled output
+  int K, Kr, Kc, k0;      // all kernels, own count, own width, own first kernel
+  int images;             // input kind
+  int Kcol;               // im2col width (images)
+  int Ktot;               // weight row length: Kcol or R*S*Cg
+  Blocks in;              // input gather geometry (gather input)
+  Blocks out;             // output gather geometry (pooled grid)
+  // workspace carve-up (bytes)
+  size_t ws_xcol, ws_z, ws_dy, ws_split, ws_dbpart, ws_total;
+  size_t off_xcol, off_z, off_dy, off_split, off_dbpart;
+  int dy_ready;           // epilogue-backward already computed for this step
+  const void* dy_key[3];
+  cudaEvent_t ev_compute, ev_comm;
+  // TMA descriptor cache lives in the TC module (opaque)
+  void* tc_cache;
+};
+
+}  // namespace cp

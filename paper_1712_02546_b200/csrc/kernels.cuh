@@ -1,0 +1,38 @@
+// kernels.cuh — internal launchers (namespace cp).  All enqueue on `s` and count launches.
+#pragma once
+#include "common.cuh"
+
+namespace cp {
+
+// ---- layout / elementwise (kernels_simt.cu)
+int launch_im2col(const Layer& L, const float* x, float* xcol, bool round_tf32, cudaStream_t s);
+int launch_relu_pool(const Layer& L, const float* z, float* y_block, uint8_t* saved, bool round_tf32,
+                     cudaStream_t s);
+int launch_unpool(const Layer& L, const float* dy_block, const uint8_t* saved, const float* y_block,
+                  float* dY, bool round_tf32, cudaStream_t s);
+int launch_bias_grad(const Layer& L, const float* dy_block, const float* y_block, float* db, float* part,
+                     cudaStream_t s);
+
+// ---- FP32 SIMT reference convolutions (kernels_simt.cu)
+int launch_fwd_simt(const Layer& L, const float* x, const float* xcol, const float* w, const float* b,
+                    float* z, cudaStream_t s);
+int launch_dgrad_simt(const Layer& L, const float* dY, const float* w, float* dx, cudaStream_t s);
+int launch_wgrad_simt(const Layer& L, const float* dY, const float* x, const float* xcol, float* dw,
+                      cudaStream_t s);
+int launch_fill(float* p, float v, int64_t n, cudaStream_t s);
+int launch_random_fill(float* p, int64_t n, uint32_t seed, float scale, cudaStream_t s);
+
+// ---- tcgen05 / TMA tensor-core convolutions (kernels_tc.cu)
+size_t tc_workspace_bytes(const Layer& L);
+int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved,
+           void* ws, cudaStream_t s);
+int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s);
+int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s);
+void tc_release(Layer& L);
+
+// ---- NCCL collectives (comm.cu)
+int comm_check_plan(cp_comm c, const Layer& L);
+int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s);
+int comm_sum_blocks(cp_comm c, float* buf, const Blocks& g, int dx_mode, cudaStream_t s);
+
+}  // namespace cp

@@ -1,0 +1,360 @@
+// layer.cu — the C-ABI entry points of a kernel-partitioned conv layer (convpart.h).
+//
+// Orchestration of one rank's share of the method (Alg. 1/2) as SPMD:
+// every rank is a peer holding the same input and its own contiguous kernel slice; the
+// master/slave socket protocol becomes stream-ordered kernels plus NCCL collectives.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace cp {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+std::atomic<int64_t>& launch_counter() {
+  static std::atomic<int64_t> c{0};
+  return c;
+}
+
+static std::string shp(std::initializer_list<int64_t> v) {
+  std::string s = "[";
+  bool first = true;
+  for (auto x : v) {
+    s += (first ? "" : ",") + std::to_string(x);
+    first = false;
+  }
+  return s + "]";
+}
+
+static int validate_part(const cp_partition& p, const char* what) {
+  if (p.n_ranks < 1 || p.n_ranks > CP_MAX_RANKS)
+    CP_FAIL(CP_ERR_CONFIG, std::string(what) + ": n_ranks out of [1,16]");
+  int b = 0;
+  for (int r = 0; r < p.n_ranks; ++r) {
+    if (p.k_begin[r] != b || p.k_count[r] < 0 || p.k_width[r] < p.k_count[r] || p.k_width[r] % 8)
+      CP_FAIL(CP_ERR_CONFIG, std::string(what) + ": ranges must be contiguous in rank order with widths = "
+                                                 "multiples of 8 >= counts");
+    b += p.k_count[r];
+  }
+  if (b != p.num_k) CP_FAIL(CP_ERR_CONFIG, std::string(what) + ": counts do not sum to num_k");
+  return CP_OK;
+}
+
+static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+static int derive(Layer& L, const cp_conv_desc& d) {
+  L.d = d;
+  if (d.batch < 1 || d.in_c < 1 || d.in_h < 1 || d.in_w < 1 || d.num_k < 1 || d.k_h < 1 || d.k_w < 1)
+    CP_FAIL(CP_ERR_SHAPE, "conv_part_create: nonpositive dimension");
+  if (d.in_h < d.k_h || d.in_w < d.k_w)
+    CP_FAIL(CP_ERR_SHAPE, "dimension error: input " + shp({d.batch, d.in_c, d.in_h, d.in_w}) + " vs kernels " +
+                              shp({d.num_k, d.in_c, d.k_h, d.k_w}));
+  if (d.math != CP_MATH_TF32 && d.math != CP_MATH_FP32_SIMT) CP_FAIL(CP_ERR_CONFIG, "unknown math mode");
+  if (d.input_kind != CP_INPUT_IMAGES && d.input_kind != CP_INPUT_GATHER) CP_FAIL(CP_ERR_CONFIG, "unknown input kind");
+  CP_TRY(validate_part(d.out_part, "out_part"));
+  if (d.out_part.num_k != d.num_k)
+    CP_FAIL(CP_ERR_SHAPE, "out_part.num_k=" + std::to_string(d.out_part.num_k) + " vs num_k=" + std::to_string(d.num_k));
+  if (d.world != d.out_part.n_ranks || d.rank < 0 || d.rank >= d.world)
+    CP_FAIL(CP_ERR_CONFIG, "rank/world inconsistent with out_part");
+  L.images = d.input_kind == CP_INPUT_IMAGES;
+  L.B = d.batch;
+  L.Bp = roundup(d.batch, 32);
+  L.C = d.in_c; L.H = d.in_h; L.W = d.in_w; L.R = d.k_h; L.S = d.k_w;
+  L.Ho = L.H - L.R + 1; L.Wo = L.W - L.S + 1;
+  if (d.pool && ((L.Ho & 1) || (L.Wo & 1)))
+    CP_FAIL(CP_ERR_SHAPE, "dimension error: pooling input " + shp({L.Ho, L.Wo}) + " not divisible by stride 2");
+  L.Hp = d.pool ? L.Ho / 2 : L.Ho;
+  L.Wp = d.pool ? L.Wo / 2 : L.Wo;
+  L.K = d.num_k;
+  L.Kr = d.out_part.k_count[d.rank];
+  L.Kc = d.out_part.k_width[d.rank];
+  L.k0 = d.out_part.k_begin[d.rank];
+  if (L.images) {
+    L.Kcol = roundup(L.R * L.S * L.C, 8);
+    L.Ktot = L.Kcol;
+    L.in = Blocks{};
+  } else {
+    CP_TRY(validate_part(d.in_part, "in_part"));
+    if (d.in_part.num_k != d.in_c)
+      CP_FAIL(CP_ERR_SHAPE, "in_part.num_k=" + std::to_string(d.in_part.num_k) + " vs in_c=" + std::to_string(d.in_c));
+    L.in = make_blocks(d.in_part, L.H, L.W, L.Bp);
+    L.Kcol = 0;
+    L.Ktot = L.R * L.S * L.in.Cg;
+  }
+  L.out = make_blocks(d.out_part, L.Hp, L.Wp, L.Bp);
+  // workspace carve-up
+  size_t off = 0;
+  L.off_xcol = off; L.ws_xcol = L.images ? al256((size_t)L.Ho * L.Wo * L.Bp * L.Kcol * 4) : 0; off += L.ws_xcol;
+  L.off_z = off; L.ws_z = d.math == CP_MATH_FP32_SIMT ? al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 4) : 0; off += L.ws_z;
+  L.off_dy = off; L.ws_dy = al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 4); off += L.ws_dy;
+  L.off_dbpart = off; L.ws_dbpart = al256((size_t)64 * std::max(L.Kc, 8) * 4); off += L.ws_dbpart;
+  L.off_split = off; L.ws_split = d.math == CP_MATH_TF32 ? al256(tc_workspace_bytes(L)) : 0; off += L.ws_split;
+  L.ws_total = off + 256;
+  L.dy_ready = 0;
+  return CP_OK;
+}
+
+static char* WS(void* ws, size_t off) { return (char*)ws + off; }
+
+// epilogue backward of this rank's block (shared by backward_data and backward_filter)
+static int ensure_dy(Layer& L, const float* dy_g, const uint8_t* saved, const float* y_g, void* ws, cudaStream_t s) {
+  if (L.dy_ready && L.dy_key[0] == dy_g && L.dy_key[1] == saved && L.dy_key[2] == y_g) return CP_OK;
+  const int64_t o = L.out.start[L.d.rank];
+  CP_TRY(launch_unpool(L, dy_g + o, saved, y_g + o, (float*)WS(ws, L.off_dy), L.d.math == CP_MATH_TF32, s));
+  L.dy_ready = 1;
+  L.dy_key[0] = dy_g; L.dy_key[1] = saved; L.dy_key[2] = y_g;
+  return CP_OK;
+}
+
+static int fork_comm(Layer& L, cudaStream_t s, cudaStream_t cs) {
+  if (cs == s) return CP_OK;
+  CP_CUDA(cudaEventRecord(L.ev_compute, s));
+  CP_CUDA(cudaStreamWaitEvent(cs, L.ev_compute, 0));
+  return CP_OK;
+}
+static int join_comm(Layer& L, cudaStream_t s, cudaStream_t cs) {
+  if (cs == s) return CP_OK;
+  CP_CUDA(cudaEventRecord(L.ev_comm, cs));
+  CP_CUDA(cudaStreamWaitEvent(s, L.ev_comm, 0));
+  return CP_OK;
+}
+
+}  // namespace cp
+
+using namespace cp;
+
+struct cp_layer_s : Layer {};
+
+extern "C" {
+
+const char* cp_last_error(void) { return g_last_error.c_str(); }
+int64_t cp_launch_count(void) { return launch_counter().load(); }
+
+int conv_part_create(const cp_conv_desc* desc, cp_comm comm, cp_layer* out) {
+  if (!desc || !out) CP_FAIL(CP_ERR_ARG, "conv_part_create: null pointer");
+  auto* L = new cp_layer_s();
+  int rc = derive(*L, *desc);
+  if (rc == CP_OK) {
+    L->comm = comm;
+    rc = comm_check_plan(comm, *L);
+  }
+  if (rc == CP_OK && cudaEventCreateWithFlags(&L->ev_compute, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("cudaEventCreate failed");
+    rc = CP_ERR_CUDA;
+  }
+  if (rc == CP_OK && cudaEventCreateWithFlags(&L->ev_comm, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("cudaEventCreate failed");
+    rc = CP_ERR_CUDA;
+  }
+  if (rc != CP_OK) {
+    delete L;
+    return rc;
+  }
+  *out = L;
+  return CP_OK;
+}
+
+int conv_part_query(cp_layer L, cp_sizes* o) {
+  if (!L || !o) CP_FAIL(CP_ERR_ARG, "conv_part_query: null pointer");
+  o->w = (size_t)L->Kr * L->Ktot * 4;
+  o->b = (size_t)L->Kr * 4;
+  o->x = L->images ? (size_t)L->B * L->C * L->H * L->W * 4 : (size_t)L->in.start[L->in.n] * 4;
+  o->y = (size_t)L->out.start[L->out.n] * 4;
+  o->y_block = (size_t)(L->out.start[L->d.rank + 1] - L->out.start[L->d.rank]) * 4;
+  o->y_offset = (size_t)L->out.start[L->d.rank] * 4;
+  o->saved = L->d.pool ? (size_t)L->Hp * L->Wp * L->Bp * L->Kc : 0;
+  o->dx = o->x;
+  o->workspace = L->ws_total;
+  return CP_OK;
+}
+
+int conv_part_destroy(cp_layer L) {
+  if (!L) return CP_OK;
+  tc_release(*L);
+  if (L->ev_compute) cudaEventDestroy(L->ev_compute);
+  if (L->ev_comm) cudaEventDestroy(L->ev_comm);
+  delete L;
+  return CP_OK;
+}
+
+int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b, float* y, uint8_t* saved,
+                      void* ws, void* stream, void* comm_stream) {
+  if (!L || !x || !w || !y || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_forward: null pointer");
+  if (L->d.bias && !b) CP_FAIL(CP_ERR_ARG, "conv_part_forward: bias enabled but b is null");
+  if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_forward: pooling needs saved");
+  cudaStream_t s = (cudaStream_t)stream, cs = comm_stream ? (cudaStream_t)comm_stream : s;
+  L->dy_ready = 0;
+  float* yb = y + L->out.start[L->d.rank];
+  const bool tf32 = L->d.math == CP_MATH_TF32;
+  const float* xin = x;
+  if (L->images) {
+    float* xcol = (float*)WS(ws, L->off_xcol);
+    CP_TRY(launch_im2col(*L, x, xcol, tf32, s));
+    xin = xcol;
+  }
+  if (L->Kr > 0 || L->Kc > 0) {
+    if (tf32) {
+      CP_TRY(tc_fwd(*L, xin, w, b, yb, saved, ws, s));
+    } else {
+      float* z = (float*)WS(ws, L->off_z);
+      CP_TRY(launch_fwd_simt(*L, x, xin, w, b, z, s));
+      CP_TRY(launch_relu_pool(*L, z, yb, saved, false, s));
+    }
+  }
+  if (L->comm && L->d.world > 1) {
+    CP_TRY(fork_comm(*L, s, cs));
+    CP_TRY(comm_allgather_blocks(L->comm, y, L->out, cs));
+    CP_TRY(join_comm(*L, s, cs));
+  }
+  return CP_OK;
+}
+
+int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved, const float* y_g, const float* w,
+                            float* dx, int32_t dx_mode, void* ws, void* stream, void* comm_stream) {
+  if (!L || !dy_g || !y_g || !w || !dx || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_backward_data: null pointer");
+  if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_data: pooling needs saved");
+  const bool async = (dx_mode & CP_DX_ASYNC) != 0;
+  dx_mode &= ~CP_DX_ASYNC;
+  if (dx_mode < CP_DX_ALLREDUCE || dx_mode > CP_DX_LOCAL) CP_FAIL(CP_ERR_ARG, "bad dx_mode");
+  if (L->images && dx_mode == CP_DX_REDUCE_SCATTER)
+    CP_FAIL(CP_ERR_UNSUPPORTED, "reduce-scatter of dX needs a gather-layout input (images use all-reduce)");
+  cudaStream_t s = (cudaStream_t)stream, cs = comm_stream ? (cudaStream_t)comm_stream : s;
+  CP_TRY(ensure_dy(*L, dy_g, saved, y_g, ws, s));
+  const float* dY = (const float*)WS(ws, L->off_dy);
+  if (L->d.math == CP_MATH_TF32 && !L->images) {
+    CP_TRY(tc_dgrad(*L, dY, w, dx, ws, s));
+  } else {
+    CP_TRY(launch_dgrad_simt(*L, dY, w, dx, s));
+  }
+  if (L->comm && L->d.world > 1 && dx_mode != CP_DX_LOCAL) {
+    CP_TRY(fork_comm(*L, s, cs));
+    if (L->images) {
+      Blocks flat{};
+      flat.n = 1;
+      flat.start[0] = 0;
+      flat.start[1] = (int64_t)L->B * L->C * L->H * L->W;
+      CP_TRY(comm_sum_blocks(L->comm, dx, flat, CP_DX_ALLREDUCE, cs));
+    } else {
+      CP_TRY(comm_sum_blocks(L->comm, dx, L->in, dx_mode, cs));
+    }
+    if (async && cs != s) {
+      CP_CUDA(cudaEventRecord(L->ev_comm, cs));
+    } else {
+      CP_TRY(join_comm(*L, s, cs));
+    }
+  }
+  return CP_OK;
+}
+
+int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* saved, const float* y_g, const float* x,
+                              float* dw, float* db, void* ws, void* stream) {
+  if (!L || !dy_g || !y_g || !x || !dw || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: null pointer");
+  if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: pooling needs saved");
+  cudaStream_t s = (cudaStream_t)stream;
+  CP_TRY(ensure_dy(*L, dy_g, saved, y_g, ws, s));
+  const int64_t o = L->out.start[L->d.rank];
+  if (db && L->Kr > 0) CP_TRY(launch_bias_grad(*L, dy_g + o, y_g + o, db, (float*)WS(ws, L->off_dbpart), s));
+  if (L->Kr == 0) return CP_OK;
+  const float* dY = (const float*)WS(ws, L->off_dy);
+  const float* xcol = L->images ? (const float*)WS(ws, L->off_xcol) : nullptr;
+  if (L->d.math == CP_MATH_TF32) {
+    CP_TRY(tc_wgrad(*L, dY, L->images ? xcol : x, dw, ws, s));
+  } else {
+    CP_TRY(launch_wgrad_simt(*L, dY, x, xcol, dw, s));
+  }
+  return CP_OK;
+}
+
+int conv_part_wait(cp_layer L, void* stream) {
+  if (!L) CP_FAIL(CP_ERR_ARG, "conv_part_wait: null layer");
+  CP_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, L->ev_comm, 0));
+  return CP_OK;
+}
+
+int conv_part_sgd_step(cp_layer L, float* w, float* b, const float* dw, const float* db, float lr, void* stream) {
+  if (!L || !w || !dw) CP_FAIL(CP_ERR_ARG, "conv_part_sgd_step: null pointer");
+  CP_TRY(cp_sgd(w, dw, (int64_t)L->Kr * L->Ktot, lr, stream));
+  if (b && db) CP_TRY(cp_sgd(b, db, L->Kr, lr, stream));
+  return CP_OK;
+}
+
+int conv_part_probe_bytes(const cp_conv_desc* desc, size_t* bytes) {
+  if (!desc || !bytes) CP_FAIL(CP_ERR_ARG, "conv_part_probe_bytes: null pointer");
+  cp_conv_desc d = *desc;
+  d.out_part = cp_partition{};
+  d.out_part.n_ranks = 1;
+  d.out_part.num_k = d.num_k;
+  d.out_part.k_count[0] = d.num_k;
+  d.out_part.k_width[0] = roundup(d.num_k, 8);
+  d.rank = 0;
+  d.world = 1;
+  Layer L{};
+  CP_TRY(derive(L, d));
+  const size_t x = L.images ? (size_t)L.B * L.C * L.H * L.W * 4 : (size_t)L.in.start[L.in.n] * 4;
+  *bytes = al256(x) + al256((size_t)L.Kr * L.Ktot * 4) + al256((size_t)L.Kc * 4) +
+           al256((size_t)L.out.start[1] * 4) + al256((size_t)L.Hp * L.Wp * L.Bp * L.Kc) + al256(L.ws_total);
+  return CP_OK;
+}
+
+int conv_part_probe(const cp_conv_desc* desc, int32_t warmups, int32_t reps, void* scratch, size_t scratch_bytes,
+                    void* stream, double* median_s) {
+  if (!desc || !scratch || !median_s) CP_FAIL(CP_ERR_ARG, "conv_part_probe: null pointer");
+  if (reps < 1 || warmups < 0) CP_FAIL(CP_ERR_ARG, "conv_part_probe: reps >= 1, warmups >= 0");
+  size_t need = 0;
+  CP_TRY(conv_part_probe_bytes(desc, &need));
+  if (scratch_bytes < need) CP_FAIL(CP_ERR_ARG, "conv_part_probe: scratch too small, need " + std::to_string(need));
+  cp_conv_desc d = *desc;
+  d.out_part = cp_partition{};
+  d.out_part.n_ranks = 1;
+  d.out_part.num_k = d.num_k;
+  d.out_part.k_count[0] = d.num_k;
+  d.out_part.k_width[0] = roundup(d.num_k, 8);
+  d.rank = 0;
+  d.world = 1;
+  cp_layer L = nullptr;
+  CP_TRY(conv_part_create(&d, nullptr, &L));
+  cudaStream_t s = (cudaStream_t)stream;
+  char* p = (char*)scratch;
+  const size_t xb = L->images ? (size_t)L->B * L->C * L->H * L->W * 4 : (size_t)L->in.start[L->in.n] * 4;
+  float* x = (float*)p; p += al256(xb);
+  float* w = (float*)p; p += al256((size_t)L->Kr * L->Ktot * 4);
+  float* b = (float*)p; p += al256((size_t)L->Kc * 4);
+  float* y = (float*)p; p += al256((size_t)L->out.start[1] * 4);
+  uint8_t* sv = (uint8_t*)p; p += al256((size_t)L->Hp * L->Wp * L->Bp * L->Kc);
+  void* ws = p;
+  // "The convolution is run using random values, since only the time spent performing
+  // calculations is relevant".
+  int rc = launch_random_fill(x, xb / 4, 1234u, 1.0f, s);
+  if (rc == CP_OK) rc = launch_random_fill(w, (int64_t)L->Kr * L->Ktot, 5678u, 0.01f, s);
+  if (rc == CP_OK) rc = launch_fill(b, 0.f, L->Kc, s);
+  std::vector<double> t;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (rc == CP_OK && (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)) {
+    set_error("conv_part_probe: event create failed");
+    rc = CP_ERR_CUDA;
+  }
+  for (int i = 0; rc == CP_OK && i < warmups + reps; ++i) {
+    cudaEventRecord(e0, s);
+    rc = conv_part_forward(L, x, w, b, y, sv, ws, s, s);
+    cudaEventRecord(e1, s);
+    if (rc == CP_OK && cudaEventSynchronize(e1) != cudaSuccess) {
+      set_error("conv_part_probe: kernel failure");
+      rc = CP_ERR_CUDA;
+    }
+    float ms = 0;
+    if (rc == CP_OK) cudaEventElapsedTime(&ms, e0, e1);
+    if (i >= warmups) t.push_back(ms * 1e-3);
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  conv_part_destroy(L);
+  if (rc != CP_OK) return rc;
+  std::sort(t.begin(), t.end());
+  *median_s = t[t.size() / 2];
+  return CP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+"""Kernel-partitioned training of the paper's CNN on one rank (SPMD over P ranks).
+
+Host-side orchestration only: allocation of caller-owned device buffers (torch), and
+the order of C-ABI calls that make one SGD training step of the §5.2 network
+(P:L267-276): conv(5x5)+bias+ReLU+2x2 max-pool per conv layer (each rank its own
+contiguous kernel slice, Alg. 1), channel AllGather of every conv output,
+replicated FC + softmax loss head ("the master node is in charge of training
+the remaining network"), backward with the same split: dgrad of the own slice and a
+cross-rank sum of partial dX, wgrad local, SGD on the own slice.
+
+Every arithmetic step runs in libconvpart's kernels; nothing here computes.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import convpart as cp
+
+
+def _dev_bytes(n, device):
+    return torch.empty(max(int(n), 16), dtype=torch.uint8, device=device)
+
+
+def _f32(nbytes, device):
+    return torch.zeros(max(int(nbytes) // 4, 4), dtype=torch.float32, device=device)
+
+
+class PartitionedNet:
+    """One rank's share of the kernel-partitioned network.
+
+    kernels: conv kernel counts per layer (paper: (500, 1500)); parts: one cp_partition per
+    conv layer (same n_ranks); comm: cp_comm handle or None (no collectives).
+    """
+
+    def __init__(self, kernels, batch, parts, rank=0, comm=None, math=cp.CP_MATH_TF32, in_c=3, in_hw=32,
+                 ksize=5, classes=10, relu=True, pool=True, bias=True, device="cuda"):
+        self.device = torch.device(device)
+        self.B, self.Bp, self.O = batch, (batch + 31) // 32 * 32, classes
+        self.rank, self.world = rank, parts[0].n_ranks
+        self.parts, self.comm, self.math = parts, comm, math
+        self.layers, self.descs, self.sizes, self.buf = [], [], [], []
+        c, h, prev = in_c, in_hw, None
+        for i, K in enumerate(kernels):
+            d = cp.cp_conv_desc()
+            d.batch, d.in_c, d.in_h, d.in_w = batch, c, h, h
+            d.num_k, d.k_h, d.k_w = K, ksize, ksize
+            d.bias, d.relu, d.pool, d.math = int(bias), int(relu), int(pool), math
+            d.input_kind = cp.CP_INPUT_IMAGES if prev is None else cp.CP_INPUT_GATHER
+            d.out_part = parts[i]
+            if prev is not None:
+                d.in_part = prev
+            d.rank, d.world = rank, self.world
+            hnd = cp.conv_part_create(d, comm)
+            sz = cp.conv_part_query(hnd)
+            self.layers.append(hnd)
+            self.descs.append(d)
+            self.sizes.append(sz)
+            b = {
+                "w": _f32(sz.w, self.device), "b": _f32(sz.b, self.device),
+                "dw": _f32(sz.w, self.device), "db": _f32(sz.b, self.device),
+                "y": _f32(sz.y, self.device), "saved": _dev_bytes(sz.saved, self.device),
+                "ws": _dev_bytes(sz.workspace, self.device),
+            }
+            if prev is not None:
+                b["dx"] = _f32(sz.dx, self.device)
+            self.buf.append(b)
+            ho = h - ksize + 1
+            h = ho // 2 if pool else ho
+            c, prev = K, parts[i]
+        self.Hp = self.Wp = h
+        self.F = kernels[-1] * h * h
+        last = parts[-1]
+        Fg = h * h * sum(last.k_width[: last.n_ranks])
+        self.head = {
+            "wfc": torch.zeros(classes * Fg, device=self.device), "bfc": torch.zeros(classes, device=self.device),
+            "dwfc": torch.zeros(classes * Fg, device=self.device), "dbfc": torch.zeros(classes, device=self.device),
+            "logits": torch.zeros(batch * classes, device=self.device),
+            "dlogits": torch.zeros(batch * classes, device=self.device),
+            "loss": torch.zeros(4, device=self.device),
+            "da": _f32(self.sizes[-1].y, self.device),
+            "ws": _dev_bytes(cp.cp_head_workspace_bytes(batch, h, h, last, classes), self.device),
+        }
+        self.x = torch.zeros(batch * in_c * in_hw * in_hw, device=self.device)
+        self.labels = torch.zeros(batch, dtype=torch.int32, device=self.device)
+        self.in_shape = (batch, in_c, in_hw, in_hw)
+
+    # ------------------------------------------------------------ parameters
+    def load_params(self, params, stream=None):
+        """params: dict of full fp32 numpy arrays (KCRS conv, [O,F] fc).  Packs this rank's slice."""
+        for i, d in enumerate(self.descs):
+            wfull = torch.from_numpy(np.ascontiguousarray(params[f"w{i}"], np.float32)).to(self.device)
+            cp.cp_pack_conv_weights(d, wfull, self.buf[i]["w"], stream)
+            k0, kr = self.parts[i].k_begin[self.rank], self.parts[i].k_count[self.rank]
+            if kr:
+                self.buf[i]["b"][:kr].copy_(torch.from_numpy(np.ascontiguousarray(params[f"b{i}"][k0:k0 + kr])))
+        wfc = torch.from_numpy(np.ascontiguousarray(params["wfc"], np.float32)).to(self.device)
+        cp.cp_pack_fc_weights(wfc, self.O, self.Hp, self.Wp, self.parts[-1], self.head["wfc"], stream)
+        self.head["bfc"].copy_(torch.from_numpy(np.ascontiguousarray(params["bfc"], np.float32)))
+        torch.cuda.synchronize(self.device)
+
+    def export_params(self):
+        """This rank's rows (KCRS) of every conv layer and the full FC head, as numpy."""
+        out = {}
+        for i, d in enumerate(self.descs):
+            kr = self.parts[i].k_count[self.rank]
+            t = torch.zeros(max(kr * d.in_c * d.k_h * d.k_w, 1), device=self.device)
+            if kr:
+                cp.cp_unpack_conv_weights(d, self.buf[i]["w"], t)
+            out[f"w{i}"] = t[: kr * d.in_c * d.k_h * d.k_w].reshape(kr, d.in_c, d.k_h, d.k_w)
+            out[f"b{i}"] = self.buf[i]["b"][:kr]
+        wfc = torch.zeros(self.O * self.F, device=self.device)
+        cp.cp_unpack_fc_weights(self.head["wfc"], self.O, self.Hp, self.Wp, self.parts[-1], wfc)
+        out["wfc"] = wfc.reshape(self.O, self.F)
+        out["bfc"] = self.head["bfc"]
+        torch.cuda.synchronize(self.device)
+        return {k: v.detach().cpu().numpy().copy() for k, v in out.items()}
+
+    def set_batch(self, x, labels):
+        self.x.copy_(x.reshape(-1), non_blocking=True)
+        self.labels.copy_(labels.reshape(-1), non_blocking=True)
+
+    # ------------------------------------------------------------ one training step
+    def forward(self, stream=None, comm_stream=None):
+        inp = self.x
+        for i, L in enumerate(self.layers):
+            b = self.buf[i]
+            cp.conv_part_forward(L, inp, b["w"], b["b"], b["y"], b["saved"], b["ws"], stream, comm_stream)
+            inp = b["y"]
+        hd, last = self.head, self.parts[-1]
+        cp.cp_fc_forward(inp, self.B, self.Hp, self.Wp, last, hd["wfc"], hd["bfc"], self.O, hd["logits"], hd["ws"],
+                         stream)
+        cp.cp_softmax_xent(hd["logits"], self.labels, self.B, self.O, hd["loss"], hd["dlogits"], stream)
+
+    def backward(self, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True):
+        hd, last = self.head, self.parts[-1]
+        top = self.buf[-1]["y"]
+        cp.cp_fc_backward(hd["dlogits"], top, self.B, self.Hp, self.Wp, last, hd["wfc"], self.O, hd["da"],
+                          hd["dwfc"], hd["dbfc"], hd["ws"], stream)
+        da = hd["da"]
+        n = len(self.layers)
+        for i in reversed(range(n)):
+            L, b = self.layers[i], self.buf[i]
+            xin = self.x if i == 0 else self.buf[i - 1]["y"]
+            if i > 0:
+                mode = dx_mode | (cp.CP_DX_ASYNC if overlap else 0)
+                cp.conv_part_backward_data(L, da, b["saved"], b["y"], b["w"], b["dx"], mode, b["ws"], stream,
+                                           comm_stream)
+            # wgrad needs no communication: it overlaps the dX reduction on the comm stream (§8(e))
+            cp.conv_part_backward_filter(L, da, b["saved"], b["y"], xin, b["dw"], b["db"], b["ws"], stream)
+            if i > 0:
+                if overlap:
+                    cp.conv_part_wait(L, stream)
+                da = b["dx"]
+
+    def sgd(self, lr, stream=None):
+        for L, b in zip(self.layers, self.buf):
+            cp.conv_part_sgd_step(L, b["w"], b["b"], b["dw"], b["db"], lr, stream)
+        cp.cp_sgd(self.head["wfc"], self.head["dwfc"], lr, stream)
+        cp.cp_sgd(self.head["bfc"], self.head["dbfc"], lr, stream)
+
+    def step(self, lr=0.01, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True):
+        self.forward(stream, comm_stream)
+        self.backward(dx_mode, stream, comm_stream, overlap)
+        self.sgd(lr, stream)
+
+    def loss(self):
+        return float(self.head["loss"][0].item())
+
+    def close(self):
+        for L in self.layers:
+            cp.conv_part_destroy(L)
+        self.layers = []
+
+
+def plan_even(kernels, world):
+    return [cp.cp_partition_plan([1.0] * world, K) for K in kernels]

@@ -1,0 +1,206 @@
+"""GPU parity of every pass through the C ABI against the fp64 oracle (-m gpu).
+
+Per-pass parity on identical inputs: the oracle receives the same fp32
+values the GPU holds (widened), including the GPU's own outputs of the previous pass;
+backward passes replay the GPU's argmax/ReLU decisions (reading R15).
+Tolerance: max|gpu-ref| <= tol * max|ref| per tensor, tol = 1e-5 (FP32 SIMT) or 2e-3
+(TF32 tensor cores) — north_star.  P ranks are simulated on one GPU in LOCAL mode.
+Sizes span several M/N tiles with ragged tails (B=40 -> padded batch 64; 300 kernels ->
+two 256-wide N tiles; 70 input channels -> 32+32+8 channel chunks).
+"""
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_1712_02546_b200 import convpart as cp
+    from gpu_util import TOL, LocalLayer, assert_close, dev, pack, unpack
+else:  # collected on CPU but skipped
+    cp = None
+
+MATHS = ["simt", "tf32"]
+
+
+def math_id(m):
+    return cp.CP_MATH_FP32_SIMT if m == "simt" else cp.CP_MATH_TF32
+
+
+def parts_for(P, K):
+    if P == 1:
+        return cp.cp_partition_plan([1.0], K)
+    if P == 2:
+        return cp.cp_partition_plan([1.0, 1.0], K)
+    return cp.cp_partition_plan([1.0, 1.3, 2.1], K)        # uneven Eq. 1 map
+
+
+def layer_data(B=40, H=20, K1=70, K2=300, seed=3):
+    x, _ = synth.images(B, 3, H, H, step=seed)
+    w1 = synth.normal((K1, 3, 5, 5), seed + 1, 0.05)
+    b1 = synth.normal((K1,), seed + 2, 0.05)
+    w2 = synth.normal((K2, K1, 5, 5), seed + 3, 0.02)
+    b2 = synth.normal((K2,), seed + 4, 0.02)
+    return x, w1, b1, w2, b2
+
+
+def window_gap(z, relu=True):
+    """Gap between the best and second-best value of each 2x2 window (after ReLU)."""
+    if relu:
+        z = np.maximum(z, 0)
+    B, K, H, W = z.shape
+    v = z.reshape(B, K, H // 2, 2, W // 2, 2).transpose(0, 1, 2, 4, 3, 5).reshape(B, K, H // 2, W // 2, 4)
+    s = np.sort(v, -1)
+    return s[..., 3] - s[..., 2]
+
+
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_forward_parity(orc, math, P):
+    m = math_id(math)
+    x, w1, b1, w2, b2 = layer_data()
+    B, K1, K2 = x.shape[0], w1.shape[0], w2.shape[0]
+    p1, p2 = parts_for(P, K1), parts_for(P, K2)
+    L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
+    L1.load(w1, b1)
+    xd = dev(x)
+    L1.forward(xd)
+    z1 = orc.conv_fwd(x.astype(np.float64), w1.astype(np.float64), b1.astype(np.float64))
+    a1, am1 = orc.relu_pool_fwd(z1)
+    y1 = L1.y_nchw()
+    assert_close(y1, a1, TOL[m], f"conv1 fwd ({math}, P={P})")
+    gap = window_gap(z1)
+    bad = (L1.argmax_nchw() != am1) & (gap > 1e-4 * np.abs(a1).max()) & (a1 > 0)
+    assert bad.sum() == 0, f"argmax disagreements on well-separated windows: {bad.sum()}"
+
+    L2 = LocalLayer(B, K1, 8, K2, 5, p2, p1, m)
+    L2.load(w2, b2)
+    L2.forward(L1.y)
+    z2 = orc.conv_fwd(y1, w2.astype(np.float64), b2.astype(np.float64))     # GPU's own A1 as input
+    a2, am2 = orc.relu_pool_fwd(z2)
+    assert_close(L2.y_nchw(), a2, TOL[m], f"conv2 fwd ({math}, P={P})")
+    bad = (L2.argmax_nchw() != am2) & (window_gap(z2) > 1e-3 * np.abs(a2).max()) & (a2 > 0)
+    assert bad.sum() == 0
+    # padding slots and padded images are exactly zero
+    y = L2.y.cpu().numpy()
+    ref = orc.pack_gather(L2.y_nchw(), 64, *[np.array(v) for v in p2.as_tuple()])
+    assert np.array_equal(y, ref.astype(np.float32))
+    L1.close(); L2.close()
+
+
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_backward_parity(orc, math, P):
+    m = math_id(math)
+    x, w1, b1, w2, b2 = layer_data()
+    B, K1, K2 = x.shape[0], w1.shape[0], w2.shape[0]
+    p1, p2 = parts_for(P, K1), parts_for(P, K2)
+    L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
+    L1.load(w1, b1)
+    xd = dev(x)
+    L1.forward(xd)
+    L2 = LocalLayer(B, K1, 8, K2, 5, p2, p1, m)
+    L2.load(w2, b2)
+    L2.forward(L1.y)
+    y1, y2 = L1.y_nchw(), L2.y_nchw()
+    am2 = L2.argmax_nchw()
+    da2 = synth.normal(y2.shape, 99, 1.0).astype(np.float32)
+    dxs, dw2, db2 = L2.backward(pack(da2, p2), L1.y)
+    # oracle with decision replay (GPU argmax codes + GPU outputs)
+    dy2 = orc.unpool_relu_bwd(da2.astype(np.float64), am2, y2)
+    assert_close(unpack(dxs, B, K1, 8, p1), orc.conv_dgrad(dy2, w2.astype(np.float64)), TOL[m],
+                 f"conv2 dgrad ({math}, P={P})")
+    assert_close(dw2, orc.conv_wgrad(dy2, y1, 5, 5), TOL[m], f"conv2 wgrad ({math}, P={P})")
+    assert_close(db2, orc.bias_grad(dy2), 1e-5, f"conv2 bias grad ({math}, P={P})")
+    # conv1 backward_filter from the (replayed) gradient of its pooled output
+    da1 = unpack(dxs, B, K1, 8, p1).astype(np.float32)
+    _, dw1, db1 = L1.backward(pack(da1, p1), xd)
+    dy1 = orc.unpool_relu_bwd(da1.astype(np.float64), L1.argmax_nchw(), y1)
+    assert_close(dw1, orc.conv_wgrad(dy1, x.astype(np.float64), 5, 5), TOL[m], f"conv1 wgrad ({math}, P={P})")
+    assert_close(db1, orc.bias_grad(dy1), 1e-5, f"conv1 bias grad ({math}, P={P})")
+    L1.close(); L2.close()
+
+
+def test_pack_roundtrip_bitexact(orc):
+    g = np.random.default_rng(5)
+    for P, counts in [(1, [13]), (3, [5, 0, 9]), (4, [8, 8, 8, 7])]:
+        part = cp.cp_partition.from_counts(counts)
+        x = g.standard_normal((37, sum(counts), 3, 3)).astype(np.float32)
+        gd = pack(x, part)
+        ref = orc.pack_gather(x.astype(np.float64), 64, *[np.array(v) for v in part.as_tuple()])
+        assert np.array_equal(gd.cpu().numpy(), ref.astype(np.float32))
+        assert np.array_equal(unpack(gd, 37, sum(counts), 3, part), x.astype(np.float64))
+
+
+def test_head_parity(orc):
+    B, K, H, O = 40, 37, 5, 10
+    part = cp.cp_partition_plan([1.0, 2.0], K)
+    a = np.maximum(synth.normal((B, K, H, H), 7), 0).astype(np.float32)
+    wfc = synth.normal((O, K * H * H), 8, 0.05)
+    bfc = synth.normal((O,), 9, 0.05)
+    y = synth.images(B, step=4)[1]
+    ag = pack(a, part)
+    wg = torch.zeros(O * H * H * sum(part.k_width[:2]), device="cuda")
+    cp.cp_pack_fc_weights(dev(wfc), O, H, H, part, wg)
+    ws = torch.zeros(cp.cp_head_workspace_bytes(B, H, H, part, O), dtype=torch.uint8, device="cuda")
+    logits = torch.zeros(B * O, device="cuda")
+    cp.cp_fc_forward(ag, B, H, H, part, wg, dev(bfc), O, logits, ws)
+    ref = orc.fc_fwd(a.astype(np.float64), wfc.astype(np.float64), bfc.astype(np.float64))
+    assert_close(logits.reshape(B, O).cpu().numpy(), ref, 1e-5, "fc fwd")
+    loss = torch.zeros(1, device="cuda")
+    dl = torch.zeros(B * O, device="cuda")
+    cp.cp_softmax_xent(logits, dev(y, torch.int32), B, O, loss, dl)
+    rl, rdl = orc.softmax_xent(logits.reshape(B, O).cpu().numpy().astype(np.float64), y)
+    assert abs(loss.item() - rl) <= 1e-5 * abs(rl)
+    assert_close(dl.reshape(B, O).cpu().numpy(), rdl, 1e-5, "softmax grad")
+    dxg = torch.full((ag.numel(),), float("nan"), device="cuda")
+    dwg = torch.zeros_like(wg)
+    dbf = torch.zeros(O, device="cuda")
+    cp.cp_fc_backward(dl, ag, B, H, H, part, wg, O, dxg, dwg, dbf, ws)
+    rda, rdw, rdb = orc.fc_bwd(dl.reshape(B, O).cpu().numpy().astype(np.float64), a.astype(np.float64),
+                               wfc.astype(np.float64))
+    assert_close(unpack(dxg, B, K, H, part), rda, 1e-5, "fc dx")
+    dw = torch.zeros(O * K * H * H, device="cuda")
+    cp.cp_unpack_fc_weights(dwg, O, H, H, part, dw)
+    assert_close(dw.reshape(O, -1).cpu().numpy(), rdw, 1e-5, "fc dW")
+    assert_close(dbf.cpu().numpy(), rdb, 1e-5, "fc db")
+    # padded feature slots of dW stay exactly zero
+    back = torch.zeros_like(wg)
+    cp.cp_pack_fc_weights(dw, O, H, H, part, back)
+    assert torch.equal(back, dwg)
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_full_step_p1(orc, math):
+    """One whole training step (fwd, head, bwd, SGD) through PartitionedNet vs the oracle step
+    with decision replay; every updated parameter within tolerance."""
+    from paper_1712_02546_b200.net import PartitionedNet, plan_even
+    m = math_id(math)
+    net = synth.NetSpec(kernels=(24, 40), in_hw=20, name="small")
+    B = 40
+    params = synth.params(net, seed=11, std=0.05, bias_std=0.01)
+    x, y = synth.images(B, 3, 20, 20, step=1)
+    pn = PartitionedNet(net.kernels, B, plan_even(net.kernels, 1), math=m, in_hw=20)
+    pn.load_params(params)
+    pn.set_batch(dev(x), dev(y, torch.int32))
+    pn.forward()
+    torch.cuda.synchronize()
+    rep = []
+    for i, K in enumerate(net.kernels):
+        hp = (20 - 4) // 2 if i == 0 else 2
+        a = unpack(pn.buf[i]["y"], B, K, hp, pn.parts[i])
+        am = torch.zeros(B * K * hp * hp, dtype=torch.uint8, device="cuda")
+        cp.cp_unpack_saved(pn.buf[i]["saved"], B, hp, hp, pn.parts[i], 0, am)
+        rep.append({"a": a, "argmax": am.reshape(B, K, hp, hp).cpu().numpy()})
+    pn.backward()
+    pn.sgd(0.01)
+    new = pn.export_params()
+    p64 = {k: v.astype(np.float64) for k, v in params.items()}
+    tr = orc.net_step(p64, x.astype(np.float64), y, 0.01, net.layers(), replay=rep)
+    assert abs(pn.loss() - tr["loss"]) <= TOL[m] * abs(tr["loss"])
+    for k in p64:
+        # compare the update (new - old) so the tolerance applies to the gradient step
+        assert_close(new[k] - params[k], tr["new_params"][k] - p64[k], max(TOL[m], 1e-4), f"update of {k} ({math})")
+    pn.close()
