@@ -1,16 +1,648 @@
-// kernels_tc.cu — tcgen05/TMEM/TMA tensor-core convolutions (placeholder, being written).
+// kernels_tc.cu — the three convolution passes of a rank's kernel slice as implicit GEMMs on
+// the 5th-generation tensor cores (tcgen05, kind::tf32, fp32 accumulation in TMEM), operands
+// staged by TMA into 128B-swizzled shared memory through a 4-stage mbarrier ring.
+//
+//   FWD   (conv of own kernels, P:L175-177 / P:L212-214):
+//         Z[(p,q,b)][k] = sum_{tap,c'} A_in[p+r][q+s][b][c'] * W[k][tap][c']  (+bias, ReLU, 2x2 pool)
+//   DGRAD (input gradient of own kernels = the rank's partial dX, north_star):
+//         dX[(h,w,b)][c'] = sum_{tap,k} dY[h-r][w-s][b][k] * W[k][tap][c']
+//   WGRAD (weight gradient of own kernels, stays local, north_star):
+//         dW[k][(tap,c')] = sum_{(p,q,b)} dY[p][q][b][k] * A_in[p+r][q+s][b][c']
+//
+// M tiles of 128 rows: FWD/DGRAD rows are one 2x2 spatial window x 32 images (a 4-D TMA box
+// {32 ch, 32 b, 2 w, 2 h}), so a pooling window's four positions sit in the four TMEM lane
+// quadrants, i.e. in the four epilogue warps; WGRAD rows are 128 kernels.  N tiles <= 256.
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4-7 epilogue.
+// Persistent: grid = min(units, #SMs); two TMEM accumulators (2 x 256 columns) let the
+// epilogue of tile t overlap the MMAs of tile t+1.
+#include <vector>
+
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace cp {
-size_t tc_workspace_bytes(const Layer&) { return 0; }
-int tc_fwd(Layer&, const float*, const float*, const float*, float*, uint8_t*, void*, cudaStream_t) {
-  CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 forward not built yet");
+using namespace tc;
+
+namespace {
+
+enum { PASS_FWD = 0, PASS_DGRAD = 1, PASS_WGRAD = 2 };
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 4;          // 16 KB
+constexpr int B_BYTES = BN * BK * 4;          // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARP0 = 4;
+constexpr int POOL_LD = 33;                   // padded row of the pooling exchange buffer
+constexpr int POOL_BYTES = 4 * 32 * POOL_LD * 4;
+constexpr int MAX_NT = 64;
+constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + POOL_BYTES + 256;
+
+struct TcParams {
+  CUtensorMap maps[CP_MAX_RANKS + 1];  // per-block input maps [0..nblk) ; maps[16] = W (fwd/dgrad) or dY (wgrad/dgrad A)
+  int nblk;
+  int kw[CP_MAX_RANKS], coff[CP_MAX_RANKS];
+  long long start[CP_MAX_RANKS];
+  int Cg;              // concatenated input slots (or Kcol for images)
+  int R, S;
+  int Ho, Wo;          // conv output grid
+  int Hin, Win;        // conv input grid
+  int Wp;              // pooled width (fwd)
+  int Bp, B;
+  int Kr, Kc;          // own kernels / own slots
+  int Ktot;            // weight row length
+  int relu, pool, images;
+  int numM, numN, split, units, chunks_per_split, chunks_total;
+  int bn_box;          // fwd: B box rows
+  int nt_rb[MAX_NT], nt_n0[MAX_NT], nt_n[MAX_NT];  // dgrad / wgrad N-tile list (per tap for wgrad)
+  const float* bias;
+  float* out;          // fwd: y block ; dgrad: dx (full gather) ; wgrad: dW or split partials
+  uint8_t* saved;
+};
+
+struct Unit {
+  int mt, nt, sp;
+  int i, j, bc;        // spatial window / batch chunk (fwd, dgrad)
+  int n0, n;           // N origin (within own slots or block) and width
+  int rb, tap;         // dgrad: output block; wgrad: input block and tap
+};
+
+template <int PASS>
+__device__ __forceinline__ Unit decode_unit(const TcParams& p, int u) {
+  Unit t{};
+  t.mt = u % p.numM;
+  const int rest = u / p.numM;
+  t.nt = rest % p.numN;
+  t.sp = rest / p.numN;
+  if (PASS == PASS_FWD || PASS == PASS_DGRAD) {
+    const int nbc = p.Bp / 32;
+    const int W2 = (PASS == PASS_FWD ? p.Wo : p.Win) / 2;
+    t.bc = t.mt % nbc;
+    const int ij = t.mt / nbc;
+    t.j = ij % W2;
+    t.i = ij / W2;
+  }
+  if (PASS == PASS_FWD) {
+    t.n0 = t.nt * BN;
+    t.n = min(BN, p.Kc - t.n0);
+  } else if (PASS == PASS_DGRAD) {
+    t.rb = p.nt_rb[t.nt];
+    t.n0 = p.nt_n0[t.nt];
+    t.n = p.nt_n[t.nt];
+  } else {
+    const int per_tap = p.numN / (p.R * p.S);
+    t.tap = t.nt / per_tap;
+    const int e = t.nt % per_tap;
+    t.rb = p.nt_rb[e];
+    t.n0 = p.nt_n0[e];
+    t.n = p.nt_n[e];
+  }
+  return t;
 }
-int tc_dgrad(Layer&, const float*, const float*, float*, void*, cudaStream_t) {
-  CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad not built yet");
+
+// Visit the K-chunks of a unit in order: f(ksteps, c0..c3 of A, ...) is pass specific, so the
+// visitor hands back the raw loop indices and both warps derive coordinates identically.
+struct Chunk {
+  int tap, rb, c;     // fwd: tap, input block, channel chunk ; dgrad: tap, -, kernel chunk ; wgrad: -, -, k-chunk index
+  int ksteps;
+};
+
+template <int PASS, class F>
+__device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t, F f) {
+  if (PASS == PASS_FWD) {
+    for (int tap = 0; tap < p.R * p.S; ++tap)
+      for (int rb = 0; rb < p.nblk; ++rb) {
+        const int kw = p.kw[rb];
+        for (int c = 0; c * BK < kw; ++c) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8});
+      }
+  } else if (PASS == PASS_DGRAD) {
+    for (int r = 0; r < p.R; ++r) {
+      // rows 2i, 2i+1 of the input grid read dY rows 2i-r, 2i+1-r
+      const int h0 = 2 * t.i - r;
+      if (h0 + 1 < 0 || h0 >= p.Ho) continue;
+      for (int s = 0; s < p.S; ++s) {
+        const int w0 = 2 * t.j - s;
+        if (w0 + 1 < 0 || w0 >= p.Wo) continue;
+        for (int c = 0; c * BK < p.Kc; ++c) f(Chunk{r * p.S + s, 0, c, min(BK, p.Kc - c * BK) / 8});
+      }
+    }
+  } else {
+    const int c0 = t.sp * p.chunks_per_split;
+    const int c1 = min(p.chunks_total, c0 + p.chunks_per_split);
+    for (int c = c0; c < c1; ++c) f(Chunk{0, 0, c, BK / 8});
+  }
 }
-int tc_wgrad(Layer&, const float*, const float*, float*, void*, cudaStream_t) {
-  CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 wgrad not built yet");
+
+__device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], int n) {
+  if (n >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < n) dst[q] = v[q];
+  }
 }
+
+template <int PASS>
+__global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  float* pool_buf = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + POOL_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+    for (int m = 0; m < p.nblk; ++m) tma_prefetch(&p.maps[m]);
+    tma_prefetch(&p.maps[CP_MAX_RANKS]);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ======================= TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit t = decode_unit<PASS>(p, u);
+        for_each_chunk<PASS>(p, t, [&](const Chunk& ch) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a = sA + stage * A_BYTES;
+          uint8_t* b = sB + stage * B_BYTES;
+          if (PASS == PASS_FWD) {
+            const int r = ch.tap / p.S, s = ch.tap % p.S;
+            mbar_arrive_expect_tx(&full[stage], A_BYTES + p.bn_box * BK * 4);
+            tma_load_4d(a, &p.maps[ch.rb], &full[stage], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
+            tma_load_2d(b, &p.maps[CP_MAX_RANKS], &full[stage], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, t.n0);
+          } else if (PASS == PASS_DGRAD) {
+            const int r = ch.tap / p.S, s = ch.tap % p.S;
+            const int nb = (t.n + 31) / 32;
+            mbar_arrive_expect_tx(&full[stage], A_BYTES + nb * 4096);
+            tma_load_4d(a, &p.maps[0], &full[stage], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
+            for (int q = 0; q < nb; ++q)
+              tma_load_3d(b + q * 4096, &p.maps[CP_MAX_RANKS], &full[stage], p.coff[t.rb] + t.n0 + 32 * q,
+                          ch.c * BK, ch.tap);
+          } else {
+            const int nbc = p.Bp / 32;
+            const int bc = ch.c % nbc, pq = ch.c / nbc, q = pq % p.Wo, pp = pq / p.Wo;
+            const int r = t.tap / p.S, s = t.tap % p.S;
+            const int nb = (t.n + 31) / 32;
+            mbar_arrive_expect_tx(&full[stage], A_BYTES + nb * 4096);
+            for (int m = 0; m < 4; ++m)
+              tma_load_4d(a + m * 4096, &p.maps[CP_MAX_RANKS], &full[stage], t.mt * BM + 32 * m, bc * 32, q, pp);
+            for (int m = 0; m < nb; ++m)
+              tma_load_4d(b + m * 4096, &p.maps[t.rb], &full[stage], t.n0 + 32 * m, bc * 32, q + s, pp + r);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        });
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (one thread)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+        const Unit t = decode_unit<PASS>(p, u);
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int n_mma = (t.n + 7) / 8 * 8;
+        const uint32_t idesc = PASS == PASS_FWD    ? idesc_tf32(BM, n_mma, 0, 0)
+                               : PASS == PASS_DGRAD ? idesc_tf32(BM, n_mma, 0, 1)
+                                                    : idesc_tf32(BM, n_mma, 1, 1);
+        uint32_t accumulate = 0;
+        for_each_chunk<PASS>(p, t, [&](const Chunk& ch) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
+          for (int k = 0; k < ch.ksteps; ++k) {
+            const uint64_t ad = PASS == PASS_WGRAD ? sdesc_mn(a_addr, k) : sdesc_k(a_addr, k);
+            const uint64_t bd = PASS == PASS_FWD ? sdesc_k(b_addr, k) : sdesc_mn(b_addr, k);
+            mma_tf32(d_tmem, ad, bd, idesc, accumulate);
+            accumulate = 1;
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        });
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ======================= epilogue: TMEM -> registers -> global
+    const int quad = warp - EPI_WARP0;  // TMEM lane quadrant of this warp
+    const int row = quad * 32 + lane;   // accumulator row = TMEM lane
+    int local = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+      const Unit t = decode_unit<PASS>(p, u);
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      const int nchunk = (t.n + 31) / 32;
+      for (int cc = 0; cc < nchunk; ++cc) {
+        float v[32];
+        tmem_ld_32x32b_x32(tbase + cc * 32, v);
+        const int ncol = min(32, t.n - cc * 32);
+        if (PASS == PASS_FWD) {
+          const int nbase = t.n0 + cc * 32;  // own slot index of column 0
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int n = nbase + q;
+            float x = v[q] + ((p.bias && n < p.Kr) ? __ldg(p.bias + n) : 0.f);
+            if (p.relu && !(x > 0.f)) x = 0.f;
+            v[q] = x;
+          }
+          if (p.pool) {
+            // exchange through smem: quadrant = window position (dh, dw), lane = image
+            float* mine = pool_buf + (quad * 32 + lane) * POOL_LD;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) mine[q] = v[q];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..127
+            const int b = et >> 2, cb = (et & 3) * 8;
+            const int bb = t.bc * 32 + b;
+            float best[8];
+            uint32_t code[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              best[q] = pool_buf[(0 * 32 + b) * POOL_LD + cb + q];
+              code[q] = 0;
+            }
+#pragma unroll
+            for (int w4 = 1; w4 < 4; ++w4)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float x = pool_buf[(w4 * 32 + b) * POOL_LD + cb + q];
+                if (x > best[q]) {
+                  best[q] = x;
+                  code[q] = w4;
+                }
+              }
+            const int64_t o = ((int64_t)(t.i * p.Wp + t.j) * p.Bp + bb) * p.Kc + nbase + cb;
+            const bool real_b = bb < p.B;
+            float ov[8];
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const bool ok = real_b && (nbase + cb + q) < p.Kr;
+              ov[q] = ok ? tf32_rna(best[q]) : 0.f;
+              const uint32_t cq = ok ? code[q] : 0u;
+              if (q < 4) lo |= cq << (8 * q);
+              else hi |= cq << (8 * (q - 4));
+            }
+            if (cb < ncol) {
+              if (cb + 8 <= ncol) {
+                reinterpret_cast<float4*>(p.out + o)[0] = make_float4(ov[0], ov[1], ov[2], ov[3]);
+                reinterpret_cast<float4*>(p.out + o)[1] = make_float4(ov[4], ov[5], ov[6], ov[7]);
+                *reinterpret_cast<uint2*>(p.saved + o) = make_uint2(lo, hi);
+              } else {
+                for (int q = 0; q < 8 && cb + q < ncol; ++q) {
+                  p.out[o + q] = ov[q];
+                  p.saved[o + q] = (uint8_t)(q < 4 ? (lo >> (8 * q)) : (hi >> (8 * (q - 4))));
+                }
+              }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+          } else {
+            const int dh = quad >> 1, dw = quad & 1;
+            const int bb = t.bc * 32 + lane;
+            const int64_t o = ((int64_t)((2 * t.i + dh) * p.Wo + 2 * t.j + dw) * p.Bp + bb) * p.Kc + nbase;
+            const bool real_b = bb < p.B;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = (real_b && nbase + q < p.Kr) ? tf32_rna(v[q]) : 0.f;
+            store_f32x32(p.out + o, v, ncol);
+          }
+        } else if (PASS == PASS_DGRAD) {
+          const int dh = quad >> 1, dw = quad & 1;
+          const int bb = t.bc * 32 + lane;
+          const int kw = p.kw[t.rb];
+          const int64_t o = p.start[t.rb] +
+                            ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb) * kw + t.n0 + cc * 32;
+          store_f32x32(p.out + o, v, ncol);
+        } else {
+          const int kk = t.mt * BM + row;
+          if (kk < p.Kr) {
+            const int64_t col = (int64_t)t.tap * p.Cg + p.coff[t.rb] + t.n0 + cc * 32;
+            const int64_t o = ((int64_t)t.sp * p.Kr + kk) * p.Ktot + col;
+            store_f32x32(p.out + o, v, ncol);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// deterministic split-K reduction: dW[i] = sum_s part[s][i] in split order
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ out, int64_t n, int S) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= n) return;
+  if (i + 3 < n) {
+    float4 acc = *reinterpret_cast<const float4*>(part + i);
+    for (int s = 1; s < S; ++s) {
+      const float4 x = *reinterpret_cast<const float4*>(part + (int64_t)s * n + i);
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    *reinterpret_cast<float4*>(out + i) = acc;
+  } else {
+    for (int64_t j = i; j < n; ++j) {
+      float acc = part[j];
+      for (int s = 1; s < S; ++s) acc += part[(int64_t)s * n + j];
+      out[j] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int get_encoder(EncodeTiledFn* fn) {
+  static EncodeTiledFn f = nullptr;
+  if (!f) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !ptr)
+      CP_FAIL(CP_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    f = (EncodeTiledFn)ptr;
+  }
+  *fn = f;
+  return CP_OK;
+}
+
+// fp32 tensor map, zero OOB fill.  dims innermost first; strides in bytes for dims 1..
+// K-major operand tiles: SWIZZLE_128B; MN-major tiles: SWIZZLE_128B_ATOM_32B (see tc_common.cuh).
+int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+             const uint32_t* box, bool mn_major = false) {
+  EncodeTiledFn enc;
+  CP_TRY(get_encoder(&enc));
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+    if (i + 1 < rank) gs[i] = strides[i];
+  }
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), gd, gs, bx, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) CP_FAIL(CP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return CP_OK;
+}
+
+// 4-D map over an activation block [H][W][Bp][kw] with box {32, 32, bw, bh}
+int map_act(CUtensorMap* m, const float* base, int kw, int Bp, int W, int H, int bw, int bh, bool mn_major) {
+  const uint64_t dims[4] = {(uint64_t)kw, (uint64_t)Bp, (uint64_t)W, (uint64_t)H};
+  const uint64_t str[3] = {(uint64_t)kw * 4, (uint64_t)kw * Bp * 4, (uint64_t)kw * Bp * W * 4};
+  const uint32_t box[4] = {32, 32, (uint32_t)bw, (uint32_t)bh};
+  return make_map(m, base, 4, dims, str, box, mn_major);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int PASS>
+int launch(const TcParams& p, cudaStream_t s) {
+  if (p.units <= 0) return CP_OK;
+  static bool attr = false;
+  if (!attr) {
+    CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    attr = true;
+  }
+  const int grid = std::min(p.units, num_sms());
+  conv_tc_kernel<PASS><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(p);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
+void fill_blocks(TcParams& p, const Layer& L) {
+  if (L.images) {
+    p.nblk = 1;
+    p.kw[0] = L.Kcol;
+    p.coff[0] = 0;
+    p.start[0] = 0;
+    p.Cg = L.Kcol;
+  } else {
+    p.nblk = L.in.n;
+    for (int r = 0; r < L.in.n; ++r) {
+      p.kw[r] = L.in.kw[r];
+      p.coff[r] = L.in.coff[r];
+      p.start[r] = L.in.start[r];
+    }
+    p.Cg = L.in.Cg;
+  }
+}
+
+void fill_common(TcParams& p, const Layer& L) {
+  fill_blocks(p, L);
+  p.R = L.images ? 1 : L.R;
+  p.S = L.images ? 1 : L.S;
+  p.Ho = L.Ho;
+  p.Wo = L.Wo;
+  p.Hin = L.images ? L.Ho : L.H;   // images: im2col rows live on the output grid
+  p.Win = L.images ? L.Wo : L.W;
+  p.Wp = L.Wp;
+  p.Bp = L.Bp;
+  p.B = L.B;
+  p.Kr = L.Kr;
+  p.Kc = L.Kc;
+  p.Ktot = L.Ktot;
+  p.relu = L.d.relu;
+  p.pool = L.d.pool;
+  p.images = L.images;
+}
+
+// wgrad split-K factor: enough units for ~2 waves, >= 16 k-chunks per split
+void wgrad_split(const Layer& L, int tiles, int chunks, int* split, int* per) {
+  int S = 1;
+  const int target = 2 * num_sms();
+  if (tiles < target) S = std::min((target + tiles - 1) / tiles, std::max(1, chunks / 16));
+  S = std::max(1, std::min(S, 64));
+  int pc = (chunks + S - 1) / S;
+  S = (chunks + pc - 1) / pc;
+  *split = S;
+  *per = pc;
+  (void)L;
+}
+
+int wgrad_ntiles(const Layer& L, TcParams& p) {
+  // N tiles per tap: every input block cut into <=256-wide chunks
+  int n = 0;
+  for (int rb = 0; rb < p.nblk; ++rb)
+    for (int n0 = 0; n0 < p.kw[rb]; n0 += BN) {
+      if (n >= MAX_NT) return -1;
+      p.nt_rb[n] = rb;
+      p.nt_n0[n] = n0;
+      p.nt_n[n] = std::min(BN, p.kw[rb] - n0);
+      ++n;
+    }
+  (void)L;
+  return n;
+}
+
+}  // namespace
+
+size_t tc_workspace_bytes(const Layer& L) {
+  TcParams p{};
+  fill_common(p, L);
+  const int per_tap = wgrad_ntiles(L, p);
+  if (per_tap <= 0 || L.Kr == 0) return 0;
+  const int tiles = ((L.Kc + BM - 1) / BM) * per_tap * p.R * p.S;
+  const int chunks = L.Ho * L.Wo * (L.Bp / 32);
+  int S, per;
+  wgrad_split(L, tiles, chunks, &S, &per);
+  return S > 1 ? (size_t)S * L.Kr * L.Ktot * 4 : 0;
+}
+
+int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
+           cudaStream_t s) {
+  (void)ws;
+  if (L.Kc == 0) return CP_OK;
+  if ((L.Ho & 1) || (L.Wo & 1))
+    CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 forward needs an even conv output grid (2x2 window tiles)");
+  TcParams p{};
+  fill_common(p, L);
+  if (L.images) {
+    CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 2, 2, false));
+  } else {
+    for (int r = 0; r < L.in.n; ++r)
+      if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false));
+  }
+  p.bn_box = std::min(BN, L.Kc);
+  {
+    const uint64_t dims[2] = {(uint64_t)L.Ktot, (uint64_t)std::max(L.Kr, 1)};
+    const uint64_t str[1] = {(uint64_t)L.Ktot * 4};
+    const uint32_t box[2] = {32, (uint32_t)p.bn_box};
+    CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 2, dims, str, box));
+  }
+  p.numM = (L.Ho / 2) * (L.Wo / 2) * (L.Bp / 32);
+  p.numN = (L.Kc + BN - 1) / BN;
+  p.split = 1;
+  p.units = p.numM * p.numN;
+  p.bias = L.d.bias ? b : nullptr;
+  p.out = y_block;
+  p.saved = saved;
+  return launch<PASS_FWD>(p, s);
+}
+
+int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s) {
+  (void)ws;
+  if (L.images) CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad onto images");
+  if ((L.H & 1) || (L.W & 1)) CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad needs an even input grid");
+  if (L.Kc == 0 || L.Kr == 0) {
+    CP_CUDA(cudaMemsetAsync(dx, 0, (size_t)L.in.start[L.in.n] * 4, s));
+    return CP_OK;
+  }
+  TcParams p{};
+  fill_common(p, L);
+  CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false));
+  {
+    // W [Kr][RS][Cg] viewed as (c', k, tap): MN-major boxes {32 c', 32 k, 1}
+    const uint64_t dims[3] = {(uint64_t)L.in.Cg, (uint64_t)L.Kr, (uint64_t)(L.R * L.S)};
+    const uint64_t str[2] = {(uint64_t)L.Ktot * 4, (uint64_t)L.in.Cg * 4};
+    const uint32_t box[3] = {32, 32, 1};
+    CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 3, dims, str, box, true));
+  }
+  int n = 0;
+  for (int rb = 0; rb < L.in.n; ++rb)
+    for (int n0 = 0; n0 < L.in.kw[rb]; n0 += BN) {
+      if (n >= MAX_NT) CP_FAIL(CP_ERR_UNSUPPORTED, "too many dgrad N tiles");
+      p.nt_rb[n] = rb;
+      p.nt_n0[n] = n0;
+      p.nt_n[n] = std::min(BN, L.in.kw[rb] - n0);
+      ++n;
+    }
+  p.numM = (L.H / 2) * (L.W / 2) * (L.Bp / 32);
+  p.numN = n;
+  p.split = 1;
+  p.units = p.numM * p.numN;
+  p.out = dx;
+  return launch<PASS_DGRAD>(p, s);
+}
+
+int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s) {
+  if (L.Kr == 0) return CP_OK;
+  TcParams p{};
+  fill_common(p, L);
+  const int per_tap = wgrad_ntiles(L, p);
+  if (per_tap <= 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many wgrad N tiles");
+  if (L.images) {
+    CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 1, 1, true));
+  } else {
+    for (int r = 0; r < L.in.n; ++r)
+      if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 1, 1, true));
+  }
+  CP_TRY(map_act(&p.maps[CP_MAX_RANKS], dY, L.Kc, L.Bp, L.Wo, L.Ho, 1, 1, true));
+  p.numM = (L.Kc + BM - 1) / BM;
+  p.numN = per_tap * p.R * p.S;
+  p.chunks_total = L.Ho * L.Wo * (L.Bp / 32);
+  int S, per;
+  wgrad_split(L, p.numM * p.numN, p.chunks_total, &S, &per);
+  p.split = S;
+  p.chunks_per_split = per;
+  p.units = p.numM * p.numN * S;
+  float* part = S > 1 ? (float*)((char*)ws + L.off_split) : dw;
+  p.out = part;
+  CP_TRY(launch<PASS_WGRAD>(p, s));
+  if (S > 1) {
+    const int64_t n = (int64_t)L.Kr * L.Ktot;
+    splitk_reduce_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, s>>>(part, dw, n, S);
+    CP_LAUNCHED();
+  }
+  return CP_OK;
+}
+
 void tc_release(Layer&) {}
+
 }  // namespace cp

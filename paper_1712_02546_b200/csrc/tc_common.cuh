@@ -117,17 +117,30 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, float (&v)[32
 }
 
 // ---------------------------------------------------------------- UMMA descriptors
-// Shared-memory matrix descriptor, SWIZZLE_128B, version 1 (sm_100):
+// Shared-memory matrix descriptor, version 1 (sm_100):
 //  [0,14) start>>4  [16,30) LBO>>4  [32,46) SBO>>4  [46,48) version=1  [49,52) base offset=0
-//  [52] lbo mode=0  [61,64) layout (SWIZZLE_128B = 2)
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+//  [52] lbo mode=0  [61,64) layout type
+// K-major operands use SWIZZLE_128B (type 2): 8-row x 128 B atoms, SBO = 1024 B.
+// MN-major TF32 operands must use SWIZZLE_128B_BASE32B (type 1): 32-byte granules swizzled
+// within 128 B rows, 4-row atoms (TMA mode CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B); LBO = stride
+// between 32-element MN atoms, SBO = stride between 4-row K groups.
+constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128Base32B = 1;
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
+}
+// K-major, 128B swizzle: K-step of 8 tf32 = +32 bytes inside the 128 B row
+__device__ __forceinline__ uint64_t sdesc_k(uint32_t tile_addr, int kstep) {
+  return sdesc(tile_addr + kstep * 32, 16, 1024, kLayoutSW128);
+}
+// MN-major, 128B/32B-atom swizzle, 32x32 boxes stacked at 4 KB: K-step of 8 rows = +1024 bytes
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t tile_addr, int kstep) {
+  return sdesc(tile_addr + kstep * 1024, 4096, 512, kLayoutSW128Base32B);
 }
 // Instruction descriptor, kind::tf32 with fp32 accumulator:
 //  [4,6) c_format=1 (F32)  [7,10) a_format=2 (TF32)  [10,13) b_format=2 (TF32)

@@ -72,7 +72,7 @@ def test_forward_parity(orc, math, P):
     y1 = L1.y_nchw()
     assert_close(y1, a1, TOL[m], f"conv1 fwd ({math}, P={P})")
     gap = window_gap(z1)
-    bad = (L1.argmax_nchw() != am1) & (gap > 1e-4 * np.abs(a1).max()) & (a1 > 0)
+    bad = (L1.argmax_nchw() != am1) & (gap > 2 * TOL[m] * np.abs(a1).max()) & (a1 > 0)
     assert bad.sum() == 0, f"argmax disagreements on well-separated windows: {bad.sum()}"
 
     L2 = LocalLayer(B, K1, 8, K2, 5, p2, p1, m)
@@ -81,7 +81,7 @@ def test_forward_parity(orc, math, P):
     z2 = orc.conv_fwd(y1, w2.astype(np.float64), b2.astype(np.float64))     # GPU's own A1 as input
     a2, am2 = orc.relu_pool_fwd(z2)
     assert_close(L2.y_nchw(), a2, TOL[m], f"conv2 fwd ({math}, P={P})")
-    bad = (L2.argmax_nchw() != am2) & (window_gap(z2) > 1e-3 * np.abs(a2).max()) & (a2 > 0)
+    bad = (L2.argmax_nchw() != am2) & (window_gap(z2) > 2 * TOL[m] * np.abs(a2).max()) & (a2 > 0)
     assert bad.sum() == 0
     # padding slots and padded images are exactly zero
     y = L2.y.cpu().numpy()
