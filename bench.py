@@ -1,0 +1,369 @@
+"""Benchmark: kernel-partitioned training of the paper's 500:1500 CIFAR-10-shaped CNN on B200.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` (N>1 under torchrun, one rank
+per GPU, NCCL).  Prints ONE JSON line on rank 0.
+
+  * step   = one SGD training step of the whole network (conv1 fwd, AllGather, conv2 fwd,
+             AllGather, FC + softmax loss head, FC bwd, conv2 dgrad + ReduceScatter of dX,
+             conv2 wgrad, conv1 wgrad, SGD) — every conv layer kernel-partitioned across ranks
+             (arXiv 1712.02546 §4, Alg. 1).
+  * value  = images/s of the whole job: global batch / device-timed step time (max over ranks).
+             Every rank processes the same B images (its own kernels), so the batch counts once.
+  * e2e    = the same metric through the public API with host (pinned) buffers: the H2D copy of
+             the step's images + labels and the D2H read of the loss are inside the timed region.
+  * roofline = the dominant conv kernel (tcgen05 TF32 implicit GEMM), algorithmic FLOPs per launch
+             / CUDA-event duration, against the TF32 peak derived from MEASURED_PEAKS.json.
+  * cpu_baseline = the fp64 oracle (oracle/) timed on this host's cores on a bounded sample.
+  * --impl reference = the oracle itself as the reference arm (this tier has no reference code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense peaks (tf32 1.1, bf16 2.25 PF)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--net", default="500:1500")
+    ap.add_argument("--math", default="tf32", choices=["tf32", "simt"])
+    ap.add_argument("--partition", default="even", choices=["even", "probe"],
+                    help="even split, or Eq. 1 from the paper's probe (times all-gathered)")
+    ap.add_argument("--dx", default="rs", choices=["rs", "ar"])
+    ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+    except Exception:
+        pass
+    if "bf16_tflops_sustained" in p:
+        return {"tf32_sustained": p["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16,
+                "tf32_burst": p["bf16_tflops"] * NOMINAL_TF32_OVER_BF16, "hbm": p.get("hbm_gbs", 6449.1),
+                "source": "MEASURED_PEAKS.json bf16 x nominal tf32/bf16 (1.1/2.25)"}
+    return {"tf32_sustained": 1400.0 * NOMINAL_TF32_OVER_BF16, "tf32_burst": 1590.0 * NOMINAL_TF32_OVER_BF16,
+            "hbm": 6650.0, "source": "fallback B200_PROFILING.md x nominal tf32/bf16"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
+def oracle_images_per_s(net, target_s, step=0):
+    """Time the oracle's full training step on a bounded sample of the same workload."""
+    import numpy as np
+
+    import oracle
+    import synth
+    oracle.build()
+    params = {k: v.astype(np.float64) for k, v in synth.params(net, seed=42).items()}
+    b, elapsed, done = 1, 0.0, 0
+    while True:
+        x, y = synth.images(b, 3, net.in_hw, net.in_hw, step=step)
+        t0 = time.perf_counter()
+        oracle.net_step(params, x.astype(np.float64), y, 0.01, net.layers())
+        dt = time.perf_counter() - t0
+        elapsed += dt
+        done += b
+        if elapsed >= target_s * 0.5 or dt * 2 > target_s:
+            break
+        b = max(1, min(64, int(b * max(2.0, (target_s - elapsed) / max(dt, 1e-3) * 0.5))))
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return done / elapsed, cores, f"{done} images of the B=128 step's workload ({net.name}), fp64 oracle net_step, {elapsed:.1f} s"
+
+
+def run_reference(args):
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    net = synth.paper_net(args.net)
+    vals = []
+    for k in range(args.warmup + args.steps):
+        v, cores, sample = oracle_images_per_s(net, max(1.0, args.cpu_seconds / max(1, args.steps)), step=k)
+        if k >= args.warmup:
+            vals.append(v)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": "conv-layer train images/sec", "value": v, "unit": "images/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.batch / v * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"paper net {args.net}, CIFAR-10-shaped 32x32x3, batch "
+                                                        f"{args.batch}, CPU fp64 oracle (bounded sample per step)",
+                                            "global_batch": args.batch},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_1712_02546_b200 import convpart as cp
+    from paper_1712_02546_b200.net import PartitionedNet
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    net = synth.paper_net(args.net)
+    B = args.batch
+    math = cp.CP_MATH_TF32 if args.math == "tf32" else cp.CP_MATH_FP32_SIMT
+
+    # ---- communicator: unique id from rank 0 through torch.distributed (plumbing)
+    comm = None
+    if world > 1:
+        uid = [cp.cp_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = cp.cp_comm_create(uid[0], rank, world)
+
+    # ---- partition map: even, or Eq. 1 from the paper's probe convolution (§4.1.1)
+    probe_times = None
+    if args.partition == "probe" and world > 1:
+        d = cp.cp_conv_desc()
+        c, h = net.shapes()[1][0], net.shapes()[1][1]
+        d.batch, d.in_c, d.in_h, d.in_w, d.num_k, d.k_h, d.k_w = B, c, h, h, net.kernels[1], 5, 5
+        d.bias, d.relu, d.pool, d.math, d.input_kind = 1, 1, 1, math, cp.CP_INPUT_GATHER
+        d.in_part = cp.cp_partition_plan([1.0], c)
+        d.out_part = cp.cp_partition_plan([1.0], net.kernels[1])
+        d.rank, d.world = 0, 1
+        scratch = torch.empty(cp.conv_part_probe_bytes(d), dtype=torch.uint8, device=dev)
+        t = cp.conv_part_probe(d, scratch, warmups=1, reps=3)
+        del scratch
+        allt = [None] * world
+        dist.all_gather_object(allt, t)
+        probe_times = allt
+        parts = [cp.cp_partition_plan(allt, K) for K in net.kernels]
+    else:
+        parts = [cp.cp_partition_plan([1.0] * world, K) for K in net.kernels]
+
+    pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev)
+    params = synth.params(net, seed=42)
+    pn.load_params(params)
+    x, y = synth.images(B, 3, 32, 32, step=0)
+    x_host = torch.from_numpy(x).pin_memory()
+    y_host = torch.from_numpy(y).pin_memory()
+    pn.set_batch(x_host.to(dev), y_host.to(dev))
+    s = torch.cuda.current_stream(dev)
+    cs = torch.cuda.Stream(dev)
+    dx_mode = cp.CP_DX_REDUCE_SCATTER if args.dx == "rs" else cp.CP_DX_ALLREDUCE
+    overlap = not args.no_overlap
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        pn.step(0.01, dx_mode, s, cs, overlap)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    # ---- device-timed region: K steps, L2 flushed between steps (outside the step events)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    n0 = cp.cp_launch_count()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.fill_(k & 0xFF)
+        ev[k][0].record(s)
+        step()
+        ev[k][1].record(s)
+    torch.cuda.synchronize(dev)
+    launches = cp.cp_launch_count() - n0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = B / (ms_per_step / 1e3)
+
+    # ---- end to end through the public API: pinned host images/labels in, loss out, per step
+    h2d = x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size()
+    d2h = 4
+    loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        if flush is not None:
+            flush.fill_(k & 0xFF)
+        e2e_ev[k][0].record(s)
+        pn.x.copy_(x_host.reshape(-1), non_blocking=True)
+        pn.labels.copy_(y_host, non_blocking=True)
+        step()
+        loss_host.copy_(pn.head["loss"][:1], non_blocking=True)
+        e2e_ev[k][1].record(s)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = B / (e2e_ms / args.steps / 1e3)
+
+    # ---- per-pass kernel timing of conv2 (the dominant kernels) on a no-collective clone
+    L2d = pn.descs[1]
+    h2 = cp.conv_part_create(L2d, None)
+    b2 = pn.buf[1]
+    ws2 = torch.empty_like(b2["ws"])
+    y2 = b2["y"].clone()
+    sv2 = b2["saved"].clone()
+    dw2 = torch.empty_like(b2["dw"])
+    db2 = torch.empty_like(b2["db"])
+    dx2 = torch.empty_like(b2["dx"])
+    a1 = pn.buf[0]["y"]
+    da2 = pn.head["da"]
+    reps = 5
+    tim = {"fwd": [], "wgrad": [], "dgrad": []}
+    for r in range(reps + 1):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        if flush is not None:
+            flush.fill_(r)
+        e[0].record(s)
+        cp.conv_part_forward(h2, a1, b2["w"], b2["b"], y2, sv2, ws2, s, s)
+        e[1].record(s)
+        cp.conv_part_backward_filter(h2, da2, sv2, y2, a1, dw2, db2, ws2, s)
+        e[2].record(s)
+        cp.conv_part_backward_data(h2, da2, sv2, y2, b2["w"], dx2, cp.CP_DX_LOCAL, ws2, s, s)
+        e[3].record(s)
+        torch.cuda.synchronize(dev)
+        if r:
+            tim["fwd"].append(e[0].elapsed_time(e[1]))
+            tim["wgrad"].append(e[1].elapsed_time(e[2]))
+            tim["dgrad"].append(e[2].elapsed_time(e[3]))
+    cp.conv_part_destroy(h2)
+    Kr2 = parts[1].k_count[rank]
+    C2, H2o = net.kernels[0], 10
+    flop_pass = 2.0 * B * Kr2 * C2 * 25 * H2o * H2o   # algorithmic MACs x2 of one conv2 pass, own slice
+    pk = peaks()
+    per = {k: statistics.median(v) for k, v in tim.items()}
+    dom = max(per, key=per.get)
+    achieved = flop_pass / (per[dom] / 1e3) / 1e12
+    conv2_tflops = {k: flop_pass / (v / 1e3) / 1e12 for k, v in per.items()}
+    loss = pn.loss()
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, sample = oracle_images_per_s(net, args.cpu_seconds)
+            cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle", "sample": sample}
+        step_flop = 11.368e9 * B  # algorithmic training FLOPs per image (paper net)
+        line = {
+            "metric": "conv-layer train images/sec (whole-network SGD step, kernel-partitioned)",
+            "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "tf32" if math == cp.CP_MATH_TF32 else "f32", "data": "synthetic",
+            "config": {
+                "workload": f"paper net {args.net} (conv5x5 {net.kernels[0]} -> pool -> conv5x5 {net.kernels[1]} -> "
+                            f"pool -> FC 37500->10 -> softmax), CIFAR-10-shaped 32x32x3, batch {B}",
+                "global_batch": B, "partition": [list(p.k_count[:p.n_ranks]) for p in parts],
+                "partition_source": "Eq.1 from probe" if probe_times else "even",
+                "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
+                "parallelism": f"kernel-split x{world}",
+                "l2": "flushed between timed steps (256 MiB write outside the step events)" if flush is not None
+                      else "not flushed (step working set ~700 MB > 126 MB L2)"},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "kernel": f"conv2 {dom} (tcgen05 kind::tf32 implicit GEMM)",
+                         "achieved": achieved, "peak": pk["tf32_sustained"], "unit": "TFLOP/s",
+                         "frac": achieved / pk["tf32_sustained"], "traffic": None,
+                         "flop_per_launch": flop_pass, "launch_ms": per[dom],
+                         "peak_source": pk["source"] + " (sustained)",
+                         "conv2_pass_ms": per, "conv2_pass_tflops": conv2_tflops},
+            "tc_frac_whole_step": step_flop / (ms_per_step / 1e3) / 1e12 / pk["tf32_sustained"],
+            "clocks": clk, "loss": loss,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    pn.close()
+    if comm is not None:
+        cp.cp_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
