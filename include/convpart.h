@@ -137,6 +137,8 @@ typedef struct {
   int32_t rank, world;         /* this rank; world == out_part.n_ranks            */
 } cp_conv_desc;
 
+/* w, x, y and dx include 256 bytes of read slack past the tensor (TMA atoms of 32 columns may
+ * read, but never use, a few elements beyond the last row). */
 typedef struct {
   size_t w;         /* bytes of this rank's GPU-layout weights                    */
   size_t b;         /* bytes of this rank's bias                                  */

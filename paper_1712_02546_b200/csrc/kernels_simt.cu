@@ -7,6 +7,8 @@
 // Method cites: conv = valid cross-correlation, stride 1; ReLU + 2x2/2
 // max-pool with first-max ties; FC + softmax loss (P:L275-276,
 // S:L98-115); SGD.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace cp {
@@ -213,25 +215,34 @@ int launch_wgrad_simt(const Layer& L, const float* dY, const float* x, const flo
 }
 
 // ============================================================== layout / elementwise
+// im2col of the images for conv1: rows (p,q,b) of the output grid, columns (r,s,c) padded to Kcol.
+// One thread per 4 consecutive columns (float4 store); reads are tiny and L2/L1-resident.
 __global__ void im2col_kernel(const float* __restrict__ x, float* __restrict__ xcol, int B, int C, int H,
-                              int W, int R, int S, int Wo, int Bp, int Kcol, int64_t total, int round) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= total) return;
-  const int col = e % Kcol;
-  const int64_t m = e / Kcol;
+                              int W, int R, int S, int Wo, int Bp, int Kcol, int64_t total4, int round) {
+  const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e4 >= total4) return;
+  const int kc4 = Kcol >> 2;
+  const int col0 = (int)(e4 % kc4) * 4;
+  const int m = (int)(e4 / kc4);
   const int b = m % Bp, pq = m / Bp, q = pq % Wo, p = pq / Wo;
-  float v = 0.f;
-  if (b < B && col < R * S * C) {
-    const int c = col % C, tap = col / C, r = tap / S, s = tap % S;
-    v = x[(((int64_t)b * C + c) * H + p + r) * W + q + s];
+  float v[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int col = col0 + t;
+    float u = 0.f;
+    if (b < B && col < R * S * C) {
+      const int c = col % C, tap = col / C, r = tap / S, s = tap - r * S;
+      u = __ldg(x + (((int64_t)b * C + c) * H + p + r) * W + q + s);
+    }
+    v[t] = round ? tf32_rna(u) : u;
   }
-  xcol[e] = round ? tf32_rna(v) : v;
+  reinterpret_cast<float4*>(xcol)[e4] = make_float4(v[0], v[1], v[2], v[3]);
 }
 
 int launch_im2col(const Layer& L, const float* x, float* xcol, bool round_tf32, cudaStream_t s) {
-  const int64_t total = (int64_t)L.Ho * L.Wo * L.Bp * L.Kcol;
-  im2col_kernel<<<grid1d(total, 256), 256, 0, s>>>(x, xcol, L.B, L.C, L.H, L.W, L.R, L.S, L.Wo, L.Bp, L.Kcol,
-                                                   total, round_tf32 ? 1 : 0);
+  const int64_t total4 = (int64_t)L.Ho * L.Wo * L.Bp * (L.Kcol / 4);
+  im2col_kernel<<<grid1d(total4, 256), 256, 0, s>>>(x, xcol, L.B, L.C, L.H, L.W, L.R, L.S, L.Wo, L.Bp, L.Kcol,
+                                                    total4, round_tf32 ? 1 : 0);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -283,34 +294,52 @@ int launch_relu_pool(const Layer& L, const float* z, float* y_block, uint8_t* sa
   return CP_OK;
 }
 
-// Epilogue backward: dY[h][w][b][slot] = dy_pooled routed to the argmax position, times ReLU'.
+// Epilogue backward: dY[h][w][b][slot] = dy_pooled routed to the argmax position, times ReLU'
+// (ReLU'(0)=0, reading R7).  One thread per (pooled position, image, 4 slots): it reads
+// dy/y/codes once (float4 + 4 bytes) and writes the four window positions (4 x float4), so every
+// pre-pool element is written exactly once with coalesced 16-byte stores.
 __global__ void unpool_kernel(const float* __restrict__ dyp, const uint8_t* __restrict__ am,
                               const float* __restrict__ y, float* __restrict__ dY, int Wo, int Wp, int Bp,
-                              int Kc, int64_t total, int relu, int pool, int round) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= total) return;
-  const int slot = e % Kc;
-  const int64_t rest = e / Kc;
-  const int b = rest % Bp;
-  const int64_t hw = rest / Bp;
-  float v;
-  if (pool) {
-    const int w = hw % Wo, h = hw / Wo;
-    const int64_t pe = ((int64_t)((h >> 1) * Wp + (w >> 1)) * Bp + b) * Kc + slot;
-    const int code = am[pe];
-    const bool hit = code == (((h & 1) << 1) | (w & 1));
-    v = (hit && (!relu || y[pe] > 0.f)) ? dyp[pe] : 0.f;
-  } else {
-    v = (!relu || y[e] > 0.f) ? dyp[e] : 0.f;
+                              int Kc, int64_t total4, int relu, int pool, int round) {
+  const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e4 >= total4) return;
+  const int kc4 = Kc >> 2;
+  const int slot = (int)(e4 % kc4) * 4;
+  const int64_t rest = e4 / kc4;  // pooled row index (i*Wp + j)*Bp + b
+  const int b = (int)(rest % Bp);
+  const int ij = (int)(rest / Bp);
+  const int64_t pe = rest * Kc + slot;
+  const float4 g = *reinterpret_cast<const float4*>(dyp + pe);
+  const float4 yy = *reinterpret_cast<const float4*>(y + pe);
+  float gv[4] = {g.x, g.y, g.z, g.w};
+  const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    if (relu && !(yv[t] > 0.f)) gv[t] = 0.f;
+    if (round) gv[t] = tf32_rna(gv[t]);
   }
-  dY[e] = round ? tf32_rna(v) : v;
+  if (!pool) {
+    *reinterpret_cast<float4*>(dY + pe) = make_float4(gv[0], gv[1], gv[2], gv[3]);
+    return;
+  }
+  const uint32_t codes = *reinterpret_cast<const uint32_t*>(am + pe);
+  const int j = ij % Wp, i = ij / Wp;
+#pragma unroll
+  for (int pos = 0; pos < 4; ++pos) {
+    const int h = 2 * i + (pos >> 1), w = 2 * j + (pos & 1);
+    float o[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) o[t] = ((codes >> (8 * t)) & 0xFFu) == (uint32_t)pos ? gv[t] : 0.f;
+    *reinterpret_cast<float4*>(dY + ((int64_t)(h * Wo + w) * Bp + b) * Kc + slot) = make_float4(o[0], o[1], o[2], o[3]);
+  }
 }
 
 int launch_unpool(const Layer& L, const float* dy_block, const uint8_t* saved, const float* y_block, float* dY,
                   bool round_tf32, cudaStream_t s) {
-  const int64_t total = (int64_t)L.Ho * L.Wo * L.Bp * L.Kc;
-  unpool_kernel<<<grid1d(total, 256), 256, 0, s>>>(dy_block, saved, y_block, dY, L.Wo, L.Wp, L.Bp, L.Kc, total,
-                                                   L.d.relu, L.d.pool, round_tf32 ? 1 : 0);
+  const int64_t total4 = (int64_t)L.Hp * L.Wp * L.Bp * (L.Kc / 4);
+  if (total4 == 0) return CP_OK;
+  unpool_kernel<<<grid1d(total4, 256), 256, 0, s>>>(dy_block, saved, y_block, dY, L.Wo, L.Wp, L.Bp, L.Kc, total4,
+                                                    L.d.relu, L.d.pool, round_tf32 ? 1 : 0);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -490,25 +519,46 @@ __global__ void unpack_w_images_kernel(const float* __restrict__ wg, float* __re
 // FC features in gather order: block r, position pos = h*Wp+w, slot; f' = Hp*Wp*coff[r] + pos*kw[r] + slot.
 constexpr int kMaxO = 16;
 
-__global__ void fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg, float* __restrict__ part,
-                               Blocks g, int B, int O, int PW) {
-  const int u = blockIdx.x;  // unit = (block r, position pos)
-  const int r = u / PW, pos = u % PW;
+// Units of the FC reduction: (rank block r, position pos, 256-slot chunk sc); partial logits per
+// (unit, image) are summed in unit order by fc_fwd_reduce (fixed order -> bitwise identical on
+// every rank).  Grid (units, Bp/32): 8 warps x 4 images; lane = slot; weights held in registers.
+constexpr int kFcChunk = 256;
+__host__ __device__ inline int fc_nsc(const Blocks& g) {
+  int m = 0;
+  for (int r = 0; r < g.n; ++r) m = g.kw[r] > m ? g.kw[r] : m;
+  return (m + kFcChunk - 1) / kFcChunk;
+}
+
+__global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
+                                                      float* __restrict__ part, Blocks g, int B, int O, int PW,
+                                                      int nsc) {
+  const int u = blockIdx.x;
+  const int sc = u % nsc, rp = u / nsc;
+  const int r = rp / PW, pos = rp % PW;
   const int kw = g.kw[r];
   const int64_t F = (int64_t)PW * g.Cg;
   const int64_t foff = (int64_t)PW * g.coff[r] + (int64_t)pos * kw;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int b = warp; b < g.Bp; b += blockDim.x >> 5) {
+  float wr[8][kMaxO];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int sl = sc * kFcChunk + t * 32 + lane;
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o) wr[t][o] = (sl < kw && o < O) ? __ldg(wg + o * F + foff + sl) : 0.f;
+  }
+  for (int q = 0; q < 4; ++q) {
+    const int b = blockIdx.y * 32 + warp * 4 + q;
     float acc[kMaxO];
 #pragma unroll
     for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
     if (b < B) {
       const float* xr = x + g.start[r] + ((int64_t)pos * g.Bp + b) * kw;
-      for (int sl = lane; sl < kw; sl += 32) {
-        const float xv = xr[sl];
 #pragma unroll
-        for (int o = 0; o < kMaxO; ++o)
-          if (o < O) acc[o] = fmaf(xv, wg[(int64_t)o * F + foff + sl], acc[o]);
+      for (int t = 0; t < 8; ++t) {
+        const int sl = sc * kFcChunk + t * 32 + lane;
+        const float xv = sl < kw ? __ldg(xr + sl) : 0.f;
+#pragma unroll
+        for (int o = 0; o < kMaxO; ++o) acc[o] = fmaf(xv, wr[t][o], acc[o]);
       }
     }
 #pragma unroll
@@ -557,50 +607,62 @@ __global__ void softmax_xent_kernel(const float* __restrict__ logits, const int*
   }
 }
 
+// dA2 in gather layout: dx[(r,pos,b,slot)] = sum_o dlogits[b][o] * W[o][f(r,pos,slot)], zero for b >= B.
+// Grid (r*PW + pos, ceil(Bp*kw/4 / 256)); one thread per 4 slots (float4).
 __global__ void fc_bwd_dx(const float* __restrict__ dl, const float* __restrict__ wg, float* __restrict__ dx,
                           Blocks g, int B, int O, int PW) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= g.start[g.n]) return;
-  const int r = block_of_elem(g, e);
-  const int64_t l = e - g.start[r];
+  const int rp = blockIdx.x;
+  const int r = rp / PW, pos = rp % PW;
   const int kw = g.kw[r];
-  const int slot = l % kw;
-  const int64_t rest = l / kw;
-  const int b = rest % g.Bp;
-  const int pos = rest / g.Bp;
-  float acc = 0.f;
+  const int kw4 = kw >> 2;
+  const int e4 = blockIdx.y * blockDim.x + threadIdx.x;
+  if (e4 >= g.Bp * kw4) return;
+  const int b = e4 / kw4, slot = (e4 % kw4) * 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (b < B) {
     const int64_t F = (int64_t)PW * g.Cg;
     const int64_t f = (int64_t)PW * g.coff[r] + (int64_t)pos * kw + slot;
-    for (int o = 0; o < O; ++o) acc = fmaf(dl[(int64_t)b * O + o], wg[(int64_t)o * F + f], acc);
+    for (int o = 0; o < O; ++o) {
+      const float d = __ldg(dl + b * O + o);
+      const float4 w = __ldg(reinterpret_cast<const float4*>(wg + o * F + f));
+      acc.x = fmaf(d, w.x, acc.x); acc.y = fmaf(d, w.y, acc.y);
+      acc.z = fmaf(d, w.z, acc.z); acc.w = fmaf(d, w.w, acc.w);
+    }
   }
-  dx[e] = acc;
+  *reinterpret_cast<float4*>(dx + g.start[r] + ((int64_t)pos * g.Bp + b) * kw + slot) = acc;
 }
 
-__global__ void fc_bwd_dw(const float* __restrict__ dl, const float* __restrict__ x, float* __restrict__ dwg,
-                          Blocks g, int B, int O, int PW) {
-  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// dW_fc[o][f] = sum_b dlogits[b][o] * x(b, f): one thread per 4 features, b ascending (fixed order).
+__global__ void __launch_bounds__(64) fc_bwd_dw(const float* __restrict__ dl, const float* __restrict__ x,
+                                                float* __restrict__ dwg, Blocks g, int B, int O, int PW) {
   const int64_t F = (int64_t)PW * g.Cg;
+  const int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (f >= F) return;
-  // f -> (r, pos, slot)
   int r = 0;
   while (r + 1 < g.n && f >= (int64_t)PW * g.coff[r + 1]) ++r;
   const int64_t l = f - (int64_t)PW * g.coff[r];
   const int kw = g.kw[r];
-  const int pos = l / kw, slot = l % kw;
-  float acc[kMaxO];
+  const int pos = (int)(l / kw), slot = (int)(l % kw);
+  float acc[kMaxO][4];
 #pragma unroll
-  for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
+  for (int o = 0; o < kMaxO; ++o)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc[o][t] = 0.f;
   const float* xp = x + g.start[r] + (int64_t)pos * g.Bp * kw + slot;
   for (int b = 0; b < B; ++b) {
-    const float xv = xp[(int64_t)b * kw];
+    const float4 xv = __ldg(reinterpret_cast<const float4*>(xp + (int64_t)b * kw));
 #pragma unroll
-    for (int o = 0; o < kMaxO; ++o)
-      if (o < O) acc[o] = fmaf(dl[(int64_t)b * O + o], xv, acc[o]);
+    for (int o = 0; o < kMaxO; ++o) {
+      if (o < O) {
+        const float d = __ldg(dl + b * O + o);
+        acc[o][0] = fmaf(d, xv.x, acc[o][0]); acc[o][1] = fmaf(d, xv.y, acc[o][1]);
+        acc[o][2] = fmaf(d, xv.z, acc[o][2]); acc[o][3] = fmaf(d, xv.w, acc[o][3]);
+      }
+    }
   }
 #pragma unroll
   for (int o = 0; o < kMaxO; ++o)
-    if (o < O) dwg[(int64_t)o * F + f] = acc[o];
+    if (o < O) *reinterpret_cast<float4*>(dwg + o * F + f) = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
 }
 
 __global__ void fc_bwd_db(const float* __restrict__ dl, float* dbfc, int B, int O) {
@@ -754,7 +816,8 @@ int cp_head_workspace_bytes(int32_t B, int32_t Hp, int32_t Wp, const cp_partitio
                             size_t* bytes) {
   CP_TRY(check_part(part));
   if (!bytes) CP_FAIL(CP_ERR_ARG, "null bytes");
-  *bytes = (size_t)part->n_ranks * Hp * Wp * roundup(B, 32) * O * sizeof(float) + 256;
+  Blocks g = make_blocks(*part, Hp, Wp, roundup(B, 32));
+  *bytes = (size_t)part->n_ranks * Hp * Wp * fc_nsc(g) * g.Bp * O * sizeof(float) + 256;
   return CP_OK;
 }
 
@@ -789,10 +852,10 @@ int cp_fc_forward(const float* x, int32_t B, int32_t Hp, int32_t Wp, const cp_pa
   if (!x || !wg || !logits || !ws) CP_FAIL(CP_ERR_ARG, "cp_fc_forward: null pointer");
   if (O < 1 || O > kMaxO) CP_FAIL(CP_ERR_UNSUPPORTED, "cp_fc_forward: O must be in [1,16]");
   Blocks g = make_blocks(*part, Hp, Wp, roundup(B, 32));
-  const int PW = Hp * Wp, U = g.n * PW;
+  const int PW = Hp * Wp, nsc = fc_nsc(g), U = g.n * PW * nsc;
   float* part_buf = (float*)ws;
   cudaStream_t s = (cudaStream_t)stream;
-  fc_fwd_partial<<<U, 256, 0, s>>>(x, wg, part_buf, g, B, O, PW);
+  fc_fwd_partial<<<dim3(U, g.Bp / 32), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
   CP_LAUNCHED();
   fc_fwd_reduce<<<cdiv(B * O, 128), 128, 0, s>>>(part_buf, bfc, logits, U, g.Bp, B, O);
   CP_LAUNCHED();
@@ -817,11 +880,13 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
   const int PW = Hp * Wp;
   cudaStream_t s = (cudaStream_t)stream;
   if (dx) {
-    fc_bwd_dx<<<grid1d(g.start[g.n], 256), 256, 0, s>>>(dl, wg, dx, g, B, O, PW);
+    int maxkw = 0;
+    for (int r = 0; r < g.n; ++r) maxkw = std::max(maxkw, g.kw[r]);
+    fc_bwd_dx<<<dim3(g.n * PW, cdiv((int64_t)g.Bp * (maxkw / 4), 256)), 256, 0, s>>>(dl, wg, dx, g, B, O, PW);
     CP_LAUNCHED();
   }
   if (dwg) {
-    fc_bwd_dw<<<grid1d((int64_t)PW * g.Cg, 128), 128, 0, s>>>(dl, x, dwg, g, B, O, PW);
+    fc_bwd_dw<<<grid1d((int64_t)PW * g.Cg / 4, 64), 64, 0, s>>>(dl, x, dwg, g, B, O, PW);
     CP_LAUNCHED();
   }
   if (dbfc) {

@@ -26,19 +26,27 @@ using namespace tc;
 namespace {
 
 enum { PASS_FWD = 0, PASS_DGRAD = 1, PASS_WGRAD = 2 };
-constexpr int BM = 128, BN = 256, BK = 32, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 4;          // 16 KB
-constexpr int B_BYTES = BN * BK * 4;          // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128, BN = 256, BK = 32;
+constexpr int A_BYTES = BM * BK * 4;          // 16 KB: this CTA's 128 rows x 32 k
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARP0 = 4;
 constexpr int POOL_LD = 33;                   // padded row of the pooling exchange buffer
 constexpr int POOL_BYTES = 4 * 32 * POOL_LD * 4;
 constexpr int MAX_NT = 64;
-constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + POOL_BYTES + 256;
+
+// CG = CTAs per MMA (cta_group::1 or ::2).  With a CTA pair the MMA is M=256 (128 rows per CTA)
+// and each CTA stages only half of B (N/2 columns), so per-SM operand traffic drops by 1/3 and
+// the freed shared memory buys a deeper ring.
+template <int CG>
+struct Cfg {
+  static constexpr int B_BYTES = CG == 1 ? BN * BK * 4 : (BN / 2) * BK * 4;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + POOL_BYTES + 256;
+};
 
 struct TcParams {
-  CUtensorMap maps[CP_MAX_RANKS + 1];  // per-block input maps [0..nblk) ; maps[16] = W (fwd/dgrad) or dY (wgrad/dgrad A)
+  CUtensorMap maps[CP_MAX_RANKS + 1];  // per-block input maps [0..nblk) ; maps[16] = W (fwd/dgrad) or dY (wgrad); dgrad A = maps[0]
   int nblk;
   int kw[CP_MAX_RANKS], coff[CP_MAX_RANKS];
   long long start[CP_MAX_RANKS];
@@ -51,8 +59,9 @@ struct TcParams {
   int Kr, Kc;          // own kernels / own slots
   int Ktot;            // weight row length
   int relu, pool, images;
-  int numM, numN, split, units, chunks_per_split, chunks_total;
+  int numM, numN, split, units, chunks_per_split, chunks_total;  // numM counts M tiles per CTA group
   int bn_box;          // fwd: B box rows
+  int wide;            // MN-major operands loaded as one 5-D box of 32-column atoms (else per-atom boxes)
   int nt_rb[MAX_NT], nt_n0[MAX_NT], nt_n[MAX_NT];  // dgrad / wgrad N-tile list (per tap for wgrad)
   const float* bias;
   float* out;          // fwd: y block ; dgrad: dx (full gather) ; wgrad: dW or split partials
@@ -66,20 +75,26 @@ struct Unit {
   int rb, tap;         // dgrad: output block; wgrad: input block and tap
 };
 
-template <int PASS>
-__device__ __forceinline__ Unit decode_unit(const TcParams& p, int u) {
+// Unit u of this CTA group -> the tile of CTA `rank` (rank = 0 for CG=1).  With CG=2 the pair's
+// two M tiles are two consecutive 32-image chunks of the same 2x2 window (FWD/DGRAD: identical
+// tap lists, so both CTAs run the same K loop) or two consecutive 128-kernel tiles (WGRAD).
+template <int PASS, int CG>
+__device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) {
   Unit t{};
-  t.mt = u % p.numM;
+  const int mg = u % p.numM;
   const int rest = u / p.numM;
   t.nt = rest % p.numN;
   t.sp = rest / p.numN;
   if (PASS == PASS_FWD || PASS == PASS_DGRAD) {
-    const int nbc = p.Bp / 32;
+    const int nbcg = p.Bp / 32 / CG;
     const int W2 = (PASS == PASS_FWD ? p.Wo : p.Win) / 2;
-    t.bc = t.mt % nbc;
-    const int ij = t.mt / nbc;
+    t.bc = (mg % nbcg) * CG + rank;
+    const int ij = mg / nbcg;
     t.j = ij % W2;
     t.i = ij / W2;
+    t.mt = mg;
+  } else {
+    t.mt = mg * CG + rank;
   }
   if (PASS == PASS_FWD) {
     t.n0 = t.nt * BN;
@@ -132,6 +147,16 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
   }
 }
 
+// MMA N for a tile of n columns: multiple of 8 (1 CTA) / 16 (pair); with a pair and MN-major B
+// each CTA's half must be whole 32-column atoms, so N is rounded to 64 (extra columns are zero
+// or neighbouring data and are never stored).
+template <int PASS, int CG>
+__host__ __device__ __forceinline__ int mma_n(int n) {
+  if (CG == 1) return (n + 7) / 8 * 8;
+  if (PASS == PASS_FWD) return (n + 15) / 16 * 16;
+  return (n + 63) / 64 * 64;
+}
+
 __device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], int n) {
   if (n >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
@@ -144,76 +169,103 @@ __device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], i
   }
 }
 
-template <int PASS>
+template <int PASS, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
+  using C = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  float* pool_buf = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + POOL_BYTES);
+  uint8_t* sB = smem + C::STAGES * A_BYTES;
+  float* pool_buf = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + POOL_BYTES);
   uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;
+  uint64_t* tempty = bars + 2 * C::STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const int group = blockIdx.x / CG, ngroups = gridDim.x / CG;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CG);
     }
     fence_barrier_init();
     for (int m = 0; m < p.nblk; ++m) tma_prefetch(&p.maps[m]);
     tma_prefetch(&p.maps[CP_MAX_RANKS]);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) tmem_alloc<CG>(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ======================= TMA producer
+    // ======================= TMA producer (both CTAs of a pair load their own halves)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const Unit t = decode_unit<PASS>(p, u);
+      for (int u = group; u < p.units; u += ngroups) {
+        const Unit t = decode_unit<PASS, CG>(p, u, rank);
+        const int n_mma = mma_n<PASS, CG>(t.n);
+        const int nb_own = CG == 2 ? n_mma / 2 : n_mma;          // B columns staged by this CTA
+        const int nb0 = t.n0 + (int)rank * nb_own;                // first B column of this CTA
+        const int nboxes = p.wide ? (CG == 2 ? 4 : 8) : (nb_own + 31) / 32;  // MN-major B: 32-column atoms
+        const uint32_t tx_cta = PASS == PASS_FWD ? A_BYTES + p.bn_box * BK * 4 : A_BYTES + nboxes * 4096;
         for_each_chunk<PASS>(p, t, [&](const Chunk& ch) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * A_BYTES;
-          uint8_t* b = sB + stage * B_BYTES;
+          uint8_t* b = sB + stage * C::B_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], tx_cta * CG);
+          const uint32_t lbar = CG == 2 ? mapa(smem_u32(&full[stage]), 0) : 0u;
+          auto ld2 = [&](void* d, const CUtensorMap* m, int c0, int c1) {
+            if (CG == 2) tma_load_2d_cg2(d, m, lbar, c0, c1); else tma_load_2d(d, m, &full[stage], c0, c1);
+          };
+          auto ld3 = [&](void* d, const CUtensorMap* m, int c0, int c1, int c2) {
+            if (CG == 2) tma_load_3d_cg2(d, m, lbar, c0, c1, c2); else tma_load_3d(d, m, &full[stage], c0, c1, c2);
+          };
+          auto ld4 = [&](void* d, const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+            if (CG == 2) tma_load_4d_cg2(d, m, lbar, c0, c1, c2, c3);
+            else tma_load_4d(d, m, &full[stage], c0, c1, c2, c3);
+          };
+          auto ld5 = [&](void* d, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4) {
+            if (CG == 2) tma_load_5d_cg2(d, m, lbar, c0, c1, c2, c3, c4);
+            else tma_load_5d(d, m, &full[stage], c0, c1, c2, c3, c4);
+          };
           if (PASS == PASS_FWD) {
             const int r = ch.tap / p.S, s = ch.tap % p.S;
-            mbar_arrive_expect_tx(&full[stage], A_BYTES + p.bn_box * BK * 4);
-            tma_load_4d(a, &p.maps[ch.rb], &full[stage], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
-            tma_load_2d(b, &p.maps[CP_MAX_RANKS], &full[stage], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, t.n0);
+            ld4(a, &p.maps[ch.rb], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
+            ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.tap / p.S, s = ch.tap % p.S;
-            const int nb = (t.n + 31) / 32;
-            mbar_arrive_expect_tx(&full[stage], A_BYTES + nb * 4096);
-            tma_load_4d(a, &p.maps[0], &full[stage], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
-            for (int q = 0; q < nb; ++q)
-              tma_load_3d(b + q * 4096, &p.maps[CP_MAX_RANKS], &full[stage], p.coff[t.rb] + t.n0 + 32 * q,
-                          ch.c * BK, ch.tap);
+            ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
+            if (p.wide) {
+              ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BK, (p.coff[t.rb] + nb0) >> 5, ch.tap);
+            } else {
+              for (int q = 0; q < nboxes; ++q)
+                ld3(b + q * 4096, &p.maps[CP_MAX_RANKS], p.coff[t.rb] + nb0 + 32 * q, ch.c * BK, ch.tap);
+            }
           } else {
             const int nbc = p.Bp / 32;
             const int bc = ch.c % nbc, pq = ch.c / nbc, q = pq % p.Wo, pp = pq / p.Wo;
             const int r = t.tap / p.S, s = t.tap % p.S;
-            const int nb = (t.n + 31) / 32;
-            mbar_arrive_expect_tx(&full[stage], A_BYTES + nb * 4096);
-            for (int m = 0; m < 4; ++m)
-              tma_load_4d(a + m * 4096, &p.maps[CP_MAX_RANKS], &full[stage], t.mt * BM + 32 * m, bc * 32, q, pp);
-            for (int m = 0; m < nb; ++m)
-              tma_load_4d(b + m * 4096, &p.maps[t.rb], &full[stage], t.n0 + 32 * m, bc * 32, q + s, pp + r);
+            if (p.wide) {
+              ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
+              ld5(b, &p.maps[t.rb], 0, bc * 32, nb0 >> 5, q + s, pp + r);
+            } else {
+              for (int m = 0; m < 4; ++m)
+                ld4(a + m * 4096, &p.maps[CP_MAX_RANKS], t.mt * BM + 32 * m, bc * 32, q, pp);
+              for (int m = 0; m < nboxes; ++m)
+                ld4(b + m * 4096, &p.maps[t.rb], nb0 + 32 * m, bc * 32, q + s, pp + r);
+            }
           }
-          if (++stage == STAGES) {
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -221,50 +273,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer (one thread)
-    if (lane == 0) {
+    // ======================= MMA issuer (one thread of the leader CTA)
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
-        const Unit t = decode_unit<PASS>(p, u);
+      for (int u = group; u < p.units; u += ngroups, ++local) {
+        const Unit t = decode_unit<PASS, CG>(p, u, 0);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int n_mma = (t.n + 7) / 8 * 8;
-        const uint32_t idesc = PASS == PASS_FWD    ? idesc_tf32(BM, n_mma, 0, 0)
-                               : PASS == PASS_DGRAD ? idesc_tf32(BM, n_mma, 0, 1)
-                                                    : idesc_tf32(BM, n_mma, 1, 1);
+        const int n_mma = mma_n<PASS, CG>(t.n);
+        const int a_mn = PASS == PASS_WGRAD, b_mn = PASS != PASS_FWD;
+        const uint32_t idesc = idesc_tf32(BM * CG, n_mma, a_mn, b_mn);
         uint32_t accumulate = 0;
         for_each_chunk<PASS>(p, t, [&](const Chunk& ch) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
           for (int k = 0; k < ch.ksteps; ++k) {
-            const uint64_t ad = PASS == PASS_WGRAD ? sdesc_mn(a_addr, k) : sdesc_k(a_addr, k);
-            const uint64_t bd = PASS == PASS_FWD ? sdesc_k(b_addr, k) : sdesc_mn(b_addr, k);
-            mma_tf32(d_tmem, ad, bd, idesc, accumulate);
+            const uint64_t ad = a_mn ? sdesc_mn(a_addr, k) : sdesc_k(a_addr, k);
+            const uint64_t bd = b_mn ? sdesc_mn(b_addr, k) : sdesc_k(b_addr, k);
+            if (CG == 2) mma_tf32_cg2(d_tmem, ad, bd, idesc, accumulate);
+            else mma_tf32(d_tmem, ad, bd, idesc, accumulate);
             accumulate = 1;
           }
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) {
+          if (CG == 2) mma_commit_cg2(&empty[stage]); else mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         });
-        mma_commit(&tfull[acc]);
+        if (CG == 2) mma_commit_cg2(&tfull[acc]); else mma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= EPI_WARP0) {
-    // ======================= epilogue: TMEM -> registers -> global
+    // ======================= epilogue: TMEM -> registers -> global (each CTA its own 128 rows)
     const int quad = warp - EPI_WARP0;  // TMEM lane quadrant of this warp
-    const int row = quad * 32 + lane;   // accumulator row = TMEM lane
+    const int row = quad * 32 + lane;   // accumulator row of this CTA = TMEM lane
     int local = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
-      const Unit t = decode_unit<PASS>(p, u);
+    for (int u = group; u < p.units; u += ngroups, ++local) {
+      const Unit t = decode_unit<PASS, CG>(p, u, rank);
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
@@ -361,13 +413,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(mapa(smem_u32(&tempty[acc]), 0));
+        else mbar_arrive(&tempty[acc]);
+      }
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc<CG>(tmem_base, 512);
   }
 }
 
@@ -441,6 +497,17 @@ int map_act(CUtensorMap* m, const float* base, int kw, int Bp, int W, int H, int
   return make_map(m, base, 4, dims, str, box, mn_major);
 }
 
+// 5-D map over an activation block [H][W][Bp][kw] as (32-slot atom lane, b, atom, w, h): one box
+// {32, 32, natoms, 1, 1} lands as natoms stacked MN-major 32x32 atoms (the canonical layout).
+// Slots past kw inside the last atom read neighbouring data: they only feed output columns/rows
+// that are never stored, and every buffer carries read slack (conv_part_query).
+int map_act_wide(CUtensorMap* m, const float* base, int kw, int Bp, int W, int H, int natoms) {
+  const uint64_t dims[5] = {32, (uint64_t)Bp, (uint64_t)((kw + 31) / 32), (uint64_t)W, (uint64_t)H};
+  const uint64_t str[4] = {(uint64_t)kw * 4, 128, (uint64_t)kw * Bp * 4, (uint64_t)kw * Bp * W * 4};
+  const uint32_t box[5] = {32, 32, (uint32_t)natoms, 1, 1};
+  return make_map(m, base, 5, dims, str, box, true);
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -452,18 +519,41 @@ int num_sms() {
   return n;
 }
 
-template <int PASS>
-int launch(const TcParams& p, cudaStream_t s) {
+template <int PASS, int CG>
+int launch_cg(const TcParams& p, cudaStream_t s) {
   if (p.units <= 0) return CP_OK;
   static bool attr = false;
   if (!attr) {
-    CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Cfg<CG>::SMEM));
     attr = true;
   }
-  const int grid = std::min(p.units, num_sms());
-  conv_tc_kernel<PASS><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(p);
+  const int groups = std::min(p.units, num_sms() / CG);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(groups * CG);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = Cfg<CG>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CP_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<PASS, CG>, p));
   CP_LAUNCHED();
   return CP_OK;
+}
+
+// 2-CTA pairs unless disabled (CP_TC_CTA_GROUP=1) or the pass cannot pair its M tiles.
+bool use_pairs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CP_TC_CTA_GROUP");
+    v = (e && atoi(e) == 1) ? 0 : 1;
+  }
+  return v == 1;
 }
 
 void fill_blocks(TcParams& p, const Layer& L) {
@@ -503,17 +593,16 @@ void fill_common(TcParams& p, const Layer& L) {
   p.images = L.images;
 }
 
-// wgrad split-K factor: enough units for ~2 waves, >= 16 k-chunks per split
-void wgrad_split(const Layer& L, int tiles, int chunks, int* split, int* per) {
+// wgrad split-K factor: enough units for ~2 waves of CTA groups, >= 16 k-chunks per split
+void wgrad_split(int units, int chunks, int groups, int* split, int* per) {
   int S = 1;
-  const int target = 2 * num_sms();
-  if (tiles < target) S = std::min((target + tiles - 1) / tiles, std::max(1, chunks / 16));
+  const int target = 2 * groups;
+  if (units < target) S = std::min((target + units - 1) / units, std::max(1, chunks / 16));
   S = std::max(1, std::min(S, 64));
   int pc = (chunks + S - 1) / S;
   S = (chunks + pc - 1) / pc;
   *split = S;
   *per = pc;
-  (void)L;
 }
 
 int wgrad_ntiles(const Layer& L, TcParams& p) {
@@ -533,16 +622,30 @@ int wgrad_ntiles(const Layer& L, TcParams& p) {
 
 }  // namespace
 
+// wgrad work decomposition shared by the workspace query and the launch
+struct WgradPlan {
+  bool pair;
+  int per_tap, numM, numN, S, per, chunks;
+};
+static WgradPlan wgrad_plan(const Layer& L, TcParams& p) {
+  WgradPlan w{};
+  w.pair = use_pairs();
+  w.per_tap = wgrad_ntiles(L, p);
+  const int CG = w.pair ? 2 : 1;
+  w.numM = ((L.Kc + BM - 1) / BM + CG - 1) / CG;
+  w.numN = w.per_tap * p.R * p.S;
+  w.chunks = L.Ho * L.Wo * (L.Bp / 32);
+  wgrad_split(w.numM * w.numN, w.chunks, num_sms() / CG, &w.S, &w.per);
+  return w;
+}
+
 size_t tc_workspace_bytes(const Layer& L) {
   TcParams p{};
   fill_common(p, L);
-  const int per_tap = wgrad_ntiles(L, p);
-  if (per_tap <= 0 || L.Kr == 0) return 0;
-  const int tiles = ((L.Kc + BM - 1) / BM) * per_tap * p.R * p.S;
-  const int chunks = L.Ho * L.Wo * (L.Bp / 32);
-  int S, per;
-  wgrad_split(L, tiles, chunks, &S, &per);
-  return S > 1 ? (size_t)S * L.Kr * L.Ktot * 4 : 0;
+  if (L.Kr == 0) return 0;
+  const WgradPlan w = wgrad_plan(L, p);
+  if (w.per_tap <= 0) return 0;
+  return w.S > 1 ? (size_t)w.S * L.Kr * L.Ktot * 4 : 0;
 }
 
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
@@ -559,21 +662,22 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     for (int r = 0; r < L.in.n; ++r)
       if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false));
   }
-  p.bn_box = std::min(BN, L.Kc);
+  const bool pair = use_pairs() && (L.Bp / 32) % 2 == 0;
+  p.bn_box = pair ? BN / 2 : std::min(BN, L.Kc);
   {
     const uint64_t dims[2] = {(uint64_t)L.Ktot, (uint64_t)std::max(L.Kr, 1)};
     const uint64_t str[1] = {(uint64_t)L.Ktot * 4};
     const uint32_t box[2] = {32, (uint32_t)p.bn_box};
     CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 2, dims, str, box));
   }
-  p.numM = (L.Ho / 2) * (L.Wo / 2) * (L.Bp / 32);
+  p.numM = (L.Ho / 2) * (L.Wo / 2) * (L.Bp / 32) / (pair ? 2 : 1);
   p.numN = (L.Kc + BN - 1) / BN;
   p.split = 1;
   p.units = p.numM * p.numN;
   p.bias = L.d.bias ? b : nullptr;
   p.out = y_block;
   p.saved = saved;
-  return launch<PASS_FWD>(p, s);
+  return pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s);
 }
 
 int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s) {
@@ -587,7 +691,17 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   TcParams p{};
   fill_common(p, L);
   CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false));
-  {
+  const bool pair = use_pairs() && (L.Bp / 32) % 2 == 0;
+  p.wide = 1;
+  for (int r = 0; r < L.in.n; ++r)
+    if (L.in.coff[r] % 32) p.wide = 0;
+  if (p.wide) {
+    // W [Kr][RS][Cg] viewed as (c' lane, k, c' atom, tap): one box {32, 32, natoms, 1}
+    const uint64_t dims[4] = {32, (uint64_t)L.Kr, (uint64_t)((L.in.Cg + 31) / 32), (uint64_t)(L.R * L.S)};
+    const uint64_t str[3] = {(uint64_t)L.Ktot * 4, 128, (uint64_t)L.in.Cg * 4};
+    const uint32_t box[4] = {32, 32, (uint32_t)(pair ? 4 : 8), 1};
+    CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 4, dims, str, box, true));
+  } else {
     // W [Kr][RS][Cg] viewed as (c', k, tap): MN-major boxes {32 c', 32 k, 1}
     const uint64_t dims[3] = {(uint64_t)L.in.Cg, (uint64_t)L.Kr, (uint64_t)(L.R * L.S)};
     const uint64_t str[2] = {(uint64_t)L.Ktot * 4, (uint64_t)L.in.Cg * 4};
@@ -603,41 +717,41 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
       p.nt_n[n] = std::min(BN, L.in.kw[rb] - n0);
       ++n;
     }
-  p.numM = (L.H / 2) * (L.W / 2) * (L.Bp / 32);
+  p.numM = (L.H / 2) * (L.W / 2) * (L.Bp / 32) / (pair ? 2 : 1);
   p.numN = n;
   p.split = 1;
   p.units = p.numM * p.numN;
   p.out = dx;
-  return launch<PASS_DGRAD>(p, s);
+  return pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s);
 }
 
 int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s) {
   if (L.Kr == 0) return CP_OK;
   TcParams p{};
   fill_common(p, L);
-  const int per_tap = wgrad_ntiles(L, p);
-  if (per_tap <= 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many wgrad N tiles");
+  const WgradPlan w = wgrad_plan(L, p);
+  if (w.per_tap <= 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many wgrad N tiles");
+  p.wide = 1;
+  const int nat = w.pair ? 4 : 8;
   if (L.images) {
-    CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 1, 1, true));
+    CP_TRY(map_act_wide(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, nat));
   } else {
     for (int r = 0; r < L.in.n; ++r)
-      if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 1, 1, true));
+      if (L.in.kw[r] > 0) CP_TRY(map_act_wide(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, nat));
   }
-  CP_TRY(map_act(&p.maps[CP_MAX_RANKS], dY, L.Kc, L.Bp, L.Wo, L.Ho, 1, 1, true));
-  p.numM = (L.Kc + BM - 1) / BM;
-  p.numN = per_tap * p.R * p.S;
-  p.chunks_total = L.Ho * L.Wo * (L.Bp / 32);
-  int S, per;
-  wgrad_split(L, p.numM * p.numN, p.chunks_total, &S, &per);
-  p.split = S;
-  p.chunks_per_split = per;
-  p.units = p.numM * p.numN * S;
-  float* part = S > 1 ? (float*)((char*)ws + L.off_split) : dw;
+  CP_TRY(map_act_wide(&p.maps[CP_MAX_RANKS], dY, L.Kc, L.Bp, L.Wo, L.Ho, 4));
+  p.numM = w.numM;
+  p.numN = w.numN;
+  p.chunks_total = w.chunks;
+  p.split = w.S;
+  p.chunks_per_split = w.per;
+  p.units = p.numM * p.numN * w.S;
+  float* part = w.S > 1 ? (float*)((char*)ws + L.off_split) : dw;
   p.out = part;
-  CP_TRY(launch<PASS_WGRAD>(p, s));
-  if (S > 1) {
+  CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2>(p, s) : launch_cg<PASS_WGRAD, 1>(p, s)));
+  if (w.S > 1) {
     const int64_t n = (int64_t)L.Kr * L.Ktot;
-    splitk_reduce_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, s>>>(part, dw, n, S);
+    splitk_reduce_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, s>>>(part, dw, n, w.S);
     CP_LAUNCHED();
   }
   return CP_OK;

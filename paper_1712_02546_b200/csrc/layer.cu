@@ -159,10 +159,11 @@ int conv_part_create(const cp_conv_desc* desc, cp_comm comm, cp_layer* out) {
 
 int conv_part_query(cp_layer L, cp_sizes* o) {
   if (!L || !o) CP_FAIL(CP_ERR_ARG, "conv_part_query: null pointer");
-  o->w = (size_t)L->Kr * L->Ktot * 4;
+  // +256 B read slack on every operand the tensor-core path streams with 32-column atoms
+  o->w = (size_t)L->Kr * L->Ktot * 4 + 256;
   o->b = (size_t)L->Kr * 4;
-  o->x = L->images ? (size_t)L->B * L->C * L->H * L->W * 4 : (size_t)L->in.start[L->in.n] * 4;
-  o->y = (size_t)L->out.start[L->out.n] * 4;
+  o->x = (L->images ? (size_t)L->B * L->C * L->H * L->W * 4 : (size_t)L->in.start[L->in.n] * 4) + 256;
+  o->y = (size_t)L->out.start[L->out.n] * 4 + 256;
   o->y_block = (size_t)(L->out.start[L->d.rank + 1] - L->out.start[L->d.rank]) * 4;
   o->y_offset = (size_t)L->out.start[L->d.rank] * 4;
   o->saved = L->d.pool ? (size_t)L->Hp * L->Wp * L->Bp * L->Kc : 0;
@@ -294,8 +295,8 @@ int conv_part_probe_bytes(const cp_conv_desc* desc, size_t* bytes) {
   Layer L{};
   CP_TRY(derive(L, d));
   const size_t x = L.images ? (size_t)L.B * L.C * L.H * L.W * 4 : (size_t)L.in.start[L.in.n] * 4;
-  *bytes = al256(x) + al256((size_t)L.Kr * L.Ktot * 4) + al256((size_t)L.Kc * 4) +
-           al256((size_t)L.out.start[1] * 4) + al256((size_t)L.Hp * L.Wp * L.Bp * L.Kc) + al256(L.ws_total);
+  *bytes = al256(x + 256) + al256((size_t)L.Kr * L.Ktot * 4 + 256) + al256((size_t)L.Kc * 4) +
+           al256((size_t)L.out.start[1] * 4 + 256) + al256((size_t)L.Hp * L.Wp * L.Bp * L.Kc) + al256(L.ws_total);
   return CP_OK;
 }
 
@@ -319,10 +320,10 @@ int conv_part_probe(const cp_conv_desc* desc, int32_t warmups, int32_t reps, voi
   cudaStream_t s = (cudaStream_t)stream;
   char* p = (char*)scratch;
   const size_t xb = L->images ? (size_t)L->B * L->C * L->H * L->W * 4 : (size_t)L->in.start[L->in.n] * 4;
-  float* x = (float*)p; p += al256(xb);
-  float* w = (float*)p; p += al256((size_t)L->Kr * L->Ktot * 4);
+  float* x = (float*)p; p += al256(xb + 256);
+  float* w = (float*)p; p += al256((size_t)L->Kr * L->Ktot * 4 + 256);
   float* b = (float*)p; p += al256((size_t)L->Kc * 4);
-  float* y = (float*)p; p += al256((size_t)L->out.start[1] * 4);
+  float* y = (float*)p; p += al256((size_t)L->out.start[1] * 4 + 256);
   uint8_t* sv = (uint8_t*)p; p += al256((size_t)L->Hp * L->Wp * L->Bp * L->Kc);
   void* ws = p;
   // "The convolution is run using random values, since only the time spent performing
