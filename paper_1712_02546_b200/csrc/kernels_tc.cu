@@ -15,6 +15,7 @@
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4-7 epilogue.
 // Persistent: grid = min(units, #SMs); two TMEM accumulators (2 x 256 columns) let the
 // epilogue of tile t overlap the MMAs of tile t+1.
+#include <cmath>
 #include <vector>
 
 #include "kernels.cuh"
@@ -62,6 +63,10 @@ struct TcParams {
   int numM, numN, split, units, chunks_per_split, chunks_total;  // numM counts M tiles per CTA group
   int bn_box;          // fwd: B box rows
   int wide;            // MN-major operands loaded as one 5-D box of 32-column atoms (else per-atom boxes)
+  int span;            // dgrad/wgrad N tiles run over the concatenated slots of all input blocks
+  int apb;             // wgrad span: atoms per B box (every block width is a multiple of 32*apb)
+  int cpt;             // fwd: K-chunks per tap (sum over input blocks)
+  long long part_stride;  // split-K: floats between split partial buffers (fwd/dgrad)
   int nt_rb[MAX_NT], nt_n0[MAX_NT], nt_n[MAX_NT];  // dgrad / wgrad N-tile list (per tap for wgrad)
   const float* bias;
   float* out;          // fwd: y block ; dgrad: dx (full gather) ; wgrad: dW or split partials
@@ -121,24 +126,43 @@ struct Chunk {
   int ksteps;
 };
 
+// dgrad: taps (r,s) whose shifted 2x2 window hits the dY grid: r in [r_lo, r_hi], s in [s_lo, s_hi]
+__device__ __forceinline__ void dgrad_taps(const TcParams& p, const Unit& t, int& r_lo, int& nr, int& s_lo, int& ns) {
+  r_lo = max(0, 2 * t.i - p.Ho + 1);
+  const int r_hi = min(p.R - 1, 2 * t.i + 1);
+  s_lo = max(0, 2 * t.j - p.Wo + 1);
+  const int s_hi = min(p.S - 1, 2 * t.j + 1);
+  nr = r_hi - r_lo + 1;
+  ns = s_hi - s_lo + 1;
+}
+
+// Visit the K-chunks of split `t.sp` of a unit, in order.  A unit's chunk sequence is
+// FWD: (tap, input block, 32-channel chunk); DGRAD: (valid tap, 32-kernel chunk);
+// WGRAD: (position, 32-image chunk).  Split sp covers [sp*per, (sp+1)*per) of it.
 template <int PASS, class F>
 __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t, F f) {
   if (PASS == PASS_FWD) {
+    const int total = p.R * p.S * p.cpt;
+    const int per = (total + p.split - 1) / p.split;
+    const int lo = t.sp * per, hi = min(total, lo + per);
+    int idx = 0;
     for (int tap = 0; tap < p.R * p.S; ++tap)
       for (int rb = 0; rb < p.nblk; ++rb) {
         const int kw = p.kw[rb];
-        for (int c = 0; c * BK < kw; ++c) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8});
+        for (int c = 0; c * BK < kw; ++c, ++idx)
+          if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8});
       }
   } else if (PASS == PASS_DGRAD) {
-    for (int r = 0; r < p.R; ++r) {
-      // rows 2i, 2i+1 of the input grid read dY rows 2i-r, 2i+1-r
-      const int h0 = 2 * t.i - r;
-      if (h0 + 1 < 0 || h0 >= p.Ho) continue;
-      for (int s = 0; s < p.S; ++s) {
-        const int w0 = 2 * t.j - s;
-        if (w0 + 1 < 0 || w0 >= p.Wo) continue;
-        for (int c = 0; c * BK < p.Kc; ++c) f(Chunk{r * p.S + s, 0, c, min(BK, p.Kc - c * BK) / 8});
-      }
+    int r_lo, nr, s_lo, ns;
+    dgrad_taps(p, t, r_lo, nr, s_lo, ns);
+    const int kc = (p.Kc + BK - 1) / BK;
+    const int total = nr * ns * kc;
+    const int per = (total + p.split - 1) / p.split;
+    const int lo = t.sp * per, hi = min(total, lo + per);
+    for (int idx = lo; idx < hi; ++idx) {
+      const int ti = idx / kc, c = idx - ti * kc;
+      const int r = r_lo + ti / ns, sx = s_lo + ti % ns;
+      f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8});
     }
   } else {
     const int c0 = t.sp * p.chunks_per_split;
@@ -246,7 +270,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             const int r = ch.tap / p.S, s = ch.tap % p.S;
             ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
             if (p.wide) {
-              ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BK, (p.coff[t.rb] + nb0) >> 5, ch.tap);
+              ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BK, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> 5, ch.tap);
             } else {
               for (int q = 0; q < nboxes; ++q)
                 ld3(b + q * 4096, &p.maps[CP_MAX_RANKS], p.coff[t.rb] + nb0 + 32 * q, ch.c * BK, ch.tap);
@@ -255,7 +279,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             const int nbc = p.Bp / 32;
             const int bc = ch.c % nbc, pq = ch.c / nbc, q = pq % p.Wo, pp = pq / p.Wo;
             const int r = t.tap / p.S, s = t.tap % p.S;
-            if (p.wide) {
+            if (p.span) {
+              ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
+              for (int jb = 0; jb * p.apb * 32 < (CG == 2 ? BN / 2 : BN); ++jb) {  // always the full box set
+                const int sl = nb0 + jb * p.apb * 32;   // concatenated slot of this box
+                int rb = 0;
+                while (rb + 1 < p.nblk && sl >= p.coff[rb + 1]) ++rb;
+                ld5(b + jb * p.apb * 4096, &p.maps[rb], 0, bc * 32, (sl - p.coff[rb]) >> 5, q + s, pp + r);
+              }
+            } else if (p.wide) {
               ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
               ld5(b, &p.maps[t.rb], 0, bc * 32, nb0 >> 5, q + s, pp + r);
             } else {
@@ -326,7 +358,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         float v[32];
         tmem_ld_32x32b_x32(tbase + cc * 32, v);
         const int ncol = min(32, t.n - cc * 32);
-        if (PASS == PASS_FWD) {
+        if (PASS == PASS_FWD && p.split > 1) {
+          // split-K partial of the pre-pool tile: [sp][Ho][Wo][Bp][Kc]
+          const int dh = quad >> 1, dw = quad & 1;
+          const int bb = t.bc * 32 + lane;
+          const int64_t o = (int64_t)t.sp * p.part_stride +
+                            ((int64_t)((2 * t.i + dh) * p.Wo + 2 * t.j + dw) * p.Bp + bb) * p.Kc + t.n0 + cc * 32;
+          store_f32x32(p.out + o, v, ncol);
+        } else if (PASS == PASS_FWD) {
           const int nbase = t.n0 + cc * 32;  // own slot index of column 0
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
@@ -398,14 +437,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         } else if (PASS == PASS_DGRAD) {
           const int dh = quad >> 1, dw = quad & 1;
           const int bb = t.bc * 32 + lane;
-          const int kw = p.kw[t.rb];
-          const int64_t o = p.start[t.rb] +
-                            ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb) * kw + t.n0 + cc * 32;
-          store_f32x32(p.out + o, v, ncol);
+          int rb = t.rb, slot = t.n0 + cc * 32;
+          if (p.span) {  // 32-column chunk -> its input block (block widths are multiples of 32)
+            rb = 0;
+            while (rb + 1 < p.nblk && slot >= p.coff[rb + 1]) ++rb;
+            slot -= p.coff[rb];
+          }
+          if (!p.span || slot < p.kw[rb]) {
+            const int kw = p.kw[rb];
+            const int64_t o = (int64_t)t.sp * p.part_stride + p.start[rb] +
+                              ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb) * kw + slot;
+            store_f32x32(p.out + o, v, ncol);
+          }
         } else {
           const int kk = t.mt * BM + row;
           if (kk < p.Kr) {
-            const int64_t col = (int64_t)t.tap * p.Cg + p.coff[t.rb] + t.n0 + cc * 32;
+            const int64_t col = (int64_t)t.tap * p.Cg + (p.span ? 0 : p.coff[t.rb]) + t.n0 + cc * 32;
             const int64_t o = ((int64_t)t.sp * p.Kr + kk) * p.Ktot + col;
             store_f32x32(p.out + o, v, ncol);
           }
@@ -445,6 +492,60 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, float* __re
       out[j] = acc;
     }
   }
+}
+
+// forward split-K finish: z = sum_s part[s] + bias, then ReLU, 2x2 max-pool (first max wins),
+// argmax code and RN-tf32 rounding, exactly as the fused epilogue does.
+// One thread per (pooled position, image, 4 slots).
+__global__ void splitk_fwd_finish(const float* __restrict__ part, int S, long long stride,
+                                  const float* __restrict__ bias, float* __restrict__ y, uint8_t* __restrict__ saved,
+                                  int Wo, int Wp, int Bp, int B, int Kr, int Kc, long long total4, int relu, int pool) {
+  const long long e4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e4 >= total4) return;
+  const int kc4 = Kc >> 2;
+  const int slot = (int)(e4 % kc4) * 4;
+  const long long rest = e4 / kc4;
+  const int b = (int)(rest % Bp);
+  const int ij = (int)(rest / Bp);
+  float bs[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) bs[t] = (bias && slot + t < Kr) ? bias[slot + t] : 0.f;
+  const int npos = pool ? 4 : 1;
+  float best[4] = {0.f, 0.f, 0.f, 0.f};
+  uint32_t code[4] = {0u, 0u, 0u, 0u};
+  for (int pos = 0; pos < npos; ++pos) {
+    long long zo;
+    if (pool) {
+      const int j = ij % Wp, i = ij / Wp;
+      zo = ((long long)((2 * i + (pos >> 1)) * Wo + 2 * j + (pos & 1)) * Bp + b) * Kc + slot;
+    } else {
+      zo = rest * Kc + slot;
+    }
+    float4 acc = *reinterpret_cast<const float4*>(part + zo);
+    for (int sp = 1; sp < S; ++sp) {
+      const float4 x = *reinterpret_cast<const float4*>(part + sp * stride + zo);
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    float v[4] = {acc.x + bs[0], acc.y + bs[1], acc.z + bs[2], acc.w + bs[3]};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (relu && !(v[t] > 0.f)) v[t] = 0.f;
+      if (pos == 0 || v[t] > best[t]) {
+        best[t] = v[t];
+        code[t] = pos;
+      }
+    }
+  }
+  float o[4];
+  uint32_t packed = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const bool ok = b < B && slot + t < Kr;
+    o[t] = ok ? tf32_rna(best[t]) : 0.f;
+    packed |= (ok ? code[t] : 0u) << (8 * t);
+  }
+  *reinterpret_cast<float4*>(y + rest * Kc + slot) = make_float4(o[0], o[1], o[2], o[3]);
+  if (pool) *reinterpret_cast<uint32_t*>(saved + rest * Kc + slot) = packed;
 }
 
 // ---------------------------------------------------------------- host side
@@ -593,21 +694,52 @@ void fill_common(TcParams& p, const Layer& L) {
   p.images = L.images;
 }
 
-// wgrad split-K factor: enough units for ~2 waves of CTA groups, >= 16 k-chunks per split
-void wgrad_split(int units, int chunks, int groups, int* split, int* per) {
-  int S = 1;
-  const int target = 2 * groups;
-  if (units < target) S = std::min((target + units - 1) / units, std::max(1, chunks / 16));
-  S = std::max(1, std::min(S, 64));
-  int pc = (chunks + S - 1) / S;
-  S = (chunks + pc - 1) / pc;
-  *split = S;
-  *per = pc;
+// Split-K factor from a small cost model, in units of one K-chunk's MMA time (~512 SM cycles):
+// rounds(S) * chunks/S for the GEMM plus the HBM time to write and re-read S fp32 partials.
+// Splitting fixes wave quantisation when a rank's slice yields fewer tiles than CTA groups.
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
-int wgrad_ntiles(const Layer& L, TcParams& p) {
-  // N tiles per tap: every input block cut into <=256-wide chunks
+int choose_split(int units, int groups, double chunks, double out_bytes, int maxS) {
+  const double chunk_us = 512.0 / 1.4e3;  // ~1.4 GHz under load
+  const double hbm_bytes_per_us = 6.0e6;
+  int best = 1;
+  double best_t = 1e300;
+  for (int S = 1; S <= maxS; ++S) {
+    if (S > 1 && chunks / S < 8) break;
+    const double rounds = std::ceil((double)units * S / groups);
+    double t = rounds * std::ceil(chunks / S) * chunk_us;
+    if (S > 1) t += (2 * S + 1) * out_bytes / hbm_bytes_per_us;  // write + re-read partials, write result
+    if (t < best_t * 0.9) {
+      best_t = t;
+      best = S;
+    }
+  }
+  return best;
+}
+
+// N tiles span input blocks when every block width is a multiple of 32 (and there are several)
+bool span_ok(const TcParams& p) {
+  if (p.images || p.nblk < 2) return false;
+  for (int r = 0; r < p.nblk; ++r)
+    if (p.kw[r] % 32) return false;
+  return true;
+}
+
+int build_ntiles(TcParams& p) {
   int n = 0;
+  if (p.span) {
+    for (int n0 = 0; n0 < p.Cg; n0 += BN) {
+      if (n >= MAX_NT) return -1;
+      p.nt_rb[n] = 0;
+      p.nt_n0[n] = n0;
+      p.nt_n[n] = std::min(BN, p.Cg - n0);
+      ++n;
+    }
+    return n;
+  }
   for (int rb = 0; rb < p.nblk; ++rb)
     for (int n0 = 0; n0 < p.kw[rb]; n0 += BN) {
       if (n >= MAX_NT) return -1;
@@ -616,72 +748,151 @@ int wgrad_ntiles(const Layer& L, TcParams& p) {
       p.nt_n[n] = std::min(BN, p.kw[rb] - n0);
       ++n;
     }
-  (void)L;
   return n;
+}
+
+int wgrad_ntiles(const Layer& L, TcParams& p) {
+  p.span = span_ok(p) ? 1 : 0;
+  (void)L;
+  return build_ntiles(p);
 }
 
 }  // namespace
 
-// wgrad work decomposition shared by the workspace query and the launch
-struct WgradPlan {
+// ---------------------------------------------------------------- work decomposition (host)
+// Shared by the workspace query and the launches so both agree on split factors.
+struct Plan {
   bool pair;
-  int per_tap, numM, numN, S, per, chunks;
+  int numM, numN, S, per, chunks;  // chunks = K-chunks per unit before splitting (average for dgrad)
+  int apb;                         // wgrad span: atoms per B box
 };
-static WgradPlan wgrad_plan(const Layer& L, TcParams& p) {
-  WgradPlan w{};
-  w.pair = use_pairs();
-  w.per_tap = wgrad_ntiles(L, p);
+
+static Plan fwd_plan(const Layer& L, TcParams& p) {
+  Plan w{};
+  w.pair = use_pairs() && (L.Bp / 32) % 2 == 0;
   const int CG = w.pair ? 2 : 1;
+  int cpt = 0;
+  for (int r = 0; r < p.nblk; ++r) cpt += (p.kw[r] + BK - 1) / BK;
+  p.cpt = cpt;
+  w.numM = (L.Ho / 2) * (L.Wo / 2) * (L.Bp / 32) / CG;
+  w.numN = (L.Kc + BN - 1) / BN;
+  w.chunks = p.R * p.S * cpt;
+  // forward split-K re-reads the whole pre-pool tile from HBM; measured slower at every P, so it
+  // is only used when forced (tests exercise it with CP_TC_SPLIT_FWD)
+  w.S = env_int("CP_TC_SPLIT_FWD", 1);
+  w.S = std::max(1, std::min(w.S, w.chunks));
+  return w;
+}
+
+static Plan dgrad_plan(const Layer& L, TcParams& p) {
+  Plan w{};
+  w.pair = use_pairs() && (L.Bp / 32) % 2 == 0;
+  const int CG = w.pair ? 2 : 1;
+  p.span = span_ok(p) ? 1 : 0;
+  w.numN = build_ntiles(p);
+  w.numM = (L.H / 2) * (L.W / 2) * (L.Bp / 32) / CG;
+  // average valid taps of a 2x2 window: (sum over window rows of valid r) * (same for s) / windows
+  auto avg_valid = [](int Hin, int Ho, int R) {
+    double t = 0;
+    for (int i = 0; i < Hin / 2; ++i)
+      t += std::min(R - 1, 2 * i + 1) - std::max(0, 2 * i - Ho + 1) + 1;
+    return t / (Hin / 2);
+  };
+  const double kc = (L.Kc + BK - 1) / BK;
+  w.chunks = (int)(avg_valid(L.H, L.Ho, L.R) * avg_valid(L.W, L.Wo, L.S) * kc + 0.5);
+  w.S = env_int("CP_TC_SPLIT_DGRAD", 0);
+  if (w.S <= 0) w.S = choose_split(w.numM * w.numN, num_sms() / CG, w.chunks, (double)L.in.start[L.in.n] * 4, 16);
+  return w;
+}
+
+static Plan wgrad_plan(const Layer& L, TcParams& p) {
+  Plan w{};
+  w.pair = use_pairs();
+  const int CG = w.pair ? 2 : 1;
+  p.span = span_ok(p) ? 1 : 0;
+  const int per_tap = build_ntiles(p);
   w.numM = ((L.Kc + BM - 1) / BM + CG - 1) / CG;
-  w.numN = w.per_tap * p.R * p.S;
+  w.numN = per_tap < 0 ? -1 : per_tap * p.R * p.S;
   w.chunks = L.Ho * L.Wo * (L.Bp / 32);
-  wgrad_split(w.numM * w.numN, w.chunks, num_sms() / CG, &w.S, &w.per);
+  w.S = env_int("CP_TC_SPLIT_WGRAD", 0);
+  if (w.S <= 0) w.S = choose_split(std::max(1, w.numM * w.numN), num_sms() / CG, w.chunks, (double)L.Kr * L.Ktot * 4, 32);
+  w.S = std::max(1, std::min(w.S, w.chunks));
+  w.per = (w.chunks + w.S - 1) / w.S;
+  w.S = (w.chunks + w.per - 1) / w.per;
+  // atoms per B box: every block holds whole boxes
+  const int own_atoms = (CG == 2 ? BN / 2 : BN) / 32;
+  w.apb = own_atoms;
+  if (p.span)
+    for (int r = 0; r < p.nblk; ++r)
+      while (w.apb > 1 && (p.kw[r] / 32) % w.apb) w.apb >>= 1;
   return w;
 }
 
 size_t tc_workspace_bytes(const Layer& L) {
-  TcParams p{};
-  fill_common(p, L);
-  if (L.Kr == 0) return 0;
-  const WgradPlan w = wgrad_plan(L, p);
-  if (w.per_tap <= 0) return 0;
-  return w.S > 1 ? (size_t)w.S * L.Kr * L.Ktot * 4 : 0;
+  size_t need = 0;
+  {
+    TcParams p{};
+    fill_common(p, L);
+    const Plan w = fwd_plan(L, p);
+    if (w.S > 1) need = std::max(need, (size_t)w.S * L.Ho * L.Wo * L.Bp * L.Kc * 4);
+  }
+  if (!L.images && L.Kr > 0) {
+    TcParams p{};
+    fill_common(p, L);
+    const Plan w = dgrad_plan(L, p);
+    if (w.S > 1) need = std::max(need, (size_t)w.S * L.in.start[L.in.n] * 4);
+  }
+  if (L.Kr > 0) {
+    TcParams p{};
+    fill_common(p, L);
+    const Plan w = wgrad_plan(L, p);
+    if (w.numN > 0 && w.S > 1) need = std::max(need, (size_t)w.S * L.Kr * L.Ktot * 4);
+  }
+  return need;
 }
 
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
            cudaStream_t s) {
-  (void)ws;
   if (L.Kc == 0) return CP_OK;
   if ((L.Ho & 1) || (L.Wo & 1))
     CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 forward needs an even conv output grid (2x2 window tiles)");
   TcParams p{};
   fill_common(p, L);
+  const Plan pl = fwd_plan(L, p);
   if (L.images) {
     CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 2, 2, false));
   } else {
     for (int r = 0; r < L.in.n; ++r)
       if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false));
   }
-  const bool pair = use_pairs() && (L.Bp / 32) % 2 == 0;
-  p.bn_box = pair ? BN / 2 : std::min(BN, L.Kc);
+  p.bn_box = pl.pair ? BN / 2 : std::min(BN, L.Kc);
   {
     const uint64_t dims[2] = {(uint64_t)L.Ktot, (uint64_t)std::max(L.Kr, 1)};
     const uint64_t str[1] = {(uint64_t)L.Ktot * 4};
     const uint32_t box[2] = {32, (uint32_t)p.bn_box};
     CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 2, dims, str, box));
   }
-  p.numM = (L.Ho / 2) * (L.Wo / 2) * (L.Bp / 32) / (pair ? 2 : 1);
-  p.numN = (L.Kc + BN - 1) / BN;
-  p.split = 1;
-  p.units = p.numM * p.numN;
+  p.numM = pl.numM;
+  p.numN = pl.numN;
+  p.split = pl.S;
+  p.units = p.numM * p.numN * pl.S;
   p.bias = L.d.bias ? b : nullptr;
-  p.out = y_block;
   p.saved = saved;
-  return pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s);
+  float* part = (float*)((char*)ws + L.off_split);
+  p.part_stride = (long long)L.Ho * L.Wo * L.Bp * L.Kc;
+  p.out = pl.S > 1 ? part : y_block;
+  CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
+  if (pl.S > 1) {
+    const long long total4 = (long long)L.Hp * L.Wp * L.Bp * (L.Kc / 4);
+    splitk_fwd_finish<<<(unsigned)((total4 + 255) / 256), 256, 0, s>>>(
+        part, pl.S, p.part_stride, L.d.bias ? b : nullptr, y_block, saved, L.Wo, L.Wp, L.Bp, L.B, L.Kr, L.Kc, total4,
+        L.d.relu, L.d.pool);
+    CP_LAUNCHED();
+  }
+  return CP_OK;
 }
 
 int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s) {
-  (void)ws;
   if (L.images) CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad onto images");
   if ((L.H & 1) || (L.W & 1)) CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad needs an even input grid");
   if (L.Kc == 0 || L.Kr == 0) {
@@ -690,8 +901,9 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   }
   TcParams p{};
   fill_common(p, L);
+  const Plan pl = dgrad_plan(L, p);
+  if (pl.numN < 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many dgrad N tiles");
   CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false));
-  const bool pair = use_pairs() && (L.Bp / 32) % 2 == 0;
   p.wide = 1;
   for (int r = 0; r < L.in.n; ++r)
     if (L.in.coff[r] % 32) p.wide = 0;
@@ -699,7 +911,7 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     // W [Kr][RS][Cg] viewed as (c' lane, k, c' atom, tap): one box {32, 32, natoms, 1}
     const uint64_t dims[4] = {32, (uint64_t)L.Kr, (uint64_t)((L.in.Cg + 31) / 32), (uint64_t)(L.R * L.S)};
     const uint64_t str[3] = {(uint64_t)L.Ktot * 4, 128, (uint64_t)L.in.Cg * 4};
-    const uint32_t box[4] = {32, 32, (uint32_t)(pair ? 4 : 8), 1};
+    const uint32_t box[4] = {32, 32, (uint32_t)(pl.pair ? 4 : 8), 1};
     CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 4, dims, str, box, true));
   } else {
     // W [Kr][RS][Cg] viewed as (c', k, tap): MN-major boxes {32 c', 32 k, 1}
@@ -708,31 +920,31 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     const uint32_t box[3] = {32, 32, 1};
     CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 3, dims, str, box, true));
   }
-  int n = 0;
-  for (int rb = 0; rb < L.in.n; ++rb)
-    for (int n0 = 0; n0 < L.in.kw[rb]; n0 += BN) {
-      if (n >= MAX_NT) CP_FAIL(CP_ERR_UNSUPPORTED, "too many dgrad N tiles");
-      p.nt_rb[n] = rb;
-      p.nt_n0[n] = n0;
-      p.nt_n[n] = std::min(BN, L.in.kw[rb] - n0);
-      ++n;
-    }
-  p.numM = (L.H / 2) * (L.W / 2) * (L.Bp / 32) / (pair ? 2 : 1);
-  p.numN = n;
-  p.split = 1;
-  p.units = p.numM * p.numN;
-  p.out = dx;
-  return pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s);
+  p.numM = pl.numM;
+  p.numN = pl.numN;
+  p.split = pl.S;
+  p.units = p.numM * p.numN * pl.S;
+  float* part = (float*)((char*)ws + L.off_split);
+  p.part_stride = pl.S > 1 ? (long long)L.in.start[L.in.n] : 0;
+  p.out = pl.S > 1 ? part : dx;
+  CP_TRY((pl.pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s)));
+  if (pl.S > 1) {
+    const int64_t n = L.in.start[L.in.n];
+    splitk_reduce_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, s>>>(part, dx, n, pl.S);
+    CP_LAUNCHED();
+  }
+  return CP_OK;
 }
 
 int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s) {
   if (L.Kr == 0) return CP_OK;
   TcParams p{};
   fill_common(p, L);
-  const WgradPlan w = wgrad_plan(L, p);
-  if (w.per_tap <= 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many wgrad N tiles");
+  const Plan w = wgrad_plan(L, p);
+  if (w.numN <= 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many wgrad N tiles");
   p.wide = 1;
-  const int nat = w.pair ? 4 : 8;
+  p.apb = w.apb;
+  const int nat = p.span ? w.apb : (w.pair ? 4 : 8);
   if (L.images) {
     CP_TRY(map_act_wide(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, nat));
   } else {

@@ -1,0 +1,129 @@
+"""Multi-GPU parity of the kernel-partitioned step over real NCCL collectives (torchrun, one rank
+per GPU).  Launched by tests/test_gpu_multi.py; exits non-zero on any mismatch.
+
+Checks (north_star invariants):
+  * every rank holds the same gathered conv outputs (AllGather along channels), bitwise;
+  * the gathered outputs equal the oracle's unsplit layer on the same inputs (TF32 tolerance);
+  * summed partial dX (ReduceScatter / AllReduce) equals the oracle's unsplit dgrad;
+  * each rank's dW / db slice equals the oracle's rows (decision replay);
+  * the replicated head (loss, FC update) is bitwise identical on all ranks.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from gpu_util import TOL, rel_err, unpack  # noqa: E402
+from paper_1712_02546_b200 import convpart as cp  # noqa: E402
+from paper_1712_02546_b200.net import PartitionedNet  # noqa: E402
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    uid = [cp.cp_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = cp.cp_comm_create(uid[0], rank, world)
+    failures = []
+    for mode_name, dx_mode, times in [("even+RS", cp.CP_DX_REDUCE_SCATTER, [1.0] * world),
+                                      ("eq1+AR", cp.CP_DX_ALLREDUCE, [1.0 + 0.35 * r for r in range(world)])]:
+        net = synth.NetSpec(kernels=(36, 72), in_hw=20, name="multi")
+        B = 40
+        parts = [cp.cp_partition_plan(times, K) for K in net.kernels]
+        params = synth.params(net, seed=21, std=0.05, bias_std=0.01)
+        x, y = synth.images(B, 3, 20, 20, step=3)
+        pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20)
+        pn.load_params(params)
+        pn.set_batch(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
+        s = torch.cuda.current_stream(dev)
+        cs = torch.cuda.Stream(dev)
+        pn.forward(s, cs)
+        torch.cuda.synchronize(dev)
+        hp = [8, 2]
+        rep = []
+        for i, K in enumerate(net.kernels):
+            a = unpack(pn.buf[i]["y"], B, K, hp[i], parts[i])
+            allv = [None] * world
+            dist.all_gather_object(allv, a.tobytes())
+            if any(v != allv[0] for v in allv):
+                failures.append(f"{mode_name}: gathered output of conv{i + 1} differs across ranks")
+            kr = parts[i].k_count[rank]
+            am = torch.zeros(max(B * kr * hp[i] * hp[i], 1), dtype=torch.uint8, device=dev)
+            if kr:
+                cp.cp_unpack_saved(pn.buf[i]["saved"], B, hp[i], hp[i], parts[i], rank, am)
+            mine = am[: B * kr * hp[i] * hp[i]].reshape(B, kr, hp[i], hp[i]).cpu().numpy()
+            codes = [None] * world
+            dist.all_gather_object(codes, mine)
+            rep.append({"a": a, "argmax": np.concatenate([c for c in codes if c.shape[1]], 1)})
+        p64 = {k: v.astype(np.float64) for k, v in params.items()}
+        tr = oracle.net_step(p64, x.astype(np.float64), y, 0.01, net.layers(), replay=rep)
+        # forward parity per layer on identical inputs (GPU's own previous output as input)
+        z1 = oracle.conv_fwd(x.astype(np.float64), p64["w0"], p64["b0"])
+        a1, _ = oracle.relu_pool_fwd(z1)
+        e = rel_err(rep[0]["a"], a1)
+        if e > TOL[cp.CP_MATH_TF32]:
+            failures.append(f"{mode_name}: conv1 fwd rel err {e:.2e}")
+        z2 = oracle.conv_fwd(rep[0]["a"], p64["w1"], p64["b1"])
+        a2, _ = oracle.relu_pool_fwd(z2)
+        e = rel_err(rep[1]["a"], a2)
+        if e > TOL[cp.CP_MATH_TF32]:
+            failures.append(f"{mode_name}: conv2 fwd rel err {e:.2e}")
+        pn.backward(dx_mode, s, cs, overlap=True)
+        torch.cuda.synchronize(dev)
+        # summed partial dX of conv2 = gradient w.r.t. A1 (this rank's block for RS, all for AR)
+        dy2 = oracle.unpool_relu_bwd(tr["da1"], rep[1]["argmax"], rep[1]["a"])
+        ref_da1 = oracle.conv_dgrad(dy2, p64["w1"])
+        got = unpack(pn.buf[1]["dx"], B, net.kernels[0], 8, parts[0])
+        k0, kr = parts[0].k_begin[rank], parts[0].k_count[rank]
+        sl = slice(k0, k0 + kr) if dx_mode == cp.CP_DX_REDUCE_SCATTER else slice(0, net.kernels[0])
+        if kr or dx_mode != cp.CP_DX_REDUCE_SCATTER:
+            e = rel_err(got[:, sl], ref_da1[:, sl])
+            if e > TOL[cp.CP_MATH_TF32]:
+                failures.append(f"{mode_name}: summed dX rel err {e:.2e}")
+        loss = pn.loss()
+        losses = [None] * world
+        dist.all_gather_object(losses, loss)
+        if any(v != losses[0] for v in losses):
+            failures.append(f"{mode_name}: loss differs across ranks {losses}")
+        if abs(loss - tr["loss"]) > TOL[cp.CP_MATH_TF32] * abs(tr["loss"]):
+            failures.append(f"{mode_name}: loss {loss} vs oracle {tr['loss']}")
+        # weight gradients of this rank's slices (oracle with the GPU's own replayed decisions)
+        pn.sgd(0.01, s)
+        torch.cuda.synchronize(dev)
+        new = pn.export_params()
+        for i in range(2):
+            kb, kr = parts[i].k_begin[rank], parts[i].k_count[rank]
+            if not kr:
+                continue
+            upd = new[f"w{i}"] - params[f"w{i}"][kb:kb + kr]
+            ref = tr["new_params"][f"w{i}"][kb:kb + kr] - p64[f"w{i}"][kb:kb + kr]
+            e = rel_err(upd, ref)
+            if e > 5e-3:
+                failures.append(f"{mode_name}: conv{i + 1} weight update rel err {e:.2e}")
+        fc = [None] * world
+        dist.all_gather_object(fc, new["wfc"].tobytes())
+        if any(v != fc[0] for v in fc):
+            failures.append(f"{mode_name}: replicated FC weights differ across ranks")
+        pn.close()
+    cp.cp_comm_destroy(comm)
+    allf = [None] * world
+    dist.all_gather_object(allf, failures)
+    dist.destroy_process_group()
+    if rank == 0:
+        flat = [f"rank {r}: {m}" for r, fl in enumerate(allf) for m in fl]
+        print("\n".join(flat) if flat else f"multi-GPU parity OK on {world} ranks")
+        sys.exit(1 if flat else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -29,12 +29,10 @@ def math_id(m):
     return cp.CP_MATH_FP32_SIMT if m == "simt" else cp.CP_MATH_TF32
 
 
-def parts_for(P, K):
-    if P == 1:
-        return cp.cp_partition_plan([1.0], K)
-    if P == 2:
-        return cp.cp_partition_plan([1.0, 1.0], K)
-    return cp.cp_partition_plan([1.0, 1.3, 2.1], K)        # uneven Eq. 1 map
+def parts_for(P, K, align=8):
+    if P == 3:
+        return cp.cp_partition_plan([1.0, 1.3, 2.1], K, align)   # uneven Eq. 1 map
+    return cp.cp_partition_plan([1.0] * P, K, align)
 
 
 def layer_data(B=40, H=20, K1=70, K2=300, seed=3):
@@ -56,16 +54,18 @@ def window_gap(z, relu=True):
     return s[..., 3] - s[..., 2]
 
 
-PB = [(1, 40), (2, 40), (3, 40), (1, 20)]   # B=20 -> one 32-image chunk: single-CTA tensor-core tiles
+# (P, B, align): B=20 -> one 32-image chunk (single-CTA tiles); align=32 -> block widths multiple
+# of 32, so dgrad/wgrad N tiles span rank blocks
+PB = [(1, 40, 8), (2, 40, 8), (3, 40, 8), (1, 20, 8), (2, 40, 32), (4, 40, 32)]
 
 
 @pytest.mark.parametrize("math", MATHS)
-@pytest.mark.parametrize("P,B", PB)
-def test_forward_parity(orc, math, P, B):
+@pytest.mark.parametrize("P,B,align", PB)
+def test_forward_parity(orc, math, P, B, align):
     m = math_id(math)
     x, w1, b1, w2, b2 = layer_data(B=B)
     B, K1, K2 = x.shape[0], w1.shape[0], w2.shape[0]
-    p1, p2 = parts_for(P, K1), parts_for(P, K2)
+    p1, p2 = parts_for(P, K1, align), parts_for(P, K2, align)
     L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
     L1.load(w1, b1)
     xd = dev(x)
@@ -94,12 +94,12 @@ def test_forward_parity(orc, math, P, B):
 
 
 @pytest.mark.parametrize("math", MATHS)
-@pytest.mark.parametrize("P,B", PB)
-def test_backward_parity(orc, math, P, B):
+@pytest.mark.parametrize("P,B,align", PB)
+def test_backward_parity(orc, math, P, B, align):
     m = math_id(math)
     x, w1, b1, w2, b2 = layer_data(B=B)
     B, K1, K2 = x.shape[0], w1.shape[0], w2.shape[0]
-    p1, p2 = parts_for(P, K1), parts_for(P, K2)
+    p1, p2 = parts_for(P, K1, align), parts_for(P, K2, align)
     L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
     L1.load(w1, b1)
     xd = dev(x)
