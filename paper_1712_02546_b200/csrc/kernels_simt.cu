@@ -519,10 +519,12 @@ __global__ void unpack_w_images_kernel(const float* __restrict__ wg, float* __re
 // FC features in gather order: block r, position pos = h*Wp+w, slot; f' = Hp*Wp*coff[r] + pos*kw[r] + slot.
 constexpr int kMaxO = 16;
 
-// Units of the FC reduction: (rank block r, position pos, 256-slot chunk sc); partial logits per
-// (unit, image) are summed in unit order by fc_fwd_reduce (fixed order -> bitwise identical on
-// every rank).  Grid (units, Bp/32): 8 warps x 4 images; lane = slot; weights held in registers.
-constexpr int kFcChunk = 256;
+// FC forward over the gather layout.  CTA = (rank block r, position pos, 128-slot chunk): the
+// weight slice W[o][f(r,pos,chunk)] is staged in shared memory; thread (image b, slot half)
+// streams 64 contiguous slots of x with float4 loads and accumulates all O logits.  The two
+// halves combine by one shuffle; fc_fwd_reduce then adds the units in unit order (fixed order,
+// bitwise identical on every rank).
+constexpr int kFcChunk = 128;
 __host__ __device__ inline int fc_nsc(const Blocks& g) {
   int m = 0;
   for (int r = 0; r < g.n; ++r) m = g.kw[r] > m ? g.kw[r] : m;
@@ -532,53 +534,59 @@ __host__ __device__ inline int fc_nsc(const Blocks& g) {
 __global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
                                                       float* __restrict__ part, Blocks g, int B, int O, int PW,
                                                       int nsc) {
+  __shared__ float4 ws[kMaxO][kFcChunk / 4];
   const int u = blockIdx.x;
   const int sc = u % nsc, rp = u / nsc;
   const int r = rp / PW, pos = rp % PW;
   const int kw = g.kw[r];
+  const int s0 = sc * kFcChunk;
   const int64_t F = (int64_t)PW * g.Cg;
-  const int64_t foff = (int64_t)PW * g.coff[r] + (int64_t)pos * kw;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float wr[8][kMaxO];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int sl = sc * kFcChunk + t * 32 + lane;
-#pragma unroll
-    for (int o = 0; o < kMaxO; ++o) wr[t][o] = (sl < kw && o < O) ? __ldg(wg + o * F + foff + sl) : 0.f;
+  const int64_t foff = (int64_t)PW * g.coff[r] + (int64_t)pos * kw + s0;
+  for (int i = threadIdx.x; i < kMaxO * (kFcChunk / 4); i += blockDim.x) {
+    const int o = i / (kFcChunk / 4), q4 = (i % (kFcChunk / 4)) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (o < O && s0 + q4 < kw) v = __ldg(reinterpret_cast<const float4*>(wg + o * F + foff + q4));
+    ws[o][i % (kFcChunk / 4)] = v;
   }
-  for (int q = 0; q < 4; ++q) {
-    const int b = blockIdx.y * 32 + warp * 4 + q;
-    float acc[kMaxO];
+  __syncthreads();
+  const int b = blockIdx.y * 128 + (threadIdx.x >> 1), half = threadIdx.x & 1;
+  float acc[kMaxO];
 #pragma unroll
-    for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
-    if (b < B) {
-      const float* xr = x + g.start[r] + ((int64_t)pos * g.Bp + b) * kw;
+  for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
+  if (b < B) {
+    const float* xr = x + g.start[r] + ((int64_t)pos * g.Bp + b) * kw + s0;
+    const int n4 = min(kFcChunk, kw - s0) / 4;
+#pragma unroll 4
+    for (int q = half * (kFcChunk / 8); q < (half + 1) * (kFcChunk / 8); ++q) {
+      if (q >= n4) break;
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(xr) + q);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int sl = sc * kFcChunk + t * 32 + lane;
-        const float xv = sl < kw ? __ldg(xr + sl) : 0.f;
-#pragma unroll
-        for (int o = 0; o < kMaxO; ++o) acc[o] = fmaf(xv, wr[t][o], acc[o]);
+      for (int o = 0; o < kMaxO; ++o) {
+        if (o < O) {
+          const float4 w = ws[o][q];
+          acc[o] = fmaf(xv.x, w.x, fmaf(xv.y, w.y, fmaf(xv.z, w.z, fmaf(xv.w, w.w, acc[o]))));
+        }
       }
     }
-#pragma unroll
-    for (int o = 0; o < kMaxO; ++o) {
-      float v = acc[o];
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-      if (lane == 0 && o < O) part[((int64_t)u * g.Bp + b) * O + o] = v;
-    }
   }
+#pragma unroll
+  for (int o = 0; o < kMaxO; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
+  if (half == 0 && b < g.Bp)
+    for (int o = 0; o < O; ++o) part[((int64_t)u * g.Bp + b) * O + o] = acc[o];
 }
 
+// logits[b][o] = bias[o] + sum_u part[u][b][o]: one warp per (b, o); lanes take units in strides
+// of 32 (ascending), then a fixed xor-shuffle tree — a fixed order, identical on every rank.
 __global__ void fc_fwd_reduce(const float* __restrict__ part, const float* __restrict__ bfc, float* logits,
                               int U, int Bp, int B, int O) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (e >= B * O) return;
   const int b = e / O, o = e % O;
   float t = 0.f;
-  for (int u = 0; u < U; ++u) t += part[((int64_t)u * Bp + b) * O + o];
-  logits[e] = t + (bfc ? bfc[o] : 0.f);
+  for (int u = lane; u < U; u += 32) t += part[((int64_t)u * Bp + b) * O + o];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+  if (lane == 0) logits[e] = t + (bfc ? bfc[o] : 0.f);
 }
 
 __global__ void softmax_xent_kernel(const float* __restrict__ logits, const int* __restrict__ y, int B, int O,
@@ -632,37 +640,58 @@ __global__ void fc_bwd_dx(const float* __restrict__ dl, const float* __restrict_
   *reinterpret_cast<float4*>(dx + g.start[r] + ((int64_t)pos * g.Bp + b) * kw + slot) = acc;
 }
 
-// dW_fc[o][f] = sum_b dlogits[b][o] * x(b, f): one thread per 4 features, b ascending (fixed order).
-__global__ void __launch_bounds__(64) fc_bwd_dw(const float* __restrict__ dl, const float* __restrict__ x,
-                                                float* __restrict__ dwg, Blocks g, int B, int O, int PW) {
+// dW_fc[o][f] = sum_b dlogits[b][o] * x(b, f): thread (4 features, batch quarter); the four
+// quarters are added in order in shared memory (fixed order).
+__global__ void __launch_bounds__(128) fc_bwd_dw(const float* __restrict__ dl, const float* __restrict__ x,
+                                                 float* __restrict__ dwg, Blocks g, int B, int O, int PW) {
+  __shared__ float4 red[3][32][kMaxO];
   const int64_t F = (int64_t)PW * g.Cg;
-  const int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (f >= F) return;
-  int r = 0;
-  while (r + 1 < g.n && f >= (int64_t)PW * g.coff[r + 1]) ++r;
-  const int64_t l = f - (int64_t)PW * g.coff[r];
-  const int kw = g.kw[r];
-  const int pos = (int)(l / kw), slot = (int)(l % kw);
+  const int64_t f = ((int64_t)blockIdx.x * 32 + threadIdx.x) * 4;
+  const int qb = threadIdx.y;
   float acc[kMaxO][4];
 #pragma unroll
   for (int o = 0; o < kMaxO; ++o)
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[o][t] = 0.f;
-  const float* xp = x + g.start[r] + (int64_t)pos * g.Bp * kw + slot;
-  for (int b = 0; b < B; ++b) {
-    const float4 xv = __ldg(reinterpret_cast<const float4*>(xp + (int64_t)b * kw));
+  if (f < F) {
+    int r = 0;
+    while (r + 1 < g.n && f >= (int64_t)PW * g.coff[r + 1]) ++r;
+    const int64_t l = f - (int64_t)PW * g.coff[r];
+    const int kw = g.kw[r];
+    const int pos = (int)(l / kw), slot = (int)(l % kw);
+    const float* xp = x + g.start[r] + (int64_t)pos * g.Bp * kw + slot;
+    const int bq = (B + 3) / 4;
+    const int b0 = qb * bq, b1 = min(B, b0 + bq);
+    for (int b = b0; b < b1; ++b) {
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(xp + (int64_t)b * kw));
 #pragma unroll
-    for (int o = 0; o < kMaxO; ++o) {
-      if (o < O) {
-        const float d = __ldg(dl + b * O + o);
-        acc[o][0] = fmaf(d, xv.x, acc[o][0]); acc[o][1] = fmaf(d, xv.y, acc[o][1]);
-        acc[o][2] = fmaf(d, xv.z, acc[o][2]); acc[o][3] = fmaf(d, xv.w, acc[o][3]);
+      for (int o = 0; o < kMaxO; ++o) {
+        if (o < O) {
+          const float d = __ldg(dl + b * O + o);
+          acc[o][0] = fmaf(d, xv.x, acc[o][0]); acc[o][1] = fmaf(d, xv.y, acc[o][1]);
+          acc[o][2] = fmaf(d, xv.z, acc[o][2]); acc[o][3] = fmaf(d, xv.w, acc[o][3]);
+        }
       }
     }
   }
+  if (qb > 0) {
 #pragma unroll
-  for (int o = 0; o < kMaxO; ++o)
-    if (o < O) *reinterpret_cast<float4*>(dwg + o * F + f) = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
+    for (int o = 0; o < kMaxO; ++o) red[qb - 1][threadIdx.x][o] = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
+  }
+  __syncthreads();
+  if (qb == 0 && f < F) {
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o) {
+      if (o >= O) continue;
+      float4 t = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        const float4 u = red[q - 1][threadIdx.x][o];
+        t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+      }
+      *reinterpret_cast<float4*>(dwg + o * F + f) = t;
+    }
+  }
 }
 
 __global__ void fc_bwd_db(const float* __restrict__ dl, float* dbfc, int B, int O) {
@@ -817,7 +846,7 @@ int cp_head_workspace_bytes(int32_t B, int32_t Hp, int32_t Wp, const cp_partitio
   CP_TRY(check_part(part));
   if (!bytes) CP_FAIL(CP_ERR_ARG, "null bytes");
   Blocks g = make_blocks(*part, Hp, Wp, roundup(B, 32));
-  *bytes = (size_t)part->n_ranks * Hp * Wp * fc_nsc(g) * g.Bp * O * sizeof(float) + 256;
+  *bytes = (size_t)g.n * Hp * Wp * fc_nsc(g) * g.Bp * O * sizeof(float) + 256;
   return CP_OK;
 }
 
@@ -855,9 +884,9 @@ int cp_fc_forward(const float* x, int32_t B, int32_t Hp, int32_t Wp, const cp_pa
   const int PW = Hp * Wp, nsc = fc_nsc(g), U = g.n * PW * nsc;
   float* part_buf = (float*)ws;
   cudaStream_t s = (cudaStream_t)stream;
-  fc_fwd_partial<<<dim3(U, g.Bp / 32), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
+  fc_fwd_partial<<<dim3(U, (g.Bp + 127) / 128), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
   CP_LAUNCHED();
-  fc_fwd_reduce<<<cdiv(B * O, 128), 128, 0, s>>>(part_buf, bfc, logits, U, g.Bp, B, O);
+  fc_fwd_reduce<<<cdiv((int64_t)B * O * 32, 256), 256, 0, s>>>(part_buf, bfc, logits, U, g.Bp, B, O);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -886,7 +915,7 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
     CP_LAUNCHED();
   }
   if (dwg) {
-    fc_bwd_dw<<<grid1d((int64_t)PW * g.Cg / 4, 64), 64, 0, s>>>(dl, x, dwg, g, B, O, PW);
+    fc_bwd_dw<<<grid1d((int64_t)PW * g.Cg / 4, 32), dim3(32, 4), 0, s>>>(dl, x, dwg, g, B, O, PW);
     CP_LAUNCHED();
   }
   if (dbfc) {

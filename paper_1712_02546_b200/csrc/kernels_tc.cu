@@ -29,8 +29,9 @@ namespace {
 enum { PASS_FWD = 0, PASS_DGRAD = 1, PASS_WGRAD = 2 };
 constexpr int BM = 128, BN = 256, BK = 32;
 constexpr int A_BYTES = BM * BK * 4;          // 16 KB: this CTA's 128 rows x 32 k
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;             // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-w11 epilogue
 constexpr int EPI_WARP0 = 4;
+constexpr int EPI_GROUPS = 2;                // two 4-warp epilogue groups share the 32-column chunks
 constexpr int POOL_LD = 33;                   // padded row of the pooling exchange buffer
 constexpr int POOL_BYTES = 4 * 32 * POOL_LD * 4;
 constexpr int MAX_NT = 64;
@@ -38,12 +39,13 @@ constexpr int MAX_NT = 64;
 // CG = CTAs per MMA (cta_group::1 or ::2).  With a CTA pair the MMA is M=256 (128 rows per CTA)
 // and each CTA stages only half of B (N/2 columns), so per-SM operand traffic drops by 1/3 and
 // the freed shared memory buys a deeper ring.
-template <int CG>
+template <int CG, int PASS>
 struct Cfg {
   static constexpr int B_BYTES = CG == 1 ? BN * BK * 4 : (BN / 2) * BK * 4;
+  static constexpr int POOL = PASS == 0 ? EPI_GROUPS * POOL_BYTES : 0;   // pooling exchange (forward only)
   static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + POOL_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + POOL + 256;
 };
 
 struct TcParams {
@@ -62,6 +64,8 @@ struct TcParams {
   int relu, pool, images;
   int numM, numN, split, units, chunks_per_split, chunks_total;  // numM counts M tiles per CTA group
   int bn_box;          // fwd: B box rows
+  int epi_groups;      // 1 or 2 epilogue warp groups (blockDim = 128 + 128*groups; CP_TC_EPI_GROUPS)
+  int max_chunks;      // longest K loop of a unit (after split), for the launch heuristics
   int wide;            // MN-major operands loaded as one 5-D box of 32-column atoms (else per-atom boxes)
   int span;            // dgrad/wgrad N tiles run over the concatenated slots of all input blocks
   int apb;             // wgrad span: atoms per B box (every block width is a multiple of 32*apb)
@@ -159,11 +163,12 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     const int total = nr * ns * kc;
     const int per = (total + p.split - 1) / p.split;
     const int lo = t.sp * per, hi = min(total, lo + per);
-    for (int idx = lo; idx < hi; ++idx) {
-      const int ti = idx / kc, c = idx - ti * kc;
-      const int r = r_lo + ti / ns, sx = s_lo + ti % ns;
-      f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8});
-    }
+    // nested loops with a running index: no integer division on the MMA issue path
+    int idx = 0;
+    for (int r = r_lo; r < r_lo + nr; ++r)
+      for (int sx = s_lo; sx < s_lo + ns; ++sx)
+        for (int c = 0; c < kc; ++c, ++idx)
+          if (idx >= lo && idx < hi) f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8});
   } else {
     const int c0 = t.sp * p.chunks_per_split;
     const int c1 = min(p.chunks_total, c0 + p.chunks_per_split);
@@ -195,13 +200,16 @@ __device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], i
 
 template <int PASS, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, PASS>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base (128B swizzle atoms); offsetting the __shared__ array keeps the
+  // pointer in the shared address space (ld/st.shared, not generic accesses)
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * A_BYTES;
-  float* pool_buf = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + POOL_BYTES);
+  float* pool_all = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::POOL);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);
+      mbar_init(&tempty[a], 4 * p.epi_groups * CG);
     }
     fence_barrier_init();
     for (int m = 0; m < p.nblk; ++m) tma_prefetch(&p.maps[m]);
@@ -344,8 +352,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     }
   } else if (warp >= EPI_WARP0) {
     // ======================= epilogue: TMEM -> registers -> global (each CTA its own 128 rows)
-    const int quad = warp - EPI_WARP0;  // TMEM lane quadrant of this warp
-    const int row = quad * 32 + lane;   // accumulator row of this CTA = TMEM lane
+    const int quad = warp & 3;                     // TMEM lane quadrant this warp may access
+    const int grp = (warp - EPI_WARP0) >> 2;       // epilogue group: handles chunks cc = grp (mod 2)
+    const int row = quad * 32 + lane;              // accumulator row of this CTA = TMEM lane
+    float* pool_buf = pool_all + grp * (POOL_BYTES / 4);
     int local = 0;
     for (int u = group; u < p.units; u += ngroups, ++local) {
       const Unit t = decode_unit<PASS, CG>(p, u, rank);
@@ -354,7 +364,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       const int nchunk = (t.n + 31) / 32;
-      for (int cc = 0; cc < nchunk; ++cc) {
+      if (grp >= p.epi_groups) break;
+      for (int cc = grp; cc < nchunk; cc += p.epi_groups) {
         float v[32];
         tmem_ld_32x32b_x32(tbase + cc * 32, v);
         const int ncol = min(32, t.n - cc * 32);
@@ -367,10 +378,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           store_f32x32(p.out + o, v, ncol);
         } else if (PASS == PASS_FWD) {
           const int nbase = t.n0 + cc * 32;  // own slot index of column 0
+          // bias: one load per lane, broadcast by shuffle
+          const float bl = (p.bias && nbase + lane < p.Kr) ? __ldg(p.bias + nbase + lane) : 0.f;
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const int n = nbase + q;
-            float x = v[q] + ((p.bias && n < p.Kr) ? __ldg(p.bias + n) : 0.f);
+            float x = v[q] + __shfl_sync(0xffffffffu, bl, q);
             if (p.relu && !(x > 0.f)) x = 0.f;
             v[q] = x;
           }
@@ -379,8 +391,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             float* mine = pool_buf + (quad * 32 + lane) * POOL_LD;
 #pragma unroll
             for (int q = 0; q < 32; ++q) mine[q] = v[q];
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..127
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+            const int et = quad * 32 + lane;  // 0..127 within the group
             const int b = et >> 2, cb = (et & 3) * 8;
             const int bb = t.bc * 32 + b;
             float best[8];
@@ -424,7 +436,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                 }
               }
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
           } else {
             const int dh = quad >> 1, dw = quad & 1;
             const int bb = t.bc * 32 + lane;
@@ -598,6 +610,11 @@ int map_act(CUtensorMap* m, const float* base, int kw, int Bp, int W, int H, int
   return make_map(m, base, 4, dims, str, box, mn_major);
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 // 5-D map over an activation block [H][W][Bp][kw] as (32-slot atom lane, b, atom, w, h): one box
 // {32, 32, natoms, 1, 1} lands as natoms stacked MN-major 32x32 atoms (the canonical layout).
 // Slots past kw inside the last atom read neighbouring data: they only feed output columns/rows
@@ -626,14 +643,19 @@ int launch_cg(const TcParams& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Cfg<CG>::SMEM));
+                                 (int)Cfg<CG, PASS>::SMEM));
     attr = true;
   }
   const int groups = std::min(p.units, num_sms() / CG);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(groups * CG);
-  cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = Cfg<CG>::SMEM;
+  // short K loops (conv1: 3 chunks per tile) are epilogue-bound -> two epilogue warp groups;
+  // long ones keep one group (fewer warps polling barriers next to the MMA issuer)
+  TcParams* pp = const_cast<TcParams*>(&p);
+  if (pp->epi_groups <= 0) pp->epi_groups = p.max_chunks < 64 ? 2 : 1;
+  pp->epi_groups = std::max(1, std::min(EPI_GROUPS, pp->epi_groups));
+  cfg.blockDim = dim3(128 + 128 * pp->epi_groups);
+  cfg.dynamicSmemBytes = Cfg<CG, PASS>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -677,6 +699,7 @@ void fill_blocks(TcParams& p, const Layer& L) {
 
 void fill_common(TcParams& p, const Layer& L) {
   fill_blocks(p, L);
+  p.epi_groups = env_int("CP_TC_EPI_GROUPS", 0);  // 0: decided per launch from the K-loop length
   p.R = L.images ? 1 : L.R;
   p.S = L.images ? 1 : L.S;
   p.Ho = L.Ho;
@@ -697,11 +720,6 @@ void fill_common(TcParams& p, const Layer& L) {
 // Split-K factor from a small cost model, in units of one K-chunk's MMA time (~512 SM cycles):
 // rounds(S) * chunks/S for the GEMM plus the HBM time to write and re-read S fp32 partials.
 // Splitting fixes wave quantisation when a rank's slice yields fewer tiles than CTA groups.
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
 int choose_split(int units, int groups, double chunks, double out_bytes, int maxS) {
   const double chunk_us = 512.0 / 1.4e3;  // ~1.4 GHz under load
   const double hbm_bytes_per_us = 6.0e6;
@@ -876,6 +894,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   p.numN = pl.numN;
   p.split = pl.S;
   p.units = p.numM * p.numN * pl.S;
+  p.max_chunks = (pl.chunks + pl.S - 1) / pl.S;
   p.bias = L.d.bias ? b : nullptr;
   p.saved = saved;
   float* part = (float*)((char*)ws + L.off_split);
@@ -924,6 +943,7 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   p.numN = pl.numN;
   p.split = pl.S;
   p.units = p.numM * p.numN * pl.S;
+  p.max_chunks = (pl.chunks + pl.S - 1) / pl.S;
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = pl.S > 1 ? (long long)L.in.start[L.in.n] : 0;
   p.out = pl.S > 1 ? part : dx;
@@ -957,6 +977,7 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   p.chunks_total = w.chunks;
   p.split = w.S;
   p.chunks_per_split = w.per;
+  p.max_chunks = w.per;
   p.units = p.numM * p.numN * w.S;
   float* part = w.S > 1 ? (float*)((char*)ws + L.off_split) : dw;
   p.out = part;
