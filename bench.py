@@ -46,6 +46,8 @@ def parse():
                     help="even split, or Eq. 1 from the paper's probe (times all-gathered)")
     ap.add_argument("--dx", default="rs", choices=["rs", "ar"])
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--head", default="partitioned", choices=["partitioned", "replicated"],
+                    help="FC head: rank-local columns + AllReduce of logits, or all-gathered + replicated")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -176,7 +178,15 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        sys.stdout.flush()
+        fd = os.dup(1)
+        os.dup2(2, 1)   # keep NCCL's init banner off stdout
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+        finally:
+            sys.stdout.flush()
+            os.dup2(fd, 1)
+            os.close(fd)
     net = synth.paper_net(args.net)
     B = args.batch
     math = cp.CP_MATH_TF32 if args.math == "tf32" else cp.CP_MATH_FP32_SIMT
@@ -186,7 +196,16 @@ def main():
     if world > 1:
         uid = [cp.cp_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        comm = cp.cp_comm_create(uid[0], rank, world)
+        # NCCL prints its version banner on stdout at init: keep stdout for the one JSON line
+        sys.stdout.flush()
+        saved_fd = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            comm = cp.cp_comm_create(uid[0], rank, world)
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved_fd, 1)
+            os.close(saved_fd)
 
     # ---- partition map: even, or Eq. 1 from the paper's probe convolution (§4.1.1)
     probe_times = None
@@ -208,7 +227,7 @@ def main():
     else:
         parts = [cp.cp_partition_plan([1.0] * world, K) for K in net.kernels]
 
-    pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev)
+    pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev, head=args.head)
     params = synth.params(net, seed=42)
     pn.load_params(params)
     x, y = synth.images(B, 3, 32, 32, step=0)
@@ -341,6 +360,7 @@ def main():
                 "global_batch": B, "partition": [list(p.k_count[:p.n_ranks]) for p in parts],
                 "partition_source": "Eq.1 from probe" if probe_times else "even",
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
+                "head": pn.head_mode,
                 "parallelism": f"kernel-split x{world}",
                 "l2": "flushed between timed steps (256 MiB write outside the step events)" if flush is not None
                       else "not flushed (step working set ~700 MB > 126 MB L2)"},

@@ -135,6 +135,10 @@ typedef struct {
   cp_partition out_part;       /* this layer's kernel split (num_k == num_k)      */
   cp_partition in_part;        /* split of the input channels (CP_INPUT_GATHER)   */
   int32_t rank, world;         /* this rank; world == out_part.n_ranks            */
+  int32_t local_output;        /* 0: all-gather the output along channels (default);
+                                  1: keep only this rank's block (y_gathered holds the own block at
+                                  its offset) - for a layer whose consumer is itself partitioned,
+                                  e.g. the FC head with rank-local columns      */
 } cp_conv_desc;
 
 /* w, x, y and dx include 256 bytes of read slack past the tensor (TMA atoms of 32 columns may
@@ -246,6 +250,11 @@ int cp_fc_backward(const float* dlogits, const float* x_gathered, int32_t B, int
                    float* dx_gathered, float* dwfc_g, float* dbfc, void* ws, void* stream);
 /* p -= lr*g over n floats. */
 int cp_sgd(float* p, const float* g, int64_t n, float lr, void* stream);
+
+/* In-place sum over all ranks of n floats (NCCL AllReduce on `stream`); the result is identical
+ * on every rank.  Used by the partitioned head to sum per-rank partial logits.  comm == NULL or a
+ * single rank: no-op. */
+int cp_allreduce_sum(cp_comm comm, float* buf, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

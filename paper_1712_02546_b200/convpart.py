@@ -28,6 +28,7 @@ EXPORTS = [
     "cp_launch_count", "cp_last_error", "cp_pack_nchw", "cp_unpack_nchw", "cp_unpack_saved",
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
+    "cp_allreduce_sum",
 ]
 
 
@@ -60,7 +61,7 @@ class cp_conv_desc(ctypes.Structure):
                 ("k_w", ctypes.c_int32), ("bias", ctypes.c_int32), ("relu", ctypes.c_int32),
                 ("pool", ctypes.c_int32), ("math", ctypes.c_int32), ("input_kind", ctypes.c_int32),
                 ("out_part", cp_partition), ("in_part", cp_partition), ("rank", ctypes.c_int32),
-                ("world", ctypes.c_int32)]
+                ("world", ctypes.c_int32), ("local_output", ctypes.c_int32)]
 
 
 class cp_sizes(ctypes.Structure):
@@ -113,6 +114,7 @@ def lib():
             "cp_softmax_xent": [P, P, I32, I32, P, P, P],
             "cp_fc_backward": [P, P, I32, I32, I32, pp, P, I32, P, P, P, P, P],
             "cp_sgd": [P, P, I64, ctypes.c_float, P],
+            "cp_allreduce_sum": [P, P, I64, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -285,6 +287,10 @@ def cp_softmax_xent(logits, labels, B, O, loss, dlogits, stream=None):
 def cp_fc_backward(dl, x, B, Hp, Wp, part, wg, O, dx, dwg, dbfc, ws, stream=None):
     _call("cp_fc_backward", _ptr(dl), _ptr(x), B, Hp, Wp, ctypes.byref(part), _ptr(wg), O, _ptr(dx), _ptr(dwg),
           _ptr(dbfc), _ptr(ws), _stream(stream))
+
+
+def cp_allreduce_sum(comm, buf, stream=None):
+    _call("cp_allreduce_sum", comm, _ptr(buf), buf.numel(), _stream(stream))
 
 
 def cp_sgd(p, g, lr, stream=None):

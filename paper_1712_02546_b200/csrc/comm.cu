@@ -64,6 +64,13 @@ extern "C" int cp_comm_destroy(cp_comm c) {
   return CP_OK;
 }
 
+extern "C" int cp_allreduce_sum(cp_comm c, float* buf, int64_t n, void* stream) {
+  if (!c || c->world == 1 || n == 0) return CP_OK;
+  if (!buf || n < 0) CP_FAIL(CP_ERR_ARG, "cp_allreduce_sum: bad arguments");
+  CP_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclFloat, ncclSum, c->comm, (cudaStream_t)stream));
+  return CP_OK;
+}
+
 namespace cp {
 
 static int async_error(cp_comm c) {

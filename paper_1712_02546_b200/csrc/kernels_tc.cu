@@ -66,6 +66,7 @@ struct TcParams {
   int bn_box;          // fwd: B box rows
   int epi_groups;      // 1 or 2 epilogue warp groups (blockDim = 128 + 128*groups; CP_TC_EPI_GROUPS)
   int max_chunks;      // longest K loop of a unit (after split), for the launch heuristics
+  int dbg;             // timing experiments only (CP_TC_DEBUG): 1 = fwd B from contiguous rows, 2 = fwd A contiguous
   int wide;            // MN-major operands loaded as one 5-D box of 32-column atoms (else per-atom boxes)
   int span;            // dgrad/wgrad N tiles run over the concatenated slots of all input blocks
   int apb;             // wgrad span: atoms per B box (every block width is a multiple of 32*apb)
@@ -90,10 +91,20 @@ struct Unit {
 template <int PASS, int CG>
 __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) {
   Unit t{};
-  const int mg = u % p.numM;
-  const int rest = u / p.numM;
-  t.nt = rest % p.numN;
-  t.sp = rest / p.numN;
+  int mg;
+  if (PASS == PASS_WGRAD) {
+    // N fastest: a wave covers few kernel tiles x many (tap, slot) tiles, so it streams one
+    // kernel slice of dY and the (shared, shifted) activations once per position
+    t.nt = u % p.numN;
+    const int rest = u / p.numN;
+    mg = rest % p.numM;
+    t.sp = rest / p.numM;
+  } else {
+    mg = u % p.numM;
+    const int rest = u / p.numM;
+    t.nt = rest % p.numN;
+    t.sp = rest / p.numN;
+  }
   if (PASS == PASS_FWD || PASS == PASS_DGRAD) {
     const int nbcg = p.Bp / 32 / CG;
     const int W2 = (PASS == PASS_FWD ? p.Wo : p.Win) / 2;
@@ -141,7 +152,7 @@ __device__ __forceinline__ void dgrad_taps(const TcParams& p, const Unit& t, int
 }
 
 // Visit the K-chunks of split `t.sp` of a unit, in order.  A unit's chunk sequence is
-// FWD: (tap, input block, 32-channel chunk); DGRAD: (valid tap, 32-kernel chunk);
+// FWD: (tap, input block, 32-channel chunk); DGRAD: (32-kernel chunk, valid tap);
 // WGRAD: (position, 32-image chunk).  Split sp covers [sp*per, (sp+1)*per) of it.
 template <int PASS, class F>
 __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t, F f) {
@@ -163,11 +174,13 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     const int total = nr * ns * kc;
     const int per = (total + p.split - 1) / p.split;
     const int lo = t.sp * per, hi = min(total, lo + per);
-    // nested loops with a running index: no integer division on the MMA issue path
+    // kernel chunk outermost: all CTAs of a wave stream the same 32-kernel slice of W and dY at
+    // the same time (a few MB live in L2) instead of every tap of the whole tensors.  Nested loops
+    // with a running index: no integer division on the MMA issue path.
     int idx = 0;
-    for (int r = r_lo; r < r_lo + nr; ++r)
-      for (int sx = s_lo; sx < s_lo + ns; ++sx)
-        for (int c = 0; c < kc; ++c, ++idx)
+    for (int c = 0; c < kc; ++c)
+      for (int r = r_lo; r < r_lo + nr; ++r)
+        for (int sx = s_lo; sx < s_lo + ns; ++sx, ++idx)
           if (idx >= lo && idx < hi) f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8});
   } else {
     const int c0 = t.sp * p.chunks_per_split;
@@ -272,8 +285,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           };
           if (PASS == PASS_FWD) {
             const int r = ch.tap / p.S, s = ch.tap % p.S;
-            ld4(a, &p.maps[ch.rb], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
-            ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
+            if (p.dbg & 2)
+              ld2(a, &p.maps[CP_MAX_RANKS - 1], 0, ((ch.tap * 16 + ch.c) * 128) % 8192);
+            else
+              ld4(a, &p.maps[ch.rb], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
+            if (p.dbg & 1)
+              ld2(b, &p.maps[CP_MAX_RANKS - 2], 0, ((ch.tap * 16 + ch.c) * 128 + nb0) % 8192);
+            else
+              ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.tap / p.S, s = ch.tap % p.S;
             ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
@@ -884,6 +903,15 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
       if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false));
   }
   p.bn_box = pl.pair ? BN / 2 : std::min(BN, L.Kc);
+  p.dbg = env_int("CP_TC_DEBUG", 0);
+  if (p.dbg) {  // contiguous 128-byte-row views of the same buffers (wrong values, timing only)
+    const uint64_t dims[2] = {32, 8192};
+    const uint64_t str[1] = {128};
+    const uint32_t boxb[2] = {32, (uint32_t)p.bn_box};
+    const uint32_t boxa[2] = {32, 128};
+    CP_TRY(make_map(&p.maps[CP_MAX_RANKS - 2], w, 2, dims, str, boxb));
+    CP_TRY(make_map(&p.maps[CP_MAX_RANKS - 1], xin, 2, dims, str, boxa));
+  }
   {
     const uint64_t dims[2] = {(uint64_t)L.Ktot, (uint64_t)std::max(L.Kr, 1)};
     const uint64_t str[1] = {(uint64_t)L.Ktot * 4};

@@ -205,7 +205,7 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
       CP_TRY(launch_relu_pool(*L, z, yb, saved, false, s));
     }
   }
-  if (L->comm && L->d.world > 1) {
+  if (L->comm && L->d.world > 1 && !L->d.local_output) {
     CP_TRY(fork_comm(*L, s, cs));
     CP_TRY(comm_allgather_blocks(L->comm, y, L->out, cs));
     CP_TRY(join_comm(*L, s, cs));

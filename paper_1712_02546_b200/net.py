@@ -34,8 +34,13 @@ class PartitionedNet:
     """
 
     def __init__(self, kernels, batch, parts, rank=0, comm=None, math=cp.CP_MATH_TF32, in_c=3, in_hw=32,
-                 ksize=5, classes=10, relu=True, pool=True, bias=True, device="cuda"):
+                 ksize=5, classes=10, relu=True, pool=True, bias=True, device="cuda", head="replicated"):
+        """head: "replicated" - the last conv output is all-gathered and every rank runs the full FC
+        head (the paper's master-side head, replicated); "partitioned" - the last conv output stays
+        rank-local, each rank owns the FC columns of its channels, partial logits are summed with
+        one AllReduce (identical logits/loss on every rank; no AllGather of the last layer)."""
         self.device = torch.device(device)
+        self.head_mode = head if parts[0].n_ranks > 1 else "replicated"
         self.B, self.Bp, self.O = batch, (batch + 31) // 32 * 32, classes
         self.rank, self.world = rank, parts[0].n_ranks
         self.parts, self.comm, self.math = parts, comm, math
@@ -51,6 +56,8 @@ class PartitionedNet:
             if prev is not None:
                 d.in_part = prev
             d.rank, d.world = rank, self.world
+            if i == len(kernels) - 1 and self.head_mode == "partitioned":
+                d.local_output = 1
             hnd = cp.conv_part_create(d, comm)
             sz = cp.conv_part_query(hnd)
             self.layers.append(hnd)
@@ -71,6 +78,17 @@ class PartitionedNet:
         self.Hp = self.Wp = h
         self.F = kernels[-1] * h * h
         last = parts[-1]
+        if self.head_mode == "partitioned":
+            # the head sees only this rank's block: a one-block partition of the own channels
+            hp = cp.cp_partition()
+            hp.n_ranks, hp.num_k = 1, last.k_count[rank]
+            hp.k_begin[0], hp.k_count[0], hp.k_width[0] = 0, last.k_count[rank], last.k_width[rank]
+            self.head_part = hp
+            self.head_off = self.sizes[-1].y_offset // 4
+        else:
+            self.head_part = last
+            self.head_off = 0
+        last = self.head_part
         Fg = h * h * sum(last.k_width[: last.n_ranks])
         self.head = {
             "wfc": torch.zeros(classes * Fg, device=self.device), "bfc": torch.zeros(classes, device=self.device),
@@ -81,6 +99,8 @@ class PartitionedNet:
             "da": _f32(self.sizes[-1].y, self.device),
             "ws": _dev_bytes(cp.cp_head_workspace_bytes(batch, h, h, last, classes), self.device),
         }
+        self.head_x = self.buf[-1]["y"][self.head_off:]
+        self.head_da = self.head["da"][self.head_off:]
         self.x = torch.zeros(batch * in_c * in_hw * in_hw, device=self.device)
         self.labels = torch.zeros(batch, dtype=torch.int32, device=self.device)
         self.in_shape = (batch, in_c, in_hw, in_hw)
@@ -94,8 +114,12 @@ class PartitionedNet:
             k0, kr = self.parts[i].k_begin[self.rank], self.parts[i].k_count[self.rank]
             if kr:
                 self.buf[i]["b"][:kr].copy_(torch.from_numpy(np.ascontiguousarray(params[f"b{i}"][k0:k0 + kr])))
-        wfc = torch.from_numpy(np.ascontiguousarray(params["wfc"], np.float32)).to(self.device)
-        cp.cp_pack_fc_weights(wfc, self.O, self.Hp, self.Wp, self.parts[-1], self.head["wfc"], stream)
+        wfc_np = np.ascontiguousarray(params["wfc"], np.float32)
+        if self.head_mode == "partitioned":
+            k0, kr = self.parts[-1].k_begin[self.rank], self.parts[-1].k_count[self.rank]
+            wfc_np = np.ascontiguousarray(wfc_np.reshape(self.O, -1, self.Hp * self.Wp)[:, k0:k0 + kr])
+        wfc = torch.from_numpy(wfc_np.reshape(self.O, -1)).to(self.device)
+        cp.cp_pack_fc_weights(wfc, self.O, self.Hp, self.Wp, self.head_part, self.head["wfc"], stream)
         self.head["bfc"].copy_(torch.from_numpy(np.ascontiguousarray(params["bfc"], np.float32)))
         torch.cuda.synchronize(self.device)
 
@@ -109,9 +133,11 @@ class PartitionedNet:
                 cp.cp_unpack_conv_weights(d, self.buf[i]["w"], t)
             out[f"w{i}"] = t[: kr * d.in_c * d.k_h * d.k_w].reshape(kr, d.in_c, d.k_h, d.k_w)
             out[f"b{i}"] = self.buf[i]["b"][:kr]
-        wfc = torch.zeros(self.O * self.F, device=self.device)
-        cp.cp_unpack_fc_weights(self.head["wfc"], self.O, self.Hp, self.Wp, self.parts[-1], wfc)
-        out["wfc"] = wfc.reshape(self.O, self.F)
+        nf = self.head_part.num_k * self.Hp * self.Wp
+        wfc = torch.zeros(max(self.O * nf, 1), device=self.device)
+        if nf:
+            cp.cp_unpack_fc_weights(self.head["wfc"], self.O, self.Hp, self.Wp, self.head_part, wfc)
+        out["wfc"] = wfc[: self.O * nf].reshape(self.O, nf)   # own columns only when partitioned
         out["bfc"] = self.head["bfc"]
         torch.cuda.synchronize(self.device)
         return {k: v.detach().cpu().numpy().copy() for k, v in out.items()}
@@ -127,16 +153,18 @@ class PartitionedNet:
             b = self.buf[i]
             cp.conv_part_forward(L, inp, b["w"], b["b"], b["y"], b["saved"], b["ws"], stream, comm_stream)
             inp = b["y"]
-        hd, last = self.head, self.parts[-1]
-        cp.cp_fc_forward(inp, self.B, self.Hp, self.Wp, last, hd["wfc"], hd["bfc"], self.O, hd["logits"], hd["ws"],
-                         stream)
+        hd = self.head
+        bias = hd["bfc"] if (self.head_mode == "replicated" or self.rank == 0) else None
+        cp.cp_fc_forward(self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], bias, self.O, hd["logits"],
+                         hd["ws"], stream)
+        if self.head_mode == "partitioned":
+            cp.cp_allreduce_sum(self.comm, hd["logits"], stream)
         cp.cp_softmax_xent(hd["logits"], self.labels, self.B, self.O, hd["loss"], hd["dlogits"], stream)
 
     def backward(self, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True):
-        hd, last = self.head, self.parts[-1]
-        top = self.buf[-1]["y"]
-        cp.cp_fc_backward(hd["dlogits"], top, self.B, self.Hp, self.Wp, last, hd["wfc"], self.O, hd["da"],
-                          hd["dwfc"], hd["dbfc"], hd["ws"], stream)
+        hd = self.head
+        cp.cp_fc_backward(hd["dlogits"], self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], self.O,
+                          self.head_da, hd["dwfc"], hd["dbfc"], hd["ws"], stream)
         da = hd["da"]
         n = len(self.layers)
         for i in reversed(range(n)):

@@ -35,14 +35,18 @@ def main():
     dist.broadcast_object_list(uid, src=0)
     comm = cp.cp_comm_create(uid[0], rank, world)
     failures = []
-    for mode_name, dx_mode, times in [("even+RS", cp.CP_DX_REDUCE_SCATTER, [1.0] * world),
-                                      ("eq1+AR", cp.CP_DX_ALLREDUCE, [1.0 + 0.35 * r for r in range(world)])]:
+    for mode_name, dx_mode, times, head in [
+            ("even+RS", cp.CP_DX_REDUCE_SCATTER, [1.0] * world, "replicated"),
+            ("eq1+AR", cp.CP_DX_ALLREDUCE, [1.0 + 0.35 * r for r in range(world)], "replicated"),
+            ("even+RS+partitioned-head", cp.CP_DX_REDUCE_SCATTER, [1.0] * world, "partitioned"),
+            ("eq1+RS+partitioned-head", cp.CP_DX_REDUCE_SCATTER, [1.0 + 0.35 * r for r in range(world)],
+             "partitioned")]:
         net = synth.NetSpec(kernels=(36, 72), in_hw=20, name="multi")
         B = 40
         parts = [cp.cp_partition_plan(times, K) for K in net.kernels]
         params = synth.params(net, seed=21, std=0.05, bias_std=0.01)
         x, y = synth.images(B, 3, 20, 20, step=3)
-        pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20)
+        pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20, head=head)
         pn.load_params(params)
         pn.set_batch(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
         s = torch.cuda.current_stream(dev)
@@ -52,11 +56,19 @@ def main():
         hp = [8, 2]
         rep = []
         for i, K in enumerate(net.kernels):
-            a = unpack(pn.buf[i]["y"], B, K, hp[i], parts[i])
-            allv = [None] * world
-            dist.all_gather_object(allv, a.tobytes())
-            if any(v != allv[0] for v in allv):
-                failures.append(f"{mode_name}: gathered output of conv{i + 1} differs across ranks")
+            if head == "partitioned" and i == len(net.kernels) - 1:
+                # rank-local last layer: assemble the full map from every rank's own block
+                a_own = unpack(pn.buf[i]["y"], B, K, hp[i], parts[i])
+                k0, kr = parts[i].k_begin[rank], parts[i].k_count[rank]
+                pieces = [None] * world
+                dist.all_gather_object(pieces, a_own[:, k0:k0 + kr])
+                a = np.concatenate(pieces, 1)
+            else:
+                a = unpack(pn.buf[i]["y"], B, K, hp[i], parts[i])
+                allv = [None] * world
+                dist.all_gather_object(allv, a.tobytes())
+                if any(v != allv[0] for v in allv):
+                    failures.append(f"{mode_name}: gathered output of conv{i + 1} differs across ranks")
             kr = parts[i].k_count[rank]
             am = torch.zeros(max(B * kr * hp[i] * hp[i], 1), dtype=torch.uint8, device=dev)
             if kr:
@@ -110,10 +122,22 @@ def main():
             e = rel_err(upd, ref)
             if e > 5e-3:
                 failures.append(f"{mode_name}: conv{i + 1} weight update rel err {e:.2e}")
-        fc = [None] * world
-        dist.all_gather_object(fc, new["wfc"].tobytes())
-        if any(v != fc[0] for v in fc):
-            failures.append(f"{mode_name}: replicated FC weights differ across ranks")
+        if head == "replicated":
+            fc = [None] * world
+            dist.all_gather_object(fc, new["wfc"].tobytes())
+            if any(v != fc[0] for v in fc):
+                failures.append(f"{mode_name}: replicated FC weights differ across ranks")
+            fc_ref = tr["new_params"]["wfc"] - p64["wfc"]
+            fc_got = new["wfc"] - params["wfc"]
+        else:
+            k0, kr = parts[1].k_begin[rank], parts[1].k_count[rank]
+            cols = lambda m: m.reshape(m.shape[0], -1, 4)[:, k0:k0 + kr].reshape(m.shape[0], -1)  # noqa: E731
+            fc_ref = cols(tr["new_params"]["wfc"] - p64["wfc"])
+            fc_got = new["wfc"] - cols(params["wfc"])
+        if fc_got.size:
+            e = rel_err(fc_got, fc_ref)
+            if e > 5e-3:
+                failures.append(f"{mode_name}: FC weight update rel err {e:.2e}")
         pn.close()
     cp.cp_comm_destroy(comm)
     allf = [None] * world
