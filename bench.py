@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--head", default="partitioned", choices=["partitioned", "replicated"],
                     help="FC head: rank-local columns + AllReduce of logits, or all-gathered + replicated")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -240,12 +241,30 @@ def main():
     overlap = not args.no_overlap
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step():
-        pn.step(0.01, dx_mode, s, cs, overlap)
+    def step_eager():
+        # the current stream (torch's capture stream while a CUDA graph is being captured)
+        pn.step(0.01, dx_mode, torch.cuda.current_stream(dev), cs, overlap)
 
     for _ in range(args.warmup):
-        step()
+        step_eager()
     torch.cuda.synchronize(dev)
+    # ---- CUDA graph of one whole step (kernels + NCCL collectives + stream fork/join): removes
+    # the host launch path from the step; every kernel in it is one of ours (counted at capture)
+    graph, launches_per_step = None, None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        c0 = cp.cp_launch_count()
+        with torch.cuda.graph(graph):
+            step_eager()
+        launches_per_step = cp.cp_launch_count() - c0
+        graph.replay()
+        torch.cuda.synchronize(dev)
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step_eager()
     if world > 1:
         dist.barrier()
 
@@ -264,7 +283,7 @@ def main():
         step()
         ev[k][1].record(s)
     torch.cuda.synchronize(dev)
-    launches = cp.cp_launch_count() - n0
+    launches = cp.cp_launch_count() - n0 if graph is None else launches_per_step * args.steps
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -360,7 +379,7 @@ def main():
                 "global_batch": B, "partition": [list(p.k_count[:p.n_ranks]) for p in parts],
                 "partition_source": "Eq.1 from probe" if probe_times else "even",
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
-                "head": pn.head_mode,
+                "head": pn.head_mode, "cuda_graph": graph is not None,
                 "parallelism": f"kernel-split x{world}",
                 "l2": "flushed between timed steps (256 MiB write outside the step events)" if flush is not None
                       else "not flushed (step working set ~700 MB > 126 MB L2)"},
@@ -378,6 +397,13 @@ def main():
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
+    # teardown: the graph holds NCCL work of our communicator -> free it first, sync, then the comm
+    torch.cuda.synchronize(dev)
+    if graph is not None:
+        del graph
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     pn.close()
     if comm is not None:
         cp.cp_comm_destroy(comm)

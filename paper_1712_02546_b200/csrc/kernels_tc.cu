@@ -64,6 +64,7 @@ struct TcParams {
   int relu, pool, images;
   int numM, numN, split, units, chunks_per_split, chunks_total;  // numM counts M tiles per CTA group
   int bn_box;          // fwd: B box rows
+  int nw;              // fwd: N tile width (balanced: Kc split into equal tiles)
   int epi_groups;      // 1 or 2 epilogue warp groups (blockDim = 128 + 128*groups; CP_TC_EPI_GROUPS)
   int max_chunks;      // longest K loop of a unit (after split), for the launch heuristics
   int dbg;             // timing experiments only (CP_TC_DEBUG): 1 = fwd B from contiguous rows, 2 = fwd A contiguous
@@ -117,8 +118,8 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     t.mt = mg * CG + rank;
   }
   if (PASS == PASS_FWD) {
-    t.n0 = t.nt * BN;
-    t.n = min(BN, p.Kc - t.n0);
+    t.n0 = t.nt * p.nw;
+    t.n = min(p.nw, p.Kc - t.n0);
   } else if (PASS == PASS_DGRAD) {
     t.rb = p.nt_rb[t.nt];
     t.n0 = p.nt_n0[t.nt];
@@ -812,7 +813,30 @@ static Plan fwd_plan(const Layer& L, TcParams& p) {
   for (int r = 0; r < p.nblk; ++r) cpt += (p.kw[r] + BK - 1) / BK;
   p.cpt = cpt;
   w.numM = (L.Ho / 2) * (L.Wo / 2) * (L.Bp / 32) / CG;
-  w.numN = (L.Kc + BN - 1) / BN;
+  // Balanced N tiles: Kc split into T equal tiles (width a multiple of 16 / 8).  Choose T by
+  // rounds of CTA groups x per-chunk time, the latter ~ bytes staged per chunk (A 16 KB + B
+  // columns): the kernel is bound by operand delivery, not by MMA issue.
+  {
+    const int gran = CG == 2 ? 16 : 8, groups = num_sms() / CG;
+    double best = 1e300;
+    int bestT = (L.Kc + BN - 1) / BN;
+    for (int T = (L.Kc + BN - 1) / BN; T <= (L.Kc + BN - 1) / BN + 4; ++T) {
+      const int nw = ((L.Kc + T - 1) / T + gran - 1) / gran * gran;
+      if (nw > BN || nw <= 0) continue;
+      const int tiles = (L.Kc + nw - 1) / nw;
+      const double rounds = std::ceil((double)w.numM * tiles / groups);
+      const double t = rounds * (16384.0 + 128.0 * nw / CG);
+      if (t < best * 0.98) {
+        best = t;
+        bestT = tiles;
+        p.nw = nw;
+      }
+    }
+    if (env_int("CP_TC_FWD_NW", 0) > 0) p.nw = env_int("CP_TC_FWD_NW", 0);
+    if (p.nw <= 0) p.nw = BN;
+    (void)bestT;
+    w.numN = (L.Kc + p.nw - 1) / p.nw;
+  }
   w.chunks = p.R * p.S * cpt;
   // forward split-K re-reads the whole pre-pool tile from HBM; measured slower at every P, so it
   // is only used when forced (tests exercise it with CP_TC_SPLIT_FWD)
@@ -844,6 +868,8 @@ static Plan dgrad_plan(const Layer& L, TcParams& p) {
 
 static Plan wgrad_plan(const Layer& L, TcParams& p) {
   Plan w{};
+  // CTA pairs even when the last pair is partly empty (measured: single-CTA tiles are slower at
+  // P=4 and P=8 despite the wasted rows)
   w.pair = use_pairs();
   const int CG = w.pair ? 2 : 1;
   p.span = span_ok(p) ? 1 : 0;
@@ -902,7 +928,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     for (int r = 0; r < L.in.n; ++r)
       if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false));
   }
-  p.bn_box = pl.pair ? BN / 2 : std::min(BN, L.Kc);
+  p.bn_box = pl.pair ? p.nw / 2 : std::min(p.nw, L.Kc);
   p.dbg = env_int("CP_TC_DEBUG", 0);
   if (p.dbg) {  // contiguous 128-byte-row views of the same buffers (wrong values, timing only)
     const uint64_t dims[2] = {32, 8192};
