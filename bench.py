@@ -70,6 +70,17 @@ def peaks():
             "hbm": 6650.0, "source": "fallback B200_PROFILING.md x nominal tf32/bf16"}
 
 
+def ncu_traffic(pass_name):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the conv2 kernel of this pass, from
+    the committed ncu --set full summary (the longest launch of that pass = conv2)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_conv_tc.json")) as f:
+            rows = [r for r in json.load(f) if r.get("pass") == pass_name]
+        return max(rows, key=lambda r: r.get("duration_us", 0))["traffic_bytes"] if rows else None
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -387,7 +398,8 @@ def main():
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "kernel": f"conv2 {dom} (tcgen05 kind::tf32 implicit GEMM)",
                          "achieved": achieved, "peak": pk["tf32_sustained"], "unit": "TFLOP/s",
-                         "frac": achieved / pk["tf32_sustained"], "traffic": None,
+                         "frac": achieved / pk["tf32_sustained"], "traffic": ncu_traffic(dom) if world == 1 else None,
+                         "traffic_source": "profiles/r01_ncu_conv_tc.json (ncu --set full, same kernel, P=1)",
                          "flop_per_launch": flop_pass, "launch_ms": per[dom],
                          "peak_source": pk["source"] + " (sustained)",
                          "conv2_pass_ms": per, "conv2_pass_tflops": conv2_tflops},

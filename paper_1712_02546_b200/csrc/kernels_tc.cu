@@ -15,6 +15,7 @@
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4-7 epilogue.
 // Persistent: grid = min(units, #SMs); two TMEM accumulators (2 x 256 columns) let the
 // epilogue of tile t overlap the MMAs of tile t+1.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -35,6 +36,7 @@ constexpr int EPI_GROUPS = 2;                // two 4-warp epilogue groups share
 constexpr int POOL_LD = 33;                   // padded row of the pooling exchange buffer
 constexpr int POOL_BYTES = 4 * 32 * POOL_LD * 4;
 constexpr int MAX_NT = 64;
+constexpr int MAX_WIN = 512;                  // dgrad LPT window table (larger grids: natural order)
 
 // CG = CTAs per MMA (cta_group::1 or ::2).  With a CTA pair the MMA is M=256 (128 rows per CTA)
 // and each CTA stages only half of B (N/2 columns), so per-SM operand traffic drops by 1/3 and
@@ -74,6 +76,8 @@ struct TcParams {
   int cpt;             // fwd: K-chunks per tap (sum over input blocks)
   long long part_stride;  // split-K: floats between split partial buffers (fwd/dgrad)
   int nt_rb[MAX_NT], nt_n0[MAX_NT], nt_n[MAX_NT];  // dgrad / wgrad N-tile list (per tap for wgrad)
+  int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
+  short win_order[MAX_WIN];
   const float* bias;
   float* out;          // fwd: y block ; dgrad: dx (full gather) ; wgrad: dW or split partials
   uint8_t* saved;
@@ -100,6 +104,15 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     const int rest = u / p.numN;
     mg = rest % p.numM;
     t.sp = rest / p.numM;
+  } else if (PASS == PASS_DGRAD && p.nwin_order > 0) {
+    // heaviest windows first: all tiles of a window are consecutive units, windows in descending
+    // order of valid taps (host-sorted), so round-robin dispatch approximates LPT scheduling
+    t.sp = u % p.split;
+    const int rest = u / p.split;
+    t.nt = rest % p.numN;
+    const int rest2 = rest / p.numN;
+    const int nbcg = p.Bp / 32 / CG;
+    mg = p.win_order[rest2 / nbcg] * nbcg + rest2 % nbcg;
   } else {
     mg = u % p.numM;
     const int rest = u / p.numM;
@@ -998,6 +1011,26 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   p.split = pl.S;
   p.units = p.numM * p.numN * pl.S;
   p.max_chunks = (pl.chunks + pl.S - 1) / pl.S;
+  {
+    // LPT order of the 2x2 windows by valid-tap count (descending, stable)
+    const int H2 = L.H / 2, W2 = L.W / 2;
+    // off by default: measured slower at P=1/2/4 (heavy windows dispatched together lose the
+    // spatial L2 locality of the natural order)
+    if (H2 * W2 <= MAX_WIN && env_int("CP_TC_DGRAD_LPT", 0)) {
+      std::vector<std::pair<int, int>> wk;
+      for (int i = 0; i < H2; ++i)
+        for (int j = 0; j < W2; ++j) {
+          const int nr = std::min(L.R - 1, 2 * i + 1) - std::max(0, 2 * i - L.Ho + 1) + 1;
+          const int ns = std::min(L.S - 1, 2 * j + 1) - std::max(0, 2 * j - L.Wo + 1) + 1;
+          wk.push_back({-nr * ns, i * W2 + j});
+        }
+      std::stable_sort(wk.begin(), wk.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+        return a.first < b.first;
+      });
+      p.nwin_order = H2 * W2;
+      for (int k = 0; k < H2 * W2; ++k) p.win_order[k] = (short)wk[k].second;
+    }
+  }
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = pl.S > 1 ? (long long)L.in.start[L.in.n] : 0;
   p.out = pl.S > 1 ? part : dx;
