@@ -199,7 +199,7 @@ def main():
             sys.stdout.flush()
             os.dup2(fd, 1)
             os.close(fd)
-    net = synth.paper_net(args.net)
+    net = synth.scaled_net() if args.net == "scaled" else synth.paper_net(args.net)
     B = args.batch
     math = cp.CP_MATH_TF32 if args.math == "tf32" else cp.CP_MATH_FP32_SIMT
 
@@ -239,10 +239,11 @@ def main():
     else:
         parts = [cp.cp_partition_plan([1.0] * world, K) for K in net.kernels]
 
-    pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev, head=args.head)
+    pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev, head=args.head,
+                        in_hw=net.in_hw)
     params = synth.params(net, seed=42)
     pn.load_params(params)
-    x, y = synth.images(B, 3, 32, 32, step=0)
+    x, y = synth.images(B, 3, net.in_hw, net.in_hw, step=0)
     x_host = torch.from_numpy(x).pin_memory()
     y_host = torch.from_numpy(y).pin_memory()
     pn.set_batch(x_host.to(dev), y_host.to(dev))
@@ -364,7 +365,7 @@ def main():
             tim["dgrad"].append(e[2].elapsed_time(e[3]))
     cp.conv_part_destroy(h2)
     Kr2 = parts[1].k_count[rank]
-    C2, H2o = net.kernels[0], 10
+    C2, H2o = net.kernels[0], net.shapes()[1][3]
     flop_pass = 2.0 * B * Kr2 * C2 * 25 * H2o * H2o   # algorithmic MACs x2 of one conv2 pass, own slice
     pk = peaks()
     per = {k: statistics.median(v) for k, v in tim.items()}
@@ -378,15 +379,20 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             v, cores, sample = oracle_images_per_s(net, args.cpu_seconds)
             cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle", "sample": sample}
-        step_flop = 11.368e9 * B  # algorithmic training FLOPs per image (paper net)
+        # algorithmic training FLOPs per image (11.368 GFLOP for the paper net):
+        # conv1 fwd + wgrad, conv2 fwd + dgrad + wgrad, 2 FLOP per MAC (head: negligible)
+        (c1, _, k1, o1, _), (c2, _, k2, o2, _) = net.shapes()
+        per_img = 2.0 * (2 * k1 * c1 * 25 * o1 * o1 + 3 * k2 * c2 * 25 * o2 * o2)
+        step_flop = per_img * B
         line = {
             "metric": "conv-layer train images/sec (whole-network SGD step, kernel-partitioned)",
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "tf32" if math == cp.CP_MATH_TF32 else "f32", "data": "synthetic",
             "config": {
-                "workload": f"paper net {args.net} (conv5x5 {net.kernels[0]} -> pool -> conv5x5 {net.kernels[1]} -> "
-                            f"pool -> FC 37500->10 -> softmax), CIFAR-10-shaped 32x32x3, batch {B}",
+                "workload": f"{net.name} (conv5x5 {net.kernels[0]} -> pool -> conv5x5 {net.kernels[1]} -> "
+                            f"pool -> FC {net.fc_in}->10 -> softmax), {net.in_hw}x{net.in_hw}x3 synthetic images, "
+                            f"batch {B}",
                 "global_batch": B, "partition": [list(p.k_count[:p.n_ranks]) for p in parts],
                 "partition_source": "Eq.1 from probe" if probe_times else "even",
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
