@@ -76,6 +76,8 @@ struct TcParams {
   int cpt;             // fwd: K-chunks per tap (sum over input blocks)
   long long part_stride;  // split-K: floats between split partial buffers (fwd/dgrad)
   int nt_rb[MAX_NT], nt_n0[MAX_NT], nt_n[MAX_NT];  // dgrad / wgrad N-tile list (per tap for wgrad)
+  int tail_full, tail_st, tail_per;  // wgrad tail split: units >= tail_full are (tail unit, K piece)
+  float* tail_buf;     // wgrad tail partials [tail unit][piece][CTA of pair][128 rows][256 cols]
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
   short win_order[MAX_WIN];
   const float* bias;
@@ -85,6 +87,7 @@ struct TcParams {
 
 struct Unit {
   int mt, nt, sp;
+  int tail, tu, piece; // wgrad: K-piece `piece` of tail unit `tu` (last-round units split over all groups)
   int i, j, bc;        // spatial window / batch chunk (fwd, dgrad)
   int n0, n;           // N origin (within own slots or block) and width
   int rb, tap;         // dgrad: output block; wgrad: input block and tap
@@ -97,6 +100,14 @@ template <int PASS, int CG>
 __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) {
   Unit t{};
   int mg;
+  if (PASS == PASS_WGRAD && p.tail_st > 0 && u >= p.tail_full) {
+    // the last (partial) round of equal wgrad tiles is split along K over every CTA group
+    const int v = u - p.tail_full;
+    t.tail = 1;
+    t.tu = v / p.tail_st;
+    t.piece = v - t.tu * p.tail_st;
+    u = p.tail_full + t.tu;
+  }
   if (PASS == PASS_WGRAD) {
     // N fastest: a wave covers few kernel tiles x many (tap, slot) tiles, so it streams one
     // kernel slice of dY and the (shared, shifted) activations once per position
@@ -197,8 +208,8 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
         for (int sx = s_lo; sx < s_lo + ns; ++sx, ++idx)
           if (idx >= lo && idx < hi) f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8});
   } else {
-    const int c0 = t.sp * p.chunks_per_split;
-    const int c1 = min(p.chunks_total, c0 + p.chunks_per_split);
+    const int c0 = t.tail ? t.piece * p.tail_per : t.sp * p.chunks_per_split;
+    const int c1 = min(p.chunks_total, c0 + (t.tail ? p.tail_per : p.chunks_per_split));
     for (int c = c0; c < c1; ++c) f(Chunk{0, 0, c, BK / 8});
   }
 }
@@ -494,6 +505,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                               ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb) * kw + slot;
             store_f32x32(p.out + o, v, ncol);
           }
+        } else if (t.tail) {
+          // tail piece: raw partial tile, summed in piece order by wgrad_tail_reduce
+          float* dst = p.tail_buf + ((((int64_t)t.tu * p.tail_st + t.piece) * CG + rank) * BM + row) * BN + cc * 32;
+          store_f32x32(dst, v, 32);
         } else {
           const int kk = t.mt * BM + row;
           if (kk < p.Kr) {
@@ -517,6 +532,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, 512);
   }
+}
+
+// wgrad tail: dW[kk0 + row][col0 + c] = sum over pieces (in order) of the partial tiles.
+constexpr int MAX_TAIL = 148;
+struct TailInfo {
+  int n;                      // tail units
+  int st, cg;                 // pieces per unit, CTAs per tile
+  int Kr, Ktot;
+  int kk0[MAX_TAIL];          // first kernel row of the unit's tile (CTA 0)
+  int col0[MAX_TAIL];         // first dW column
+  int ncol[MAX_TAIL];         // valid columns
+};
+__global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restrict__ dw, const __grid_constant__ TailInfo ti) {
+  const int tu = blockIdx.z, rank = blockIdx.y, row = blockIdx.x;
+  const int c = threadIdx.x;  // 256 columns
+  const int kk = ti.kk0[tu] + rank * BM + row;
+  if (kk >= ti.Kr || c >= ti.ncol[tu]) return;
+  float acc = 0.f;
+  for (int pc = 0; pc < ti.st; ++pc)
+    acc += buf[((((int64_t)tu * ti.st + pc) * ti.cg + rank) * BM + row) * BN + c];
+  dw[(int64_t)kk * ti.Ktot + ti.col0[tu] + c] = acc;
 }
 
 // deterministic split-K reduction: dW[i] = sum_s part[s][i] in split order
@@ -891,7 +927,20 @@ static Plan wgrad_plan(const Layer& L, TcParams& p) {
   w.numN = per_tap < 0 ? -1 : per_tap * p.R * p.S;
   w.chunks = L.Ho * L.Wo * (L.Bp / 32);
   w.S = env_int("CP_TC_SPLIT_WGRAD", 0);
-  if (w.S <= 0) w.S = choose_split(std::max(1, w.numM * w.numN), num_sms() / CG, w.chunks, (double)L.Kr * L.Ktot * 4, 32);
+  if (w.S <= 0) {
+    const int units = std::max(1, w.numM * w.numN), G = num_sms() / CG;
+    w.S = choose_split(units, G, w.chunks, (double)L.Kr * L.Ktot * 4, 32);
+    if (w.S > 1 && env_int("CP_TC_WGRAD_TAIL", 1)) {
+      // S = 1 with the last round split along K (tc_wgrad) vs the whole-tensor split-K
+      const int rounds = (units + G - 1) / G, T = units - (rounds - 1) * G;
+      const double chunk_us = 512.0 / 1.4e3;
+      const double t_tail = (rounds - 1 + ((rounds > 1 && 2 * T <= G) ? 1.0 / std::max(1, G / std::max(T, 1)) : 1.0)) *
+                            w.chunks * chunk_us;
+      const double t_split = std::ceil((double)units * w.S / G) * std::ceil((double)w.chunks / w.S) * chunk_us +
+                             (2 * w.S + 1) * (double)L.Kr * L.Ktot * 4 / 6.0e6;
+      if (t_tail < t_split) w.S = 1;
+    }
+  }
   w.S = std::max(1, std::min(w.S, w.chunks));
   w.per = (w.chunks + w.S - 1) / w.S;
   w.S = (w.chunks + w.per - 1) / w.per;
@@ -923,6 +972,8 @@ size_t tc_workspace_bytes(const Layer& L) {
     fill_common(p, L);
     const Plan w = wgrad_plan(L, p);
     if (w.numN > 0 && w.S > 1) need = std::max(need, (size_t)w.S * L.Kr * L.Ktot * 4);
+    // tail-split partials: at most one round of CTA groups x CG tiles of 128 x 256 floats
+    if (w.numN > 0 && w.S == 1) need = std::max(need, (size_t)num_sms() * BM * BN * 4);
   }
   return need;
 }
@@ -1068,7 +1119,40 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   p.units = p.numM * p.numN * w.S;
   float* part = w.S > 1 ? (float*)((char*)ws + L.off_split) : dw;
   p.out = part;
+  // Tail split: when the last round of equal tiles is at most half full, split only those tiles
+  // along K over all CTA groups (their partials are tiny; everything else is written directly).
+  TailInfo ti{};
+  const int CG = w.pair ? 2 : 1, G = num_sms() / CG;
+  const int rounds = (p.units + G - 1) / G, T = p.units - (rounds - 1) * G;
+  if (w.S == 1 && rounds > 1 && T > 0 && 2 * T <= G && T <= MAX_TAIL && env_int("CP_TC_WGRAD_TAIL", 1)) {
+    int st = std::max(1, std::min(G / T, w.chunks));
+    const int per = (w.chunks + st - 1) / st;
+    st = (w.chunks + per - 1) / per;                   // every piece non-empty
+    p.tail_full = (rounds - 1) * G;
+    p.tail_st = st;
+    p.tail_per = per;
+    p.tail_buf = (float*)((char*)ws + L.off_split);
+    ti.n = T;
+    ti.st = st;
+    ti.cg = CG;
+    ti.Kr = L.Kr;
+    ti.Ktot = L.Ktot;
+    const int per_tap = p.numN / (p.R * p.S);
+    for (int k = 0; k < T; ++k) {                      // host mirror of decode_unit<WGRAD>
+      const int u = p.tail_full + k;
+      const int nt = u % p.numN, mg = (u / p.numN) % p.numM;
+      const int tap = nt / per_tap, e = nt % per_tap;
+      ti.kk0[k] = mg * CG * BM;
+      ti.col0[k] = tap * p.Cg + (p.span ? 0 : p.coff[p.nt_rb[e]]) + p.nt_n0[e];
+      ti.ncol[k] = p.nt_n[e];
+    }
+    p.units = p.tail_full + T * st;
+  }
   CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2>(p, s) : launch_cg<PASS_WGRAD, 1>(p, s)));
+  if (p.tail_st > 0) {
+    wgrad_tail_reduce<<<dim3(BM, CG, ti.n), BN, 0, s>>>(p.tail_buf, dw, ti);
+    CP_LAUNCHED();
+  }
   if (w.S > 1) {
     const int64_t n = (int64_t)L.Kr * L.Ktot;
     splitk_reduce_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, s>>>(part, dw, n, w.S);
