@@ -69,9 +69,10 @@ struct TcParams {
   int nw;              // fwd: N tile width (balanced: Kc split into equal tiles)
   int epi_groups;      // 1 or 2 epilogue warp groups (blockDim = 128 + 128*groups; CP_TC_EPI_GROUPS)
   int max_chunks;      // longest K loop of a unit (after split), for the launch heuristics
-  int dbg;             // timing experiments only (CP_TC_DEBUG): 1 = fwd B from contiguous rows, 2 = fwd A contiguous
   int wide;            // MN-major operands loaded as one 5-D box of 32-column atoms (else per-atom boxes)
   int span;            // dgrad/wgrad N tiles run over the concatenated slots of all input blocks
+  int unified;         // equal-width input blocks: ONE tensor map (block = outermost dim) in maps[0]
+                       // for fwd A / wgrad B, so the TMA unit does not cycle through P descriptors
   int apb;             // wgrad span: atoms per B box (every block width is a multiple of 32*apb)
   int cpt;             // fwd: K-chunks per tap (sum over input blocks)
   long long part_stride;  // split-K: floats between split partial buffers (fwd/dgrad)
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       mbar_init(&tempty[a], 4 * p.epi_groups * CG);
     }
     fence_barrier_init();
-    for (int m = 0; m < p.nblk; ++m) tma_prefetch(&p.maps[m]);
+    for (int m = 0; m < (p.unified ? 1 : p.nblk); ++m) tma_prefetch(&p.maps[m]);
     tma_prefetch(&p.maps[CP_MAX_RANKS]);
   }
   if (warp == 2) tmem_alloc<CG>(tmem_slot, 512);
@@ -310,14 +311,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           };
           if (PASS == PASS_FWD) {
             const int r = ch.tap / p.S, s = ch.tap % p.S;
-            if (p.dbg & 2)
-              ld2(a, &p.maps[CP_MAX_RANKS - 1], 0, ((ch.tap * 16 + ch.c) * 128) % 8192);
+            if (p.unified)
+              ld5(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
             else
               ld4(a, &p.maps[ch.rb], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
-            if (p.dbg & 1)
-              ld2(b, &p.maps[CP_MAX_RANKS - 2], 0, ((ch.tap * 16 + ch.c) * 128 + nb0) % 8192);
-            else
-              ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
+            ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.tap / p.S, s = ch.tap % p.S;
             ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
@@ -337,7 +335,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                 const int sl = nb0 + jb * p.apb * 32;   // concatenated slot of this box
                 int rb = 0;
                 while (rb + 1 < p.nblk && sl >= p.coff[rb + 1]) ++rb;
-                ld5(b + jb * p.apb * 4096, &p.maps[rb], 0, bc * 32, (sl - p.coff[rb]) >> 5, q + s, pp + r);
+                if (p.unified)
+                  ld5(b + jb * p.apb * 4096, &p.maps[0], 0, bc * 32, (sl - p.coff[rb]) >> 5, (pp + r) * p.Win + q + s,
+                      rb);
+                else
+                  ld5(b + jb * p.apb * 4096, &p.maps[rb], 0, bc * 32, (sl - p.coff[rb]) >> 5, q + s, pp + r);
               }
             } else if (p.wide) {
               ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
@@ -695,6 +697,14 @@ int map_act_wide(CUtensorMap* m, const float* base, int kw, int Bp, int W, int H
   return make_map(m, base, 5, dims, str, box, true);
 }
 
+// all input rank blocks have the same (nonzero) width and there are several of them
+bool equal_blocks(const Layer& L) {
+  if (L.images || L.in.n < 2 || !env_int("CP_TC_UNIFIED", 1)) return false;
+  for (int r = 0; r < L.in.n; ++r)
+    if (L.in.kw[r] != L.in.kw[0] || L.in.kw[r] == 0) return false;
+  return true;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -988,20 +998,21 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   const Plan pl = fwd_plan(L, p);
   if (L.images) {
     CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 2, 2, false));
+  } else if (equal_blocks(L)) {
+    // one 5-D map over all rank blocks: (slot, b, w, h, block)
+    const int kw = L.in.kw[0];
+    const uint64_t dims[5] = {(uint64_t)kw, (uint64_t)L.Bp, (uint64_t)L.W, (uint64_t)L.H, (uint64_t)L.in.n};
+    const uint64_t str[4] = {(uint64_t)kw * 4, (uint64_t)kw * L.Bp * 4, (uint64_t)kw * L.Bp * L.W * 4,
+                             (uint64_t)kw * L.Bp * L.W * L.H * 4};
+    const uint32_t box[5] = {32, 32, 2, 2, 1};
+    CP_TRY(make_map(&p.maps[0], xin, 5, dims, str, box, false));
+    p.unified = 1;
   } else {
     for (int r = 0; r < L.in.n; ++r)
       if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false));
   }
   p.bn_box = pl.pair ? p.nw / 2 : std::min(p.nw, L.Kc);
-  p.dbg = env_int("CP_TC_DEBUG", 0);
-  if (p.dbg) {  // contiguous 128-byte-row views of the same buffers (wrong values, timing only)
-    const uint64_t dims[2] = {32, 8192};
-    const uint64_t str[1] = {128};
-    const uint32_t boxb[2] = {32, (uint32_t)p.bn_box};
-    const uint32_t boxa[2] = {32, 128};
-    CP_TRY(make_map(&p.maps[CP_MAX_RANKS - 2], w, 2, dims, str, boxb));
-    CP_TRY(make_map(&p.maps[CP_MAX_RANKS - 1], xin, 2, dims, str, boxa));
-  }
+
   {
     const uint64_t dims[2] = {(uint64_t)L.Ktot, (uint64_t)std::max(L.Kr, 1)};
     const uint64_t str[1] = {(uint64_t)L.Ktot * 4};
@@ -1105,6 +1116,14 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   const int nat = p.span ? w.apb : (w.pair ? 4 : 8);
   if (L.images) {
     CP_TRY(map_act_wide(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, nat));
+  } else if (p.span && equal_blocks(L)) {
+    // one 5-D map over all rank blocks: (slot lane, b, 32-slot atom, h*W + w, block)
+    const int kw = L.in.kw[0];
+    const uint64_t dims[5] = {32, (uint64_t)L.Bp, (uint64_t)(kw / 32), (uint64_t)L.H * L.W, (uint64_t)L.in.n};
+    const uint64_t str[4] = {(uint64_t)kw * 4, 128, (uint64_t)kw * L.Bp * 4, (uint64_t)kw * L.Bp * L.W * L.H * 4};
+    const uint32_t box[5] = {32, 32, (uint32_t)nat, 1, 1};
+    CP_TRY(make_map(&p.maps[0], xin, 5, dims, str, box, true));
+    p.unified = 1;
   } else {
     for (int r = 0; r < L.in.n; ++r)
       if (L.in.kw[r] > 0) CP_TRY(map_act_wide(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, nat));
