@@ -101,8 +101,8 @@ template <int PASS, int CG>
 __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) {
   Unit t{};
   int mg;
-  if (PASS == PASS_WGRAD && p.tail_st > 0 && u >= p.tail_full) {
-    // the last (partial) round of equal wgrad tiles is split along K over every CTA group
+  if ((PASS == PASS_WGRAD || PASS == PASS_FWD) && p.tail_st > 0 && u >= p.tail_full) {
+    // the last (partial) round of equal tiles is split along K over every CTA group
     const int v = u - p.tail_full;
     t.tail = 1;
     t.tu = v / p.tail_st;
@@ -184,8 +184,8 @@ template <int PASS, class F>
 __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t, F f) {
   if (PASS == PASS_FWD) {
     const int total = p.R * p.S * p.cpt;
-    const int per = (total + p.split - 1) / p.split;
-    const int lo = t.sp * per, hi = min(total, lo + per);
+    const int per = t.tail ? p.tail_per : (total + p.split - 1) / p.split;
+    const int lo = (t.tail ? t.piece : t.sp) * per, hi = min(total, lo + per);
     int idx = 0;
     for (int tap = 0; tap < p.R * p.S; ++tap)
       for (int rb = 0; rb < p.nblk; ++rb) {
@@ -415,7 +415,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         float v[32];
         tmem_ld_32x32b_x32(tbase + cc * 32, v);
         const int ncol = min(32, t.n - cc * 32);
-        if (PASS == PASS_FWD && p.split > 1) {
+        if ((PASS == PASS_FWD || PASS == PASS_WGRAD) && t.tail) {
+          // tail piece: raw partial tile, finished by fwd_tail_finish / wgrad_tail_reduce
+          float* dst = p.tail_buf + ((((int64_t)t.tu * p.tail_st + t.piece) * CG + rank) * BM + row) * BN + cc * 32;
+          store_f32x32(dst, v, 32);
+        } else if (PASS == PASS_FWD && p.split > 1) {
           // split-K partial of the pre-pool tile: [sp][Ho][Wo][Bp][Kc]
           const int dh = quad >> 1, dw = quad & 1;
           const int bb = t.bc * 32 + lane;
@@ -507,10 +511,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                               ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb) * kw + slot;
             store_f32x32(p.out + o, v, ncol);
           }
-        } else if (t.tail) {
-          // tail piece: raw partial tile, summed in piece order by wgrad_tail_reduce
-          float* dst = p.tail_buf + ((((int64_t)t.tu * p.tail_st + t.piece) * CG + rank) * BM + row) * BN + cc * 32;
-          store_f32x32(dst, v, 32);
         } else {
           const int kk = t.mt * BM + row;
           if (kk < p.Kr) {
@@ -555,6 +555,47 @@ __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restri
   for (int pc = 0; pc < ti.st; ++pc)
     acc += buf[((((int64_t)tu * ti.st + pc) * ti.cg + rank) * BM + row) * BN + c];
   dw[(int64_t)kk * ti.Ktot + ti.col0[tu] + c] = acc;
+}
+
+// forward tail: the tile's pre-pool accumulator = sum over pieces (in order) of the partial tiles;
+// then bias, ReLU, 2x2 max-pool (rows q*32+b of a CTA's tile are window position q, image b),
+// argmax code and RN-tf32 rounding, exactly as the fused epilogue.
+struct FwdTailInfo {
+  int n, st, cg, Wo, Wp, Bp, B, Kr, Kc, relu, pool;
+  int i[MAX_TAIL], j[MAX_TAIL], bc0[MAX_TAIL], n0[MAX_TAIL], ncol[MAX_TAIL];
+};
+__global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __restrict__ bias, float* __restrict__ y,
+                                uint8_t* __restrict__ saved, const __grid_constant__ FwdTailInfo ti) {
+  const int tu = blockIdx.z, rank = blockIdx.y, b = blockIdx.x;
+  const int c = threadIdx.x;
+  if (c >= ti.ncol[tu]) return;
+  const int n = ti.n0[tu] + c;
+  const int bb = ti.bc0[tu] + rank * 32 + b;
+  const bool ok = bb < ti.B && n < ti.Kr;
+  const float bs = (bias && n < ti.Kr) ? bias[n] : 0.f;
+  float best = 0.f;
+  int code = 0;
+  for (int q = 0; q < 4; ++q) {
+    float z = 0.f;
+    for (int pc = 0; pc < ti.st; ++pc)
+      z += buf[((((int64_t)tu * ti.st + pc) * ti.cg + rank) * BM + q * 32 + b) * BN + c];
+    z += bs;
+    if (ti.relu && !(z > 0.f)) z = 0.f;
+    if (ti.pool) {
+      if (q == 0 || z > best) {
+        best = z;
+        code = q;
+      }
+    } else {
+      const int64_t o = ((int64_t)((2 * ti.i[tu] + (q >> 1)) * ti.Wo + 2 * ti.j[tu] + (q & 1)) * ti.Bp + bb) * ti.Kc + n;
+      y[o] = ok ? tf32_rna(z) : 0.f;
+    }
+  }
+  if (ti.pool) {
+    const int64_t o = ((int64_t)(ti.i[tu] * ti.Wp + ti.j[tu]) * ti.Bp + bb) * ti.Kc + n;
+    y[o] = ok ? tf32_rna(best) : 0.f;
+    saved[o] = ok ? (uint8_t)code : 0;
+  }
 }
 
 // deterministic split-K reduction: dW[i] = sum_s part[s][i] in split order
@@ -883,7 +924,11 @@ static Plan fwd_plan(const Layer& L, TcParams& p) {
       const int nw = ((L.Kc + T - 1) / T + gran - 1) / gran * gran;
       if (nw > BN || nw <= 0) continue;
       const int tiles = (L.Kc + nw - 1) / nw;
-      const double rounds = std::ceil((double)w.numM * tiles / groups);
+      const int units = w.numM * tiles;
+      double rounds = std::ceil((double)units / groups);
+      const int last = units - ((int)rounds - 1) * groups;    // tiles in the last round
+      if (rounds > 1 && 2 * last <= groups && env_int("CP_TC_FWD_TAIL", 1))
+        rounds = rounds - 1 + (double)last / groups * 1.1;    // tail split (tc_fwd), ~10 % overhead
       const double t = rounds * (16384.0 + 128.0 * nw / CG);
       if (t < best * 0.98) {
         best = t;
@@ -970,6 +1015,7 @@ size_t tc_workspace_bytes(const Layer& L) {
     fill_common(p, L);
     const Plan w = fwd_plan(L, p);
     if (w.S > 1) need = std::max(need, (size_t)w.S * L.Ho * L.Wo * L.Bp * L.Kc * 4);
+    need = std::max(need, (size_t)num_sms() * BM * BN * 4);   // forward tail-split partials
   }
   if (!L.images && L.Kr > 0) {
     TcParams p{};
@@ -1029,7 +1075,43 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = (long long)L.Ho * L.Wo * L.Bp * L.Kc;
   p.out = pl.S > 1 ? part : y_block;
+  // Tail split of the last partial round of equal tiles (see tc_wgrad); the pooled epilogue of
+  // those tiles runs in fwd_tail_finish after the deterministic sum of the pieces.
+  FwdTailInfo ti{};
+  {
+    const int CG = pl.pair ? 2 : 1, G = num_sms() / CG;
+    const int rounds = (p.units + G - 1) / G, T = p.units - (rounds - 1) * G;
+    const int chunks = p.R * p.S * p.cpt;
+    if (pl.S == 1 && rounds > 1 && T > 0 && 2 * T <= G && T <= MAX_TAIL && chunks >= 16 &&
+        env_int("CP_TC_FWD_TAIL", 1)) {
+      int st = std::max(1, std::min(G / T, chunks / 8));
+      const int per = (chunks + st - 1) / st;
+      st = (chunks + per - 1) / per;
+      p.tail_full = (rounds - 1) * G;
+      p.tail_st = st;
+      p.tail_per = per;
+      p.tail_buf = part;
+      ti.n = T; ti.st = st; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B;
+      ti.Kr = L.Kr; ti.Kc = L.Kc; ti.relu = L.d.relu; ti.pool = L.d.pool;
+      const int nbcg = L.Bp / 32 / CG, W2 = L.Wo / 2;
+      for (int k = 0; k < T; ++k) {                    // host mirror of decode_unit<FWD>
+        const int u = p.tail_full + k;
+        const int mg = u % p.numM, nt = (u / p.numM) % p.numN;
+        const int ij = mg / nbcg;
+        ti.bc0[k] = (mg % nbcg) * CG * 32;
+        ti.j[k] = ij % W2;
+        ti.i[k] = ij / W2;
+        ti.n0[k] = nt * p.nw;
+        ti.ncol[k] = std::min(p.nw, L.Kc - ti.n0[k]);
+      }
+      p.units = p.tail_full + T * st;
+    }
+  }
   CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
+  if (p.tail_st > 0) {
+    fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
+    CP_LAUNCHED();
+  }
   if (pl.S > 1) {
     const long long total4 = (long long)L.Hp * L.Wp * L.Bp * (L.Kc / 4);
     splitk_fwd_finish<<<(unsigned)((total4 + 255) / 256), 256, 0, s>>>(
