@@ -37,6 +37,8 @@ constexpr int POOL_LD = 33;                   // padded row of the pooling excha
 constexpr int POOL_BYTES = 4 * 32 * POOL_LD * 4;
 constexpr int MAX_NT = 64;
 constexpr int MAX_WIN = 512;                  // dgrad LPT window table (larger grids: natural order)
+constexpr int MAX_GROUPS = 148;               // CTA groups (one per SM or SM pair)
+constexpr int MAX_SCHED = 1024;               // units in an explicit per-group schedule
 
 // CG = CTAs per MMA (cta_group::1 or ::2).  With a CTA pair the MMA is M=256 (128 rows per CTA)
 // and each CTA stages only half of B (N/2 columns), so per-SM operand traffic drops by 1/3 and
@@ -79,6 +81,9 @@ struct TcParams {
   int nt_rb[MAX_NT], nt_n0[MAX_NT], nt_n[MAX_NT];  // dgrad / wgrad N-tile list (per tap for wgrad)
   int tail_full, tail_st, tail_per;  // wgrad tail split: units >= tail_full are (tail unit, K piece)
   float* tail_buf;     // wgrad tail partials [tail unit][piece][CTA of pair][128 rows][256 cols]
+  int nsched;          // >0: per-group unit lists (host LPT schedule); 0: static round-robin
+  short sched_off[MAX_GROUPS + 1];
+  short sched[MAX_SCHED];
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
   short win_order[MAX_WIN];
   const float* bias;
@@ -158,6 +163,18 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     t.n = p.nt_n[e];
   }
   return t;
+}
+
+// k-th unit processed by CTA group `group`: the host's per-group list (LPT-balanced, see
+// tc_dgrad) or static round-robin; -1 when the group is done.  Producer, MMA issuer and
+// epilogue walk the identical sequence.
+__device__ __forceinline__ int unit_at(const TcParams& p, int group, int ngroups, int k) {
+  if (p.nsched > 0) {
+    const int b = p.sched_off[group], e = p.sched_off[group + 1];
+    return b + k < e ? (int)p.sched[b + k] : -1;
+  }
+  const int u = group + k * ngroups;
+  return u < p.units ? u : -1;
 }
 
 // Visit the K-chunks of a unit in order: f(ksteps, c0..c3 of A, ...) is pass specific, so the
@@ -282,7 +299,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = group; u < p.units; u += ngroups) {
+      for (int k = 0;; ++k) {
+        const int u = unit_at(p, group, ngroups, k);
+        if (u < 0) break;
         const Unit t = decode_unit<PASS, CG>(p, u, rank);
         const int n_mma = mma_n<PASS, CG>(t.n);
         const int nb_own = CG == 2 ? n_mma / 2 : n_mma;          // B columns staged by this CTA
@@ -364,7 +383,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int u = group; u < p.units; u += ngroups, ++local) {
+      for (int k = 0;; ++k, ++local) {
+        const int u = unit_at(p, group, ngroups, k);
+        if (u < 0) break;
         const Unit t = decode_unit<PASS, CG>(p, u, 0);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
@@ -403,7 +424,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     const int row = quad * 32 + lane;              // accumulator row of this CTA = TMEM lane
     float* pool_buf = pool_all + grp * (POOL_BYTES / 4);
     int local = 0;
-    for (int u = group; u < p.units; u += ngroups, ++local) {
+    for (int k = 0;; ++k, ++local) {
+      const int u = unit_at(p, group, ngroups, k);
+      if (u < 0) break;
       const Unit t = decode_unit<PASS, CG>(p, u, rank);
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
@@ -1178,6 +1201,42 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = pl.S > 1 ? (long long)L.in.start[L.in.n] : 0;
   p.out = pl.S > 1 ? part : dx;
+  {
+    // Static LPT schedule: tiles carry 4..25 valid taps, so round-robin dispatch leaves SMs idle.
+    // Assign each unit (heaviest first) to the least-loaded CTA group; a group then walks its units
+    // in natural order (keeps the spatial L2 locality of neighbouring windows).
+    const int CG = pl.pair ? 2 : 1, G = std::min(p.units, num_sms() / CG);
+    if (p.nwin_order == 0 && p.units <= MAX_SCHED && G <= MAX_GROUPS && env_int("CP_TC_DGRAD_SCHED", 1)) {
+      const int nbcg = L.Bp / 32 / CG, W2 = L.W / 2, kc = (L.Kc + BK - 1) / BK;
+      std::vector<std::pair<long long, int>> wk(p.units);
+      for (int u = 0; u < p.units; ++u) {
+        const int mg = u % p.numM;
+        const int ij = mg / nbcg, i = ij / W2, j = ij % W2;
+        const int nr = std::min(L.R - 1, 2 * i + 1) - std::max(0, 2 * i - L.Ho + 1) + 1;
+        const int ns = std::min(L.S - 1, 2 * j + 1) - std::max(0, 2 * j - L.Wo + 1) + 1;
+        const long long work = ((long long)nr * ns * kc + pl.S - 1) / pl.S;
+        wk[u] = {-work, u};
+      }
+      std::stable_sort(wk.begin(), wk.end());
+      std::vector<long long> load(G, 0);
+      std::vector<std::vector<int>> lists(G);
+      for (const auto& e : wk) {
+        int g = 0;
+        for (int q = 1; q < G; ++q)
+          if (load[q] < load[g]) g = q;
+        load[g] += -e.first;
+        lists[g].push_back(e.second);
+      }
+      int off = 0;
+      for (int g = 0; g < G; ++g) {
+        std::sort(lists[g].begin(), lists[g].end());
+        p.sched_off[g] = (short)off;
+        for (int u : lists[g]) p.sched[off++] = (short)u;
+      }
+      p.sched_off[G] = (short)off;
+      p.nsched = off;
+    }
+  }
   CP_TRY((pl.pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s)));
   if (pl.S > 1) {
     const int64_t n = L.in.start[L.in.n];
