@@ -88,12 +88,13 @@ class ClockSampler:
         self.index, self.rows, self.proc = index, [], None
 
     def start(self):
+        self.t0 = time.time()
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
@@ -325,7 +326,15 @@ def main():
         loss_host.copy_(pn.head["loss"][:1], non_blocking=True)
         e2e_ev[k][1].record(s)
     torch.cuda.synchronize(dev)
+    # the timed window is tens of ms; keep the same load (identical, untimed steps) until the
+    # sampler has seen >= 1.5 s so the clock record is meaningful
+    # (step count from the max-over-ranks ms_per_step: identical on every rank, the steps hold
+    # collectives)
+    for _ in range(min(2000, int(1500.0 / max(ms_per_step, 0.05)) + 1)):
+        step()
+    torch.cuda.synchronize(dev)
     clk = clocks.stop()
+    clk["window"] = "timed steps + e2e steps + identical untimed steps to >= 1.5 s"
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
