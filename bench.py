@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--no-overlap", action="store_true")
     ap.add_argument("--head", default="partitioned", choices=["partitioned", "replicated"],
                     help="FC head: rank-local columns + AllReduce of logits, or all-gathered + replicated")
+    ap.add_argument("--fused", default="on", choices=["on", "off"],
+                    help="on: collectives fused into the GEMM epilogues over NVLink peer memory (channel "
+                         "gather from the forward epilogue, dX reduce-scatter from the dgrad epilogue); "
+                         "off: NCCL AllGather / ReduceScatter kernels")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
@@ -241,7 +245,7 @@ def main():
         parts = [cp.cp_partition_plan([1.0] * world, K) for K in net.kernels]
 
     pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev, head=args.head,
-                        in_hw=net.in_hw)
+                        in_hw=net.in_hw, fused=args.fused == "on")
     params = synth.params(net, seed=42)
     pn.load_params(params)
     x, y = synth.images(B, 3, net.in_hw, net.in_hw, step=0)
@@ -406,6 +410,10 @@ def main():
                 "partition_source": "Eq.1 from probe" if probe_times else "even",
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
                 "head": pn.head_mode, "cuda_graph": graph is not None,
+                "collectives": ("fused into the GEMM epilogues over NVLink peer memory (gather: forward "
+                                "epilogue stores + arrival flags; dX reduce-scatter: dgrad epilogue stores "
+                                "+ slot sum)" if pn.sym else "NCCL AllGather / ReduceScatter")
+                               if world > 1 else "none (N=1)",
                 "parallelism": f"kernel-split x{world}",
                 "l2": "flushed between timed steps (256 MiB write outside the step events)" if flush is not None
                       else "not flushed (step working set ~700 MB > 126 MB L2)"},

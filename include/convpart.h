@@ -81,9 +81,14 @@ typedef enum {
   CP_DX_ALLREDUCE = 0,       /* full summed dX on every rank                       */
   CP_DX_REDUCE_SCATTER = 1,  /* rank r receives the summed dX of its own block only */
   CP_DX_LOCAL = 2,           /* no collective: dx holds this rank's partial sum     */
-  CP_DX_ASYNC = 16           /* OR-flag: do not make `stream` wait for the dX collective;
+  CP_DX_ASYNC = 16,          /* OR-flag: do not make `stream` wait for the dX collective;
                                 call conv_part_wait() before reading dx (lets independent
                                 work such as wgrad overlap the reduction, §8(e))        */
+  CP_DX_ORDERED = 64         /* OR-flag (fused reduce-scatter only): the caller guarantees
+                                that a collective on every rank separates consecutive
+                                backward_data calls of this layer (e.g. the forward's
+                                gather or the logits AllReduce), so the overwrite guard
+                                barrier is skipped                                      */
 } cp_dx_mode;
 
 typedef enum {
@@ -124,6 +129,24 @@ int cp_comm_unique_id(uint8_t id_out[128]);
 int cp_comm_create(const uint8_t id[128], int32_t rank, int32_t world, cp_comm* out);
 int cp_comm_destroy(cp_comm comm);
 
+/* Symmetric buffers for the fused channel AllGather (the gather is Alg. 1's
+ * "concatenate the output of all nodes").  cp_symmetric_alloc allocates `bytes` of
+ * zeroed device memory on every rank (collective: all ranks, same size, same order), exchanges CUDA
+ * IPC handles over the communicator and maps every peer's copy (plus a small arrival-flag line
+ * behind the data).  Semantics when a layer's y_gathered is symmetric (conv_part_forward):
+ *   producer: after a one-word AllReduce (no rank may overwrite a copy a peer still reads), the TF32
+ *     forward epilogue stores this rank's block into every peer's copy over NVLink, then sets this
+ *     rank's arrival flag in every peer's flag line (no AllGather kernel);
+ *   consumer: conv_part_forward whose x is a symmetric gathered buffer consumes its own block first
+ *     and each peer block only after that peer's flag is set (gather overlapped with the GEMM), and
+ *     resets the flags.  Any other reader of a symmetric gathered output calls cp_symmetric_wait
+ *     (waits for all peers' flags on `stream`, then resets them) before reading it.
+ * cp_symmetric_free (collective) or cp_comm_destroy releases the buffers.  Errors: CP_ERR_ARG for a
+ * pointer that is not a symmetric buffer of `comm`; CUDA/NCCL errors as CP_ERR_CUDA/CP_ERR_NCCL. */
+int cp_symmetric_alloc(cp_comm comm, size_t bytes, void** local_out);
+int cp_symmetric_free(cp_comm comm, void* local);
+int cp_symmetric_wait(cp_comm comm, void* local, void* stream);
+
 /* ---------------------------------------------------------------- conv layer */
 typedef struct {
   int32_t batch;               /* B (real images)                                 */
@@ -153,6 +176,9 @@ typedef struct {
   size_t saved;     /* bytes of this rank's argmax codes (0 without pooling)      */
   size_t dx;        /* bytes of the input gradient (same shape as x)              */
   size_t workspace; /* bytes of per-layer scratch; must persist fwd -> bwd        */
+  size_t dx_peer;   /* bytes of dx for the fused reduce-scatter: the gather layout
+                       followed by n_ranks receive slots of the largest input block
+                       (allocate with cp_symmetric_alloc; 0 for image input)       */
 } cp_sizes;
 
 typedef struct cp_layer_s* cp_layer;
@@ -187,7 +213,14 @@ int conv_part_forward(cp_layer layer, const float* x, const float* w, const floa
  * channels, then the cross-rank sum selected by dx_mode.  dx has the shape of x.
  * For CP_DX_REDUCE_SCATTER only this rank's input block of dx is valid.  With the
  * CP_DX_ASYNC flag and comm_stream != stream, `stream` is not made to wait for the
- * collective: call conv_part_wait(layer, stream) before consuming dx. */
+ * collective: call conv_part_wait(layer, stream) before consuming dx.
+ * Fused reduce-scatter (SURVEY §8(f) f1, TF32 path): when dx is a symmetric buffer of
+ * at least dx_peer bytes (cp_symmetric_alloc) and dx_mode is CP_DX_REDUCE_SCATTER, the
+ * dgrad epilogue stores each input block's partial straight into its owner's receive
+ * slot (peers over NVLink), sets this rank's arrival flag at every peer, and the sum of
+ * the n_ranks slots (ascending rank order) lands in this rank's block of dx on
+ * comm_stream - no NCCL collective.  Unless CP_DX_ORDERED is given, a one-word
+ * AllReduce first guards the receive slots against overwrite while a peer still sums. */
 int conv_part_backward_data(cp_layer layer, const float* dy_gathered, const uint8_t* saved,
                             const float* y_gathered, const float* w, float* dx, int32_t dx_mode,
                             void* workspace, void* stream, void* comm_stream);

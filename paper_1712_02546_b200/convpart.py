@@ -17,7 +17,7 @@ CP_OK = 0
 ERRORS = {-1: "CP_ERR_ARG", -2: "CP_ERR_SHAPE", -3: "CP_ERR_CONFIG", -4: "CP_ERR_DATA", -5: "CP_ERR_CUDA",
           -6: "CP_ERR_NCCL", -7: "CP_ERR_STATE", -8: "CP_ERR_UNSUPPORTED"}
 CP_MATH_TF32, CP_MATH_FP32_SIMT = 0, 1
-CP_DX_ALLREDUCE, CP_DX_REDUCE_SCATTER, CP_DX_LOCAL, CP_DX_ASYNC = 0, 1, 2, 16
+CP_DX_ALLREDUCE, CP_DX_REDUCE_SCATTER, CP_DX_LOCAL, CP_DX_ASYNC, CP_DX_ORDERED = 0, 1, 2, 16, 64
 CP_INPUT_IMAGES, CP_INPUT_GATHER = 0, 1
 
 # every symbol include/convpart.h declares (checked by tests/test_abi.py)
@@ -28,7 +28,7 @@ EXPORTS = [
     "cp_launch_count", "cp_last_error", "cp_pack_nchw", "cp_unpack_nchw", "cp_unpack_saved",
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
-    "cp_allreduce_sum",
+    "cp_allreduce_sum", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait",
 ]
 
 
@@ -65,7 +65,8 @@ class cp_conv_desc(ctypes.Structure):
 
 
 class cp_sizes(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_size_t) for n in ("w", "b", "x", "y", "y_block", "y_offset", "saved", "dx", "workspace")]
+    _fields_ = [(n, ctypes.c_size_t)
+                for n in ("w", "b", "x", "y", "y_block", "y_offset", "saved", "dx", "workspace", "dx_peer")]
 
 
 class ConvPartError(RuntimeError):
@@ -115,6 +116,9 @@ def lib():
             "cp_fc_backward": [P, P, I32, I32, I32, pp, P, I32, P, P, P, P, P],
             "cp_sgd": [P, P, I64, ctypes.c_float, P],
             "cp_allreduce_sum": [P, P, I64, P],
+            "cp_symmetric_alloc": [P, SZ, ctypes.POINTER(P)],
+            "cp_symmetric_free": [P, P],
+            "cp_symmetric_wait": [P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -291,6 +295,29 @@ def cp_fc_backward(dl, x, B, Hp, Wp, part, wg, O, dx, dwg, dbfc, ws, stream=None
 
 def cp_allreduce_sum(comm, buf, stream=None):
     _call("cp_allreduce_sum", comm, _ptr(buf), buf.numel(), _stream(stream))
+
+
+class SymmetricBuffer:
+    """Device memory from cp_symmetric_alloc, exposed to torch via __cuda_array_interface__."""
+
+    def __init__(self, comm, nbytes, device):
+        self.comm, self.nbytes = comm, int(nbytes)
+        ptr = ctypes.c_void_p()
+        _call("cp_symmetric_alloc", comm, self.nbytes, ctypes.byref(ptr))
+        self.ptr = ptr.value
+        self.__cuda_array_interface__ = {"shape": (self.nbytes // 4,), "typestr": "<f4",
+                                         "data": (self.ptr, False), "version": 2}
+        import torch
+        self.tensor = torch.as_tensor(self, device=device)
+
+    def wait(self, stream=None):
+        """Before reading the gathered buffer outside conv_part_forward: wait for every peer's block."""
+        _call("cp_symmetric_wait", self.comm, ctypes.c_void_p(self.ptr), _stream(stream))
+
+    def free(self):
+        if self.ptr:
+            _call("cp_symmetric_free", self.comm, ctypes.c_void_p(self.ptr))
+            self.ptr = None
 
 
 def cp_sgd(p, g, lr, stream=None):

@@ -15,9 +15,20 @@
 
 #include "kernels.cuh"
 
+#include <map>
+
+// A symmetric buffer: the same-sized allocation on every rank, each rank holding peer pointers
+// (CUDA IPC over NVLink) to all the others, so kernels can store directly into peers' copies.
+struct SymBuf {
+  size_t bytes, flag_off;
+  void* peers[CP_MAX_RANKS];  // peers[rank] = own pointer
+};
+
 struct cp_comm_s {
   ncclComm_t comm;
   int rank, world;
+  std::map<void*, SymBuf> sym;   // keyed by the local pointer
+  float* barrier_word = nullptr; // 1-float device scratch for the post-store barrier
 };
 
 #define CP_NCCL(call)                                                                      \
@@ -56,11 +67,87 @@ extern "C" int cp_comm_create(const uint8_t id[128], int32_t rank, int32_t world
   return CP_OK;
 }
 
+extern "C" int cp_symmetric_alloc(cp_comm c, size_t bytes, void** local_out) {
+  if (!c || !local_out || bytes == 0) CP_FAIL(CP_ERR_ARG, "cp_symmetric_alloc: bad arguments");
+  SymBuf sb{};
+  sb.bytes = bytes;
+  sb.flag_off = (bytes + 255) / 256 * 256;   // arrival flags live behind the data (one 256 B line)
+  void* mine = nullptr;
+  CP_CUDA(cudaMalloc(&mine, sb.flag_off + 256));
+  CP_CUDA(cudaMemset(mine, 0, sb.flag_off + 256));
+  cudaIpcMemHandle_t h;
+  CP_CUDA(cudaIpcGetMemHandle(&h, mine));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  // exchange the 64-byte handles with an NCCL AllGather (blocking: allocation time only)
+  uint8_t* dev = nullptr;
+  CP_CUDA(cudaMalloc(&dev, 64 * (size_t)(c->world + 1)));
+  CP_CUDA(cudaMemcpy(dev + 64 * (size_t)c->world, &h, 64, cudaMemcpyHostToDevice));
+  ncclResult_t r = ncclAllGather(dev + 64 * (size_t)c->world, dev, 64, ncclUint8, c->comm, 0);
+  std::vector<uint8_t> all(64 * (size_t)c->world);
+  cudaError_t e = cudaSuccess;
+  if (r == ncclSuccess) e = cudaMemcpy(all.data(), dev, all.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dev);
+  if (r != ncclSuccess) CP_FAIL(CP_ERR_NCCL, std::string("symmetric alloc handle exchange: ") + ncclGetErrorString(r));
+  if (e != cudaSuccess) CP_FAIL(CP_ERR_CUDA, std::string("symmetric alloc: ") + cudaGetErrorString(e));
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) {
+      sb.peers[p] = mine;
+      continue;
+    }
+    cudaIpcMemHandle_t ph;
+    memcpy(&ph, all.data() + 64 * (size_t)p, 64);
+    CP_CUDA(cudaIpcOpenMemHandle(&sb.peers[p], ph, cudaIpcMemLazyEnablePeerAccess));
+  }
+  if (!c->barrier_word) {
+    CP_CUDA(cudaMalloc(&c->barrier_word, sizeof(float)));
+    CP_CUDA(cudaMemset(c->barrier_word, 0, sizeof(float)));
+  }
+  c->sym[mine] = sb;
+  *local_out = mine;
+  return CP_OK;
+}
+
+// Unmap every peer's copy, then wait until all ranks have unmapped theirs before freeing the
+// exported allocation (no rank may still hold a mapping of memory that is being freed).
+static void sym_release(cp_comm c, void* local, SymBuf& sb) {
+  cudaDeviceSynchronize();
+  for (int p = 0; p < c->world; ++p)
+    if (p != c->rank && sb.peers[p]) cudaIpcCloseMemHandle(sb.peers[p]);
+  if (c->barrier_word && ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, 0) ==
+                             ncclSuccess)
+    cudaDeviceSynchronize();
+  cudaFree(local);
+}
+
+extern "C" int cp_symmetric_free(cp_comm c, void* local) {
+  if (!c || !local) return CP_OK;
+  auto it = c->sym.find(local);
+  if (it == c->sym.end()) CP_FAIL(CP_ERR_ARG, "cp_symmetric_free: not a symmetric buffer");
+  sym_release(c, local, it->second);
+  c->sym.erase(it);
+  return CP_OK;
+}
+
 extern "C" int cp_comm_destroy(cp_comm c) {
   if (!c) return CP_OK;
+  // every rank holds the same number of symmetric buffers, so the per-buffer barriers pair up
+  for (auto& kv : c->sym) sym_release(c, kv.first, kv.second);
+  c->sym.clear();
+  if (c->barrier_word) cudaFree(c->barrier_word);
   ncclResult_t r = ncclCommDestroy(c->comm);
   delete c;
   if (r != ncclSuccess) CP_FAIL(CP_ERR_NCCL, std::string("ncclCommDestroy: ") + ncclGetErrorString(r));
+  return CP_OK;
+}
+
+extern "C" int cp_symmetric_wait(cp_comm c, void* local, void* stream) {
+  if (!c || c->world == 1) return CP_OK;
+  void* peers[CP_MAX_RANKS];
+  uint32_t* flags[CP_MAX_RANKS];
+  if (!cp::comm_symmetric_peers(c, local, peers, flags)) CP_FAIL(CP_ERR_ARG, "cp_symmetric_wait: not a symmetric buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  CP_TRY(cp::launch_wait_flags(flags[c->rank], c->world, c->rank, s));
+  CP_CUDA(cudaMemsetAsync(flags[c->rank], 0, CP_MAX_RANKS * sizeof(uint32_t), s));
   return CP_OK;
 }
 
@@ -115,6 +202,26 @@ int comm_check_plan(cp_comm c, const Layer& L) {
   if (e != cudaSuccess) CP_FAIL(CP_ERR_CUDA, std::string("plan check: ") + cudaGetErrorString(e));
   for (int i = 0; i < 4; ++i)
     if (got[i] != host[i]) CP_FAIL(CP_ERR_CONFIG, "conv_part_create: ranks hold different partition maps");
+  return CP_OK;
+}
+
+// Peer pointers of a symmetric buffer (nullptr if `local` is not one).
+bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags) {
+  if (!c || c->world == 1) return false;
+  auto it = c->sym.find(const_cast<void*>(local));
+  if (it == c->sym.end()) return false;
+  for (int p = 0; p < c->world; ++p) {
+    peers[p] = it->second.peers[p];
+    if (flags) flags[p] = (uint32_t*)((char*)it->second.peers[p] + it->second.flag_off);
+  }
+  return true;
+}
+
+// Cross-rank barrier on `s` after peer stores: a one-word AllReduce completes on a rank only once
+// every rank has reached it, i.e. after every rank's storing kernel (stream order) has finished.
+int comm_barrier(cp_comm c, cudaStream_t s) {
+  if (!c || c->world == 1) return CP_OK;
+  CP_NCCL(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
   return CP_OK;
 }
 

@@ -99,6 +99,26 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+// ---------------------------------------------------------------- cross-GPU arrival flags
+// A producer rank sets its slot in every consumer's flag array (st.release.sys after its peer stores);
+// the consumer spins with ld.acquire.sys.  The spin is bounded (~2^35 cycles, >15 s): a missing
+// signal traps (a reported launch failure) instead of hanging the GPU.
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag_sys(const uint32_t* p) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys(p) == 0) {
+    asm volatile("nanosleep.u32 100;");
+    if (clock64() - t0 > (1ll << 35)) __trap();
+  }
+}
+
 // ---------------------------------------------------------------- layer state
 struct Layer {
   cp_conv_desc d;

@@ -8,10 +8,12 @@ namespace cp {
 int launch_im2col(const Layer& L, const float* x, float* xcol, bool round_tf32, cudaStream_t s);
 int launch_relu_pool(const Layer& L, const float* z, float* y_block, uint8_t* saved, bool round_tf32,
                      cudaStream_t s);
+// unpool + ReLU' of the own block; also writes the bias-gradient partials (bias_part, may be null)
+constexpr int kBiasSplitMax = 256;
 int launch_unpool(const Layer& L, const float* dy_block, const uint8_t* saved, const float* y_block,
-                  float* dY, bool round_tf32, cudaStream_t s);
-int launch_bias_grad(const Layer& L, const float* dy_block, const float* y_block, float* db, float* part,
-                     cudaStream_t s);
+                  float* dY, float* bias_part, bool round_tf32, cudaStream_t s);
+// db from the partials launch_unpool wrote
+int launch_bias_grad(const Layer& L, float* db, const float* part, cudaStream_t s);
 
 // ---- FP32 SIMT reference convolutions (kernels_simt.cu)
 int launch_fwd_simt(const Layer& L, const float* x, const float* xcol, const float* w, const float* b,
@@ -21,18 +23,31 @@ int launch_wgrad_simt(const Layer& L, const float* dY, const float* x, const flo
                       cudaStream_t s);
 int launch_fill(float* p, float v, int64_t n, cudaStream_t s);
 int launch_random_fill(float* p, int64_t n, uint32_t seed, float scale, cudaStream_t s);
+// cross-GPU arrival flags (fused AllGather): set slot `slot` of every peer's flag array / wait for
+// every slot of the own array except `self` (for consumers outside the tensor-core forward)
+int launch_signal_peers(uint32_t* const* peer_flags, int n, int slot, cudaStream_t s);
+int launch_wait_flags(const uint32_t* flags, int n, int self, cudaStream_t s);
 
 // ---- tcgen05 / TMA tensor-core convolutions (kernels_tc.cu)
 size_t tc_workspace_bytes(const Layer& L);
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved,
-           void* ws, cudaStream_t s);
-int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s);
+           void* ws, cudaStream_t s, float* const* peer_blocks = nullptr, int npeers = 0,
+           const uint32_t* arrive = nullptr);
+// dst_blocks (fused reduce-scatter): per input block, where this rank's partial of that block goes
+int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s,
+             float* const* dst_blocks = nullptr);
+// dx_own = sum over q (ascending) of the P receive slots (fused reduce-scatter epilogue)
+int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float* out, int64_t n, cudaStream_t s);
 int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s);
 void tc_release(Layer& L);
 
 // ---- NCCL collectives (comm.cu)
 int comm_check_plan(cp_comm c, const Layer& L);
 int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s);
+// symmetric (peer-mapped) buffer lookup: peers[r] = rank r's copy; flags[r] = rank r's arrival-flag
+// array (CP_MAX_RANKS u32, indexed by sender rank).  False if `local` is not a symmetric buffer.
+bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags = nullptr);
+int comm_barrier(cp_comm c, cudaStream_t s);
 int comm_sum_blocks(cp_comm c, float* buf, const Blocks& g, int dx_mode, cudaStream_t s);
 
 }  // namespace cp

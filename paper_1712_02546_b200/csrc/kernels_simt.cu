@@ -216,33 +216,69 @@ int launch_wgrad_simt(const Layer& L, const float* dY, const float* x, const flo
 
 // ============================================================== layout / elementwise
 // im2col of the images for conv1: rows (p,q,b) of the output grid, columns (r,s,c) padded to Kcol.
-// One thread per 4 consecutive columns (float4 store); reads are tiny and L2/L1-resident.
-__global__ void im2col_kernel(const float* __restrict__ x, float* __restrict__ xcol, int B, int C, int H,
-                              int W, int R, int S, int Wo, int Bp, int Kcol, int64_t total4, int round) {
-  const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e4 >= total4) return;
-  const int kc4 = Kcol >> 2;
-  const int col0 = (int)(e4 % kc4) * 4;
-  const int m = (int)(e4 / kc4);
-  const int b = m % Bp, pq = m / Bp, q = pq % Wo, p = pq / Wo;
-  float v[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int col = col0 + t;
-    float u = 0.f;
-    if (b < B && col < R * S * C) {
-      const int c = col % C, tap = col / C, r = tap / S, s = tap - r * S;
-      u = __ldg(x + (((int64_t)b * C + c) * H + p + r) * W + q + s);
+// One block per (output row p, nimg images).  Load phase: input rows p..p+R-1 of every channel are
+// R*W contiguous floats per (image, channel) - copied into shared memory coalesced (TF32-rounded
+// when the consumer is the tensor-core path).  Write phase: every output pixel q of the row, the
+// nimg x Kcol floats of xcol at ((p*Wo + q)*Bp + b0)*Kcol are contiguous - float4 stores, values
+// picked from shared memory through a column -> offset table.  The output stays in L2.
+constexpr int kIm2colMaxK = 256;
+__global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ x, float* __restrict__ xcol, int B,
+                                                     int C, int H, int W, int R, int S, int Wo, int Bp, int Kcol,
+                                                     int nimg, int round) {
+  extern __shared__ float xs[];                 // [nimg][C][R][W]
+  __shared__ int tab[kIm2colMaxK];              // column -> offset within one image's rows, -1 = padding
+  const int p = blockIdx.x, b0 = blockIdx.y * nimg;
+  const int RW = R * W, CRW = C * RW, RSC = R * S * C;
+  const int nt = blockDim.x * blockDim.y, tid = threadIdx.y * blockDim.x + threadIdx.x;
+  for (int col = tid; col < Kcol; col += nt) {
+    int o = -1;
+    if (col < RSC) {
+      const int c = col % C, tap = col / C, r = tap / S, sx = tap - r * S;
+      o = c * RW + r * W + sx;
     }
-    v[t] = round ? tf32_rna(u) : u;
+    tab[col] = o;
   }
-  reinterpret_cast<float4*>(xcol)[e4] = make_float4(v[0], v[1], v[2], v[3]);
+  // load: (image, channel) pairs outer (block-uniform), the pair's R*W contiguous floats inner
+  for (int bc = 0, bl = 0, c = 0; bc < nimg * C; ++bc) {
+    const int b = b0 + bl;
+    const float* src = x + (((int64_t)b * C + c) * H + p) * W;
+    for (int k = tid; k < RW; k += nt) {
+      const float u = b < B ? __ldg(src + k) : 0.f;
+      xs[bc * RW + k] = round ? tf32_rna(u) : u;
+    }
+    if (++c == C) { c = 0; ++bl; }
+  }
+  __syncthreads();
+  // write: thread x = fixed float4 column group of the pixel's nimg x Kcol floats (table lookups
+  // hoisted), thread y strides the output pixels q
+  const int e = threadIdx.x;                    // blockDim.x = nimg * Kcol / 4
+  const int bl = (4 * e) / Kcol, col0 = 4 * e - bl * Kcol;
+  int off[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) off[t] = tab[col0 + t];
+  const float* src = xs + bl * CRW;
+  float4* dst = reinterpret_cast<float4*>(xcol + ((int64_t)p * Wo * Bp + b0) * Kcol) + e;
+  const int64_t qstride4 = (int64_t)Bp * Kcol / 4;
+  for (int q = threadIdx.y; q < Wo; q += blockDim.y) {
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = off[t] >= 0 ? src[off[t] + q] : 0.f;
+    dst[q * qstride4] = make_float4(v[0], v[1], v[2], v[3]);
+  }
 }
 
 int launch_im2col(const Layer& L, const float* x, float* xcol, bool round_tf32, cudaStream_t s) {
-  const int64_t total4 = (int64_t)L.Ho * L.Wo * L.Bp * (L.Kcol / 4);
-  im2col_kernel<<<grid1d(total4, 256), 256, 0, s>>>(x, xcol, L.B, L.C, L.H, L.W, L.R, L.S, L.Wo, L.Bp, L.Kcol,
-                                                    total4, round_tf32 ? 1 : 0);
+  const size_t per_img = (size_t)L.C * L.R * L.W * 4;
+  // nimg images per block: the pixel row of nimg x Kcol floats is one float4 per thread (<= 256)
+  int nimg = 8;
+  while (nimg > 1 && ((size_t)nimg * per_img > 48 * 1024 || nimg * L.Kcol / 4 > 256)) nimg >>= 1;
+  if (L.Kcol > kIm2colMaxK || (size_t)nimg * per_img > 48 * 1024 || nimg * L.Kcol / 4 > 256 ||
+      (int64_t)L.B * L.C * L.H * L.W >= (1ll << 31))
+    CP_FAIL(CP_ERR_UNSUPPORTED, "im2col: image layer too large (Kcol > 256 or C*R*W*4 > 48 KB)");
+  const int bx = nimg * L.Kcol / 4, by = std::max(1, 256 / bx);
+  dim3 grid((unsigned)L.Ho, (unsigned)(L.Bp / nimg));
+  im2col_kernel<<<grid, dim3(bx, by), nimg * per_img, s>>>(x, xcol, L.B, L.C, L.H, L.W, L.R, L.S, L.Wo, L.Bp,
+                                                           L.Kcol, nimg, round_tf32 ? 1 : 0);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -298,92 +334,115 @@ int launch_relu_pool(const Layer& L, const float* z, float* y_block, uint8_t* sa
 // (ReLU'(0)=0, reading R7).  One thread per (pooled position, image, 4 slots): it reads
 // dy/y/codes once (float4 + 4 bytes) and writes the four window positions (4 x float4), so every
 // pre-pool element is written exactly once with coalesced 16-byte stores.
-__global__ void unpool_kernel(const float* __restrict__ dyp, const uint8_t* __restrict__ am,
-                              const float* __restrict__ y, float* __restrict__ dY, int Wo, int Wp, int Bp,
-                              int Kc, int64_t total4, int relu, int pool, int round) {
-  const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e4 >= total4) return;
+// Epilogue backward of the own block: dY (pre-pool grid) = the pooled gradient routed to
+// the argmax position of its window, masked by ReLU' (y > 0), zero elsewhere; TF32-rounded for the
+// tensor-core passes.  Fused: the bias gradient db[slot] = sum over pooled rows of dy * [y > 0]
+// (every unmasked pooled gradient reaches exactly one pre-pool position, so this is sum dY).
+// Block (32 float4 columns, 8 rows) on a contiguous row range; per-block column sums combine the
+// 8 row lanes in fixed order -> part[split][slot]; bias_grad_final adds the splits in order.
+__global__ void __launch_bounds__(256) unpool_kernel(const float* __restrict__ dyp, const uint8_t* __restrict__ am,
+                                                     const float* __restrict__ y, float* __restrict__ dY,
+                                                     float* __restrict__ part, int Wo, int Wp, int Bp, int Kc,
+                                                     int rows, int per, int relu, int pool, int round) {
+  __shared__ float4 red[8][32];
   const int kc4 = Kc >> 2;
-  const int slot = (int)(e4 % kc4) * 4;
-  const int64_t rest = e4 / kc4;  // pooled row index (i*Wp + j)*Bp + b
-  const int b = (int)(rest % Bp);
-  const int ij = (int)(rest / Bp);
-  const int64_t pe = rest * Kc + slot;
-  const float4 g = *reinterpret_cast<const float4*>(dyp + pe);
-  const float4 yy = *reinterpret_cast<const float4*>(y + pe);
-  float gv[4] = {g.x, g.y, g.z, g.w};
-  const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
+  const int c4 = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c4 < kc4) {
+    const int slot = c4 * 4;
+    for (int rest = r0 + threadIdx.y; rest < r1; rest += 8) {   // pooled row (i*Wp + j)*Bp + b
+      const int64_t pe = (int64_t)rest * Kc + slot;
+      const float4 g = *reinterpret_cast<const float4*>(dyp + pe);
+      const float4 yy = *reinterpret_cast<const float4*>(y + pe);
+      float gv[4] = {g.x, g.y, g.z, g.w};
+      const float yv[4] = {yy.x, yy.y, yy.z, yy.w};
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    if (relu && !(yv[t] > 0.f)) gv[t] = 0.f;
-    if (round) gv[t] = tf32_rna(gv[t]);
+      for (int t = 0; t < 4; ++t)
+        if (relu && !(yv[t] > 0.f)) gv[t] = 0.f;
+      acc.x += gv[0]; acc.y += gv[1]; acc.z += gv[2]; acc.w += gv[3];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (round) gv[t] = tf32_rna(gv[t]);
+      if (!pool) {
+        *reinterpret_cast<float4*>(dY + pe) = make_float4(gv[0], gv[1], gv[2], gv[3]);
+        continue;
+      }
+      const uint32_t codes = *reinterpret_cast<const uint32_t*>(am + pe);
+      const int b = rest % Bp, ij = rest / Bp;
+      const int j = ij % Wp, i = ij / Wp;
+#pragma unroll
+      for (int pos = 0; pos < 4; ++pos) {
+        const int h = 2 * i + (pos >> 1), w = 2 * j + (pos & 1);
+        float o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) o[t] = ((codes >> (8 * t)) & 0xFFu) == (uint32_t)pos ? gv[t] : 0.f;
+        *reinterpret_cast<float4*>(dY + ((int64_t)(h * Wo + w) * Bp + b) * Kc + slot) =
+            make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
   }
-  if (!pool) {
-    *reinterpret_cast<float4*>(dY + pe) = make_float4(gv[0], gv[1], gv[2], gv[3]);
-    return;
-  }
-  const uint32_t codes = *reinterpret_cast<const uint32_t*>(am + pe);
-  const int j = ij % Wp, i = ij / Wp;
+  if (!part) return;
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c4 < kc4) {
+    float4 t = red[0][threadIdx.x];
 #pragma unroll
-  for (int pos = 0; pos < 4; ++pos) {
-    const int h = 2 * i + (pos >> 1), w = 2 * j + (pos & 1);
-    float o[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) o[t] = ((codes >> (8 * t)) & 0xFFu) == (uint32_t)pos ? gv[t] : 0.f;
-    *reinterpret_cast<float4*>(dY + ((int64_t)(h * Wo + w) * Bp + b) * Kc + slot) = make_float4(o[0], o[1], o[2], o[3]);
+    for (int k = 1; k < 8; ++k) {
+      const float4 u = red[k][threadIdx.x];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    reinterpret_cast<float4*>(part + (int64_t)blockIdx.y * Kc)[c4] = t;
   }
 }
 
+// number of row splits of the unpool grid (also the number of bias partials)
+static int unpool_splits(const Layer& L) {
+  const int rows = L.Hp * L.Wp * L.Bp;
+  const int cb = cdiv(L.Kc / 4, 32);
+  int ns = cdiv(4 * 148, cb);
+  ns = std::min(ns, kBiasSplitMax);
+  ns = std::min(ns, std::max(1, rows / 8));
+  return std::max(ns, 1);
+}
+
 int launch_unpool(const Layer& L, const float* dy_block, const uint8_t* saved, const float* y_block, float* dY,
-                  bool round_tf32, cudaStream_t s) {
-  const int64_t total4 = (int64_t)L.Hp * L.Wp * L.Bp * (L.Kc / 4);
-  if (total4 == 0) return CP_OK;
-  unpool_kernel<<<grid1d(total4, 256), 256, 0, s>>>(dy_block, saved, y_block, dY, L.Wo, L.Wp, L.Bp, L.Kc, total4,
-                                                    L.d.relu, L.d.pool, round_tf32 ? 1 : 0);
+                  float* bias_part, bool round_tf32, cudaStream_t s) {
+  if (L.Kc == 0) return CP_OK;
+  const int rows = L.Hp * L.Wp * L.Bp;
+  const int ns = unpool_splits(L);
+  const int per = cdiv(rows, ns);
+  unpool_kernel<<<dim3(cdiv(L.Kc / 4, 32), ns), dim3(32, 8), 0, s>>>(
+      dy_block, saved, y_block, dY, bias_part, L.Wo, L.Wp, L.Bp, L.Kc, rows, per, L.d.relu, L.d.pool,
+      round_tf32 ? 1 : 0);
   CP_LAUNCHED();
   return CP_OK;
 }
 
-// db[slot] = sum over pooled rows of dy * [y > 0]: every pooled gradient reaches exactly one
-// pre-pool position unless masked, so this equals sum of dY.  Two fixed-order phases.
-constexpr int kBiasSplit = 64;
-__global__ void bias_grad_partial(const float* __restrict__ dy, const float* __restrict__ y, float* part,
-                                  int64_t rows, int Kc, int relu) {
-  __shared__ float sm[8][33];
+// db[slot] = sum of the unpool kernel's bias partials, splits added in ascending order:
+// block (32 slots, 8 split lanes), lanes combined in fixed order.
+__global__ void __launch_bounds__(256) bias_grad_final(const float* __restrict__ part, float* db, int ns, int Kr,
+                                                       int Kc) {
+  __shared__ float red[8][33];
   const int slot = blockIdx.x * 32 + threadIdx.x;
-  const int64_t per = (rows + kBiasSplit - 1) / kBiasSplit;
-  const int64_t r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
-  float acc = 0.f;
-  if (slot < Kc)
-    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
-      const int64_t e = r * Kc + slot;
-      const float g = dy[e];
-      acc += (!relu || y[e] > 0.f) ? g : 0.f;
-    }
-  sm[threadIdx.y][threadIdx.x] = acc;
+  const int per = (ns + 7) / 8;
+  const int s0 = threadIdx.y * per, s1 = min(ns, s0 + per);
+  float t = 0.f;
+  if (slot < Kr)
+    for (int i = s0; i < s1; ++i) t += part[(int64_t)i * Kc + slot];
+  red[threadIdx.y][threadIdx.x] = t;
   __syncthreads();
-  if (threadIdx.y == 0 && slot < Kc) {
-    float t = 0.f;
+  if (threadIdx.y == 0 && slot < Kr) {
+    float u = red[0][threadIdx.x];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += sm[i][threadIdx.x];
-    part[(int64_t)blockIdx.y * Kc + slot] = t;
+    for (int k = 1; k < 8; ++k) u += red[k][threadIdx.x];
+    db[slot] = u;
   }
 }
-__global__ void bias_grad_final(const float* __restrict__ part, float* db, int Kr, int Kc) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= Kr) return;
-  float t = 0.f;
-  for (int i = 0; i < kBiasSplit; ++i) t += part[(int64_t)i * Kc + slot];
-  db[slot] = t;
-}
 
-int launch_bias_grad(const Layer& L, const float* dy_block, const float* y_block, float* db, float* part,
-                     cudaStream_t s) {
-  const int64_t rows = (int64_t)L.Hp * L.Wp * L.Bp;
-  bias_grad_partial<<<dim3(cdiv(L.Kc, 32), kBiasSplit), dim3(32, 8), 0, s>>>(dy_block, y_block, part, rows,
-                                                                             L.Kc, L.d.relu);
-  CP_LAUNCHED();
-  bias_grad_final<<<cdiv(L.Kr > 0 ? L.Kr : 1, 128), 128, 0, s>>>(part, db, L.Kr, L.Kc);
+int launch_bias_grad(const Layer& L, float* db, const float* part, cudaStream_t s) {
+  if (L.Kr == 0) return CP_OK;
+  bias_grad_final<<<cdiv(L.Kr, 32), dim3(32, 8), 0, s>>>(part, db, unpool_splits(L), L.Kr, L.Kc);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -409,6 +468,56 @@ __global__ void random_fill_kernel(float* p, int64_t n, uint32_t seed, float sca
 int launch_random_fill(float* p, int64_t n, uint32_t seed, float scale, cudaStream_t s) {
   if (n <= 0) return CP_OK;
   random_fill_kernel<<<grid1d(n, 256), 256, 0, s>>>(p, n, seed, scale);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
+// fused reduce-scatter epilogue: out[e] = sum_{q ascending} slots[q*slot_stride + e] (float4)
+__global__ void sum_slots_kernel(const float* __restrict__ slots, int64_t slot_stride, int n_slots,
+                                 float* __restrict__ out, int64_t n4) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  float4 acc = reinterpret_cast<const float4*>(slots)[i];
+  for (int q = 1; q < n_slots; ++q) {
+    const float4 v = reinterpret_cast<const float4*>(slots + q * slot_stride)[i];
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  reinterpret_cast<float4*>(out)[i] = acc;
+}
+int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return CP_OK;
+  if ((n | slot_stride) & 3) CP_FAIL(CP_ERR_UNSUPPORTED, "sum_slots: sizes not multiples of 4");
+  sum_slots_kernel<<<grid1d(n / 4, 256), 256, 0, s>>>(slots, slot_stride, n_slots, out, n / 4);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
+struct FlagPtrs {
+  uint32_t* f[CP_MAX_RANKS];
+};
+// Runs after the storing kernel (stream order): the fence makes its peer stores visible system-wide
+// before the release store of the flag.
+__global__ void signal_peers_kernel(FlagPtrs fp, int n, int slot) {
+  __threadfence_system();
+  for (int k = 0; k < n; ++k) st_release_sys(fp.f[k] + slot, 1u);
+}
+__global__ void wait_flags_kernel(const uint32_t* flags, int n, int self) {
+  for (int r = 0; r < n; ++r)
+    if (r != self) wait_flag_sys(flags + r);
+}
+
+int launch_signal_peers(uint32_t* const* peer_flags, int n, int slot, cudaStream_t s) {
+  if (n <= 0) return CP_OK;
+  FlagPtrs fp{};
+  for (int k = 0; k < n; ++k) fp.f[k] = peer_flags[k];
+  signal_peers_kernel<<<1, 1, 0, s>>>(fp, n, slot);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
+int launch_wait_flags(const uint32_t* flags, int n, int self, cudaStream_t s) {
+  if (n <= 1) return CP_OK;
+  wait_flags_kernel<<<1, 1, 0, s>>>(flags, n, self);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -519,12 +628,13 @@ __global__ void unpack_w_images_kernel(const float* __restrict__ wg, float* __re
 // FC features in gather order: block r, position pos = h*Wp+w, slot; f' = Hp*Wp*coff[r] + pos*kw[r] + slot.
 constexpr int kMaxO = 16;
 
-// FC forward over the gather layout.  CTA = (rank block r, position pos, 128-slot chunk): the
-// weight slice W[o][f(r,pos,chunk)] is staged in shared memory; thread (image b, slot half)
-// streams 64 contiguous slots of x with float4 loads and accumulates all O logits.  The two
-// halves combine by one shuffle; fc_fwd_reduce then adds the units in unit order (fixed order,
-// bitwise identical on every rank).
-constexpr int kFcChunk = 128;
+// FC forward over the gather layout (logits = W x + b).  CTA = (rank block r, position pos,
+// 64-slot chunk) x 128-image chunk: the x tile [128 images][64 slots] and the weight slice
+// W[o][f(r,pos,chunk)] are staged in shared memory with coalesced float4 loads; thread (image b,
+// half) accumulates all O logits over 32 of the slots, the halves combine by one shuffle, and
+// fc_fwd_reduce adds the units in unit order (fixed order, bitwise identical on every rank).
+constexpr int kFcChunk = 64;
+constexpr int kFcLd = 72;     // x tile row stride (floats): conflict-free float4 reads by (b, half)
 __host__ __device__ inline int fc_nsc(const Blocks& g) {
   int m = 0;
   for (int r = 0; r < g.n; ++r) m = g.kw[r] > m ? g.kw[r] : m;
@@ -534,12 +644,14 @@ __host__ __device__ inline int fc_nsc(const Blocks& g) {
 __global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
                                                       float* __restrict__ part, Blocks g, int B, int O, int PW,
                                                       int nsc) {
+  __shared__ __align__(16) float xs[128 * kFcLd];
   __shared__ float4 ws[kMaxO][kFcChunk / 4];
   const int u = blockIdx.x;
   const int sc = u % nsc, rp = u / nsc;
   const int r = rp / PW, pos = rp % PW;
   const int kw = g.kw[r];
   const int s0 = sc * kFcChunk;
+  const int b0 = blockIdx.y * 128;
   const int64_t F = (int64_t)PW * g.Cg;
   const int64_t foff = (int64_t)PW * g.coff[r] + (int64_t)pos * kw + s0;
   for (int i = threadIdx.x; i < kMaxO * (kFcChunk / 4); i += blockDim.x) {
@@ -548,50 +660,64 @@ __global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ 
     if (o < O && s0 + q4 < kw) v = __ldg(reinterpret_cast<const float4*>(wg + o * F + foff + q4));
     ws[o][i % (kFcChunk / 4)] = v;
   }
+  const float* xb = x + g.start[r] + (int64_t)pos * g.Bp * kw + s0;
+  for (int i = threadIdx.x; i < 128 * (kFcChunk / 4); i += blockDim.x) {
+    const int row = i >> 4, q = i & 15, b = b0 + row;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (b < B && s0 + 4 * q < kw) v = __ldg(reinterpret_cast<const float4*>(xb + (int64_t)b * kw) + q);
+    *reinterpret_cast<float4*>(xs + row * kFcLd + 4 * q) = v;
+  }
   __syncthreads();
-  const int b = blockIdx.y * 128 + (threadIdx.x >> 1), half = threadIdx.x & 1;
+  const int bl = threadIdx.x >> 1, half = threadIdx.x & 1;
   float acc[kMaxO];
 #pragma unroll
   for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
-  if (b < B) {
-    const float* xr = x + g.start[r] + ((int64_t)pos * g.Bp + b) * kw + s0;
-    const int n4 = min(kFcChunk, kw - s0) / 4;
-#pragma unroll 4
-    for (int q = half * (kFcChunk / 8); q < (half + 1) * (kFcChunk / 8); ++q) {
-      if (q >= n4) break;
-      const float4 xv = __ldg(reinterpret_cast<const float4*>(xr) + q);
 #pragma unroll
-      for (int o = 0; o < kMaxO; ++o) {
-        if (o < O) {
-          const float4 w = ws[o][q];
-          acc[o] = fmaf(xv.x, w.x, fmaf(xv.y, w.y, fmaf(xv.z, w.z, fmaf(xv.w, w.w, acc[o]))));
-        }
+  for (int k = 0; k < kFcChunk / 8; ++k) {
+    const int q = 2 * k + half;
+    const float4 xv = *reinterpret_cast<const float4*>(xs + bl * kFcLd + 4 * q);
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o) {
+      if (o < O) {
+        const float4 w = ws[o][q];
+        acc[o] = fmaf(xv.x, w.x, fmaf(xv.y, w.y, fmaf(xv.z, w.z, fmaf(xv.w, w.w, acc[o]))));
       }
     }
   }
 #pragma unroll
   for (int o = 0; o < kMaxO; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
+  const int b = b0 + bl;
   if (half == 0 && b < g.Bp)
     for (int o = 0; o < O; ++o) part[((int64_t)u * g.Bp + b) * O + o] = acc[o];
 }
 
-// logits[b][o] = bias[o] + sum_u part[u][b][o]: one warp per (b, o); lanes take units in strides
-// of 32 (ascending), then a fixed xor-shuffle tree — a fixed order, identical on every rank.
-__global__ void fc_fwd_reduce(const float* __restrict__ part, const float* __restrict__ bfc, float* logits,
-                              int U, int Bp, int B, int O) {
-  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (e >= B * O) return;
-  const int b = e / O, o = e % O;
+// logits[b][o] = bias[o] + sum_u part[u][b][o].  Block (32 consecutive (b,o) elements, 32 unit
+// lanes): lane y adds units y*per.. in ascending order (coalesced rows of part), the 32 lane sums
+// combine in fixed order - identical on every rank.
+__global__ void __launch_bounds__(1024) fc_fwd_reduce(const float* __restrict__ part, const float* __restrict__ bfc,
+                                                      float* logits, int U, int Bp, int B, int O) {
+  __shared__ float red[32][33];
+  const int e = blockIdx.x * 32 + threadIdx.x;
+  const int per = (U + 31) / 32;
+  const int u0 = threadIdx.y * per, u1 = min(U, u0 + per);
   float t = 0.f;
-  for (int u = lane; u < U; u += 32) t += part[((int64_t)u * Bp + b) * O + o];
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
-  if (lane == 0) logits[e] = t + (bfc ? bfc[o] : 0.f);
+  if (e < B * O)
+    for (int u = u0; u < u1; ++u) t += part[(int64_t)u * Bp * O + e];
+  red[threadIdx.y][threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.y == 0 && e < B * O) {
+    float v = red[0][threadIdx.x];
+    for (int k = 1; k < 32; ++k) v += red[k][threadIdx.x];
+    logits[e] = v + (bfc ? bfc[e % O] : 0.f);
+  }
 }
 
-__global__ void softmax_xent_kernel(const float* __restrict__ logits, const int* __restrict__ y, int B, int O,
-                                    float* loss, float* dl) {
-  extern __shared__ float terms[];
+// softmax cross-entropy: loss = mean_b (logsumexp(l_b) - l_b[y_b]),
+// dlogits = (softmax - onehot) / B.  One block; the loss sum is a fixed-order tree.
+__global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restrict__ logits, const int* __restrict__ y,
+                                                           int B, int O, float* loss, float* dl) {
+  __shared__ float wsum[8];
+  float part = 0.f;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     const float* l = logits + (int64_t)b * O;
     float m = l[0];
@@ -601,105 +727,131 @@ __global__ void softmax_xent_kernel(const float* __restrict__ logits, const int*
     const float lse = m + logf(se);
     const int lab = y[b];
     if (lab < 0 || lab >= O) {
-      terms[b] = __int_as_float(0x7fc00000);  // NaN loss flags an out-of-range label
+      part += __int_as_float(0x7fc00000);  // NaN loss flags an out-of-range label
       continue;
     }
-    terms[b] = lse - l[lab];
+    part += lse - l[lab];
     for (int o = 0; o < O; ++o) dl[(int64_t)b * O + o] = (expf(l[o] - lse) - (o == lab ? 1.f : 0.f)) / (float)B;
   }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
     float t = 0.f;
-    for (int b = 0; b < B; ++b) t += terms[b];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wsum[w];
     *loss = t / (float)B;
   }
 }
 
 // dA2 in gather layout: dx[(r,pos,b,slot)] = sum_o dlogits[b][o] * W[o][f(r,pos,slot)], zero for b >= B.
-// Grid (r*PW + pos, ceil(Bp*kw/4 / 256)); one thread per 4 slots (float4).
-__global__ void fc_bwd_dx(const float* __restrict__ dl, const float* __restrict__ wg, float* __restrict__ dx,
-                          Blocks g, int B, int O, int PW) {
+// Grid (r*PW + pos, 32-image chunk, 256-slot chunk); the weight slice and the dlogits rows are
+// staged in shared memory; thread (float4 column q, row group) writes coalesced float4 rows.
+__global__ void __launch_bounds__(256) fc_bwd_dx(const float* __restrict__ dl, const float* __restrict__ wg,
+                                                 float* __restrict__ dx, Blocks g, int B, int O, int PW) {
+  __shared__ float4 ws[kMaxO][64];
+  __shared__ float dls[32][kMaxO];
   const int rp = blockIdx.x;
   const int r = rp / PW, pos = rp % PW;
   const int kw = g.kw[r];
-  const int kw4 = kw >> 2;
-  const int e4 = blockIdx.y * blockDim.x + threadIdx.x;
-  if (e4 >= g.Bp * kw4) return;
-  const int b = e4 / kw4, slot = (e4 % kw4) * 4;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (b < B) {
-    const int64_t F = (int64_t)PW * g.Cg;
-    const int64_t f = (int64_t)PW * g.coff[r] + (int64_t)pos * kw + slot;
-    for (int o = 0; o < O; ++o) {
-      const float d = __ldg(dl + b * O + o);
-      const float4 w = __ldg(reinterpret_cast<const float4*>(wg + o * F + f));
-      acc.x = fmaf(d, w.x, acc.x); acc.y = fmaf(d, w.y, acc.y);
-      acc.z = fmaf(d, w.z, acc.z); acc.w = fmaf(d, w.w, acc.w);
-    }
-  }
-  *reinterpret_cast<float4*>(dx + g.start[r] + ((int64_t)pos * g.Bp + b) * kw + slot) = acc;
-}
-
-// dW_fc[o][f] = sum_b dlogits[b][o] * x(b, f): thread (4 features, batch quarter); the four
-// quarters are added in order in shared memory (fixed order).
-__global__ void __launch_bounds__(128) fc_bwd_dw(const float* __restrict__ dl, const float* __restrict__ x,
-                                                 float* __restrict__ dwg, Blocks g, int B, int O, int PW) {
-  __shared__ float4 red[3][32][kMaxO];
+  const int s0 = blockIdx.z * 256;
+  if (s0 >= kw) return;
+  const int b0 = blockIdx.y * 32;
   const int64_t F = (int64_t)PW * g.Cg;
-  const int64_t f = ((int64_t)blockIdx.x * 32 + threadIdx.x) * 4;
-  const int qb = threadIdx.y;
-  float acc[kMaxO][4];
-#pragma unroll
-  for (int o = 0; o < kMaxO; ++o)
-#pragma unroll
-    for (int t = 0; t < 4; ++t) acc[o][t] = 0.f;
-  if (f < F) {
-    int r = 0;
-    while (r + 1 < g.n && f >= (int64_t)PW * g.coff[r + 1]) ++r;
-    const int64_t l = f - (int64_t)PW * g.coff[r];
-    const int kw = g.kw[r];
-    const int pos = (int)(l / kw), slot = (int)(l % kw);
-    const float* xp = x + g.start[r] + (int64_t)pos * g.Bp * kw + slot;
-    const int bq = (B + 3) / 4;
-    const int b0 = qb * bq, b1 = min(B, b0 + bq);
-    for (int b = b0; b < b1; ++b) {
-      const float4 xv = __ldg(reinterpret_cast<const float4*>(xp + (int64_t)b * kw));
-#pragma unroll
-      for (int o = 0; o < kMaxO; ++o) {
-        if (o < O) {
-          const float d = __ldg(dl + b * O + o);
-          acc[o][0] = fmaf(d, xv.x, acc[o][0]); acc[o][1] = fmaf(d, xv.y, acc[o][1]);
-          acc[o][2] = fmaf(d, xv.z, acc[o][2]); acc[o][3] = fmaf(d, xv.w, acc[o][3]);
-        }
-      }
-    }
+  const int64_t f0 = (int64_t)PW * g.coff[r] + (int64_t)pos * kw + s0;
+  for (int i = threadIdx.x; i < kMaxO * 64; i += blockDim.x) {
+    const int o = i >> 6, q = i & 63;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (o < O && s0 + 4 * q < kw) v = __ldg(reinterpret_cast<const float4*>(wg + o * F + f0) + q);
+    ws[o][q] = v;
   }
-  if (qb > 0) {
-#pragma unroll
-    for (int o = 0; o < kMaxO; ++o) red[qb - 1][threadIdx.x][o] = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
+  for (int i = threadIdx.x; i < 32 * kMaxO; i += blockDim.x) {
+    const int bl = i / kMaxO, o = i % kMaxO;
+    dls[bl][o] = (b0 + bl < B && o < O) ? __ldg(dl + (int64_t)(b0 + bl) * O + o) : 0.f;
   }
   __syncthreads();
-  if (qb == 0 && f < F) {
+  const int q = threadIdx.x & 63, rg = threadIdx.x >> 6;
+  if (s0 + 4 * q >= kw) return;
+  float* out = dx + g.start[r] + (int64_t)pos * g.Bp * kw + s0 + 4 * q;
+  for (int bl = rg; bl < 32 && b0 + bl < g.Bp; bl += 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int o = 0; o < kMaxO; ++o) {
-      if (o >= O) continue;
-      float4 t = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
-#pragma unroll
-      for (int q = 1; q < 4; ++q) {
-        const float4 u = red[q - 1][threadIdx.x][o];
-        t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+      if (o < O) {
+        const float d = dls[bl][o];
+        const float4 w = ws[o][q];
+        acc.x = fmaf(d, w.x, acc.x); acc.y = fmaf(d, w.y, acc.y);
+        acc.z = fmaf(d, w.z, acc.z); acc.w = fmaf(d, w.w, acc.w);
       }
-      *reinterpret_cast<float4*>(dwg + o * F + f) = t;
     }
+    *reinterpret_cast<float4*>(out + (int64_t)(b0 + bl) * kw) = acc;
   }
 }
 
-__global__ void fc_bwd_db(const float* __restrict__ dl, float* dbfc, int B, int O) {
-  const int o = threadIdx.x;
-  if (o >= O) return;
-  float t = 0.f;
-  for (int b = 0; b < B; ++b) t += dl[(int64_t)b * O + o];
-  dbfc[o] = t;
+// dW_fc[o][f] = sum_b dlogits[b][o] * x(b, f).  CTA = (r, pos, 64-slot chunk); per 128-image chunk
+// the x tile and dlogits rows are staged in shared memory; thread (slot, row quarter) accumulates
+// its 32 rows for all O in ascending order, the quarters combine in fixed order.
+__global__ void __launch_bounds__(256) fc_bwd_dw(const float* __restrict__ dl, const float* __restrict__ x,
+                                                 float* __restrict__ dwg, Blocks g, int B, int O, int PW, int nsc) {
+  constexpr int LD = kFcChunk + 4;
+  __shared__ __align__(16) float xs[128 * LD];      // reused for the quarter reduction
+  __shared__ float dls[128][kMaxO + 1];
+  const int u = blockIdx.x;
+  const int sc = u % nsc, rp = u / nsc;
+  const int r = rp / PW, pos = rp % PW;
+  const int kw = g.kw[r];
+  const int s0 = sc * kFcChunk;
+  const int64_t F = (int64_t)PW * g.Cg;
+  const int64_t foff = (int64_t)PW * g.coff[r] + (int64_t)pos * kw + s0;
+  const float* xb = x + g.start[r] + (int64_t)pos * g.Bp * kw + s0;
+  const int sl = threadIdx.x & 63, bq = threadIdx.x >> 6;
+  float acc[kMaxO];
+#pragma unroll
+  for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
+  for (int b0 = 0; b0 < B; b0 += 128) {
+    if (b0) __syncthreads();
+    for (int i = threadIdx.x; i < 128 * (kFcChunk / 4); i += blockDim.x) {
+      const int row = i >> 4, q = i & 15, b = b0 + row;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (b < B && s0 + 4 * q < kw) v = __ldg(reinterpret_cast<const float4*>(xb + (int64_t)b * kw) + q);
+      *reinterpret_cast<float4*>(xs + row * LD + 4 * q) = v;
+    }
+    for (int i = threadIdx.x; i < 128 * kMaxO; i += blockDim.x) {
+      const int row = i / kMaxO, o = i % kMaxO;
+      dls[row][o] = (b0 + row < B && o < O) ? __ldg(dl + (int64_t)(b0 + row) * O + o) : 0.f;
+    }
+    __syncthreads();
+    for (int row = bq * 32; row < bq * 32 + 32; ++row) {
+      const float xv = xs[row * LD + sl];
+#pragma unroll
+      for (int o = 0; o < kMaxO; ++o)
+        if (o < O) acc[o] = fmaf(dls[row][o], xv, acc[o]);
+    }
+  }
+  __syncthreads();
+  float* red = xs;   // [4][kMaxO][64]
+#pragma unroll
+  for (int o = 0; o < kMaxO; ++o) red[(bq * kMaxO + o) * 64 + sl] = acc[o];
+  __syncthreads();
+  for (int i = threadIdx.x; i < O * 64; i += blockDim.x) {
+    const int o = i >> 6, s = i & 63;
+    if (s0 + s >= kw) continue;
+    const float t = ((red[(0 * kMaxO + o) * 64 + s] + red[(1 * kMaxO + o) * 64 + s]) + red[(2 * kMaxO + o) * 64 + s]) +
+                    red[(3 * kMaxO + o) * 64 + s];
+    dwg[o * F + foff + s] = t;
+  }
+}
+
+// dbfc[o] = sum_b dlogits[b][o]: warp per class, lanes stride the batch, fixed xor tree.
+__global__ void __launch_bounds__(256) fc_bwd_db(const float* __restrict__ dl, float* dbfc, int B, int O) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int o = w; o < O; o += blockDim.x >> 5) {
+    float t = 0.f;
+    for (int b = lane; b < B; b += 32) t += dl[(int64_t)b * O + o];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+    if (lane == 0) dbfc[o] = t;
+  }
 }
 
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
@@ -886,7 +1038,7 @@ int cp_fc_forward(const float* x, int32_t B, int32_t Hp, int32_t Wp, const cp_pa
   cudaStream_t s = (cudaStream_t)stream;
   fc_fwd_partial<<<dim3(U, (g.Bp + 127) / 128), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
   CP_LAUNCHED();
-  fc_fwd_reduce<<<cdiv((int64_t)B * O * 32, 256), 256, 0, s>>>(part_buf, bfc, logits, U, g.Bp, B, O);
+  fc_fwd_reduce<<<cdiv((int64_t)B * O, 32), dim3(32, 32), 0, s>>>(part_buf, bfc, logits, U, g.Bp, B, O);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -895,7 +1047,7 @@ int cp_softmax_xent(const float* logits, const int32_t* labels, int32_t B, int32
                     void* stream) {
   if (!logits || !labels || !loss || !dl) CP_FAIL(CP_ERR_ARG, "cp_softmax_xent: null pointer");
   if (B < 1 || B > 8192 || O < 1) CP_FAIL(CP_ERR_SHAPE, "cp_softmax_xent: B must be in [1,8192]");
-  softmax_xent_kernel<<<1, 256, B * sizeof(float), (cudaStream_t)stream>>>(logits, labels, B, O, loss, dl);
+  softmax_xent_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(logits, labels, B, O, loss, dl);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -911,15 +1063,15 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
   if (dx) {
     int maxkw = 0;
     for (int r = 0; r < g.n; ++r) maxkw = std::max(maxkw, g.kw[r]);
-    fc_bwd_dx<<<dim3(g.n * PW, cdiv((int64_t)g.Bp * (maxkw / 4), 256)), 256, 0, s>>>(dl, wg, dx, g, B, O, PW);
+    fc_bwd_dx<<<dim3(g.n * PW, cdiv(g.Bp, 32), cdiv(maxkw, 256)), 256, 0, s>>>(dl, wg, dx, g, B, O, PW);
     CP_LAUNCHED();
   }
   if (dwg) {
-    fc_bwd_dw<<<grid1d((int64_t)PW * g.Cg / 4, 32), dim3(32, 4), 0, s>>>(dl, x, dwg, g, B, O, PW);
+    fc_bwd_dw<<<g.n * PW * fc_nsc(g), 256, 0, s>>>(dl, x, dwg, g, B, O, PW, fc_nsc(g));
     CP_LAUNCHED();
   }
   if (dbfc) {
-    fc_bwd_db<<<1, 32, 0, s>>>(dl, dbfc, B, O);
+    fc_bwd_db<<<1, 256, 0, s>>>(dl, dbfc, B, O);
     CP_LAUNCHED();
   }
   (void)ws;

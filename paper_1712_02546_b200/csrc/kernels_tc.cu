@@ -46,7 +46,8 @@ constexpr int MAX_SCHED = 1024;               // units in an explicit per-group 
 template <int CG, int PASS>
 struct Cfg {
   static constexpr int B_BYTES = CG == 1 ? BN * BK * 4 : (BN / 2) * BK * 4;
-  static constexpr int POOL = PASS == 0 ? EPI_GROUPS * POOL_BYTES : 0;   // pooling exchange (forward only)
+  // forward: pooling exchange; dgrad: per-warp transpose for full-line (NVLink) peer stores
+  static constexpr int POOL = PASS != 2 ? EPI_GROUPS * POOL_BYTES : 0;
   static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + POOL + 256;
@@ -89,6 +90,13 @@ struct TcParams {
   const float* bias;
   float* out;          // fwd: y block ; dgrad: dx (full gather) ; wgrad: dW or split partials
   uint8_t* saved;
+  float* peer_out[CP_MAX_RANKS];  // fwd with fused AllGather: the own block inside each peer's buffer
+  int npeers;
+  float* dst[CP_MAX_RANKS];  // dgrad with fused reduce-scatter: base of input block rb's partial (own
+  int fused_dx;              // receive slot, or this rank's slot in peer rb's receive area over NVLink)
+  const uint32_t* arrive;  // fwd over a symmetric gathered input: per-sender arrival flags (else null);
+  int self_blk;            // the own input block (ready at launch) is consumed first, a peer's block
+                           // only after its flag is set - the gather overlaps this GEMM
 };
 
 struct Unit {
@@ -204,6 +212,16 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     const int per = t.tail ? p.tail_per : (total + p.split - 1) / p.split;
     const int lo = (t.tail ? t.piece : t.sp) * per, hi = min(total, lo + per);
     int idx = 0;
+    if (p.arrive) {
+      // overlapped gather: input blocks outermost, starting with the own block
+      for (int bi = 0, rb = p.self_blk; bi < p.nblk; ++bi, rb = rb + 1 == p.nblk ? 0 : rb + 1) {
+        const int kw = p.kw[rb];
+        for (int tap = 0; tap < p.R * p.S; ++tap)
+          for (int c = 0; c * BK < kw; ++c, ++idx)
+            if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8});
+      }
+      return;
+    }
     for (int tap = 0; tap < p.R * p.S; ++tap)
       for (int rb = 0; rb < p.nblk; ++rb) {
         const int kw = p.kw[rb];
@@ -299,6 +317,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t arrived = PASS == PASS_FWD && p.arrive ? 1u << p.self_blk : ~0u;  // input blocks known present
       for (int k = 0;; ++k) {
         const int u = unit_at(p, group, ngroups, k);
         if (u < 0) break;
@@ -329,6 +348,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             else tma_load_5d(d, m, &full[stage], c0, c1, c2, c3, c4);
           };
           if (PASS == PASS_FWD) {
+            if (!((arrived >> ch.rb) & 1u)) {
+              wait_flag_sys(p.arrive + ch.rb);
+              asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written data -> TMA reads
+              arrived |= 1u << ch.rb;
+            }
             const int r = ch.tap / p.S, s = ch.tap % p.S;
             if (p.unified)
               ld5(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
@@ -429,12 +453,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       if (u < 0) break;
       const Unit t = decode_unit<PASS, CG>(p, u, rank);
       const int acc = local & 1;
+      const int nchunk = (t.n + 31) / 32;
+      // forward bias of this unit's chunks (one column per lane), loaded before the accumulator wait
+      // so the load latency overlaps it instead of stalling every chunk
+      float bias_l[BN / 32];
+      if (PASS == PASS_FWD) {
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j) {
+          const int col = t.n0 + (grp + j * p.epi_groups) * 32 + lane;
+          bias_l[j] = (p.bias && !t.tail && p.split == 1 && grp + j * p.epi_groups < nchunk && col < p.Kr)
+                          ? __ldg(p.bias + col) : 0.f;
+        }
+      }
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      const int nchunk = (t.n + 31) / 32;
       if (grp >= p.epi_groups) break;
-      for (int cc = grp; cc < nchunk; cc += p.epi_groups) {
+      for (int cc = grp, jb = 0; cc < nchunk; cc += p.epi_groups, ++jb) {
         float v[32];
         tmem_ld_32x32b_x32(tbase + cc * 32, v);
         const int ncol = min(32, t.n - cc * 32);
@@ -451,8 +486,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           store_f32x32(p.out + o, v, ncol);
         } else if (PASS == PASS_FWD) {
           const int nbase = t.n0 + cc * 32;  // own slot index of column 0
-          // bias: one load per lane, broadcast by shuffle
-          const float bl = (p.bias && nbase + lane < p.Kr) ? __ldg(p.bias + nbase + lane) : 0.f;
+          // bias: one column per lane (preloaded), broadcast by shuffle
+          float bl = 0.f;
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j)
+            if (j == jb) bl = bias_l[j];
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
             float x = v[q] + __shfl_sync(0xffffffffu, bl, q);
@@ -465,47 +503,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 #pragma unroll
             for (int q = 0; q < 32; ++q) mine[q] = v[q];
             asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+            // write mapping: 8 threads per image row, 4 columns each - every warp store instruction
+            // writes 4 full 128 B lines (NVLink peer stores are full-line packets, not masked pieces).
+            // Scalar smem reads stay conflict-free: bank = (b + c4 + q) mod 32 covers all 32 banks.
             const int et = quad * 32 + lane;  // 0..127 within the group
-            const int b = et >> 2, cb = (et & 3) * 8;
-            const int bb = t.bc * 32 + b;
-            float best[8];
-            uint32_t code[8];
+            const int c4 = (et & 7) * 4;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              best[q] = pool_buf[(0 * 32 + b) * POOL_LD + cb + q];
-              code[q] = 0;
-            }
+            for (int h = 0; h < 2; ++h) {
+              const int b = h * 16 + (et >> 3);
+              const int bb = t.bc * 32 + b;
+              float best[4];
+              uint32_t code[4];
 #pragma unroll
-            for (int w4 = 1; w4 < 4; ++w4)
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const float x = pool_buf[(w4 * 32 + b) * POOL_LD + cb + q];
-                if (x > best[q]) {
-                  best[q] = x;
-                  code[q] = w4;
-                }
+              for (int q = 0; q < 4; ++q) {
+                best[q] = pool_buf[(0 * 32 + b) * POOL_LD + c4 + q];
+                code[q] = 0;
               }
-            const int64_t o = ((int64_t)(t.i * p.Wp + t.j) * p.Bp + bb) * p.Kc + nbase + cb;
-            const bool real_b = bb < p.B;
-            float ov[8];
-            uint32_t lo = 0, hi = 0;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const bool ok = real_b && (nbase + cb + q) < p.Kr;
-              ov[q] = ok ? tf32_rna(best[q]) : 0.f;
-              const uint32_t cq = ok ? code[q] : 0u;
-              if (q < 4) lo |= cq << (8 * q);
-              else hi |= cq << (8 * (q - 4));
-            }
-            if (cb < ncol) {
-              if (cb + 8 <= ncol) {
-                reinterpret_cast<float4*>(p.out + o)[0] = make_float4(ov[0], ov[1], ov[2], ov[3]);
-                reinterpret_cast<float4*>(p.out + o)[1] = make_float4(ov[4], ov[5], ov[6], ov[7]);
-                *reinterpret_cast<uint2*>(p.saved + o) = make_uint2(lo, hi);
+              for (int w4 = 1; w4 < 4; ++w4)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float x = pool_buf[(w4 * 32 + b) * POOL_LD + c4 + q];
+                  if (x > best[q]) {
+                    best[q] = x;
+                    code[q] = w4;
+                  }
+                }
+              const int64_t o = ((int64_t)(t.i * p.Wp + t.j) * p.Bp + bb) * p.Kc + nbase + c4;
+              const bool real_b = bb < p.B;
+              float ov[4];
+              uint32_t packed = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const bool ok = real_b && (nbase + c4 + q) < p.Kr;
+                ov[q] = ok ? tf32_rna(best[q]) : 0.f;
+                packed |= (ok ? code[q] : 0u) << (8 * q);
+              }
+              if (c4 + 4 <= ncol) {
+                const float4 o4 = make_float4(ov[0], ov[1], ov[2], ov[3]);
+                *reinterpret_cast<float4*>(p.out + o) = o4;
+                *reinterpret_cast<uint32_t*>(p.saved + o) = packed;
+                // fused channel AllGather: the same pooled values straight into every peer's copy of
+                // the gathered output over NVLink (same offset: the gather layout is identical on all ranks)
+                for (int k = 0; k < p.npeers; ++k) *reinterpret_cast<float4*>(p.peer_out[k] + o) = o4;
               } else {
-                for (int q = 0; q < 8 && cb + q < ncol; ++q) {
+                for (int q = 0; q < 4 && c4 + q < ncol; ++q) {
                   p.out[o + q] = ov[q];
-                  p.saved[o + q] = (uint8_t)(q < 4 ? (lo >> (8 * q)) : (hi >> (8 * (q - 4))));
+                  p.saved[o + q] = (uint8_t)(packed >> (8 * q));
+                  for (int k = 0; k < p.npeers; ++k) p.peer_out[k][o + q] = ov[q];
                 }
               }
             }
@@ -518,6 +563,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 #pragma unroll
             for (int q = 0; q < 32; ++q) v[q] = (real_b && nbase + q < p.Kr) ? tf32_rna(v[q]) : 0.f;
             store_f32x32(p.out + o, v, ncol);
+            for (int k = 0; k < p.npeers; ++k) store_f32x32(p.peer_out[k] + o, v, ncol);
           }
         } else if (PASS == PASS_DGRAD) {
           const int dh = quad >> 1, dw = quad & 1;
@@ -528,7 +574,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             while (rb + 1 < p.nblk && slot >= p.coff[rb + 1]) ++rb;
             slot -= p.coff[rb];
           }
-          if (!p.span || slot < p.kw[rb]) {
+          if (p.fused_dx) {
+            // fused reduce-scatter: the partial goes to block rb's owner (own slot locally, a peer's
+            // over NVLink).  Warp-local transpose through shared memory so that every store
+            // instruction writes 4 full 128 B rows (8 lanes x float4 each) instead of 32 pieces.
+            float* tb = pool_buf + (quad & 3) * 32 * POOL_LD;   // this warp's 32 x 33 tile
+#pragma unroll
+            for (int q = 0; q < 32; ++q) tb[lane * POOL_LD + q] = v[q];
+            __syncwarp();
+            const bool chunk_ok = !p.span || slot < p.kw[rb];
+            if (chunk_ok) {
+              const int kw = p.kw[rb];
+              const int c4 = (lane & 7) * 4;
+              float* base = p.dst[rb] + ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + t.bc * 32) * kw + slot;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int row = k * 4 + (lane >> 3);
+                float4 o4;
+                o4.x = tb[row * POOL_LD + c4 + 0];
+                o4.y = tb[row * POOL_LD + c4 + 1];
+                o4.z = tb[row * POOL_LD + c4 + 2];
+                o4.w = tb[row * POOL_LD + c4 + 3];
+                float* d = base + (int64_t)row * kw + c4;
+                if (c4 + 4 <= ncol) {
+                  *reinterpret_cast<float4*>(d) = o4;
+                } else if (c4 < ncol) {
+                  const float e[4] = {o4.x, o4.y, o4.z, o4.w};
+                  for (int q = 0; q < ncol - c4; ++q) d[q] = e[q];
+                }
+              }
+            }
+            __syncwarp();
+          } else if (!p.span || slot < p.kw[rb]) {
             const int kw = p.kw[rb];
             const int64_t o = (int64_t)t.sp * p.part_stride + p.start[rb] +
                               ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb) * kw + slot;
@@ -550,6 +627,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         else mbar_arrive(&tempty[acc]);
       }
     }
+    if (PASS == PASS_FWD && p.npeers > 0) __threadfence_system();  // peer stores performed before exit
   }
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
@@ -574,17 +652,24 @@ __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restri
   const int c = threadIdx.x;  // 256 columns
   const int kk = ti.kk0[tu] + rank * BM + row;
   if (kk >= ti.Kr || c >= ti.ncol[tu]) return;
-  float acc = 0.f;
-  for (int pc = 0; pc < ti.st; ++pc)
-    acc += buf[((((int64_t)tu * ti.st + pc) * ti.cg + rank) * BM + row) * BN + c];
-  dw[(int64_t)kk * ti.Ktot + ti.col0[tu] + c] = acc;
+  // four independent accumulators (pieces pc = k mod 4) keep several loads in flight; fixed order
+  const float* src = buf + (((int64_t)tu * ti.st * ti.cg + rank) * BM + row) * BN + c;
+  const int64_t step = (int64_t)ti.cg * BM * BN;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  int pc = 0;
+  for (; pc + 4 <= ti.st; pc += 4)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] += src[(pc + k) * step];
+  for (; pc < ti.st; ++pc) a[pc & 3] += src[pc * step];
+  dw[(int64_t)kk * ti.Ktot + ti.col0[tu] + c] = (a[0] + a[1]) + (a[2] + a[3]);
 }
 
 // forward tail: the tile's pre-pool accumulator = sum over pieces (in order) of the partial tiles;
 // then bias, ReLU, 2x2 max-pool (rows q*32+b of a CTA's tile are window position q, image b),
 // argmax code and RN-tf32 rounding, exactly as the fused epilogue.
 struct FwdTailInfo {
-  int n, st, cg, Wo, Wp, Bp, B, Kr, Kc, relu, pool;
+  int n, st, cg, Wo, Wp, Bp, B, Kr, Kc, relu, pool, npeers;
+  float* peer[CP_MAX_RANKS];  // fused AllGather: own block inside each peer's buffer
   int i[MAX_TAIL], j[MAX_TAIL], bc0[MAX_TAIL], n0[MAX_TAIL], ncol[MAX_TAIL];
 };
 __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __restrict__ bias, float* __restrict__ y,
@@ -598,11 +683,15 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
   const float bs = (bias && n < ti.Kr) ? bias[n] : 0.f;
   float best = 0.f;
   int code = 0;
+  const int64_t step = (int64_t)ti.cg * BM * BN;
+  float zq[4] = {0.f, 0.f, 0.f, 0.f};   // the four window positions: independent load streams
+  for (int pc = 0; pc < ti.st; ++pc) {
+    const float* src = buf + (((int64_t)tu * ti.st + pc) * ti.cg + rank) * BM * BN + (int64_t)b * BN + c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) zq[q] += src[q * 32 * BN];
+  }
   for (int q = 0; q < 4; ++q) {
-    float z = 0.f;
-    for (int pc = 0; pc < ti.st; ++pc)
-      z += buf[((((int64_t)tu * ti.st + pc) * ti.cg + rank) * BM + q * 32 + b) * BN + c];
-    z += bs;
+    float z = zq[q] + bs;
     if (ti.relu && !(z > 0.f)) z = 0.f;
     if (ti.pool) {
       if (q == 0 || z > best) {
@@ -612,41 +701,63 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
     } else {
       const int64_t o = ((int64_t)((2 * ti.i[tu] + (q >> 1)) * ti.Wo + 2 * ti.j[tu] + (q & 1)) * ti.Bp + bb) * ti.Kc + n;
       y[o] = ok ? tf32_rna(z) : 0.f;
+      for (int k = 0; k < ti.npeers; ++k) ti.peer[k][o] = ok ? tf32_rna(z) : 0.f;
     }
   }
   if (ti.pool) {
     const int64_t o = ((int64_t)(ti.i[tu] * ti.Wp + ti.j[tu]) * ti.Bp + bb) * ti.Kc + n;
     y[o] = ok ? tf32_rna(best) : 0.f;
     saved[o] = ok ? (uint8_t)code : 0;
+    for (int k = 0; k < ti.npeers; ++k) ti.peer[k][o] = ok ? tf32_rna(best) : 0.f;
   }
+  if (ti.npeers) __threadfence_system();
 }
 
 // deterministic split-K reduction: dW[i] = sum_s part[s][i] in split order
-__global__ void splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ out, int64_t n, int S) {
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (i >= n) return;
-  if (i + 3 < n) {
-    float4 acc = *reinterpret_cast<const float4*>(part + i);
-    for (int s = 1; s < S; ++s) {
-      const float4 x = *reinterpret_cast<const float4*>(part + (int64_t)s * n + i);
+// out = sum_s part[s] (split-K partials).  Block (32 float4, 8 split lanes): lane y adds splits
+// y*per .. in ascending order, the 8 lane sums combine in fixed order (deterministic).  n % 4 == 0.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ out,
+                                                            int64_t n, int S) {
+  __shared__ float4 red[8][32];
+  const int64_t i4 = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int per = (S + 7) / 8;
+  const int s0 = threadIdx.y * per, s1 = min(S, s0 + per);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i4 * 4 < n)
+    for (int s = s0; s < s1; ++s) {
+      const float4 x = reinterpret_cast<const float4*>(part + (int64_t)s * n)[i4];
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
     }
-    *reinterpret_cast<float4*>(out + i) = acc;
-  } else {
-    for (int64_t j = i; j < n; ++j) {
-      float acc = part[j];
-      for (int s = 1; s < S; ++s) acc += part[(int64_t)s * n + j];
-      out[j] = acc;
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && i4 * 4 < n) {
+    float4 t = red[0][threadIdx.x];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+      const float4 u = red[k][threadIdx.x];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
     }
+    reinterpret_cast<float4*>(out)[i4] = t;
   }
+}
+static int launch_splitk_reduce(const float* part, float* out, int64_t n, int S, cudaStream_t s) {
+  if (n % 4) CP_FAIL(CP_ERR_UNSUPPORTED, "split-K reduce: size not a multiple of 4");
+  splitk_reduce_kernel<<<(unsigned)((n / 4 + 31) / 32), dim3(32, 8), 0, s>>>(part, out, n, S);
+  CP_LAUNCHED();
+  return CP_OK;
 }
 
 // forward split-K finish: z = sum_s part[s] + bias, then ReLU, 2x2 max-pool (first max wins),
 // argmax code and RN-tf32 rounding, exactly as the fused epilogue does.
 // One thread per (pooled position, image, 4 slots).
+struct PeerSet {
+  float* p[CP_MAX_RANKS];
+  int n;
+};
 __global__ void splitk_fwd_finish(const float* __restrict__ part, int S, long long stride,
                                   const float* __restrict__ bias, float* __restrict__ y, uint8_t* __restrict__ saved,
-                                  int Wo, int Wp, int Bp, int B, int Kr, int Kc, long long total4, int relu, int pool) {
+                                  int Wo, int Wp, int Bp, int B, int Kr, int Kc, long long total4, int relu, int pool,
+                                  PeerSet peers) {
   const long long e4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e4 >= total4) return;
   const int kc4 = Kc >> 2;
@@ -692,6 +803,9 @@ __global__ void splitk_fwd_finish(const float* __restrict__ part, int S, long lo
     packed |= (ok ? code[t] : 0u) << (8 * t);
   }
   *reinterpret_cast<float4*>(y + rest * Kc + slot) = make_float4(o[0], o[1], o[2], o[3]);
+  for (int k = 0; k < peers.n; ++k)
+    *reinterpret_cast<float4*>(peers.p[k] + rest * Kc + slot) = make_float4(o[0], o[1], o[2], o[3]);
+  if (peers.n) __threadfence_system();
   if (pool) *reinterpret_cast<uint32_t*>(saved + rest * Kc + slot) = packed;
 }
 
@@ -1058,7 +1172,7 @@ size_t tc_workspace_bytes(const Layer& L) {
 }
 
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
-           cudaStream_t s) {
+           cudaStream_t s, float* const* peer_blocks, int npeers, const uint32_t* arrive) {
   if (L.Kc == 0) return CP_OK;
   if ((L.Ho & 1) || (L.Wo & 1))
     CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 forward needs an even conv output grid (2x2 window tiles)");
@@ -1095,6 +1209,10 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   p.max_chunks = (pl.chunks + pl.S - 1) / pl.S;
   p.bias = L.d.bias ? b : nullptr;
   p.saved = saved;
+  p.npeers = npeers;
+  for (int k = 0; k < npeers; ++k) p.peer_out[k] = peer_blocks[k];
+  p.arrive = L.images ? nullptr : arrive;
+  p.self_blk = L.d.rank;
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = (long long)L.Ho * L.Wo * L.Bp * L.Kc;
   p.out = pl.S > 1 ? part : y_block;
@@ -1116,6 +1234,8 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
       p.tail_buf = part;
       ti.n = T; ti.st = st; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B;
       ti.Kr = L.Kr; ti.Kc = L.Kc; ti.relu = L.d.relu; ti.pool = L.d.pool;
+      ti.npeers = npeers;
+      for (int k = 0; k < npeers; ++k) ti.peer[k] = peer_blocks[k];
       const int nbcg = L.Bp / 32 / CG, W2 = L.Wo / 2;
       for (int k = 0; k < T; ++k) {                    // host mirror of decode_unit<FWD>
         const int u = p.tail_full + k;
@@ -1136,16 +1256,19 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     CP_LAUNCHED();
   }
   if (pl.S > 1) {
+    PeerSet ps{};
+    ps.n = npeers;
+    for (int k = 0; k < npeers; ++k) ps.p[k] = peer_blocks[k];
     const long long total4 = (long long)L.Hp * L.Wp * L.Bp * (L.Kc / 4);
     splitk_fwd_finish<<<(unsigned)((total4 + 255) / 256), 256, 0, s>>>(
         part, pl.S, p.part_stride, L.d.bias ? b : nullptr, y_block, saved, L.Wo, L.Wp, L.Bp, L.B, L.Kr, L.Kc, total4,
-        L.d.relu, L.d.pool);
+        L.d.relu, L.d.pool, ps);
     CP_LAUNCHED();
   }
   return CP_OK;
 }
 
-int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s) {
+int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s, float* const* dst_blocks) {
   if (L.images) CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad onto images");
   if ((L.H & 1) || (L.W & 1)) CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad needs an even input grid");
   if (L.Kc == 0 || L.Kr == 0) {
@@ -1154,8 +1277,13 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   }
   TcParams p{};
   fill_common(p, L);
-  const Plan pl = dgrad_plan(L, p);
+  Plan pl = dgrad_plan(L, p);
   if (pl.numN < 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many dgrad N tiles");
+  if (dst_blocks) {   // fused reduce-scatter: every partial tile is final (no split-K partials)
+    pl.S = 1;
+    p.fused_dx = 1;
+    for (int r = 0; r < L.in.n; ++r) p.dst[r] = dst_blocks[r];
+  }
   CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false));
   p.wide = 1;
   for (int r = 0; r < L.in.n; ++r)
@@ -1240,8 +1368,7 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   CP_TRY((pl.pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s)));
   if (pl.S > 1) {
     const int64_t n = L.in.start[L.in.n];
-    splitk_reduce_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, s>>>(part, dx, n, pl.S);
-    CP_LAUNCHED();
+    CP_TRY(launch_splitk_reduce(part, dx, n, pl.S, s));
   }
   return CP_OK;
 }
@@ -1315,8 +1442,7 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   }
   if (w.S > 1) {
     const int64_t n = (int64_t)L.Kr * L.Ktot;
-    splitk_reduce_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, s>>>(part, dw, n, w.S);
-    CP_LAUNCHED();
+    CP_TRY(launch_splitk_reduce(part, dw, n, w.S, s));
   }
   return CP_OK;
 }

@@ -90,7 +90,7 @@ static int derive(Layer& L, const cp_conv_desc& d) {
   L.off_xcol = off; L.ws_xcol = L.images ? al256((size_t)L.Ho * L.Wo * L.Bp * L.Kcol * 4) : 0; off += L.ws_xcol;
   L.off_z = off; L.ws_z = d.math == CP_MATH_FP32_SIMT ? al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 4) : 0; off += L.ws_z;
   L.off_dy = off; L.ws_dy = al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 4); off += L.ws_dy;
-  L.off_dbpart = off; L.ws_dbpart = al256((size_t)64 * std::max(L.Kc, 8) * 4); off += L.ws_dbpart;
+  L.off_dbpart = off; L.ws_dbpart = al256((size_t)kBiasSplitMax * std::max(L.Kc, 8) * 4); off += L.ws_dbpart;
   L.off_split = off; L.ws_split = d.math == CP_MATH_TF32 ? al256(tc_workspace_bytes(L)) : 0; off += L.ws_split;
   L.ws_total = off + 256;
   L.dy_ready = 0;
@@ -103,7 +103,8 @@ static char* WS(void* ws, size_t off) { return (char*)ws + off; }
 static int ensure_dy(Layer& L, const float* dy_g, const uint8_t* saved, const float* y_g, void* ws, cudaStream_t s) {
   if (L.dy_ready && L.dy_key[0] == dy_g && L.dy_key[1] == saved && L.dy_key[2] == y_g) return CP_OK;
   const int64_t o = L.out.start[L.d.rank];
-  CP_TRY(launch_unpool(L, dy_g + o, saved, y_g + o, (float*)WS(ws, L.off_dy), L.d.math == CP_MATH_TF32, s));
+  CP_TRY(launch_unpool(L, dy_g + o, saved, y_g + o, (float*)WS(ws, L.off_dy), (float*)WS(ws, L.off_dbpart),
+                       L.d.math == CP_MATH_TF32, s));
   L.dy_ready = 1;
   L.dy_key[0] = dy_g; L.dy_key[1] = saved; L.dy_key[2] = y_g;
   return CP_OK;
@@ -169,6 +170,12 @@ int conv_part_query(cp_layer L, cp_sizes* o) {
   o->saved = L->d.pool ? (size_t)L->Hp * L->Wp * L->Bp * L->Kc : 0;
   o->dx = o->x;
   o->workspace = L->ws_total;
+  o->dx_peer = 0;
+  if (!L->images) {
+    int64_t mb = 0;
+    for (int r = 0; r < L->in.n; ++r) mb = std::max(mb, L->in.start[r + 1] - L->in.start[r]);
+    o->dx_peer = (size_t)(L->in.start[L->in.n] + (int64_t)L->in.n * mb) * 4 + 256;
+  }
   return CP_OK;
 }
 
@@ -196,16 +203,54 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
     CP_TRY(launch_im2col(*L, x, xcol, tf32, s));
     xin = xcol;
   }
+  // Fused channel AllGather (B200 path).  Producer side: when y_gathered is a
+  // symmetric buffer (cp_symmetric_alloc) the forward epilogue stores this rank's pooled block into
+  // every peer's copy over NVLink, then a one-thread kernel sets this rank's arrival flag in every
+  // peer's flag array.  Consumer side: when the input x is a symmetric gathered buffer, the forward
+  // GEMM consumes its own block first and each peer block only after that peer's flag is set (the
+  // gather overlaps the GEMM), then resets the flags.  No separate AllGather kernel, no NCCL call
+  // except a one-word AllReduce guarding the buffer against overwrite while a peer still reads it.
+  void* peers[CP_MAX_RANKS];
+  uint32_t* pflags[CP_MAX_RANKS];
+  float* peer_blocks[CP_MAX_RANKS];
+  uint32_t* signal[CP_MAX_RANKS];
+  int npeers = 0;
+  const bool gathered_out = L->comm && L->d.world > 1 && !L->d.local_output;
+  const bool sym_out = gathered_out && comm_symmetric_peers(L->comm, y, peers, pflags);
+  if (sym_out) {
+    for (int r = 0; r < L->d.world; ++r)
+      if (r != L->d.rank) {
+        signal[npeers] = pflags[r];
+        peer_blocks[npeers++] = (float*)peers[r] + L->out.start[L->d.rank];
+      }
+    // WAR guard: a peer may still be reading its copy of y (e.g. the next layer's async wgrad of the
+    // previous step) - nobody writes into a peer's buffer before every rank has reached this point.
+    CP_TRY(comm_barrier(L->comm, s));
+  }
+  void* ipeers[CP_MAX_RANKS];
+  uint32_t* iflags[CP_MAX_RANKS];
+  const bool sym_in = !L->images && L->comm && L->d.world > 1 && comm_symmetric_peers(L->comm, x, ipeers, iflags);
+  const uint32_t* arrive = sym_in ? iflags[L->d.rank] : nullptr;
+  if (sym_in && !tf32) CP_TRY(launch_wait_flags(arrive, L->d.world, L->d.rank, s));
   if (L->Kr > 0 || L->Kc > 0) {
     if (tf32) {
-      CP_TRY(tc_fwd(*L, xin, w, b, yb, saved, ws, s));
+      CP_TRY(tc_fwd(*L, xin, w, b, yb, saved, ws, s, sym_out ? peer_blocks : nullptr, sym_out && tf32 ? npeers : 0,
+                    arrive));
     } else {
       float* z = (float*)WS(ws, L->off_z);
       CP_TRY(launch_fwd_simt(*L, x, xin, w, b, z, s));
       CP_TRY(launch_relu_pool(*L, z, yb, saved, false, s));
     }
+  } else if (sym_in && tf32) {
+    CP_TRY(launch_wait_flags(arrive, L->d.world, L->d.rank, s));   // no GEMM to wait inside
   }
-  if (L->comm && L->d.world > 1 && !L->d.local_output) {
+  if (sym_in) CP_CUDA(cudaMemsetAsync((void*)arrive, 0, CP_MAX_RANKS * sizeof(uint32_t), s));
+  if (sym_out) {
+    if (!tf32) {   // SIMT reference path: plain NCCL gather into the symmetric buffer, then signal
+      CP_TRY(comm_allgather_blocks(L->comm, y, L->out, s));
+    }
+    CP_TRY(launch_signal_peers(signal, npeers, L->d.rank, s));
+  } else if (gathered_out) {
     CP_TRY(fork_comm(*L, s, cs));
     CP_TRY(comm_allgather_blocks(L->comm, y, L->out, cs));
     CP_TRY(join_comm(*L, s, cs));
@@ -218,13 +263,51 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
   if (!L || !dy_g || !y_g || !w || !dx || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_backward_data: null pointer");
   if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_data: pooling needs saved");
   const bool async = (dx_mode & CP_DX_ASYNC) != 0;
-  dx_mode &= ~CP_DX_ASYNC;
+  const bool ordered = (dx_mode & CP_DX_ORDERED) != 0;
+  dx_mode &= ~(CP_DX_ASYNC | CP_DX_ORDERED);
   if (dx_mode < CP_DX_ALLREDUCE || dx_mode > CP_DX_LOCAL) CP_FAIL(CP_ERR_ARG, "bad dx_mode");
   if (L->images && dx_mode == CP_DX_REDUCE_SCATTER)
     CP_FAIL(CP_ERR_UNSUPPORTED, "reduce-scatter of dX needs a gather-layout input (images use all-reduce)");
   cudaStream_t s = (cudaStream_t)stream, cs = comm_stream ? (cudaStream_t)comm_stream : s;
   CP_TRY(ensure_dy(*L, dy_g, saved, y_g, ws, s));
   const float* dY = (const float*)WS(ws, L->off_dy);
+  // Fused reduce-scatter (B200 path): dx symmetric with receive slots behind the
+  // gather layout; the dgrad epilogue stores block q's partial into rank q's slot [this rank].
+  void* peers[CP_MAX_RANKS];
+  uint32_t* pflags[CP_MAX_RANKS];
+  const bool fused = L->d.math == CP_MATH_TF32 && !L->images && L->comm && L->d.world > 1 &&
+                     dx_mode == CP_DX_REDUCE_SCATTER && comm_symmetric_peers(L->comm, dx, peers, pflags);
+  if (fused) {
+    int64_t mb = 0;
+    for (int r = 0; r < L->in.n; ++r) mb = std::max(mb, L->in.start[r + 1] - L->in.start[r]);
+    const int64_t slots0 = L->in.start[L->in.n];   // receive slots follow the gather layout
+    const int me = L->d.rank;
+    float* dst[CP_MAX_RANKS];
+    uint32_t* signal[CP_MAX_RANKS];
+    int ns = 0;
+    for (int q = 0; q < L->in.n; ++q) {
+      dst[q] = (float*)peers[q] + slots0 + (int64_t)me * mb;
+      if (q != me) signal[ns++] = pflags[q];
+    }
+    if (!ordered) CP_TRY(comm_barrier(L->comm, s));   // no rank still sums last call's slots
+    if (L->Kr > 0 && L->Kc > 0) {
+      CP_TRY(tc_dgrad(*L, dY, w, dx, ws, s, dst));
+    } else {   // no own kernels: a zero partial for every block (peers still expect the signal)
+      for (int q = 0; q < L->in.n; ++q) CP_TRY(launch_fill(dst[q], 0.f, L->in.start[q + 1] - L->in.start[q], s));
+    }
+    CP_TRY(launch_signal_peers(signal, ns, me, s));
+    CP_TRY(fork_comm(*L, s, cs));
+    CP_TRY(launch_wait_flags(pflags[me], L->d.world, me, cs));
+    CP_TRY(launch_sum_slots(dx + slots0, mb, L->d.world, dx + L->in.start[me],
+                            L->in.start[me + 1] - L->in.start[me], cs));
+    CP_CUDA(cudaMemsetAsync(pflags[me], 0, CP_MAX_RANKS * sizeof(uint32_t), cs));
+    if (async && cs != s) {
+      CP_CUDA(cudaEventRecord(L->ev_comm, cs));
+    } else {
+      CP_TRY(join_comm(*L, s, cs));
+    }
+    return CP_OK;
+  }
   if (L->d.math == CP_MATH_TF32 && !L->images) {
     CP_TRY(tc_dgrad(*L, dY, w, dx, ws, s));
   } else {
@@ -256,8 +339,7 @@ int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* save
   if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: pooling needs saved");
   cudaStream_t s = (cudaStream_t)stream;
   CP_TRY(ensure_dy(*L, dy_g, saved, y_g, ws, s));
-  const int64_t o = L->out.start[L->d.rank];
-  if (db && L->Kr > 0) CP_TRY(launch_bias_grad(*L, dy_g + o, y_g + o, db, (float*)WS(ws, L->off_dbpart), s));
+  if (db && L->Kr > 0) CP_TRY(launch_bias_grad(*L, db, (const float*)WS(ws, L->off_dbpart), s));
   if (L->Kr == 0) return CP_OK;
   const float* dY = (const float*)WS(ws, L->off_dy);
   const float* xcol = L->images ? (const float*)WS(ws, L->off_xcol) : nullptr;

@@ -34,17 +34,23 @@ class PartitionedNet:
     """
 
     def __init__(self, kernels, batch, parts, rank=0, comm=None, math=cp.CP_MATH_TF32, in_c=3, in_hw=32,
-                 ksize=5, classes=10, relu=True, pool=True, bias=True, device="cuda", head="replicated"):
+                 ksize=5, classes=10, relu=True, pool=True, bias=True, device="cuda", head="replicated",
+                 fused=False):
         """head: "replicated" - the last conv output is all-gathered and every rank runs the full FC
         head (the paper's master-side head, replicated); "partitioned" - the last conv output stays
         rank-local, each rank owns the FC columns of its channels, partial logits are summed with
-        one AllReduce (identical logits/loss on every rank; no AllGather of the last layer)."""
+        one AllReduce (identical logits/loss on every rank; no AllGather of the last layer).
+        fused: B200 collective fusion - every all-gathered conv output and every dX is a
+        symmetric (peer-mapped) buffer: the TF32 forward epilogue stores its output block into all ranks'
+        copies over NVLink (the next layer's GEMM consumes its own block first and each peer block when
+        its arrival flag is set) and the dgrad epilogue stores each input block's partial dX into its
+        owner's receive slot (reduce-scatter without an NCCL kernel)."""
         self.device = torch.device(device)
         self.head_mode = head if parts[0].n_ranks > 1 else "replicated"
         self.B, self.Bp, self.O = batch, (batch + 31) // 32 * 32, classes
         self.rank, self.world = rank, parts[0].n_ranks
         self.parts, self.comm, self.math = parts, comm, math
-        self.layers, self.descs, self.sizes, self.buf = [], [], [], []
+        self.layers, self.descs, self.sizes, self.buf, self.sym = [], [], [], [], []
         c, h, prev = in_c, in_hw, None
         for i, K in enumerate(kernels):
             d = cp.cp_conv_desc()
@@ -66,11 +72,12 @@ class PartitionedNet:
             b = {
                 "w": _f32(sz.w, self.device), "b": _f32(sz.b, self.device),
                 "dw": _f32(sz.w, self.device), "db": _f32(sz.b, self.device),
-                "y": _f32(sz.y, self.device), "saved": _dev_bytes(sz.saved, self.device),
+                "y": self._symmetric(sz.y, fused and not d.local_output),
+                "saved": _dev_bytes(sz.saved, self.device),
                 "ws": _dev_bytes(sz.workspace, self.device),
             }
             if prev is not None:
-                b["dx"] = _f32(sz.dx, self.device)
+                b["dx"] = self._symmetric(sz.dx_peer, fused) if fused else _f32(sz.dx, self.device)
             self.buf.append(b)
             ho = h - ksize + 1
             h = ho // 2 if pool else ho
@@ -104,6 +111,13 @@ class PartitionedNet:
         self.x = torch.zeros(batch * in_c * in_hw * in_hw, device=self.device)
         self.labels = torch.zeros(batch, dtype=torch.int32, device=self.device)
         self.in_shape = (batch, in_c, in_hw, in_hw)
+
+    def _symmetric(self, nbytes, symmetric):
+        if not (symmetric and self.world > 1 and self.comm is not None and self.math == cp.CP_MATH_TF32):
+            return _f32(nbytes, self.device)
+        buf = cp.SymmetricBuffer(self.comm, max(int(nbytes), 16), self.device)
+        self.sym.append(buf)
+        return buf.tensor
 
     # ------------------------------------------------------------ parameters
     def load_params(self, params, stream=None):
@@ -154,6 +168,8 @@ class PartitionedNet:
             cp.conv_part_forward(L, inp, b["w"], b["b"], b["y"], b["saved"], b["ws"], stream, comm_stream)
             inp = b["y"]
         hd = self.head
+        if self.sym and self.sym[-1].tensor.data_ptr() == self.buf[-1]["y"].data_ptr():
+            self.sym[-1].wait(stream)   # replicated head reads the gathered last output
         bias = hd["bfc"] if (self.head_mode == "replicated" or self.rank == 0) else None
         cp.cp_fc_forward(self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], bias, self.O, hd["logits"],
                          hd["ws"], stream)
@@ -171,7 +187,9 @@ class PartitionedNet:
             L, b = self.layers[i], self.buf[i]
             xin = self.x if i == 0 else self.buf[i - 1]["y"]
             if i > 0:
-                mode = dx_mode | (cp.CP_DX_ASYNC if overlap else 0)
+                # with several ranks the forward always runs a collective on every rank (gather or logits
+                # AllReduce), which orders consecutive calls of the fused reduce-scatter (CP_DX_ORDERED)
+                mode = dx_mode | (cp.CP_DX_ASYNC if overlap else 0) | (cp.CP_DX_ORDERED if self.world > 1 else 0)
                 cp.conv_part_backward_data(L, da, b["saved"], b["y"], b["w"], b["dx"], mode, b["ws"], stream,
                                            comm_stream)
             # wgrad needs no communication: it overlaps the dX reduction on the comm stream (§8(e))
@@ -199,6 +217,12 @@ class PartitionedNet:
         for L in self.layers:
             cp.conv_part_destroy(L)
         self.layers = []
+        for b in self.buf:
+            b.pop("y", None)
+        self.head_x = None
+        for s in self.sym:   # collective: every rank closes its net in the same order
+            s.free()
+        self.sym = []
 
 
 def plan_even(kernels, world):

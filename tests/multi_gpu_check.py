@@ -35,18 +35,26 @@ def main():
     dist.broadcast_object_list(uid, src=0)
     comm = cp.cp_comm_create(uid[0], rank, world)
     failures = []
-    for mode_name, dx_mode, times, head in [
-            ("even+RS", cp.CP_DX_REDUCE_SCATTER, [1.0] * world, "replicated"),
-            ("eq1+AR", cp.CP_DX_ALLREDUCE, [1.0 + 0.35 * r for r in range(world)], "replicated"),
-            ("even+RS+partitioned-head", cp.CP_DX_REDUCE_SCATTER, [1.0] * world, "partitioned"),
-            ("eq1+RS+partitioned-head", cp.CP_DX_REDUCE_SCATTER, [1.0 + 0.35 * r for r in range(world)],
-             "partitioned")]:
+    uneven = [1.0 + 0.35 * r for r in range(world)]
+    for mode_name, dx_mode, times, head, fused in [
+            ("even+RS", cp.CP_DX_REDUCE_SCATTER, [1.0] * world, "replicated", False),
+            ("eq1+AR", cp.CP_DX_ALLREDUCE, uneven, "replicated", False),
+            ("even+RS+partitioned-head", cp.CP_DX_REDUCE_SCATTER, [1.0] * world, "partitioned", False),
+            ("eq1+RS+partitioned-head", cp.CP_DX_REDUCE_SCATTER, uneven, "partitioned", False),
+            # f1: gather fused into the forward epilogue, dX reduce-scatter fused into the dgrad epilogue
+            # (peer stores over NVLink + arrival flags), even / uneven (Eq. 1) / skewed partitions
+            ("even+RS+fused", cp.CP_DX_REDUCE_SCATTER, [1.0] * world, "replicated", True),
+            ("eq1+RS+fused+partitioned-head", cp.CP_DX_REDUCE_SCATTER, uneven, "partitioned", True),
+            ("skewed+RS+fused+partitioned-head", cp.CP_DX_REDUCE_SCATTER, [1.0] + [12.0] * (world - 1),
+             "partitioned", True),
+            ("eq1+AR+fused-gather+partitioned-head", cp.CP_DX_ALLREDUCE, uneven, "partitioned", True)]:
         net = synth.NetSpec(kernels=(36, 72), in_hw=20, name="multi")
         B = 40
         parts = [cp.cp_partition_plan(times, K) for K in net.kernels]
         params = synth.params(net, seed=21, std=0.05, bias_std=0.01)
         x, y = synth.images(B, 3, 20, 20, step=3)
-        pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20, head=head)
+        pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20, head=head,
+                            fused=fused)
         pn.load_params(params)
         pn.set_batch(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
         s = torch.cuda.current_stream(dev)
@@ -139,6 +147,47 @@ def main():
             if e > 5e-3:
                 failures.append(f"{mode_name}: FC weight update rel err {e:.2e}")
         pn.close()
+
+    # Several back-to-back steps (eager, then CUDA-graph replays) with the fused collectives vs NCCL:
+    # exercises the arrival-flag resets and the overwrite guards across steps (a missed flag or an
+    # early overwrite shows up as a diverging loss).
+    net = synth.NetSpec(kernels=(36, 72), in_hw=20, name="multi")
+    B = 40
+    parts = [cp.cp_partition_plan([1.0] * world, K) for K in net.kernels]
+    params = synth.params(net, seed=22, std=0.05, bias_std=0.01)
+    s = torch.cuda.current_stream(dev)
+    cs = torch.cuda.Stream(dev)
+    curves = {}
+    for fused in (False, True):
+        pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20, head="partitioned",
+                            fused=fused)
+        pn.load_params(params)
+        seq, graph = [], None
+        for it in range(8):
+            x, y = synth.images(B, 3, 20, 20, step=10 + it)
+            pn.set_batch(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
+            if it < 4:
+                pn.step(0.05, cp.CP_DX_REDUCE_SCATTER, s, cs, True)
+            else:
+                if graph is None:
+                    torch.cuda.synchronize(dev)
+                    graph = torch.cuda.CUDAGraph()
+                    cap = torch.cuda.Stream(dev)
+                    cap.wait_stream(s)
+                    with torch.cuda.graph(graph, stream=cap):
+                        pn.step(0.05, cp.CP_DX_REDUCE_SCATTER, cap, cs, True)
+                    s.wait_stream(cap)
+                    # the capture did not execute: run the step that was just captured
+                graph.replay()
+            torch.cuda.synchronize(dev)
+            seq.append(pn.loss())
+        del graph
+        torch.cuda.synchronize(dev)
+        pn.close()
+        curves[fused] = seq
+    a, b = np.array(curves[False]), np.array(curves[True])
+    if not np.all(np.abs(a - b) <= 2e-3 * np.abs(a)):
+        failures.append(f"fused vs NCCL collectives over 8 steps: losses {b.tolist()} vs {a.tolist()}")
     cp.cp_comm_destroy(comm)
     allf = [None] * world
     dist.all_gather_object(allf, failures)
