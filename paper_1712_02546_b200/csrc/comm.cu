@@ -21,6 +21,8 @@
 // (CUDA IPC over NVLink) to all the others, so kernels can store directly into peers' copies.
 struct SymBuf {
   size_t bytes, flag_off;
+  cudaEvent_t ev;             // (unused placeholder for copy-stream joins)
+  int64_t own_off = -1, own_elems = 0;   // this rank's block (floats), recorded by its producer
   void* peers[CP_MAX_RANKS];  // peers[rank] = own pointer
 };
 
@@ -28,8 +30,17 @@ struct cp_comm_s {
   ncclComm_t comm;
   int rank, world;
   std::map<void*, SymBuf> sym;   // keyed by the local pointer
-  float* barrier_word = nullptr; // 1-float device scratch for the post-store barrier
+  float* barrier_word = nullptr; // 1-float device scratch for the teardown barrier
+  // control line (symmetric, u32 words): [0,16) barrier slots written by the peers (their epoch),
+  // [16] this rank's barrier epoch, [17] the constant 1 (source of copy-engine flag writes)
+  uint32_t* ctl = nullptr;
+  uint32_t* ctl_peer[CP_MAX_RANKS] = {};
+  // one-shot AllReduce scratch (symmetric): [parity][source rank][kArMax] floats
+  float* ar = nullptr;
+  float* ar_peer[CP_MAX_RANKS] = {};
 };
+constexpr int kCtlEpoch = 16, kCtlOne = 17, kCtlChunks = 18, kCtlArFlags = 32, kCtlArEpoch = 48, kCtlWords = 64;
+constexpr int64_t kArMax = 1 << 16;   // one-shot AllReduce capacity (floats)
 
 #define CP_NCCL(call)                                                                      \
   do {                                                                                     \
@@ -67,9 +78,28 @@ extern "C" int cp_comm_create(const uint8_t id[128], int32_t rank, int32_t world
   return CP_OK;
 }
 
+static int sym_map(cp_comm c, size_t bytes, void** local_out, SymBuf& sb);
+
 extern "C" int cp_symmetric_alloc(cp_comm c, size_t bytes, void** local_out) {
   if (!c || !local_out || bytes == 0) CP_FAIL(CP_ERR_ARG, "cp_symmetric_alloc: bad arguments");
+  if (!c->ctl) {   // first symmetric allocation (collective): the control line
+    SymBuf cb{};
+    void* p = nullptr;
+    CP_TRY(sym_map(c, kCtlWords * 4, &p, cb));
+    c->ctl = (uint32_t*)p;
+    for (int q = 0; q < c->world; ++q) c->ctl_peer[q] = (uint32_t*)cb.peers[q];
+    const uint32_t consts[2] = {1u, (uint32_t)cp::kGatherChunks};
+    CP_CUDA(cudaMemcpy(c->ctl + kCtlOne, consts, 8, cudaMemcpyHostToDevice));
+  }
   SymBuf sb{};
+  CP_TRY(sym_map(c, bytes, local_out, sb));
+  CP_CUDA(cudaEventCreateWithFlags(&sb.ev, cudaEventDisableTiming));
+  c->sym[*local_out] = sb;
+  return CP_OK;
+}
+
+// allocate + zero `bytes` (+ a 256 B flag line), exchange IPC handles, map every peer's copy
+static int sym_map(cp_comm c, size_t bytes, void** local_out, SymBuf& sb) {
   sb.bytes = bytes;
   sb.flag_off = (bytes + 255) / 256 * 256;   // arrival flags live behind the data (one 256 B line)
   void* mine = nullptr;
@@ -102,7 +132,6 @@ extern "C" int cp_symmetric_alloc(cp_comm c, size_t bytes, void** local_out) {
     CP_CUDA(cudaMalloc(&c->barrier_word, sizeof(float)));
     CP_CUDA(cudaMemset(c->barrier_word, 0, sizeof(float)));
   }
-  c->sym[mine] = sb;
   *local_out = mine;
   return CP_OK;
 }
@@ -117,6 +146,7 @@ static void sym_release(cp_comm c, void* local, SymBuf& sb) {
                              ncclSuccess)
     cudaDeviceSynchronize();
   cudaFree(local);
+  if (sb.ev) cudaEventDestroy(sb.ev);
 }
 
 extern "C" int cp_symmetric_free(cp_comm c, void* local) {
@@ -133,6 +163,16 @@ extern "C" int cp_comm_destroy(cp_comm c) {
   // every rank holds the same number of symmetric buffers, so the per-buffer barriers pair up
   for (auto& kv : c->sym) sym_release(c, kv.first, kv.second);
   c->sym.clear();
+  if (c->ar) {
+    SymBuf ab{};
+    for (int q = 0; q < c->world; ++q) ab.peers[q] = c->ar_peer[q];
+    sym_release(c, c->ar, ab);
+  }
+  if (c->ctl) {
+    SymBuf cb{};
+    for (int q = 0; q < c->world; ++q) cb.peers[q] = c->ctl_peer[q];
+    sym_release(c, c->ctl, cb);
+  }
   if (c->barrier_word) cudaFree(c->barrier_word);
   ncclResult_t r = ncclCommDestroy(c->comm);
   delete c;
@@ -146,14 +186,81 @@ extern "C" int cp_symmetric_wait(cp_comm c, void* local, void* stream) {
   uint32_t* flags[CP_MAX_RANKS];
   if (!cp::comm_symmetric_peers(c, local, peers, flags)) CP_FAIL(CP_ERR_ARG, "cp_symmetric_wait: not a symmetric buffer");
   cudaStream_t s = (cudaStream_t)stream;
+  if (!cp::gather_push_in_epilogue()) CP_TRY(cp::comm_ce_distribute(c, local, s));
   CP_TRY(cp::launch_wait_flags(flags[c->rank], c->world, c->rank, s));
   CP_CUDA(cudaMemsetAsync(flags[c->rank], 0, CP_MAX_RANKS * sizeof(uint32_t), s));
   return CP_OK;
 }
 
+// One-shot AllReduce of a small vector over NVLink peer memory (one CTA): write the vector into
+// slot [rank] of every rank's scratch (parity = epoch & 1, so the next call cannot overwrite slots
+// still being summed: a rank two calls ahead would need this rank's flag of the call in between),
+// raise the epoch flag at every peer, wait for all peers' flags, then sum the slots in ascending
+// rank order - bitwise identical on every rank.
+struct ArPtrs {
+  float* s[CP_MAX_RANKS];
+  uint32_t* c[CP_MAX_RANKS];
+};
+__global__ void __launch_bounds__(512) oneshot_allreduce_kernel(float* buf, int n, ArPtrs peers, float* mine,
+                                                                uint32_t* ctl, int me, int world) {
+  __shared__ uint32_t e_s;
+  if (threadIdx.x == 0) e_s = ctl[kCtlArEpoch] + 1;
+  __syncthreads();
+  const uint32_t e = e_s;
+  const int par = e & 1;
+  for (int q = 0; q < world; ++q) {
+    float* dst = peers.s[q] + ((int64_t)par * world + me) * kArMax;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = buf[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl[kCtlArEpoch] = e;
+    for (int q = 0; q < world; ++q)
+      if (q != me) cp::st_release_sys(peers.c[q] + kCtlArFlags + me, e);
+  }
+  if (threadIdx.x < world && (int)threadIdx.x != me) {
+    const long long t0 = clock64();
+    while ((int)(cp::ld_acquire_sys(ctl + kCtlArFlags + threadIdx.x) - e) < 0) {
+      asm volatile("nanosleep.u32 32;");
+      if (clock64() - t0 > (1ll << 35)) __trap();
+    }
+  }
+  __syncthreads();
+  const float* src = mine + (int64_t)par * world * kArMax;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float t = src[i];
+    for (int q = 1; q < world; ++q) t += src[(int64_t)q * kArMax + i];
+    buf[i] = t;
+  }
+}
+
 extern "C" int cp_allreduce_sum(cp_comm c, float* buf, int64_t n, void* stream) {
   if (!c || c->world == 1 || n == 0) return CP_OK;
   if (!buf || n < 0) CP_FAIL(CP_ERR_ARG, "cp_allreduce_sum: bad arguments");
+  if (c->ctl && n <= kArMax) {
+    if (!c->ar) {   // collective lazy allocation - not while a graph is being captured
+      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+      CP_CUDA(cudaStreamIsCapturing((cudaStream_t)stream, &st));
+      if (st == cudaStreamCaptureStatusNone) {
+        SymBuf ab{};
+        void* p = nullptr;
+        CP_TRY(sym_map(c, (size_t)2 * c->world * kArMax * 4, &p, ab));
+        c->ar = (float*)p;
+        for (int q = 0; q < c->world; ++q) c->ar_peer[q] = (float*)ab.peers[q];
+      }
+    }
+    if (c->ar) {
+      ArPtrs ap{};
+      for (int q = 0; q < c->world; ++q) {
+        ap.s[q] = c->ar_peer[q];
+        ap.c[q] = c->ctl_peer[q];
+      }
+      oneshot_allreduce_kernel<<<1, 512, 0, (cudaStream_t)stream>>>(buf, (int)n, ap, c->ar, c->ctl, c->rank, c->world);
+      CP_LAUNCHED();
+      return CP_OK;
+    }
+  }
   CP_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclFloat, ncclSum, c->comm, (cudaStream_t)stream));
   return CP_OK;
 }
@@ -206,6 +313,37 @@ int comm_check_plan(cp_comm c, const Layer& L) {
 }
 
 // Peer pointers of a symmetric buffer (nullptr if `local` is not one).
+cudaEvent_t comm_symmetric_event(cp_comm c, const void* local) {
+  if (!c) return nullptr;
+  auto it = c->sym.find(const_cast<void*>(local));
+  return it == c->sym.end() ? nullptr : it->second.ev;
+}
+
+void comm_symmetric_set_own(cp_comm c, const void* local, int64_t off, int64_t elems) {
+  auto it = c->sym.find(const_cast<void*>(local));
+  if (it == c->sym.end()) return;
+  it->second.own_off = off;
+  it->second.own_elems = elems;
+}
+
+// Copy-engine gather (consumers outside the tensor-core forward): this rank's block into every
+// peer's copy, then the arrival flag (value 1) behind the data at every peer - no SM involved.
+int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks) {
+  auto it = c->sym.find(const_cast<void*>(local));
+  if (it == c->sym.end()) CP_FAIL(CP_ERR_ARG, "not a symmetric buffer");
+  const SymBuf& sb = it->second;
+  if (sb.own_off < 0) CP_FAIL(CP_ERR_STATE, "symmetric gather: no producer wrote this buffer yet");
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    if (sb.own_elems)
+      CP_CUDA(cudaMemcpyAsync((float*)sb.peers[q] + sb.own_off, (const float*)local + sb.own_off,
+                              (size_t)sb.own_elems * 4, cudaMemcpyDeviceToDevice, s));
+    uint32_t* f = (uint32_t*)((char*)sb.peers[q] + sb.flag_off);
+    CP_TRY(comm_signal_ce(c, &f, 1, c->rank, s, chunks));
+  }
+  return CP_OK;
+}
+
 bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags) {
   if (!c || c->world == 1) return false;
   auto it = c->sym.find(const_cast<void*>(local));
@@ -217,11 +355,47 @@ bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t**
   return true;
 }
 
-// Cross-rank barrier on `s` after peer stores: a one-word AllReduce completes on a rank only once
-// every rank has reached it, i.e. after every rank's storing kernel (stream order) has finished.
+// Cross-rank barrier on `s` through the control line: one thread bumps this rank's epoch, writes it
+// into every peer's slot [rank] (st.release.sys over NVLink) and spins until every peer's epoch
+// reached it.  Every rank calls it equally often, so the epochs pair up; no NCCL kernel, no host.
+struct CtlPtrs {
+  uint32_t* p[CP_MAX_RANKS];
+};
+__global__ void flag_barrier_kernel(CtlPtrs peer, uint32_t* mine, int me, int world) {
+  const uint32_t e = mine[kCtlEpoch] + 1;
+  mine[kCtlEpoch] = e;
+  __threadfence_system();
+  for (int q = 0; q < world; ++q)
+    if (q != me) st_release_sys(peer.p[q] + me, e);
+  const long long t0 = clock64();
+  for (int q = 0; q < world; ++q) {
+    if (q == me) continue;
+    while ((int)(ld_acquire_sys(mine + q) - e) < 0) {
+      asm volatile("nanosleep.u32 64;");
+      if (clock64() - t0 > (1ll << 35)) __trap();
+    }
+  }
+}
+
 int comm_barrier(cp_comm c, cudaStream_t s) {
   if (!c || c->world == 1) return CP_OK;
-  CP_NCCL(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
+  if (!c->ctl) {
+    CP_NCCL(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
+    return CP_OK;
+  }
+  CtlPtrs cp{};
+  for (int q = 0; q < c->world; ++q) cp.p[q] = c->ctl_peer[q];
+  flag_barrier_kernel<<<1, 1, 0, s>>>(cp, c->ctl, c->rank, c->world);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
+// Arrival flags raised by the copy engines (no SM): 4-byte copies of the constant 1 into slot
+// `slot` of each given flag array, ordered after the data copies on the same stream.
+int comm_signal_ce(cp_comm c, uint32_t* const* flags, int n, int slot, cudaStream_t s, bool chunks) {
+  for (int k = 0; k < n; ++k)
+    CP_CUDA(cudaMemcpyAsync(flags[k] + slot, c->ctl + (chunks ? kCtlChunks : kCtlOne), 4,
+                            cudaMemcpyDeviceToDevice, s));
   return CP_OK;
 }
 

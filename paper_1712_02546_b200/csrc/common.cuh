@@ -111,12 +111,16 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void wait_flag_sys(const uint32_t* p) {
+// wait until *p >= target (arrival counters / flags)
+__device__ __forceinline__ void wait_flag_sys(const uint32_t* p, uint32_t target = 1) {
   const long long t0 = clock64();
-  while (ld_acquire_sys(p) == 0) {
+  while ((int)(ld_acquire_sys(p) - target) < 0) {
     asm volatile("nanosleep.u32 100;");
     if (clock64() - t0 > (1ll << 35)) __trap();
   }
+}
+__device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // ---------------------------------------------------------------- layer state
@@ -139,6 +143,7 @@ struct Layer {
   int dy_ready;           // epilogue-backward already computed for this step
   const void* dy_key[3];
   cudaEvent_t ev_compute, ev_comm;
+
   // TMA descriptor cache lives in the TC module (opaque)
   void* tc_cache;
 };

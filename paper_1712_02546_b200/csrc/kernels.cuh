@@ -4,6 +4,8 @@
 
 namespace cp {
 
+constexpr int kGatherChunks = 256;   // pieces of a kernel-pushed gather block (= the receivers' target)
+
 // ---- layout / elementwise (kernels_simt.cu)
 int launch_im2col(const Layer& L, const float* x, float* xcol, bool round_tf32, cudaStream_t s);
 int launch_relu_pool(const Layer& L, const float* z, float* y_block, uint8_t* saved, bool round_tf32,
@@ -26,13 +28,24 @@ int launch_random_fill(float* p, int64_t n, uint32_t seed, float scale, cudaStre
 // cross-GPU arrival flags (fused AllGather): set slot `slot` of every peer's flag array / wait for
 // every slot of the own array except `self` (for consumers outside the tensor-core forward)
 int launch_signal_peers(uint32_t* const* peer_flags, int n, int slot, cudaStream_t s);
-int launch_wait_flags(const uint32_t* flags, int n, int self, cudaStream_t s);
+int launch_wait_flags(const uint32_t* flags, int n, int self, cudaStream_t s, bool chunks = false);
 
 // ---- tcgen05 / TMA tensor-core convolutions (kernels_tc.cu)
 size_t tc_workspace_bytes(const Layer& L);
+// fused all-gather -> GEMM (forward over a symmetric gathered input): the kernel's warp 3 pushes
+// this rank's input block (src, n4 float4) into each peer's copy dst[k] in `chunks` pieces, one
+// release-add on the peer's arrival counter cnt[k] per piece; the GEMM waits for `chunks` arrivals
+// from every peer before consuming that peer's block.
+struct GatherPush {
+  const float* src;
+  float* dst[CP_MAX_RANKS];
+  uint32_t* cnt[CP_MAX_RANKS];
+  int n, chunks;
+  long long n4;
+};
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved,
            void* ws, cudaStream_t s, float* const* peer_blocks = nullptr, int npeers = 0,
-           const uint32_t* arrive = nullptr);
+           const uint32_t* arrive = nullptr, const GatherPush* gp = nullptr);
 // dst_blocks (fused reduce-scatter): per input block, where this rank's partial of that block goes
 int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s,
              float* const* dst_blocks = nullptr);
@@ -47,7 +60,17 @@ int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s
 // symmetric (peer-mapped) buffer lookup: peers[r] = rank r's copy; flags[r] = rank r's arrival-flag
 // array (CP_MAX_RANKS u32, indexed by sender rank).  False if `local` is not a symmetric buffer.
 bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags = nullptr);
+cudaEvent_t comm_symmetric_event(cp_comm c, const void* local);
+// producer records its block of a symmetric gathered buffer (for copy-engine distribution)
+void comm_symmetric_set_own(cp_comm c, const void* local, int64_t off, int64_t elems);
+int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks = false);
+// CP_GATHER_PUSH=epilogue: the producer's GEMM epilogue pushes (A/B experiment), else the consumer
+bool gather_push_in_epilogue();
+// cross-rank barrier on s (device-side epoch flags once symmetric memory exists, else NCCL)
 int comm_barrier(cp_comm c, cudaStream_t s);
+// raise slot `slot` of each flag array with copy-engine writes (no SM), ordered after prior copies on s
+// (value 1, or kGatherChunks when `chunks`: stands in for a kernel push of zero bytes)
+int comm_signal_ce(cp_comm c, uint32_t* const* flags, int n, int slot, cudaStream_t s, bool chunks = false);
 int comm_sum_blocks(cp_comm c, float* buf, const Blocks& g, int dx_mode, cudaStream_t s);
 
 }  // namespace cp

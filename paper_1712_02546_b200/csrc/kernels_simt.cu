@@ -501,9 +501,9 @@ __global__ void signal_peers_kernel(FlagPtrs fp, int n, int slot) {
   __threadfence_system();
   for (int k = 0; k < n; ++k) st_release_sys(fp.f[k] + slot, 1u);
 }
-__global__ void wait_flags_kernel(const uint32_t* flags, int n, int self) {
+__global__ void wait_flags_kernel(const uint32_t* flags, int n, int self, uint32_t target) {
   for (int r = 0; r < n; ++r)
-    if (r != self) wait_flag_sys(flags + r);
+    if (r != self) wait_flag_sys(flags + r, target);
 }
 
 int launch_signal_peers(uint32_t* const* peer_flags, int n, int slot, cudaStream_t s) {
@@ -515,9 +515,9 @@ int launch_signal_peers(uint32_t* const* peer_flags, int n, int slot, cudaStream
   return CP_OK;
 }
 
-int launch_wait_flags(const uint32_t* flags, int n, int self, cudaStream_t s) {
+int launch_wait_flags(const uint32_t* flags, int n, int self, cudaStream_t s, bool chunks) {
   if (n <= 1) return CP_OK;
-  wait_flags_kernel<<<1, 1, 0, s>>>(flags, n, self);
+  wait_flags_kernel<<<1, 1, 0, s>>>(flags, n, self, chunks ? (uint32_t)kGatherChunks : 1u);
   CP_LAUNCHED();
   return CP_OK;
 }

@@ -94,9 +94,17 @@ struct TcParams {
   int npeers;
   float* dst[CP_MAX_RANKS];  // dgrad with fused reduce-scatter: base of input block rb's partial (own
   int fused_dx;              // receive slot, or this rank's slot in peer rb's receive area over NVLink)
-  const uint32_t* arrive;  // fwd over a symmetric gathered input: per-sender arrival flags (else null);
+  const uint32_t* arrive;  // fwd over a symmetric gathered input: per-sender arrival counters (else null);
   int self_blk;            // the own input block (ready at launch) is consumed first, a peer's block
-                           // only after its flag is set - the gather overlaps this GEMM
+                           // only after its counter reached arrive_target - the gather overlaps this GEMM
+  uint32_t arrive_target;
+  // fused all-gather -> GEMM: warp 3 of every CTA pushes a share of this rank's own input block into
+  // every peer's copy (push_chunks fixed-size chunks; one release-add on the peer's counter per chunk)
+  const float* push_src;
+  float* push_dst[CP_MAX_RANKS];
+  uint32_t* push_cnt[CP_MAX_RANKS];
+  int npush, push_chunks;
+  long long push_n4;
 };
 
 struct Unit {
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           };
           if (PASS == PASS_FWD) {
             if (!((arrived >> ch.rb) & 1u)) {
-              wait_flag_sys(p.arrive + ch.rb);
+              wait_flag_sys(p.arrive + ch.rb, p.arrive_target);
               asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written data -> TMA reads
               arrived |= 1u << ch.rb;
             }
@@ -439,6 +447,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           }
         });
         if (CG == 2) mma_commit_cg2(&tfull[acc]); else mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (PASS == PASS_FWD && warp == 3) {
+    // ======================= gather pusher (otherwise idle warp): this rank's input block -> peers,
+    // full 512 B per warp store instruction, while the MMA warps consume the own block
+    // peers in the order they consume this block (host-sorted: the peer that needs it soonest
+    // first), all CTAs on one peer at a time so each peer's block completes as early as possible;
+    // 8 float4 loads in flight per lane (the source block is L2-resident: just written)
+    if (p.npush > 0) {
+      const long long per = (p.push_n4 + p.push_chunks - 1) / p.push_chunks;
+      const float4* src = reinterpret_cast<const float4*>(p.push_src);
+      for (int k = 0; k < p.npush; ++k) {
+        float4* dst = reinterpret_cast<float4*>(p.push_dst[k]);
+        for (int c = blockIdx.x; c < p.push_chunks; c += gridDim.x) {
+          const long long b = (long long)c * per, e = min(p.push_n4, b + per);
+          for (long long i = b + lane; i < e; i += 256) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (i + 32 * u < e) v[u] = __ldg(src + i + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (i + 32 * u < e) dst[i + 32 * u] = v[u];
+          }
+          __threadfence_system();
+          __syncwarp();
+          if (lane == 0) red_add_release_sys(p.push_cnt[k], 1u);
+        }
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -1172,7 +1208,7 @@ size_t tc_workspace_bytes(const Layer& L) {
 }
 
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
-           cudaStream_t s, float* const* peer_blocks, int npeers, const uint32_t* arrive) {
+           cudaStream_t s, float* const* peer_blocks, int npeers, const uint32_t* arrive, const GatherPush* gp) {
   if (L.Kc == 0) return CP_OK;
   if ((L.Ho & 1) || (L.Wo & 1))
     CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 forward needs an even conv output grid (2x2 window tiles)");
@@ -1213,6 +1249,18 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   for (int k = 0; k < npeers; ++k) p.peer_out[k] = peer_blocks[k];
   p.arrive = L.images ? nullptr : arrive;
   p.self_blk = L.d.rank;
+  p.arrive_target = 1;
+  if (gp && !L.images) {
+    p.push_src = gp->src;
+    p.npush = gp->n;
+    for (int k = 0; k < gp->n; ++k) {
+      p.push_dst[k] = gp->dst[k];
+      p.push_cnt[k] = gp->cnt[k];
+    }
+    p.push_n4 = gp->n4;
+    p.push_chunks = gp->chunks;
+    p.arrive_target = (uint32_t)gp->chunks;
+  }
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = (long long)L.Ho * L.Wo * L.Bp * L.Kc;
   p.out = pl.S > 1 ? part : y_block;

@@ -99,6 +99,14 @@ static int derive(Layer& L, const cp_conv_desc& d) {
 
 static char* WS(void* ws, size_t off) { return (char*)ws + off; }
 
+bool gather_push_in_epilogue() {
+  static const bool e = [] {
+    const char* v = getenv("CP_GATHER_PUSH");
+    return v && std::string(v) == "epilogue";
+  }();
+  return e;
+}
+
 // epilogue backward of this rank's block (shared by backward_data and backward_filter)
 static int ensure_dy(Layer& L, const float* dy_g, const uint8_t* saved, const float* y_g, void* ws, cudaStream_t s) {
   if (L.dy_ready && L.dy_key[0] == dy_g && L.dy_key[1] == saved && L.dy_key[2] == y_g) return CP_OK;
@@ -184,6 +192,7 @@ int conv_part_destroy(cp_layer L) {
   tc_release(*L);
   if (L->ev_compute) cudaEventDestroy(L->ev_compute);
   if (L->ev_comm) cudaEventDestroy(L->ev_comm);
+
   delete L;
   return CP_OK;
 }
@@ -203,54 +212,76 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
     CP_TRY(launch_im2col(*L, x, xcol, tf32, s));
     xin = xcol;
   }
-  // Fused channel AllGather (B200 path).  Producer side: when y_gathered is a
-  // symmetric buffer (cp_symmetric_alloc) the forward epilogue stores this rank's pooled block into
-  // every peer's copy over NVLink, then a one-thread kernel sets this rank's arrival flag in every
-  // peer's flag array.  Consumer side: when the input x is a symmetric gathered buffer, the forward
-  // GEMM consumes its own block first and each peer block only after that peer's flag is set (the
-  // gather overlaps the GEMM), then resets the flags.  No separate AllGather kernel, no NCCL call
-  // except a one-word AllReduce guarding the buffer against overwrite while a peer still reads it.
+  // Channel AllGather over NVLink peer memory (B200 path), fused into the consumer
+  // GEMM.  Producer side: when y_gathered is a symmetric buffer (cp_symmetric_alloc), a device-side
+  // barrier first makes sure no peer still reads its copy (e.g. the next layer's async wgrad of the
+  // previous step), then the GEMM writes this rank's block locally.  Consumer side: when x is a
+  // symmetric gathered buffer, the forward kernel's otherwise idle warp 3 pushes this rank's block
+  // into every peer's copy (full-line NVLink stores, a release-add per chunk on the peer's arrival
+  // counter) while the MMA warps consume the own block first and each peer block once its counter
+  // is complete - the gather overlaps the GEMM; no AllGather kernel, no NCCL call.  Consumers outside
+  // the tensor-core forward use copy-engine copies + flags (comm_ce_distribute / cp_symmetric_wait).
+  // CP_GATHER_PUSH=epilogue instead pushes from the producer's epilogue (A/B comparison).
   void* peers[CP_MAX_RANKS];
   uint32_t* pflags[CP_MAX_RANKS];
   float* peer_blocks[CP_MAX_RANKS];
   uint32_t* signal[CP_MAX_RANKS];
   int npeers = 0;
+  const int me = L->d.rank;
+  const bool epi_push = gather_push_in_epilogue();
   const bool gathered_out = L->comm && L->d.world > 1 && !L->d.local_output;
   const bool sym_out = gathered_out && comm_symmetric_peers(L->comm, y, peers, pflags);
+  const bool push_in_epilogue = sym_out && tf32 && epi_push;
   if (sym_out) {
     for (int r = 0; r < L->d.world; ++r)
-      if (r != L->d.rank) {
+      if (r != me) {
         signal[npeers] = pflags[r];
-        peer_blocks[npeers++] = (float*)peers[r] + L->out.start[L->d.rank];
+        peer_blocks[npeers++] = (float*)peers[r] + L->out.start[me];
       }
-    // WAR guard: a peer may still be reading its copy of y (e.g. the next layer's async wgrad of the
-    // previous step) - nobody writes into a peer's buffer before every rank has reached this point.
+    comm_symmetric_set_own(L->comm, y, L->out.start[me], L->out.start[me + 1] - L->out.start[me]);
     CP_TRY(comm_barrier(L->comm, s));
   }
   void* ipeers[CP_MAX_RANKS];
   uint32_t* iflags[CP_MAX_RANKS];
   const bool sym_in = !L->images && L->comm && L->d.world > 1 && comm_symmetric_peers(L->comm, x, ipeers, iflags);
-  const uint32_t* arrive = sym_in ? iflags[L->d.rank] : nullptr;
-  if (sym_in && !tf32) CP_TRY(launch_wait_flags(arrive, L->d.world, L->d.rank, s));
-  if (L->Kr > 0 || L->Kc > 0) {
+  const uint32_t* arrive = sym_in ? iflags[me] : nullptr;
+  const bool has_gemm = L->Kr > 0 || L->Kc > 0;
+  GatherPush gp{};
+  bool kernel_push = false;
+  if (sym_in && !epi_push) {
+    const int64_t n = L->in.start[me + 1] - L->in.start[me];
+    if (tf32 && has_gemm) {
+      kernel_push = true;
+      gp.src = x + L->in.start[me];
+      gp.n4 = n / 4;
+      gp.chunks = kGatherChunks;
+      // peer q walks its input blocks from its own upwards, so it needs this rank's block after
+      // (me - q) mod P blocks: push to the soonest consumer first
+      for (int d = 1; d < L->d.world; ++d) {
+        const int q = (me - d + L->d.world) % L->d.world;
+        gp.dst[gp.n] = (float*)ipeers[q] + L->in.start[me];
+        gp.cnt[gp.n++] = iflags[q] + me;
+      }
+    } else {
+      // (a TF32 rank without kernels here signals the chunk count its peers' GEMMs wait for)
+      CP_TRY(comm_ce_distribute(L->comm, x, s, tf32));
+    }
+  }
+  if (sym_in && !(tf32 && has_gemm)) CP_TRY(launch_wait_flags(arrive, L->d.world, me, s, tf32 && !epi_push));
+  if (has_gemm) {
     if (tf32) {
-      CP_TRY(tc_fwd(*L, xin, w, b, yb, saved, ws, s, sym_out ? peer_blocks : nullptr, sym_out && tf32 ? npeers : 0,
-                    arrive));
+      CP_TRY(tc_fwd(*L, xin, w, b, yb, saved, ws, s, push_in_epilogue ? peer_blocks : nullptr,
+                    push_in_epilogue ? npeers : 0, arrive, kernel_push ? &gp : nullptr));
     } else {
       float* z = (float*)WS(ws, L->off_z);
       CP_TRY(launch_fwd_simt(*L, x, xin, w, b, z, s));
       CP_TRY(launch_relu_pool(*L, z, yb, saved, false, s));
     }
-  } else if (sym_in && tf32) {
-    CP_TRY(launch_wait_flags(arrive, L->d.world, L->d.rank, s));   // no GEMM to wait inside
   }
   if (sym_in) CP_CUDA(cudaMemsetAsync((void*)arrive, 0, CP_MAX_RANKS * sizeof(uint32_t), s));
-  if (sym_out) {
-    if (!tf32) {   // SIMT reference path: plain NCCL gather into the symmetric buffer, then signal
-      CP_TRY(comm_allgather_blocks(L->comm, y, L->out, s));
-    }
-    CP_TRY(launch_signal_peers(signal, npeers, L->d.rank, s));
-  } else if (gathered_out) {
+  if (push_in_epilogue) {
+    CP_TRY(launch_signal_peers(signal, npeers, me, s));
+  } else if (gathered_out && !sym_out) {
     CP_TRY(fork_comm(*L, s, cs));
     CP_TRY(comm_allgather_blocks(L->comm, y, L->out, cs));
     CP_TRY(join_comm(*L, s, cs));

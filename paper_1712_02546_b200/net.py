@@ -168,8 +168,9 @@ class PartitionedNet:
             cp.conv_part_forward(L, inp, b["w"], b["b"], b["y"], b["saved"], b["ws"], stream, comm_stream)
             inp = b["y"]
         hd = self.head
-        if self.sym and self.sym[-1].tensor.data_ptr() == self.buf[-1]["y"].data_ptr():
-            self.sym[-1].wait(stream)   # replicated head reads the gathered last output
+        last = next((m for m in self.sym if m.tensor.data_ptr() == self.buf[-1]["y"].data_ptr()), None)
+        if last is not None:
+            last.wait(stream)   # replicated head reads the gathered last output
         bias = hd["bfc"] if (self.head_mode == "replicated" or self.rank == 0) else None
         cp.cp_fc_forward(self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], bias, self.O, hd["logits"],
                          hd["ws"], stream)
