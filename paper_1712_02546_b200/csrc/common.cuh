@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/convpart.h"
@@ -64,6 +65,15 @@ struct Blocks {
   int Cg;                    // total slots = sum kw
 };
 
+// experiment hook: extra floats between consecutive rank blocks (L2 set-aliasing study)
+static inline int64_t block_pad() {
+  static const int64_t v = [] {
+    const char* e = getenv("CP_BLOCK_PAD");
+    return e ? (int64_t)atoll(e) / 32 * 32 : (int64_t)0;
+  }();
+  return v;
+}
+
 static inline Blocks make_blocks(const cp_partition& p, int H, int W, int Bp) {
   Blocks g{};
   g.n = p.n_ranks;
@@ -80,6 +90,7 @@ static inline Blocks make_blocks(const cp_partition& p, int H, int W, int Bp) {
     g.start[r] = s;
     c += p.k_width[r];
     s += (int64_t)H * W * Bp * p.k_width[r];
+    if (r + 1 < p.n_ranks) s += block_pad();
   }
   g.start[p.n_ranks] = s;
   g.Cg = c;

@@ -198,7 +198,11 @@ __device__ __forceinline__ int unit_at(const TcParams& p, int group, int ngroups
 struct Chunk {
   int tap, rb, c;     // fwd: tap, input block, channel chunk ; dgrad: tap, -, kernel chunk ; wgrad: -, -, k-chunk index
   int ksteps;
+  int r, s;           // fwd / dgrad: the tap's row and column
+  int bc, q, pp;      // wgrad: 32-image chunk and output position of k-chunk c
 };
+// (coordinates are produced by the loops themselves: the single TMA producer thread issues one
+// chunk per ~900 cycles of MMA, so integer divisions on its path cost tensor-pipe time)
 
 // dgrad: taps (r,s) whose shifted 2x2 window hits the dY grid: r in [r_lo, r_hi], s in [s_lo, s_hi]
 __device__ __forceinline__ void dgrad_taps(const TcParams& p, const Unit& t, int& r_lo, int& nr, int& s_lo, int& ns) {
@@ -224,18 +228,20 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
       // overlapped gather: input blocks outermost, starting with the own block
       for (int bi = 0, rb = p.self_blk; bi < p.nblk; ++bi, rb = rb + 1 == p.nblk ? 0 : rb + 1) {
         const int kw = p.kw[rb];
-        for (int tap = 0; tap < p.R * p.S; ++tap)
-          for (int c = 0; c * BK < kw; ++c, ++idx)
-            if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8});
+        for (int r = 0, tap = 0; r < p.R; ++r)
+          for (int sx = 0; sx < p.S; ++sx, ++tap)
+            for (int c = 0; c * BK < kw; ++c, ++idx)
+              if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
       }
       return;
     }
-    for (int tap = 0; tap < p.R * p.S; ++tap)
-      for (int rb = 0; rb < p.nblk; ++rb) {
-        const int kw = p.kw[rb];
-        for (int c = 0; c * BK < kw; ++c, ++idx)
-          if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8});
-      }
+    for (int r = 0, tap = 0; r < p.R; ++r)
+      for (int sx = 0; sx < p.S; ++sx, ++tap)
+        for (int rb = 0; rb < p.nblk; ++rb) {
+          const int kw = p.kw[rb];
+          for (int c = 0; c * BK < kw; ++c, ++idx)
+            if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
+        }
   } else if (PASS == PASS_DGRAD) {
     int r_lo, nr, s_lo, ns;
     dgrad_taps(p, t, r_lo, nr, s_lo, ns);
@@ -250,11 +256,24 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     for (int c = 0; c < kc; ++c)
       for (int r = r_lo; r < r_lo + nr; ++r)
         for (int sx = s_lo; sx < s_lo + ns; ++sx, ++idx)
-          if (idx >= lo && idx < hi) f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8});
+          if (idx >= lo && idx < hi) f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8, r, sx, 0, 0, 0});
   } else {
     const int c0 = t.tail ? t.piece * p.tail_per : t.sp * p.chunks_per_split;
     const int c1 = min(p.chunks_total, c0 + (t.tail ? p.tail_per : p.chunks_per_split));
-    for (int c = c0; c < c1; ++c) f(Chunk{0, 0, c, BK / 8});
+    // k-chunk c = (pq, bc): decoded once, then stepped
+    const int nbc = p.Bp / 32;
+    int bc = c0 % nbc, pq = c0 / nbc;
+    int q = pq % p.Wo, pp = pq / p.Wo;
+    for (int c = c0; c < c1; ++c) {
+      f(Chunk{0, 0, c, BK / 8, 0, 0, bc, q, pp});
+      if (++bc == nbc) {
+        bc = 0;
+        if (++q == p.Wo) {
+          q = 0;
+          ++pp;
+        }
+      }
+    }
   }
 }
 
@@ -335,6 +354,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int nb0 = t.n0 + (int)rank * nb_own;                // first B column of this CTA
         const int nboxes = p.wide ? (CG == 2 ? 4 : 8) : (nb_own + 31) / 32;  // MN-major B: 32-column atoms
         const uint32_t tx_cta = PASS == PASS_FWD ? A_BYTES + p.bn_box * BK * 4 : A_BYTES + nboxes * 4096;
+        // wgrad span: input block and atom of every B box of this unit, once per unit
+        int wb_n = 0, wb_rb[8], wb_atom[8];
+        const int wg_r = PASS == PASS_WGRAD ? t.tap / p.S : 0, wg_s = PASS == PASS_WGRAD ? t.tap % p.S : 0;
+        if (PASS == PASS_WGRAD && p.span) {
+          for (int jb = 0; jb * p.apb * 32 < (CG == 2 ? BN / 2 : BN) && jb < 8; ++jb) {
+            const int sl = nb0 + jb * p.apb * 32;   // concatenated slot of this box
+            int rb = 0;
+            while (rb + 1 < p.nblk && sl >= p.coff[rb + 1]) ++rb;
+            wb_rb[jb] = rb;
+            wb_atom[jb] = (sl - p.coff[rb]) >> 5;
+            wb_n = jb + 1;
+          }
+        }
         for_each_chunk<PASS>(p, t, [&](const Chunk& ch) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * A_BYTES;
@@ -356,19 +388,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             else tma_load_5d(d, m, &full[stage], c0, c1, c2, c3, c4);
           };
           if (PASS == PASS_FWD) {
+            const int r = ch.r, s = ch.s;
             if (!((arrived >> ch.rb) & 1u)) {
               wait_flag_sys(p.arrive + ch.rb, p.arrive_target);
               asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written data -> TMA reads
               arrived |= 1u << ch.rb;
             }
-            const int r = ch.tap / p.S, s = ch.tap % p.S;
             if (p.unified)
               ld5(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
             else
               ld4(a, &p.maps[ch.rb], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
             ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
           } else if (PASS == PASS_DGRAD) {
-            const int r = ch.tap / p.S, s = ch.tap % p.S;
+            const int r = ch.r, s = ch.s;
             ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
             if (p.wide) {
               ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BK, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> 5, ch.tap);
@@ -377,20 +409,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                 ld3(b + q * 4096, &p.maps[CP_MAX_RANKS], p.coff[t.rb] + nb0 + 32 * q, ch.c * BK, ch.tap);
             }
           } else {
-            const int nbc = p.Bp / 32;
-            const int bc = ch.c % nbc, pq = ch.c / nbc, q = pq % p.Wo, pp = pq / p.Wo;
-            const int r = t.tap / p.S, s = t.tap % p.S;
+            const int bc = ch.bc, q = ch.q, pp = ch.pp;
+            const int r = wg_r, s = wg_s;
             if (p.span) {
               ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
-              for (int jb = 0; jb * p.apb * 32 < (CG == 2 ? BN / 2 : BN); ++jb) {  // always the full box set
-                const int sl = nb0 + jb * p.apb * 32;   // concatenated slot of this box
-                int rb = 0;
-                while (rb + 1 < p.nblk && sl >= p.coff[rb + 1]) ++rb;
+              for (int jb = 0; jb < wb_n; ++jb) {   // boxes of this unit (block / atom hoisted per unit)
                 if (p.unified)
-                  ld5(b + jb * p.apb * 4096, &p.maps[0], 0, bc * 32, (sl - p.coff[rb]) >> 5, (pp + r) * p.Win + q + s,
-                      rb);
+                  ld5(b + jb * p.apb * 4096, &p.maps[0], 0, bc * 32, wb_atom[jb], (pp + r) * p.Win + q + s, wb_rb[jb]);
                 else
-                  ld5(b + jb * p.apb * 4096, &p.maps[rb], 0, bc * 32, (sl - p.coff[rb]) >> 5, q + s, pp + r);
+                  ld5(b + jb * p.apb * 4096, &p.maps[wb_rb[jb]], 0, bc * 32, wb_atom[jb], q + s, pp + r);
               }
             } else if (p.wide) {
               ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
@@ -1033,7 +1060,7 @@ int choose_split(int units, int groups, double chunks, double out_bytes, int max
 
 // N tiles span input blocks when every block width is a multiple of 32 (and there are several)
 bool span_ok(const TcParams& p) {
-  if (p.images || p.nblk < 2) return false;
+  if (p.images || p.nblk < 2 || !env_int("CP_TC_SPAN", 1)) return false;
   for (int r = 0; r < p.nblk; ++r)
     if (p.kw[r] % 32) return false;
   return true;
