@@ -460,12 +460,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
-          for (int k = 0; k < ch.ksteps; ++k) {
-            const uint64_t ad = a_mn ? sdesc_mn(a_addr, k) : sdesc_k(a_addr, k);
-            const uint64_t bd = b_mn ? sdesc_mn(b_addr, k) : sdesc_k(b_addr, k);
-            if (CG == 2) mma_tf32_cg2(d_tmem, ad, bd, idesc, accumulate);
-            else mma_tf32(d_tmem, ad, bd, idesc, accumulate);
-            accumulate = 1;
+          // descriptors built once per chunk; a K-step only advances the start-address field
+          // (16-byte units: +32 B K-major, +1024 B MN-major)
+          const uint64_t ad0 = a_mn ? sdesc_mn(a_addr, 0) : sdesc_k(a_addr, 0);
+          const uint64_t bd0 = b_mn ? sdesc_mn(b_addr, 0) : sdesc_k(b_addr, 0);
+          const uint64_t astep = a_mn ? 64 : 2, bstep = b_mn ? 64 : 2;
+          if (ch.ksteps == BK / 8) {
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              if (CG == 2) mma_tf32_cg2(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+              else mma_tf32(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+              accumulate = 1;
+            }
+          } else {
+            for (int k = 0; k < ch.ksteps; ++k) {
+              if (CG == 2) mma_tf32_cg2(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+              else mma_tf32(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+              accumulate = 1;
+            }
           }
           if (CG == 2) mma_commit_cg2(&empty[stage]); else mma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
