@@ -231,6 +231,15 @@ int conv_part_backward_filter(cp_layer layer, const float* dy_gathered, const ui
                               const float* y_gathered, const float* x, float* dw, float* db,
                               void* workspace, void* stream);
 
+/* conv_part_timing — enable (1) / disable (0) per-pass timing of this layer's tensor-core GEMM
+ * launches: CUDA events recorded on the launching stream immediately before and after the GEMM
+ * kernel (external records, so they also time inside a captured CUDA graph).
+ * conv_part_kernel_time — duration in ms of the last recorded GEMM of `pass` (0 forward,
+ * 1 backward-data, 2 backward-filter); the caller synchronizes first.  CP_ERR_STATE if timing is
+ * off; a CUDA error if that pass never ran since enabling.  (bench.py's roofline measurement) */
+int conv_part_timing(cp_layer layer, int32_t enable);
+int conv_part_kernel_time(cp_layer layer, int32_t pass, float* ms);
+
 /* conv_part_wait — make `stream` wait for the layer's last issued collective. */
 int conv_part_wait(cp_layer layer, void* stream);
 

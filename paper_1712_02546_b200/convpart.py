@@ -28,7 +28,7 @@ EXPORTS = [
     "cp_launch_count", "cp_last_error", "cp_pack_nchw", "cp_unpack_nchw", "cp_unpack_saved",
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
-    "cp_allreduce_sum", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait",
+    "cp_allreduce_sum", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait", "conv_part_timing", "conv_part_kernel_time",
 ]
 
 
@@ -119,6 +119,8 @@ def lib():
             "cp_symmetric_alloc": [P, SZ, ctypes.POINTER(P)],
             "cp_symmetric_free": [P, P],
             "cp_symmetric_wait": [P, P, P],
+            "conv_part_timing": [P, I32],
+            "conv_part_kernel_time": [P, I32, ctypes.POINTER(ctypes.c_float)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -318,6 +320,16 @@ class SymmetricBuffer:
         if self.ptr:
             _call("cp_symmetric_free", self.comm, ctypes.c_void_p(self.ptr))
             self.ptr = None
+
+
+def conv_part_timing(h, enable=True):
+    _call("conv_part_timing", h, 1 if enable else 0)
+
+
+def conv_part_kernel_time(h, pass_):
+    ms = ctypes.c_float()
+    _call("conv_part_kernel_time", h, int(pass_), ctypes.byref(ms))
+    return ms.value
 
 
 def cp_sgd(p, g, lr, stream=None):

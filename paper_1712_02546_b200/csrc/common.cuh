@@ -154,6 +154,9 @@ struct Layer {
   int dy_ready;           // epilogue-backward already computed for this step
   const void* dy_key[3];
   cudaEvent_t ev_compute, ev_comm;
+  // optional per-pass GEMM timing (conv_part_timing): events around the tensor-core kernel launch
+  int timing;
+  cudaEvent_t ev_t[3][2];
 
   // TMA descriptor cache lives in the TC module (opaque)
   void* tc_cache;

@@ -53,6 +53,9 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
 int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float* out, int64_t n, cudaStream_t s);
 int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s);
 void tc_release(Layer& L);
+// timing events around a pass's GEMM launch (no-ops unless L.timing): external records, so they
+// also time when the launch is captured into a CUDA graph
+int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s);
 
 // ---- NCCL collectives (comm.cu)
 int comm_check_plan(cp_comm c, const Layer& L);

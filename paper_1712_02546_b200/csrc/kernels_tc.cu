@@ -1246,6 +1246,15 @@ size_t tc_workspace_bytes(const Layer& L) {
   return need;
 }
 
+int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s) {
+  if (!L.timing) return CP_OK;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CP_CUDA(cudaStreamIsCapturing(s, &st));
+  CP_CUDA(cudaEventRecordWithFlags(L.ev_t[pass][end], s,
+                                   st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault));
+  return CP_OK;
+}
+
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
            cudaStream_t s, float* const* peer_blocks, int npeers, const uint32_t* arrive, const GatherPush* gp) {
   if (L.Kc == 0) return CP_OK;
@@ -1337,7 +1346,9 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
       p.units = p.tail_full + T * st;
     }
   }
+  CP_TRY(tc_time_mark(L, PASS_FWD, 0, s));
   CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
+  CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
   if (p.tail_st > 0) {
     fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
     CP_LAUNCHED();
@@ -1452,7 +1463,9 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
       p.nsched = off;
     }
   }
+  CP_TRY(tc_time_mark(L, PASS_DGRAD, 0, s));
   CP_TRY((pl.pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s)));
+  CP_TRY(tc_time_mark(L, PASS_DGRAD, 1, s));
   if (pl.S > 1) {
     const int64_t n = L.in.start[L.in.n];
     CP_TRY(launch_splitk_reduce(part, dx, n, pl.S, s));
@@ -1522,7 +1535,9 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
     }
     p.units = p.tail_full + T * st;
   }
+  CP_TRY(tc_time_mark(L, PASS_WGRAD, 0, s));
   CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2>(p, s) : launch_cg<PASS_WGRAD, 1>(p, s)));
+  CP_TRY(tc_time_mark(L, PASS_WGRAD, 1, s));
   if (p.tail_st > 0) {
     wgrad_tail_reduce<<<dim3(BM, CG, ti.n), BN, 0, s>>>(p.tail_buf, dw, ti);
     CP_LAUNCHED();

@@ -190,6 +190,9 @@ int conv_part_query(cp_layer L, cp_sizes* o) {
 int conv_part_destroy(cp_layer L) {
   if (!L) return CP_OK;
   tc_release(*L);
+  for (int p = 0; p < 3; ++p)
+    for (int e = 0; e < 2; ++e)
+      if (L->ev_t[p][e]) cudaEventDestroy(L->ev_t[p][e]);
   if (L->ev_compute) cudaEventDestroy(L->ev_compute);
   if (L->ev_comm) cudaEventDestroy(L->ev_comm);
 
@@ -379,6 +382,23 @@ int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* save
   } else {
     CP_TRY(launch_wgrad_simt(*L, dY, x, xcol, dw, s));
   }
+  return CP_OK;
+}
+
+int conv_part_timing(cp_layer L, int32_t enable) {
+  if (!L) CP_FAIL(CP_ERR_ARG, "conv_part_timing: null layer");
+  if (enable && !L->timing)
+    for (int p = 0; p < 3; ++p)
+      for (int e = 0; e < 2; ++e)
+        if (!L->ev_t[p][e]) CP_CUDA(cudaEventCreate(&L->ev_t[p][e]));
+  L->timing = enable ? 1 : 0;
+  return CP_OK;
+}
+
+int conv_part_kernel_time(cp_layer L, int32_t pass, float* ms) {
+  if (!L || !ms || pass < 0 || pass > 2) CP_FAIL(CP_ERR_ARG, "conv_part_kernel_time: bad arguments");
+  if (!L->timing) CP_FAIL(CP_ERR_STATE, "conv_part_kernel_time: timing not enabled");
+  CP_CUDA(cudaEventElapsedTime(ms, L->ev_t[pass][0], L->ev_t[pass][1]));
   return CP_OK;
 }
 
