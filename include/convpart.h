@@ -292,6 +292,10 @@ int cp_fc_backward(const float* dlogits, const float* x_gathered, int32_t B, int
                    float* dx_gathered, float* dwfc_g, float* dbfc, void* ws, void* stream);
 /* p -= lr*g over n floats. */
 int cp_sgd(float* p, const float* g, int64_t n, float lr, void* stream);
+/* The same SGD update for `count` tensors in one launch per 16 tensors: params[i]
+ * -= lr*grads[i] over sizes[i] floats (host arrays of device pointers; a tensor may be empty). */
+int cp_sgd_multi(float* const* params, const float* const* grads, const int64_t* sizes, int32_t count,
+                 float lr, void* stream);
 
 /* In-place sum over all ranks of n floats (NCCL AllReduce on `stream`); the result is identical
  * on every rank.  Used by the partitioned head to sum per-rank partial logits.  comm == NULL or a

@@ -29,6 +29,7 @@ EXPORTS = [
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
     "cp_allreduce_sum", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait", "conv_part_timing", "conv_part_kernel_time",
+    "cp_sgd_multi",
 ]
 
 
@@ -120,6 +121,7 @@ def lib():
             "cp_symmetric_free": [P, P],
             "cp_symmetric_wait": [P, P, P],
             "conv_part_timing": [P, I32],
+            "cp_sgd_multi": [ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(I64), I32, ctypes.c_float, P],
             "conv_part_kernel_time": [P, I32, ctypes.POINTER(ctypes.c_float)],
         }
         for name, args in sig.items():
@@ -330,6 +332,15 @@ def conv_part_kernel_time(h, pass_):
     ms = ctypes.c_float()
     _call("conv_part_kernel_time", h, int(pass_), ctypes.byref(ms))
     return ms.value
+
+
+def cp_sgd_multi(pairs, lr, stream=None):
+    """pairs: [(param, grad[, n])] of float32 device tensors; one fused update launch."""
+    n = len(pairs)
+    ps = (ctypes.c_void_p * max(n, 1))(*[t[0].data_ptr() for t in pairs])
+    gs = (ctypes.c_void_p * max(n, 1))(*[t[1].data_ptr() for t in pairs])
+    sz = (ctypes.c_int64 * max(n, 1))(*[int(t[2]) if len(t) > 2 else t[0].numel() for t in pairs])
+    _call("cp_sgd_multi", ps, gs, sz, n, float(lr), _stream(stream))
 
 
 def cp_sgd(p, g, lr, stream=None):

@@ -222,6 +222,7 @@ int launch_wgrad_simt(const Layer& L, const float* dY, const float* x, const flo
 // nimg x Kcol floats of xcol at ((p*Wo + q)*Bp + b0)*Kcol are contiguous - float4 stores, values
 // picked from shared memory through a column -> offset table.  The output stays in L2.
 constexpr int kIm2colMaxK = 256;
+constexpr int kIm2colMaxBC = 1024;   // (image, channel) pairs per block
 __global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ x, float* __restrict__ xcol, int B,
                                                      int C, int H, int W, int R, int S, int Wo, int Bp, int Kcol,
                                                      int nimg, int round) {
@@ -238,15 +239,35 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ x
     }
     tab[col] = o;
   }
-  // load: (image, channel) pairs outer (block-uniform), the pair's R*W contiguous floats inner
-  for (int bc = 0, bl = 0, c = 0; bc < nimg * C; ++bc) {
-    const int b = b0 + bl;
-    const float* src = x + (((int64_t)b * C + c) * H + p) * W;
-    for (int k = tid; k < RW; k += nt) {
-      const float u = b < B ? __ldg(src + k) : 0.f;
-      xs[bc * RW + k] = round ? tf32_rna(u) : u;
-    }
-    if (++c == C) { c = 0; ++bl; }
+  // load: (image, channel) pairs outer, the pair's R*W contiguous floats inner; row bases from a
+  // table, 8 independent loads in flight per thread (latency, not bandwidth, bounds this phase)
+  __shared__ long long base[kIm2colMaxBC];
+  const int nbc = nimg * C;
+  for (int bc = tid; bc < nbc; bc += nt) {
+    const int bl = bc / C, c = bc - bl * C, b = b0 + bl;
+    base[bc] = b < B ? (((long long)b * C + c) * H + p) * W : -1;
+  }
+  __syncthreads();
+  if (RW <= nt) {
+    const int k = tid;
+    if (k < RW)
+      for (int bc0 = 0; bc0 < nbc; bc0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int bc = bc0 + u;
+          v[u] = (bc < nbc && base[bc] >= 0) ? __ldg(x + base[bc] + k) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (bc0 + u < nbc) xs[(bc0 + u) * RW + k] = round ? tf32_rna(v[u]) : v[u];
+      }
+  } else {
+    for (int bc = 0; bc < nbc; ++bc)
+      for (int k = tid; k < RW; k += nt) {
+        const float u = base[bc] >= 0 ? __ldg(x + base[bc] + k) : 0.f;
+        xs[bc * RW + k] = round ? tf32_rna(u) : u;
+      }
   }
   __syncthreads();
   // write: thread x = fixed float4 column group of the pixel's nimg x Kcol floats (table lookups
@@ -272,7 +293,7 @@ int launch_im2col(const Layer& L, const float* x, float* xcol, bool round_tf32, 
   // nimg images per block: the pixel row of nimg x Kcol floats is one float4 per thread (<= 256)
   int nimg = 8;
   while (nimg > 1 && ((size_t)nimg * per_img > 48 * 1024 || nimg * L.Kcol / 4 > 256)) nimg >>= 1;
-  if (L.Kcol > kIm2colMaxK || (size_t)nimg * per_img > 48 * 1024 || nimg * L.Kcol / 4 > 256 ||
+  if (L.Kcol > kIm2colMaxK || (size_t)nimg * per_img > 48 * 1024 || nimg * L.Kcol / 4 > 256 || nimg * L.C > kIm2colMaxBC ||
       (int64_t)L.B * L.C * L.H * L.W >= (1ll << 31))
     CP_FAIL(CP_ERR_UNSUPPORTED, "im2col: image layer too large (Kcol > 256 or C*R*W*4 > 48 KB)");
   const int bx = nimg * L.Kcol / 4, by = std::max(1, 256 / bx);
@@ -1075,6 +1096,58 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
     CP_LAUNCHED();
   }
   (void)ws;
+  return CP_OK;
+}
+
+// SGD over up to kSgdMax tensors in one launch: grid-stride over the concatenated
+// float4 index space; the owning tensor is found by a scan of the (short) prefix table.
+constexpr int kSgdMax = 16;
+struct SgdList {
+  float* p[kSgdMax];
+  const float* g[kSgdMax];
+  long long n[kSgdMax];
+  long long off4[kSgdMax + 1];   // prefix of ceil(n/4)
+  int count;
+};
+__global__ void sgd_multi_kernel(const __grid_constant__ SgdList L, float lr) {
+  const long long total = L.off4[L.count];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int t = 0;
+    while (i >= L.off4[t + 1]) ++t;
+    const long long e = (i - L.off4[t]) * 4;
+    float* p = L.p[t];
+    const float* g = L.g[t];
+    if (e + 3 < L.n[t] && ((reinterpret_cast<uintptr_t>(p + e) | reinterpret_cast<uintptr_t>(g + e)) & 15) == 0) {
+      float4 a = *reinterpret_cast<float4*>(p + e);
+      const float4 b = *reinterpret_cast<const float4*>(g + e);
+      a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
+      *reinterpret_cast<float4*>(p + e) = a;
+    } else {
+      for (long long j = e; j < L.n[t] && j < e + 4; ++j) p[j] -= lr * g[j];
+    }
+  }
+}
+
+int cp_sgd_multi(float* const* params, const float* const* grads, const int64_t* sizes, int32_t count, float lr,
+                 void* stream) {
+  if (count < 0 || (count > 0 && (!params || !grads || !sizes))) CP_FAIL(CP_ERR_ARG, "cp_sgd_multi: bad arguments");
+  for (int i0 = 0; i0 < count; i0 += kSgdMax) {
+    SgdList L{};
+    L.off4[0] = 0;
+    for (int i = i0; i < count && L.count < kSgdMax; ++i) {
+      if (sizes[i] < 0 || (sizes[i] > 0 && (!params[i] || !grads[i]))) CP_FAIL(CP_ERR_ARG, "cp_sgd_multi: bad tensor");
+      const int k = L.count++;
+      L.p[k] = params[i];
+      L.g[k] = grads[i];
+      L.n[k] = sizes[i];
+      L.off4[k + 1] = L.off4[k] + (sizes[i] + 3) / 4;
+    }
+    const long long total = L.off4[L.count];
+    if (total == 0) continue;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+    sgd_multi_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(L, lr);
+    CP_LAUNCHED();
+  }
   return CP_OK;
 }
 

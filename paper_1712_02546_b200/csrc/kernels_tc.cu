@@ -1184,9 +1184,10 @@ static Plan dgrad_plan(const Layer& L, TcParams& p) {
 
 static Plan wgrad_plan(const Layer& L, TcParams& p) {
   Plan w{};
-  // CTA pairs even when the last pair is partly empty (measured: single-CTA tiles are slower at
-  // P=4 and P=8 despite the wasted rows)
+  // CTA pairs unless 128-row tiles cover the own kernels with less padding than 256-row pair tiles
+  // (measured: P=4, Kc=376 -> 384 vs 512 rows: single CTAs 10 % faster; equal padding: pairs win)
   w.pair = use_pairs();
+  if (w.pair && !getenv("CP_TC_CTA_GROUP") && roundup(L.Kc, BM) < roundup(L.Kc, 2 * BM)) w.pair = false;
   const int CG = w.pair ? 2 : 1;
   p.span = span_ok(p) ? 1 : 0;
   const int per_tap = build_ntiles(p);

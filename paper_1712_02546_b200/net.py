@@ -201,10 +201,16 @@ class PartitionedNet:
                 da = b["dx"]
 
     def sgd(self, lr, stream=None):
-        for L, b in zip(self.layers, self.buf):
-            cp.conv_part_sgd_step(L, b["w"], b["b"], b["dw"], b["db"], lr, stream)
-        cp.cp_sgd(self.head["wfc"], self.head["dwfc"], lr, stream)
-        cp.cp_sgd(self.head["bfc"], self.head["dbfc"], lr, stream)
+        """SGD on the own conv slices and the head, one fused launch (cp_sgd_multi)."""
+        pairs = []
+        for i, b in enumerate(self.buf):
+            d, kr = self.descs[i], self.parts[i].k_count[self.rank]
+            ktot = (self.sizes[i].w - 256) // 4 // max(kr, 1) if kr else 0
+            pairs.append((b["w"], b["dw"], kr * ktot))
+            pairs.append((b["b"], b["db"], kr))
+        pairs.append((self.head["wfc"], self.head["dwfc"]))
+        pairs.append((self.head["bfc"], self.head["dbfc"]))
+        cp.cp_sgd_multi(pairs, lr, stream)
 
     def step(self, lr=0.01, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True):
         self.forward(stream, comm_stream)
