@@ -328,13 +328,40 @@ def main():
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    # input pipeline: step k+1's images/labels travel host -> device on a copy stream (pinned source,
+    # two staging buffers) while step k computes, inside step k's timed window; step 0's copy is issued
+    # inside its own window.  Each step starts with a device copy staging -> the network's input
+    # buffer and ends with the loss read back to pinned host memory.  L2 flushed between steps.
+    cpy = torch.cuda.Stream(dev)
+    stage = [(torch.empty_like(pn.x), torch.empty_like(pn.labels)) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+
+    def prefetch(k):
+        j = k & 1
+        with torch.cuda.stream(cpy):
+            cpy.wait_event(free[j])
+            stage[j][0].copy_(x_host.reshape(-1), non_blocking=True)
+            stage[j][1].copy_(y_host, non_blocking=True)
+            ready[j].record(cpy)
+    for j in range(2):
+        free[j].record(s)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for k in range(args.steps):
+        j = k & 1
         if flush is not None:
             flush.fill_(k & 0xFF)
         e2e_ev[k][0].record(s)
-        pn.x.copy_(x_host.reshape(-1), non_blocking=True)
-        pn.labels.copy_(y_host, non_blocking=True)
+        if k == 0:
+            cpy.wait_stream(s)
+            prefetch(0)
+        s.wait_event(ready[j])
+        pn.x.copy_(stage[j][0])
+        pn.labels.copy_(stage[j][1])
+        free[j].record(s)
+        if k + 1 < args.steps:
+            cpy.wait_stream(s)
+            prefetch(k + 1)
         step()
         loss_host.copy_(pn.head["loss"][:1], non_blocking=True)
         e2e_ev[k][1].record(s)
