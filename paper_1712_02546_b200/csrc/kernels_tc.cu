@@ -85,6 +85,8 @@ struct TcParams {
   int nsched;          // >0: per-group unit lists (host LPT schedule); 0: static round-robin
   short sched_off[MAX_GROUPS + 1];
   short sched[MAX_SCHED];
+  int pix;             // dgrad pixel mode: a CTA's 128 rows = 128 images of ONE input pixel, a pair = two
+                       // horizontally adjacent pixels (exact valid rows, s-union only at borders)
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
   short win_order[MAX_WIN];
   const float* bias;
@@ -152,7 +154,14 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     t.nt = rest % p.numN;
     t.sp = rest / p.numN;
   }
-  if (PASS == PASS_FWD || PASS == PASS_DGRAD) {
+  if (PASS == PASS_DGRAD && p.pix) {
+    const int nbc = p.Bp / 128, W2 = p.Win / 2;
+    t.bc = mg % nbc;                  // 128-image chunk
+    const int ij = mg / nbc;
+    t.j = ij % W2;                    // pixel pair: columns 2j (CTA 0), 2j+1 (CTA 1)
+    t.i = ij / W2;                    // input row
+    t.mt = mg;
+  } else if (PASS == PASS_FWD || PASS == PASS_DGRAD) {
     const int nbcg = p.Bp / 32 / CG;
     const int W2 = (PASS == PASS_FWD ? p.Wo : p.Win) / 2;
     t.bc = (mg % nbcg) * CG + rank;
@@ -206,8 +215,10 @@ struct Chunk {
 
 // dgrad: taps (r,s) whose shifted 2x2 window hits the dY grid: r in [r_lo, r_hi], s in [s_lo, s_hi]
 __device__ __forceinline__ void dgrad_taps(const TcParams& p, const Unit& t, int& r_lo, int& nr, int& s_lo, int& ns) {
-  r_lo = max(0, 2 * t.i - p.Ho + 1);
-  const int r_hi = min(p.R - 1, 2 * t.i + 1);
+  // window mode: input rows 2i, 2i+1; pixel mode: the single input row i
+  const int h0 = p.pix ? t.i : 2 * t.i, h1 = p.pix ? t.i : 2 * t.i + 1;
+  r_lo = max(0, h0 - p.Ho + 1);
+  const int r_hi = min(p.R - 1, h1);
   s_lo = max(0, 2 * t.j - p.Wo + 1);
   const int s_hi = min(p.S - 1, 2 * t.j + 1);
   nr = r_hi - r_lo + 1;
@@ -401,7 +412,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.r, s = ch.s;
-            ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
+            if (p.pix)
+              ld4(a, &p.maps[0], ch.c * BK, t.bc * 128, 2 * t.j + (int)rank - s, t.i - r);
+            else
+              ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
             if (p.wide) {
               ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BK, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> 5, ch.tap);
             } else {
@@ -661,7 +675,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             if (chunk_ok) {
               const int kw = p.kw[rb];
               const int c4 = (lane & 7) * 4;
-              float* base = p.dst[rb] + ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + t.bc * 32) * kw + slot;
+              float* base = p.dst[rb] + (p.pix ? ((int64_t)(t.i * p.Win + 2 * t.j + (int)rank) * p.Bp + t.bc * 128 + quad * 32)
+                                                : ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + t.bc * 32)) * kw + slot;
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 const int row = k * 4 + (lane >> 3);
@@ -683,7 +698,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           } else if (!p.span || slot < p.kw[rb]) {
             const int kw = p.kw[rb];
             const int64_t o = (int64_t)t.sp * p.part_stride + p.start[rb] +
-                              ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb) * kw + slot;
+                              (p.pix ? ((int64_t)(t.i * p.Win + 2 * t.j + (int)rank) * p.Bp + t.bc * 128 + row)
+                                     : ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb)) * kw + slot;
             store_f32x32(p.out + o, v, ncol);
           }
         } else {
@@ -1167,16 +1183,20 @@ static Plan dgrad_plan(const Layer& L, TcParams& p) {
   const int CG = w.pair ? 2 : 1;
   p.span = span_ok(p) ? 1 : 0;
   w.numN = build_ntiles(p);
-  w.numM = (L.H / 2) * (L.W / 2) * (L.Bp / 32) / CG;
-  // average valid taps of a 2x2 window: (sum over window rows of valid r) * (same for s) / windows
-  auto avg_valid = [](int Hin, int Ho, int R) {
+  // pixel mode (pairs, 128-image chunks): valid taps per input row are exact, the pair's column
+  // union wastes only at the borders (paper net: 1.08x the exact MACs vs 1.17x for 2x2 windows)
+  p.pix = (w.pair && L.Bp % 128 == 0 && env_int("CP_TC_DGRAD_PIX", 1)) ? 1 : 0;
+  w.numM = p.pix ? L.H * (L.W / 2) * (L.Bp / 128) : (L.H / 2) * (L.W / 2) * (L.Bp / 32) / CG;
+  // average valid taps of a tile: (sum over tile rows of valid r) * (same for s) / tiles
+  auto avg_valid = [](int Hin, int Ho, int R, int rows) {
     double t = 0;
-    for (int i = 0; i < Hin / 2; ++i)
-      t += std::min(R - 1, 2 * i + 1) - std::max(0, 2 * i - Ho + 1) + 1;
-    return t / (Hin / 2);
+    const int n = Hin / rows;
+    for (int i = 0; i < n; ++i)
+      t += std::min(R - 1, rows * i + rows - 1) - std::max(0, rows * i - Ho + 1) + 1;
+    return t / n;
   };
   const double kc = (L.Kc + BK - 1) / BK;
-  w.chunks = (int)(avg_valid(L.H, L.Ho, L.R) * avg_valid(L.W, L.Wo, L.S) * kc + 0.5);
+  w.chunks = (int)(avg_valid(L.H, L.Ho, L.R, p.pix ? 1 : 2) * avg_valid(L.W, L.Wo, L.S, 2) * kc + 0.5);
   w.S = env_int("CP_TC_SPLIT_DGRAD", 0);
   if (w.S <= 0) w.S = choose_split(w.numM * w.numN, num_sms() / CG, w.chunks, (double)L.in.start[L.in.n] * 4, 16);
   return w;
@@ -1383,7 +1403,15 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     p.fused_dx = 1;
     for (int r = 0; r < L.in.n; ++r) p.dst[r] = dst_blocks[r];
   }
-  CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false));
+  if (p.pix) {
+    // A = dY rows of one pixel: box {32 kernels, 128 images, 1, 1}
+    const uint64_t dims[4] = {(uint64_t)L.Kc, (uint64_t)L.Bp, (uint64_t)L.Wo, (uint64_t)L.Ho};
+    const uint64_t str[3] = {(uint64_t)L.Kc * 4, (uint64_t)L.Kc * L.Bp * 4, (uint64_t)L.Kc * L.Bp * L.Wo * 4};
+    const uint32_t box[4] = {32, 128, 1, 1};
+    CP_TRY(make_map(&p.maps[0], dY, 4, dims, str, box, false));
+  } else {
+    CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false));
+  }
   p.wide = 1;
   for (int r = 0; r < L.in.n; ++r)
     if (L.in.coff[r] % 32) p.wide = 0;
@@ -1410,7 +1438,7 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     const int H2 = L.H / 2, W2 = L.W / 2;
     // off by default: measured slower at P=1/2/4 (heavy windows dispatched together lose the
     // spatial L2 locality of the natural order)
-    if (H2 * W2 <= MAX_WIN && env_int("CP_TC_DGRAD_LPT", 0)) {
+    if (!p.pix && H2 * W2 <= MAX_WIN && env_int("CP_TC_DGRAD_LPT", 0)) {
       std::vector<std::pair<int, int>> wk;
       for (int i = 0; i < H2; ++i)
         for (int j = 0; j < W2; ++j) {
@@ -1434,12 +1462,13 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     // in natural order (keeps the spatial L2 locality of neighbouring windows).
     const int CG = pl.pair ? 2 : 1, G = std::min(p.units, num_sms() / CG);
     if (p.nwin_order == 0 && p.units <= MAX_SCHED && G <= MAX_GROUPS && env_int("CP_TC_DGRAD_SCHED", 1)) {
-      const int nbcg = L.Bp / 32 / CG, W2 = L.W / 2, kc = (L.Kc + BK - 1) / BK;
+      const int nbcg = p.pix ? L.Bp / 128 : L.Bp / 32 / CG, W2 = L.W / 2, kc = (L.Kc + BK - 1) / BK;
       std::vector<std::pair<long long, int>> wk(p.units);
       for (int u = 0; u < p.units; ++u) {
         const int mg = u % p.numM;
         const int ij = mg / nbcg, i = ij / W2, j = ij % W2;
-        const int nr = std::min(L.R - 1, 2 * i + 1) - std::max(0, 2 * i - L.Ho + 1) + 1;
+        const int h0 = p.pix ? i : 2 * i, h1 = p.pix ? i : 2 * i + 1;
+        const int nr = std::min(L.R - 1, h1) - std::max(0, h0 - L.Ho + 1) + 1;
         const int ns = std::min(L.S - 1, 2 * j + 1) - std::max(0, 2 * j - L.Wo + 1) + 1;
         const long long work = ((long long)nr * ns * kc + pl.S - 1) / pl.S;
         wk[u] = {-work, u};

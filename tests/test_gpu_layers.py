@@ -55,8 +55,9 @@ def window_gap(z, relu=True):
 
 
 # (P, B, align): B=20 -> one 32-image chunk (single-CTA tiles); align=32 -> block widths multiple
-# of 32, so dgrad/wgrad N tiles span rank blocks
-PB = [(1, 40, 8), (2, 40, 8), (3, 40, 8), (1, 20, 8), (2, 40, 32), (4, 40, 32)]
+# of 32, so dgrad/wgrad N tiles span rank blocks; B=128 / 100 -> 128-image chunks: dgrad pixel
+# mode (B=100: ragged, 28 padded images per chunk)
+PB = [(1, 40, 8), (2, 40, 8), (3, 40, 8), (1, 20, 8), (2, 40, 32), (4, 40, 32), (2, 128, 8), (1, 100, 32)]
 
 
 @pytest.mark.parametrize("math", MATHS)
