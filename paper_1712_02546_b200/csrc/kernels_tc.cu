@@ -231,28 +231,74 @@ __device__ __forceinline__ void dgrad_taps(const TcParams& p, const Unit& t, int
 template <int PASS, class F>
 __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t, F f) {
   if (PASS == PASS_FWD) {
-    const int total = p.R * p.S * p.cpt;
+    const int RS = p.R * p.S;
+    const int total = RS * p.cpt;
     const int per = t.tail ? p.tail_per : (total + p.split - 1) / p.split;
     const int lo = (t.tail ? t.piece : t.sp) * per, hi = min(total, lo + per);
-    int idx = 0;
+    if (lo >= hi) return;
+    // decode chunk `lo` once, then step the coordinates (this loop runs on the single producer and
+    // MMA threads, one iteration per ~900 tensor cycles)
     if (p.arrive) {
-      // overlapped gather: input blocks outermost, starting with the own block
-      for (int bi = 0, rb = p.self_blk; bi < p.nblk; ++bi, rb = rb + 1 == p.nblk ? 0 : rb + 1) {
-        const int kw = p.kw[rb];
-        for (int r = 0, tap = 0; r < p.R; ++r)
-          for (int sx = 0; sx < p.S; ++sx, ++tap)
-            for (int c = 0; c * BK < kw; ++c, ++idx)
-              if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
+      // overlapped gather: input blocks outermost (own block first), then tap, then channel chunk
+      int rb = p.self_blk, rem = lo;
+      int nc = (p.kw[rb] + BK - 1) / BK;
+      while (rem >= nc * RS) {
+        rem -= nc * RS;
+        rb = rb + 1 == p.nblk ? 0 : rb + 1;
+        nc = (p.kw[rb] + BK - 1) / BK;
+      }
+      int tap = rem / nc, c = rem - tap * nc;
+      int r = tap / p.S, sx = tap - r * p.S;
+      int kw = p.kw[rb];
+      for (int idx = lo; idx < hi; ++idx) {
+        f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
+        if (++c == nc) {
+          c = 0;
+          ++tap;
+          if (++sx == p.S) {
+            sx = 0;
+            ++r;
+          }
+          if (tap == RS) {
+            tap = r = sx = 0;
+            do {
+              rb = rb + 1 == p.nblk ? 0 : rb + 1;
+              nc = (p.kw[rb] + BK - 1) / BK;
+            } while (nc == 0);
+            kw = p.kw[rb];
+          }
+        }
       }
       return;
     }
-    for (int r = 0, tap = 0; r < p.R; ++r)
-      for (int sx = 0; sx < p.S; ++sx, ++tap)
-        for (int rb = 0; rb < p.nblk; ++rb) {
-          const int kw = p.kw[rb];
-          for (int c = 0; c * BK < kw; ++c, ++idx)
-            if (idx >= lo && idx < hi) f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
-        }
+    // tap outermost, then input block, then channel chunk
+    int tap = lo / p.cpt, rem = lo - tap * p.cpt;
+    int rb = 0, nc = (p.kw[0] + BK - 1) / BK;
+    while (rem >= nc) {
+      rem -= nc;
+      ++rb;
+      nc = (p.kw[rb] + BK - 1) / BK;
+    }
+    int c = rem, r = tap / p.S, sx = tap - r * p.S;
+    int kw = p.kw[rb];
+    for (int idx = lo; idx < hi; ++idx) {
+      f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
+      if (++c == nc) {
+        c = 0;
+        do {
+          if (++rb == p.nblk) {
+            rb = 0;
+            ++tap;
+            if (++sx == p.S) {
+              sx = 0;
+              ++r;
+            }
+          }
+          nc = (p.kw[rb] + BK - 1) / BK;
+        } while (nc == 0 && tap < RS);
+        kw = p.kw[rb];
+      }
+    }
   } else if (PASS == PASS_DGRAD) {
     int r_lo, nr, s_lo, ns;
     dgrad_taps(p, t, r_lo, nr, s_lo, ns);
