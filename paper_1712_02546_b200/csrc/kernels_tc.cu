@@ -309,11 +309,20 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     // kernel chunk outermost: all CTAs of a wave stream the same 32-kernel slice of W and dY at
     // the same time (a few MB live in L2) instead of every tap of the whole tensors.  Nested loops
     // with a running index: no integer division on the MMA issue path.
-    int idx = 0;
-    for (int c = 0; c < kc; ++c)
-      for (int r = r_lo; r < r_lo + nr; ++r)
-        for (int sx = s_lo; sx < s_lo + ns; ++sx, ++idx)
-          if (idx >= lo && idx < hi) f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8, r, sx, 0, 0, 0});
+    if (lo >= hi) return;
+    const int nt = nr * ns;
+    int c = lo / nt, rem = lo - c * nt;
+    int r = r_lo + rem / ns, sx = s_lo + rem % ns;
+    for (int idx = lo; idx < hi; ++idx) {
+      f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8, r, sx, 0, 0, 0});
+      if (++sx == s_lo + ns) {
+        sx = s_lo;
+        if (++r == r_lo + nr) {
+          r = r_lo;
+          ++c;
+        }
+      }
+    }
   } else {
     const int c0 = t.tail ? t.piece * p.tail_per : t.sp * p.chunks_per_split;
     const int c1 = min(p.chunks_total, c0 + (t.tail ? p.tail_per : p.chunks_per_split));
