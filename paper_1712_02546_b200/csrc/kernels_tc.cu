@@ -1272,7 +1272,8 @@ static Plan wgrad_plan(const Layer& L, TcParams& p) {
   w.S = env_int("CP_TC_SPLIT_WGRAD", 0);
   if (w.S <= 0) {
     const int units = std::max(1, w.numM * w.numN), G = num_sms() / CG;
-    w.S = choose_split(units, G, w.chunks, (double)L.Kr * L.Ktot * 4, 32);
+    // up to one split per CTA group: a skinny single-tile GEMM (conv1 wgrad) needs every SM streaming K
+    w.S = choose_split(units, G, w.chunks, (double)L.Kr * L.Ktot * 4, G);
     if (w.S > 1 && env_int("CP_TC_WGRAD_TAIL", 1)) {
       // S = 1 with the last round split along K (tc_wgrad) vs the whole-tensor split-K
       const int rounds = (units + G - 1) / G, T = units - (rounds - 1) * G;
@@ -1597,7 +1598,9 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   const int CG = w.pair ? 2 : 1, G = num_sms() / CG;
   const int rounds = (p.units + G - 1) / G, T = p.units - (rounds - 1) * G;
   if (w.S == 1 && rounds > 1 && T > 0 && 2 * T <= G && T <= MAX_TAIL && env_int("CP_TC_WGRAD_TAIL", 1)) {
-    int st = std::max(1, std::min(G / T, w.chunks));
+    // pieces per tail unit: <= 16 - a few leftover units split 74 ways cost more in partial-tile
+    // traffic and reduce latency than the shorter pieces save (measured P=4, T=2)
+    int st = std::max(1, std::min(std::min(G / T, env_int("CP_TC_TAIL_MAX", 16)), w.chunks));
     const int per = (w.chunks + st - 1) / st;
     st = (w.chunks + per - 1) / per;                   // every piece non-empty
     p.tail_full = (rounds - 1) * G;
