@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--net", default="500:1500")
     ap.add_argument("--math", default="tf32", choices=["tf32", "simt"])
+    ap.add_argument("--probe-times", default=None,
+                    help="comma-separated injected per-device probe times (s): Eq. 1 partition from these "
+                         "instead of measuring (heterogeneous-device emulation, SURVEY §8(f) f3)")
     ap.add_argument("--partition", default="even", choices=["even", "probe"],
                     help="even split, or Eq. 1 from the paper's probe (times all-gathered)")
     ap.add_argument("--dx", default="rs", choices=["rs", "ar"])
@@ -226,7 +229,12 @@ def main():
 
     # ---- partition map: even, or Eq. 1 from the paper's probe convolution (§4.1.1)
     probe_times = None
-    if args.partition == "probe" and world > 1:
+    if args.probe_times and world > 1:
+        probe_times = [float(v) for v in args.probe_times.split(",")]
+        if len(probe_times) != world:
+            raise SystemExit(f"--probe-times needs {world} values")
+        parts = [cp.cp_partition_plan(probe_times, K) for K in net.kernels]
+    elif args.partition == "probe" and world > 1:
         d = cp.cp_conv_desc()
         c, h = net.shapes()[1][0], net.shapes()[1][1]
         d.batch, d.in_c, d.in_h, d.in_w, d.num_k, d.k_h, d.k_w = B, c, h, h, net.kernels[1], 5, 5
@@ -450,7 +458,8 @@ def main():
                             f"pool -> FC {net.fc_in}->10 -> softmax), {net.in_hw}x{net.in_hw}x3 synthetic images, "
                             f"batch {B}",
                 "global_batch": B, "partition": [list(p.k_count[:p.n_ranks]) for p in parts],
-                "partition_source": "Eq.1 from probe" if probe_times else "even",
+                "partition_source": ("Eq.1 from injected times" if args.probe_times else "Eq.1 from probe")
+                                    if probe_times else "even",
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
                 "head": pn.head_mode, "cuda_graph": graph is not None,
                 "collectives": ("fused into the GEMM epilogues over NVLink peer memory (gather: forward "
