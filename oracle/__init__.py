@@ -65,6 +65,8 @@ def lib():
                 "orc_bias_grad": [_D, _i, _i, _i, _i, _D],
                 "orc_relu_pool_fwd": [_D, _i, _i, _i, _i, _i, _i, _D, _U8],
                 "orc_unpool_relu_bwd": [_D, _U8, _D, _i, _i, _i, _i, _i, _i, _D],
+                "orc_lrn_fwd": [_D, _i, _i, _i, _i, _i, ctypes.c_double, ctypes.c_double, ctypes.c_double, _D],
+                "orc_lrn_bwd": [_D, _D, _i, _i, _i, _i, _i, ctypes.c_double, ctypes.c_double, ctypes.c_double, _D],
                 "orc_fc_fwd": [_D, _i, _i, _D, _D, _i, _D],
                 "orc_fc_bwd": [_D, _D, _D, _i, _i, _i, _D, _D, _D],
                 "orc_softmax_xent": [_D, _I32, _i, _i, _D, _D],
@@ -221,6 +223,28 @@ def unpool_relu_bwd(da, argmax, a, relu=True, pool=True):
     return dy
 
 
+LRN_DEFAULT = {"depth": 5, "alpha": 1e-4, "beta": 0.75, "bias": 2.0}
+
+
+def lrn_fwd(x, depth=5, alpha=1e-4, beta=0.75, bias=2.0):
+    """Cross-channel LRN (form S:L89-97): out = in * (bias + alpha*sum_window in^2)^-beta."""
+    x = _f64(x)
+    B, C, H, W = x.shape
+    out = np.empty_like(x)
+    _chk(lib().orc_lrn_fwd(_d(x), B, C, H, W, int(depth), float(alpha), float(beta), float(bias), _d(out)), "lrn_fwd")
+    return out
+
+
+def lrn_bwd(x, dout, depth=5, alpha=1e-4, beta=0.75, bias=2.0):
+    """Gradient of lrn_fwd w.r.t. its input (chain rule written out)."""
+    x, dout = _f64(x), _f64(dout)
+    B, C, H, W = x.shape
+    din = np.empty_like(x)
+    _chk(lib().orc_lrn_bwd(_d(x), _d(dout), B, C, H, W, int(depth), float(alpha), float(beta), float(bias),
+                           _d(din)), "lrn_bwd")
+    return din
+
+
 def fc_fwd(a, wfc, bfc):
     a = _f64(a).reshape(a.shape[0], -1)
     wfc, bfc = _f64(wfc), _f64(bfc)
@@ -304,13 +328,14 @@ def net_step(params, x, y, lr, layers, part=None, replay=None):
     """One SGD training step of the conv net, unsplit or kernel-partitioned.
 
     params: dict with 'w{i}', 'b{i}' per conv layer i (KCRS / K) and 'wfc' [O,F], 'bfc' [O].
-    layers: list of dicts {'relu': bool, 'pool': bool} per conv layer.
+    layers: list of dicts {'relu': bool, 'pool': bool[, 'lrn': {depth, alpha, beta, bias}]} per conv
+            layer; with 'lrn' the layer is Conv -> ReLU -> LRN -> Pool.
     part:   None (unsplit) or list per conv layer of (k_begin, k_count) arrays: the
             layer's kernels are evaluated slice by slice and concatenated in channel
             order (Alg. 1 L15-22); partial dX are summed in rank
             order (north_star "partial dX contributions are summed").
-    replay: None or per-layer dict {'argmax': uint8 NCHW, 'a': pooled output} — decision
-            replay of a GPU's argmax/ReLU decisions in the backward pass (reading R15).
+    replay: None or per-layer dict {'argmax': uint8 NCHW, 'a': pooled output[, 'pre': pre-LRN map]} —
+            decision replay of a GPU's argmax/ReLU decisions in the backward pass (reading R15).
     Returns a trace dict with every intermediate and the updated params.
     """
     tr = {"x": _f64(x)}
@@ -324,7 +349,15 @@ def net_step(params, x, y, lr, layers, part=None, replay=None):
             kb, kc = part[i]
             z = np.concatenate([conv_fwd(act, w[kb[r]:kb[r] + kc[r]], b[kb[r]:kb[r] + kc[r]])
                                 for r in range(len(kb)) if kc[r] > 0], axis=1)
-        a, am = relu_pool_fwd(z, L["relu"], L["pool"])
+        lrn = L.get("lrn")
+        if lrn:
+            # Conv -> (bias, ReLU) -> Normalization -> Pool (reading R23)
+            r_, _ = relu_pool_fwd(z, L["relu"], False)
+            nrm = lrn_fwd(r_, **lrn)
+            a, am = relu_pool_fwd(nrm, False, L["pool"])
+            tr[f"pre{i}"], tr[f"nrm{i}"] = r_, nrm
+        else:
+            a, am = relu_pool_fwd(z, L["relu"], L["pool"])
         tr[f"in{i}"], tr[f"z{i}"], tr[f"a{i}"], tr[f"argmax{i}"] = act, z, a, am
         act = a
     logits = fc_fwd(act, params["wfc"], params["bfc"])
@@ -337,7 +370,14 @@ def net_step(params, x, y, lr, layers, part=None, replay=None):
         tr[f"da{i}"] = da
         am = tr[f"argmax{i}"] if replay is None else replay[i]["argmax"]
         a = tr[f"a{i}"] if replay is None else _f64(replay[i]["a"])
-        dy = unpool_relu_bwd(da, am, a, L["relu"], L["pool"])
+        if L.get("lrn"):
+            dn = unpool_relu_bwd(da, am, a, False, L["pool"])
+            dpre = lrn_bwd(tr[f"pre{i}"], dn, **L["lrn"])
+            # ReLU' from the pre-LRN map (replay: the GPU's map decides, reading R15)
+            pre = tr[f"pre{i}"] if replay is None or "pre" not in replay[i] else _f64(replay[i]["pre"])
+            dy = unpool_relu_bwd(dpre, None, pre, L["relu"], False)
+        else:
+            dy = unpool_relu_bwd(da, am, a, L["relu"], L["pool"])
         w = params[f"w{i}"]
         R, S = w.shape[2], w.shape[3]
         inp = tr[f"in{i}"]

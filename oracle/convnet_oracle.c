@@ -21,6 +21,7 @@
 #define ORC_OK 0
 #define ORC_ERR_ARG -1
 #define ORC_ERR_SHAPE -2
+#define ORC_ERR_CONFIG -3
 #define ORC_ERR_DATA -4
 
 #define IX4(a, b, c, d, B_, C_, D_) ((((int64_t)(a) * (B_) + (b)) * (C_) + (c)) * (D_) + (d))
@@ -263,6 +264,67 @@ int orc_unpool_relu_bwd(const double* da, const uint8_t* argmax, const double* a
           if (code > 3) continue;
           if (relu && !(a[o] > 0.0)) continue;
           dy[IX4(b, k, 2 * i + (code >> 1), 2 * j + (code & 1), K, H, W)] = da[o];
+        }
+  return ORC_OK;
+}
+
+/* --------------------------------------------------------------------------
+ * Local response normalisation across channels — the paper's "Normalization layer"
+ * (form unspecified there, SPEC S:L89-97 and design decision S:L135):
+ *   s[b,c,h,w]   = bias + alpha * sum_{j=max(0,c-n/2)}^{min(C-1,c+n/2)} in[b,j,h,w]^2
+ *   out[b,c,h,w] = in[b,c,h,w] * s^(-beta)            (n = depth, odd; window clipped)
+ * Errors: depth even or < 1, bias <= 0 -> configuration error.
+ * -------------------------------------------------------------------------- */
+static double lrn_scale(const double* in, int b, int c, int h, int w, int C, int H, int W, int half,
+                        double alpha, double bias) {
+  double acc = 0.0;
+  const int j0 = c - half < 0 ? 0 : c - half, j1 = c + half > C - 1 ? C - 1 : c + half;
+  for (int j = j0; j <= j1; ++j) {
+    const double v = in[IX4(b, j, h, w, C, H, W)];
+    acc += v * v;
+  }
+  return bias + alpha * acc;
+}
+
+int orc_lrn_fwd(const double* in, int B, int C, int H, int W, int depth, double alpha, double beta,
+                double bias, double* out) {
+  if (!in || !out) return ORC_ERR_ARG;
+  if (depth < 1 || depth % 2 == 0 || !(bias > 0.0)) return ORC_ERR_CONFIG;
+  const int half = depth / 2;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int b = 0; b < B; ++b)
+    for (int c = 0; c < C; ++c)
+      for (int h = 0; h < H; ++h)
+        for (int w = 0; w < W; ++w) {
+          const double s = lrn_scale(in, b, c, h, w, C, H, W, half, alpha, bias);
+          out[IX4(b, c, h, w, C, H, W)] = in[IX4(b, c, h, w, C, H, W)] * pow(s, -beta);
+        }
+  return ORC_OK;
+}
+
+/* Backward by the chain rule written out ("backward matches finite differences"):
+ *   din[c] = sum_{j : |j-c| <= n/2, 0<=j<C} dout[j] * d out[j] / d in[c]
+ *   d out[j] / d in[c] = [j==c] s_j^(-beta) - 2 alpha beta in[j] in[c] s_j^(-beta-1)        */
+int orc_lrn_bwd(const double* in, const double* dout, int B, int C, int H, int W, int depth, double alpha,
+                double beta, double bias, double* din) {
+  if (!in || !dout || !din) return ORC_ERR_ARG;
+  if (depth < 1 || depth % 2 == 0 || !(bias > 0.0)) return ORC_ERR_CONFIG;
+  const int half = depth / 2;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int b = 0; b < B; ++b)
+    for (int c = 0; c < C; ++c)
+      for (int h = 0; h < H; ++h)
+        for (int w = 0; w < W; ++w) {
+          const double xc = in[IX4(b, c, h, w, C, H, W)];
+          double acc = 0.0;
+          const int j0 = c - half < 0 ? 0 : c - half, j1 = c + half > C - 1 ? C - 1 : c + half;
+          for (int j = j0; j <= j1; ++j) {
+            const double sj = lrn_scale(in, b, j, h, w, C, H, W, half, alpha, bias);
+            double d = -2.0 * alpha * beta * in[IX4(b, j, h, w, C, H, W)] * xc * pow(sj, -beta - 1.0);
+            if (j == c) d += pow(sj, -beta);
+            acc += dout[IX4(b, j, h, w, C, H, W)] * d;
+          }
+          din[IX4(b, c, h, w, C, H, W)] = acc;
         }
   return ORC_OK;
 }

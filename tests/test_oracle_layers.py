@@ -212,3 +212,44 @@ def test_sgd_examples(orc):
     p = rnd((7,), 33)
     assert np.array_equal(orc.sgd(p, rnd((7,), 34), 0.0), p)
     assert np.array_equal(orc.sgd(np.array([1.0]), np.array([2.0]), 0.5), [0.0])
+
+
+# ------------------------------------------------------------------ LRN (form S:L89-97)
+def test_lrn_spec_examples(orc):
+    out = orc.lrn_fwd(np.array([2.0]).reshape(1, 1, 1, 1), depth=1, alpha=1.0, beta=1.0, bias=1.0)
+    assert out[0, 0, 0, 0] == pytest.approx(0.4, abs=1e-15)
+    x = rnd((2, 5, 3, 3), 41)
+    np.testing.assert_array_equal(orc.lrn_fwd(x, alpha=0.0, bias=1.0), x)   # S:L96 identity
+    np.testing.assert_allclose(orc.lrn_fwd(x, alpha=0.0, beta=0.75, bias=2.0), x / 2.0 ** 0.75, rtol=1e-15)
+    with pytest.raises(Exception):
+        orc.lrn_fwd(x, depth=4)                                           # S:L93 even depth
+    with pytest.raises(Exception):
+        orc.lrn_fwd(x, bias=0.0)                                          # S:L92 bias > 0
+
+
+@pytest.mark.parametrize("depth,alpha,beta,bias", [(5, 1e-4, 0.75, 2.0), (3, 0.3, 0.6, 1.5), (5, 0.05, 0.75, 1.0)])
+def test_lrn_matches_torch(orc, depth, alpha, beta, bias):
+    """torch's local_response_norm divides alpha by the window size: alpha_torch = alpha * depth."""
+    x = rnd((2, 7, 4, 5), 42)
+    ref = F.local_response_norm(torch.from_numpy(x), depth, alpha=alpha * depth, beta=beta, k=bias).numpy()
+    np.testing.assert_allclose(orc.lrn_fwd(x, depth, alpha, beta, bias), ref, rtol=1e-13, atol=1e-15)
+    xt = torch.from_numpy(x).requires_grad_()
+    g = rnd(x.shape, 43)
+    F.local_response_norm(xt, depth, alpha=alpha * depth, beta=beta, k=bias).backward(torch.from_numpy(g))
+    np.testing.assert_allclose(orc.lrn_bwd(x, g, depth, alpha, beta, bias), xt.grad.numpy(), rtol=1e-12, atol=1e-14)
+
+
+def test_lrn_finite_differences(orc):
+    """random 1x5x4x4 input, backward vs central finite differences, rel err < 1e-6."""
+    x = rnd((1, 5, 4, 4), 44)
+    g = rnd(x.shape, 45)
+    kw = dict(depth=5, alpha=0.2, beta=0.75, bias=1.5)   # alpha large enough that the cross terms matter
+    din = orc.lrn_bwd(x, g, **kw)
+    eps = 1e-6
+    num = np.zeros_like(x)
+    for idx in np.ndindex(*x.shape):
+        xp, xm = x.copy(), x.copy()
+        xp[idx] += eps
+        xm[idx] -= eps
+        num[idx] = (np.sum(g * orc.lrn_fwd(xp, **kw)) - np.sum(g * orc.lrn_fwd(xm, **kw))) / (2 * eps)
+    assert np.max(np.abs(din - num)) / np.max(np.abs(num)) < 1e-6

@@ -144,3 +144,25 @@ def test_training_progress(orc):
         losses.append(tr["loss"])
         params = tr["new_params"]
     assert losses[-1] < losses[0] - 1e-3
+
+
+def test_net_step_with_lrn_matches_torch(orc):
+    """Conv -> ReLU -> LRN -> Pool per conv layer, whole step vs torch float64 autograd."""
+    net = small_net()
+    params, x, y = setup(net)
+    lrn = {"depth": 5, "alpha": 0.05, "beta": 0.75, "bias": 2.0}
+    layers = [dict(L, lrn=lrn) for L in net.layers()]
+    tr = orc.net_step(params, x, y, 0.01, layers)
+    t = {k: torch.from_numpy(v).clone().requires_grad_() for k, v in params.items()}
+    a = torch.from_numpy(x)
+    for i in range(len(net.kernels)):
+        a = F.relu(F.conv2d(a, t[f"w{i}"], t[f"b{i}"]))
+        a = F.local_response_norm(a, 5, alpha=lrn["alpha"] * 5, beta=lrn["beta"], k=lrn["bias"])
+        a = F.max_pool2d(a, 2)
+    logits = a.reshape(a.shape[0], -1) @ t["wfc"].T + t["bfc"]
+    loss = F.cross_entropy(logits, torch.from_numpy(y.astype(np.int64)))
+    loss.backward()
+    assert tr["loss"] == pytest.approx(loss.item(), rel=1e-12)
+    for k, v in t.items():
+        g = v.grad.numpy()
+        np.testing.assert_allclose(tr["grads"][k], g, rtol=1e-9, atol=1e-13 * max(1, np.abs(g).max()))
