@@ -55,6 +55,8 @@ def parse():
                     help="on: collectives fused into the GEMM epilogues over NVLink peer memory (channel "
                          "gather from the forward epilogue, dX reduce-scatter from the dgrad epilogue); "
                          "off: NCCL AllGather / ReduceScatter kernels")
+    ap.add_argument("--lrn", action="store_true",
+                    help="paper-literal net: Conv -> ReLU -> LRN -> Pool per conv layer (SPEC constants; NEXT row f2)")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
@@ -253,7 +255,7 @@ def main():
         parts = [cp.cp_partition_plan([1.0] * world, K) for K in net.kernels]
 
     pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev, head=args.head,
-                        in_hw=net.in_hw, fused=args.fused == "on")
+                        in_hw=net.in_hw, fused=args.fused == "on", lrn=cp.LRN_DEFAULT if args.lrn else None)
     params = synth.params(net, seed=42)
     pn.load_params(params)
     x, y = synth.images(B, 3, net.in_hw, net.in_hw, step=0)
@@ -454,14 +456,15 @@ def main():
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "tf32" if math == cp.CP_MATH_TF32 else "f32", "data": "synthetic",
             "config": {
-                "workload": f"{net.name} (conv5x5 {net.kernels[0]} -> pool -> conv5x5 {net.kernels[1]} -> "
-                            f"pool -> FC {net.fc_in}->10 -> softmax), {net.in_hw}x{net.in_hw}x3 synthetic images, "
-                            f"batch {B}",
+                "workload": f"{net.name} (conv5x5 {net.kernels[0]} -> {'LRN -> ' if args.lrn else ''}pool -> conv5x5 "
+                            f"{net.kernels[1]} -> {'LRN -> ' if args.lrn else ''}pool -> FC {net.fc_in}->10 -> softmax), "
+                            f"{net.in_hw}x{net.in_hw}x3 synthetic images, batch {B}",
                 "global_batch": B, "partition": [list(p.k_count[:p.n_ranks]) for p in parts],
                 "partition_source": ("Eq.1 from injected times" if args.probe_times else "Eq.1 from probe")
                                     if probe_times else "even",
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
                 "head": pn.head_mode, "cuda_graph": graph is not None,
+                "lrn": dict(cp.LRN_DEFAULT) if args.lrn else None,
                 "collectives": ("fused into the GEMM epilogues over NVLink peer memory (gather: forward "
                                 "epilogue stores + arrival flags; dX reduce-scatter: dgrad epilogue stores "
                                 "+ slot sum)" if pn.sym else "NCCL AllGather / ReduceScatter")

@@ -290,6 +290,26 @@ int cp_softmax_xent(const float* logits, const int32_t* labels, int32_t B, int32
 int cp_fc_backward(const float* dlogits, const float* x_gathered, int32_t B, int32_t Hp,
                    int32_t Wp, const cp_partition* part, const float* wfc_g, int32_t O,
                    float* dx_gathered, float* dwfc_g, float* dbfc, void* ws, void* stream);
+/* Cross-channel LRN followed by 2x2/2 max-pool (NEXT row f2: the paper's "Normalization layer",
+ * Conv -> Norm -> Pool; form and default constants S:L89-97; ReLU before the
+ * normalisation, reading R23):  s_c = bias + alpha * sum_{|j-c|<=depth/2} a_j^2,  n_c = a_c s_c^-beta.
+ * cp_lrn_pool_forward: a_gathered is the conv layer's gathered pre-pool output (a layer created with
+ * pool = 0: every rank holds all channels, H x W grid, B images); writes the pooled map for ALL
+ * channels (gather layout over part, H/2 x W/2) and the uint8 argmax codes (2*di + dj, first max),
+ * RN-tf32 rounded when round_tf32.  Every rank computes it (no second collective).
+ * cp_lrn_pool_backward: dy_gathered is the gradient of the pooled map for ALL channels (the next
+ * layer's dX summed with CP_DX_ALLREDUCE, or the replicated head's); writes this rank's block of
+ * the gradient w.r.t. a (pre-pool gather layout), which is then the dy_gathered of
+ * conv_part_backward_data / _filter of the pool = 0 conv layer (its ReLU' uses a).
+ * Errors: depth even or < 1, bias <= 0 -> CP_ERR_CONFIG; odd H or W -> CP_ERR_SHAPE; more than 2048
+ * channels -> CP_ERR_UNSUPPORTED. */
+int cp_lrn_pool_forward(const float* a_gathered, int32_t B, int32_t H, int32_t W, const cp_partition* part,
+                        int32_t depth, float alpha, float beta, float bias, int32_t round_tf32,
+                        float* y_gathered, uint8_t* codes_gathered, void* stream);
+int cp_lrn_pool_backward(const float* dy_gathered, const float* a_gathered, const uint8_t* codes_gathered,
+                         int32_t B, int32_t H, int32_t W, const cp_partition* part, int32_t rank,
+                         int32_t depth, float alpha, float beta, float bias, float* da_gathered, void* stream);
+
 /* p -= lr*g over n floats. */
 int cp_sgd(float* p, const float* g, int64_t n, float lr, void* stream);
 /* The same SGD update for `count` tensors in one launch per 16 tensors: params[i]

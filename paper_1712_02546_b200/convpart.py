@@ -29,7 +29,7 @@ EXPORTS = [
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
     "cp_allreduce_sum", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait", "conv_part_timing", "conv_part_kernel_time",
-    "cp_sgd_multi",
+    "cp_sgd_multi", "cp_lrn_pool_forward", "cp_lrn_pool_backward",
 ]
 
 
@@ -122,6 +122,10 @@ def lib():
             "cp_symmetric_wait": [P, P, P],
             "conv_part_timing": [P, I32],
             "cp_sgd_multi": [ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(I64), I32, ctypes.c_float, P],
+            "cp_lrn_pool_forward": [P, I32, I32, I32, pp, I32, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                    I32, P, P, P],
+            "cp_lrn_pool_backward": [P, P, P, I32, I32, I32, pp, I32, I32, ctypes.c_float, ctypes.c_float,
+                                     ctypes.c_float, P, P],
             "conv_part_kernel_time": [P, I32, ctypes.POINTER(ctypes.c_float)],
         }
         for name, args in sig.items():
@@ -341,6 +345,19 @@ def cp_sgd_multi(pairs, lr, stream=None):
     gs = (ctypes.c_void_p * max(n, 1))(*[t[1].data_ptr() for t in pairs])
     sz = (ctypes.c_int64 * max(n, 1))(*[int(t[2]) if len(t) > 2 else t[0].numel() for t in pairs])
     _call("cp_sgd_multi", ps, gs, sz, n, float(lr), _stream(stream))
+
+
+LRN_DEFAULT = {"depth": 5, "alpha": 1e-4, "beta": 0.75, "bias": 2.0}
+
+
+def cp_lrn_pool_forward(a, B, H, W, part, lrn, round_tf32, y, codes, stream=None):
+    _call("cp_lrn_pool_forward", _ptr(a), B, H, W, ctypes.byref(part), int(lrn["depth"]), float(lrn["alpha"]),
+          float(lrn["beta"]), float(lrn["bias"]), int(round_tf32), _ptr(y), _ptr(codes), _stream(stream))
+
+
+def cp_lrn_pool_backward(dy, a, codes, B, H, W, part, rank, lrn, da, stream=None):
+    _call("cp_lrn_pool_backward", _ptr(dy), _ptr(a), _ptr(codes), B, H, W, ctypes.byref(part), int(rank),
+          int(lrn["depth"]), float(lrn["alpha"]), float(lrn["beta"]), float(lrn["bias"]), _ptr(da), _stream(stream))
 
 
 def cp_sgd(p, g, lr, stream=None):

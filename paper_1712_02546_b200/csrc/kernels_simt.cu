@@ -1091,6 +1091,120 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
   return CP_OK;
 }
 
+// ---------------------------------------------------------------- LRN + max-pool (NEXT row f2)
+// Cross-channel local response normalisation ("Normalization layer"; form S:L89-97):
+//   s_c = bias + alpha * sum_{|j-c|<=n/2, 0<=j<C} a_j^2,  n_c = a_c * s_c^(-beta)
+// on the gathered pre-pool map (every rank holds all channels), followed by the 2x2 max-pool with
+// first-max ties.  Logical channel c lives in rank block r at slot c - k_begin[r]: the
+// per-launch channel table (shared memory) holds each channel's block offset and row stride, so
+// the window crosses rank blocks transparently.
+constexpr int kLrnMaxC = 2048;
+__device__ __forceinline__ float lrn_pow(float s, float e) { return exp2f(e * __log2f(s)); }
+
+__global__ void __launch_bounds__(256) lrn_pool_fwd_kernel(const float* __restrict__ a, float* __restrict__ y,
+                                                           uint8_t* __restrict__ codes, Blocks gi, Blocks go,
+                                                           int C, int B, int W, int half, float alpha,
+                                                           float beta, float bias, int round) {
+  __shared__ long long coff[kLrnMaxC];   // start of channel c's block + slot
+  __shared__ int cstr[kLrnMaxC];         // its row stride (block width)
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    int r = 0;
+    while (r + 1 < gi.n && c >= gi.kb[r + 1]) ++r;
+    coff[c] = gi.start[r] + (c - gi.kb[r]);
+    cstr[c] = gi.kw[r];
+  }
+  __syncthreads();
+  const int64_t total = go.start[go.n];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int r = 0;
+    while (r + 1 < go.n && e >= go.start[r + 1]) ++r;
+    const int64_t l = e - go.start[r];
+    const int kw = go.kw[r];
+    const int slot = (int)(l % kw);
+    const int64_t rowp = l / kw;                  // (i*Wp + j)*Bp + b of the pooled grid
+    const int b = (int)(rowp % go.Bp);
+    const int ij = (int)(rowp / go.Bp), j = ij % go.W, i = ij / go.W;
+    float best = 0.f;
+    uint32_t code = 0;
+    if (slot < go.kc[r] && b < B) {
+      const int c = go.kb[r] + slot;
+      const int j0 = max(0, c - half), j1 = min(C - 1, c + half);
+      for (int q = 0; q < 4; ++q) {
+        const int64_t row = ((int64_t)(2 * i + (q >> 1)) * W + 2 * j + (q & 1)) * gi.Bp + b;   // pre-pool pixel row
+        float acc = 0.f;
+        for (int jj = j0; jj <= j1; ++jj) {
+          const float v = a[coff[jj] + row * cstr[jj]];
+          acc = fmaf(v, v, acc);
+        }
+        const float n = a[coff[c] + row * cstr[c]] * lrn_pow(bias + alpha * acc, -beta);
+        if (q == 0 || n > best) {
+          best = n;
+          code = q;
+        }
+      }
+    }
+    y[e] = round ? tf32_rna(best) : best;
+    codes[e] = (uint8_t)code;
+  }
+}
+
+// Backward for this rank's own channels: dn_j = dy routed through the pooling decision, then
+//   da_c = dn_c s_c^(-beta) - 2 alpha beta a_c sum_{|j-c|<=n/2} dn_j a_j s_j^(-beta-1)
+// (needs dy and the decisions of channels c +- n/2 and a over c +- n: the full gathered maps).
+__global__ void __launch_bounds__(256) lrn_pool_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ a,
+                                                           const uint8_t* __restrict__ codes, float* __restrict__ da,
+                                                           Blocks gi, Blocks go, int rank, int C, int B, int W,
+                                                           int half, float alpha, float beta, float bias) {
+  __shared__ long long coff[kLrnMaxC], poff[kLrnMaxC];   // pre-pool / pooled channel offsets
+  __shared__ int cstr[kLrnMaxC];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    int r = 0;
+    while (r + 1 < gi.n && c >= gi.kb[r + 1]) ++r;
+    coff[c] = gi.start[r] + (c - gi.kb[r]);
+    poff[c] = go.start[r] + (c - go.kb[r]);
+    cstr[c] = gi.kw[r];
+  }
+  __syncthreads();
+  const int64_t n_own = gi.start[rank + 1] - gi.start[rank];
+  const int kw = gi.kw[rank];
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_own; l += (int64_t)gridDim.x * blockDim.x) {
+    const int slot = (int)(l % kw);
+    const int64_t row = l / kw;                   // (h*W + w)*Bp + b of the pre-pool grid
+    const int b = (int)(row % gi.Bp);
+    const int hw = (int)(row / gi.Bp), w = hw % W, h = hw / W;
+    float out = 0.f;
+    if (slot < gi.kc[rank] && b < B) {
+      const int c = gi.kb[rank] + slot;
+      const int64_t prow = ((int64_t)(h >> 1) * go.W + (w >> 1)) * go.Bp + b;   // pooled row
+      const uint32_t pos = 2 * (h & 1) + (w & 1);
+      const float ac = a[coff[c] + row * cstr[c]];
+      float sum = 0.f, own = 0.f;
+      for (int j = max(0, c - half); j <= min(C - 1, c + half); ++j) {
+        const int64_t pj = poff[j] + prow * cstr[j];
+        if (codes[pj] != pos) continue;             // dn_j = 0 unless the pool routed here
+        const float dn = dy[pj];
+        float acc = 0.f;
+        for (int i = max(0, j - half); i <= min(C - 1, j + half); ++i) {
+          const float v = a[coff[i] + row * cstr[i]];
+          acc = fmaf(v, v, acc);
+        }
+        const float sj = bias + alpha * acc;
+        const float p = lrn_pow(sj, -beta);
+        if (j == c) own = dn * p;
+        sum = fmaf(dn * a[coff[j] + row * cstr[j]], p / sj, sum);
+      }
+      out = own - 2.f * alpha * beta * ac * sum;
+    }
+    da[gi.start[rank] + l] = out;
+  }
+}
+
+int launch_lrn_check(int C, int depth, float bias) {
+  if (depth < 1 || depth % 2 == 0 || !(bias > 0.f)) CP_FAIL(CP_ERR_CONFIG, "LRN: depth must be odd >= 1 and bias > 0");
+  if (C > kLrnMaxC) CP_FAIL(CP_ERR_UNSUPPORTED, "LRN: more than 2048 channels");
+  return CP_OK;
+}
+
 // SGD over up to kSgdMax tensors in one launch: grid-stride over the concatenated
 // float4 index space; the owning tensor is found by a scan of the (short) prefix table.
 constexpr int kSgdMax = 16;
@@ -1118,6 +1232,42 @@ __global__ void sgd_multi_kernel(const __grid_constant__ SgdList L, float lr) {
       for (long long j = e; j < L.n[t] && j < e + 4; ++j) p[j] -= lr * g[j];
     }
   }
+}
+
+int cp_lrn_pool_forward(const float* a_g, int32_t B, int32_t H, int32_t W, const cp_partition* part, int32_t depth,
+                        float alpha, float beta, float bias, int32_t round_tf32, float* y_g, uint8_t* codes_g,
+                        void* stream) {
+  CP_TRY(check_part(part));
+  if (!a_g || !y_g || !codes_g) CP_FAIL(CP_ERR_ARG, "cp_lrn_pool_forward: null pointer");
+  if (B < 1 || (H & 1) || (W & 1) || H < 2 || W < 2) CP_FAIL(CP_ERR_SHAPE, "cp_lrn_pool_forward: bad map shape");
+  CP_TRY(launch_lrn_check(part->num_k, depth, bias));
+  const int Bp = roundup(B, 32);
+  const Blocks gi = make_blocks(*part, H, W, Bp), go = make_blocks(*part, H / 2, W / 2, Bp);
+  const int64_t total = go.start[go.n];
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  lrn_pool_fwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(a_g, y_g, codes_g, gi, go, part->num_k, B, W,
+                                                                depth / 2, alpha, beta, bias, round_tf32 ? 1 : 0);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
+int cp_lrn_pool_backward(const float* dy_g, const float* a_g, const uint8_t* codes_g, int32_t B, int32_t H, int32_t W,
+                         const cp_partition* part, int32_t rank, int32_t depth, float alpha, float beta, float bias,
+                         float* da_g, void* stream) {
+  CP_TRY(check_part(part));
+  if (!dy_g || !a_g || !codes_g || !da_g) CP_FAIL(CP_ERR_ARG, "cp_lrn_pool_backward: null pointer");
+  if (B < 1 || (H & 1) || (W & 1) || H < 2 || W < 2) CP_FAIL(CP_ERR_SHAPE, "cp_lrn_pool_backward: bad map shape");
+  if (rank < 0 || rank >= part->n_ranks) CP_FAIL(CP_ERR_ARG, "cp_lrn_pool_backward: bad rank");
+  CP_TRY(launch_lrn_check(part->num_k, depth, bias));
+  const int Bp = roundup(B, 32);
+  const Blocks gi = make_blocks(*part, H, W, Bp), go = make_blocks(*part, H / 2, W / 2, Bp);
+  const int64_t n = gi.start[rank + 1] - gi.start[rank];
+  if (n == 0) return CP_OK;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  lrn_pool_bwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(dy_g, a_g, codes_g, da_g, gi, go, rank, part->num_k,
+                                                                B, W, depth / 2, alpha, beta, bias);
+  CP_LAUNCHED();
+  return CP_OK;
 }
 
 int cp_sgd_multi(float* const* params, const float* const* grads, const int64_t* sizes, int32_t count, float lr,

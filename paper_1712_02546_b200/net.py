@@ -35,7 +35,7 @@ class PartitionedNet:
 
     def __init__(self, kernels, batch, parts, rank=0, comm=None, math=cp.CP_MATH_TF32, in_c=3, in_hw=32,
                  ksize=5, classes=10, relu=True, pool=True, bias=True, device="cuda", head="replicated",
-                 fused=False):
+                 fused=False, lrn=None):
         """head: "replicated" - the last conv output is all-gathered and every rank runs the full FC
         head (the paper's master-side head, replicated); "partitioned" - the last conv output stays
         rank-local, each rank owns the FC columns of its channels, partial logits are summed with
@@ -44,8 +44,15 @@ class PartitionedNet:
         symmetric (peer-mapped) buffer: the TF32 forward epilogue stores its output block into all ranks'
         copies over NVLink (the next layer's GEMM consumes its own block first and each peer block when
         its arrival flag is set) and the dgrad epilogue stores each input block's partial dX into its
-        owner's receive slot (reduce-scatter without an NCCL kernel)."""
+        owner's receive slot (reduce-scatter without an NCCL kernel).
+        lrn: None, or LRN parameters {depth, alpha, beta, bias} (convpart.LRN_DEFAULT): every conv layer
+        becomes Conv -> bias -> ReLU -> LRN -> Pool (NEXT row f2): the conv runs without
+        pooling, its pre-pool output is gathered, every rank runs cp_lrn_pool_forward over all
+        channels; backward needs the full pooled gradient (replicated head, all-reduced dX)."""
         self.device = torch.device(device)
+        self.lrn = dict(lrn) if lrn else None
+        if self.lrn:
+            head = "replicated"    # the LRN backward needs the gradient of every channel
         self.head_mode = head if parts[0].n_ranks > 1 else "replicated"
         self.B, self.Bp, self.O = batch, (batch + 31) // 32 * 32, classes
         self.rank, self.world = rank, parts[0].n_ranks
@@ -56,7 +63,7 @@ class PartitionedNet:
             d = cp.cp_conv_desc()
             d.batch, d.in_c, d.in_h, d.in_w = batch, c, h, h
             d.num_k, d.k_h, d.k_w = K, ksize, ksize
-            d.bias, d.relu, d.pool, d.math = int(bias), int(relu), int(pool), math
+            d.bias, d.relu, d.pool, d.math = int(bias), int(relu), int(pool and not self.lrn), math
             d.input_kind = cp.CP_INPUT_IMAGES if prev is None else cp.CP_INPUT_GATHER
             d.out_part = parts[i]
             if prev is not None:
@@ -78,6 +85,16 @@ class PartitionedNet:
             }
             if prev is not None:
                 b["dx"] = self._symmetric(sz.dx_peer, fused) if fused else _f32(sz.dx, self.device)
+            if self.lrn:
+                # pooled gathered map + codes (all channels, computed by every rank), pre-pool gradient
+                ho = h - ksize + 1
+                cnt = sum(parts[i].k_width[r] for r in range(self.world))
+                batch_p = (batch + 31) // 32 * 32
+                npool = (ho // 2) * (ho // 2) * batch_p * cnt
+                b["yp"] = _f32(npool * 4 + 256, self.device)
+                b["codes"] = _dev_bytes(npool, self.device)
+                b["dpre"] = _f32(sz.y, self.device)
+                b["hw"] = ho
             self.buf.append(b)
             ho = h - ksize + 1
             h = ho // 2 if pool else ho
@@ -106,7 +123,7 @@ class PartitionedNet:
             "da": _f32(self.sizes[-1].y, self.device),
             "ws": _dev_bytes(cp.cp_head_workspace_bytes(batch, h, h, last, classes), self.device),
         }
-        self.head_x = self.buf[-1]["y"][self.head_off:]
+        self.head_x = (self.buf[-1]["yp"] if self.lrn else self.buf[-1]["y"])[self.head_off:]
         self.head_da = self.head["da"][self.head_off:]
         self.x = torch.zeros(batch * in_c * in_hw * in_hw, device=self.device)
         self.labels = torch.zeros(batch, dtype=torch.int32, device=self.device)
@@ -167,9 +184,16 @@ class PartitionedNet:
             b = self.buf[i]
             cp.conv_part_forward(L, inp, b["w"], b["b"], b["y"], b["saved"], b["ws"], stream, comm_stream)
             inp = b["y"]
+            if self.lrn:
+                sym = next((m for m in self.sym if m.tensor.data_ptr() == b["y"].data_ptr()), None)
+                if sym is not None:
+                    sym.wait(stream)
+                cp.cp_lrn_pool_forward(b["y"], self.B, b["hw"], b["hw"], self.parts[i], self.lrn,
+                                       self.math == cp.CP_MATH_TF32, b["yp"], b["codes"], stream)
+                inp = b["yp"]
         hd = self.head
         last = next((m for m in self.sym if m.tensor.data_ptr() == self.buf[-1]["y"].data_ptr()), None)
-        if last is not None:
+        if last is not None and not self.lrn:
             last.wait(stream)   # replicated head reads the gathered last output
         bias = hd["bfc"] if (self.head_mode == "replicated" or self.rank == 0) else None
         cp.cp_fc_forward(self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], bias, self.O, hd["logits"],
@@ -186,11 +210,18 @@ class PartitionedNet:
         n = len(self.layers)
         for i in reversed(range(n)):
             L, b = self.layers[i], self.buf[i]
-            xin = self.x if i == 0 else self.buf[i - 1]["y"]
+            xin = self.x if i == 0 else self.buf[i - 1]["yp" if self.lrn else "y"]
+            if self.lrn:
+                # pooled gradient of every channel -> this rank's block of the pre-pool gradient
+                cp.cp_lrn_pool_backward(da, b["y"], b["codes"], self.B, b["hw"], b["hw"], self.parts[i], self.rank,
+                                        self.lrn, b["dpre"], stream)
+                da = b["dpre"]
             if i > 0:
                 # with several ranks the forward always runs a collective on every rank (gather or logits
-                # AllReduce), which orders consecutive calls of the fused reduce-scatter (CP_DX_ORDERED)
-                mode = dx_mode | (cp.CP_DX_ASYNC if overlap else 0) | (cp.CP_DX_ORDERED if self.world > 1 else 0)
+                # AllReduce), which orders consecutive calls of the fused reduce-scatter (CP_DX_ORDERED);
+                # LRN below needs every channel of the summed dX (all-reduce)
+                mode = (cp.CP_DX_ALLREDUCE if self.lrn else dx_mode) | (cp.CP_DX_ASYNC if overlap else 0) | \
+                    (cp.CP_DX_ORDERED if self.world > 1 else 0)
                 cp.conv_part_backward_data(L, da, b["saved"], b["y"], b["w"], b["dx"], mode, b["ws"], stream,
                                            comm_stream)
             # wgrad needs no communication: it overlaps the dX reduction on the comm stream (§8(e))

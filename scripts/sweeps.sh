@@ -14,3 +14,5 @@ runN 4 --partition probe > $out/probe_n4.json
 runN 4 --batch 512 > $out/batch_b512_n4.json
 runN 4 --probe-times 1,1,1.5,2 > $out/injected_1-1-1.5-2_n4.json
 runN 2 --probe-times 1,2 > $out/injected_1-2_n2.json
+run1 --lrn > $out/lrn_n1.json
+runN 4 --lrn > $out/lrn_n4.json

@@ -148,6 +148,50 @@ def main():
                 failures.append(f"{mode_name}: FC weight update rel err {e:.2e}")
         pn.close()
 
+    # Paper-literal net (Conv -> ReLU -> LRN -> Pool, NEXT row f2) over real collectives: every rank
+    # holds the pooled maps and codes of all channels, so the oracle replays them directly.
+    for fused in (False, True):
+        net = synth.NetSpec(kernels=(36, 72), in_hw=20, name="multi-lrn")
+        B = 40
+        lrn = {"depth": 5, "alpha": 0.05, "beta": 0.75, "bias": 2.0}
+        parts = [cp.cp_partition_plan(uneven, K) for K in net.kernels]
+        params = synth.params(net, seed=23, std=0.05, bias_std=0.01)
+        x, y = synth.images(B, 3, 20, 20, step=4)
+        pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20, fused=fused, lrn=lrn)
+        pn.load_params(params)
+        pn.set_batch(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
+        s = torch.cuda.current_stream(dev)
+        cs = torch.cuda.Stream(dev)
+        pn.forward(s, cs)
+        torch.cuda.synchronize(dev)
+        rep = []
+        for i, K in enumerate(net.kernels):
+            ho = pn.buf[i]["hw"]
+            rep.append({"a": unpack(pn.buf[i]["yp"], B, K, ho // 2, parts[i]),
+                        "argmax": np.rint(unpack(pn.buf[i]["codes"].float(), B, K, ho // 2, parts[i])).astype(np.uint8),
+                        "pre": unpack(pn.buf[i]["y"], B, K, ho, parts[i])})
+        pn.backward(cp.CP_DX_REDUCE_SCATTER, s, cs, overlap=True)
+        pn.sgd(0.01, s)
+        torch.cuda.synchronize(dev)
+        new = pn.export_params()
+        p64 = {k: v.astype(np.float64) for k, v in params.items()}
+        layers = [dict(L, lrn=lrn) for L in net.layers()]
+        tr = oracle.net_step(p64, x.astype(np.float64), y, 0.01, layers, replay=rep)
+        name = f"lrn{'+fused' if fused else ''}"
+        if abs(pn.loss() - tr["loss"]) > TOL[cp.CP_MATH_TF32] * abs(tr["loss"]):
+            failures.append(f"{name}: loss {pn.loss()} vs oracle {tr['loss']}")
+        for i in range(2):
+            kb, kr = parts[i].k_begin[rank], parts[i].k_count[rank]
+            if kr:
+                e = rel_err(new[f"w{i}"] - params[f"w{i}"][kb:kb + kr],
+                            tr["new_params"][f"w{i}"][kb:kb + kr] - p64[f"w{i}"][kb:kb + kr])
+                if e > 5e-3:
+                    failures.append(f"{name}: conv{i + 1} weight update rel err {e:.2e}")
+        e = rel_err(new["wfc"] - params["wfc"], tr["new_params"]["wfc"] - p64["wfc"])
+        if e > 5e-3:
+            failures.append(f"{name}: FC weight update rel err {e:.2e}")
+        pn.close()
+
     # Several back-to-back steps (eager, then CUDA-graph replays) with the fused collectives vs NCCL:
     # exercises the arrival-flag resets and the overwrite guards across steps (a missed flag or an
     # early overwrite shows up as a diverging loss).

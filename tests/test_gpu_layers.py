@@ -208,3 +208,78 @@ def test_full_step_p1(orc, math):
         # compare the update (new - old) so the tolerance applies to the gradient step
         assert_close(new[k] - params[k], tr["new_params"][k] - p64[k], max(TOL[m], 1e-4), f"update of {k} ({math})")
     pn.close()
+
+
+# ------------------------------------------------------------------ LRN + pool (NEXT row f2)
+LRN_T = {"depth": 5, "alpha": 0.05, "beta": 0.75, "bias": 2.0}   # alpha large enough to matter
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_lrn_pool_parity(orc, P):
+    """cp_lrn_pool_forward / _backward vs the oracle's LRN + pool on a gathered map whose channel
+    windows cross (uneven) rank blocks; backward with decision replay of the GPU's pooling codes."""
+    B, C, H = 40, 36, 8
+    part = parts_for(P, C)
+    a = np.abs(synth.normal((B, C, H, H), 51, 1.0)).astype(np.float32)
+    a[a < 0.3] = 0.0                                          # post-ReLU maps carry zeros
+    ag = pack(a, part)
+    Bp = 64
+    npool = (H // 2) ** 2 * Bp * sum(part.k_width[r] for r in range(part.n_ranks))
+    y = torch.zeros(npool + 64, device="cuda")
+    codes = torch.zeros(npool + 64, dtype=torch.uint8, device="cuda")
+    cp.cp_lrn_pool_forward(ag, B, H, H, part, LRN_T, 0, y, codes)
+    ref_y, _ = orc.relu_pool_fwd(orc.lrn_fwd(a.astype(np.float64), **LRN_T), relu=False)
+    got_y = unpack(y, B, C, H // 2, part)
+    assert_close(got_y, ref_y, 1e-5, f"LRN+pool forward (P={P})")
+    got_am = np.rint(unpack(codes.float(), B, C, H // 2, part)).astype(np.uint8)
+    dy = synth.normal(ref_y.shape, 52, 1.0).astype(np.float32)
+    dyg = pack(dy, part)
+    da = torch.zeros_like(ag)
+    for r in range(P):
+        cp.cp_lrn_pool_backward(dyg, ag, codes, B, H, H, part, r, LRN_T, da)
+    dn = orc.unpool_relu_bwd(dy.astype(np.float64), got_am, got_y, relu=False)
+    ref_da = orc.lrn_bwd(a.astype(np.float64), dn, **LRN_T)
+    assert_close(unpack(da, B, C, H, part), ref_da, 1e-5, f"LRN+pool backward (P={P})")
+
+
+def test_lrn_bad_config():
+    part = parts_for(1, 8)
+    t = torch.zeros(1024, device="cuda")
+    c = torch.zeros(1024, dtype=torch.uint8, device="cuda")
+    with pytest.raises(cp.ConvPartError):
+        cp.cp_lrn_pool_forward(t, 4, 4, 4, part, dict(LRN_T, depth=4), 0, t, c)
+    with pytest.raises(cp.ConvPartError):
+        cp.cp_lrn_pool_forward(t, 4, 4, 4, part, dict(LRN_T, bias=0.0), 0, t, c)
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_full_step_lrn_p1(orc, math):
+    """Whole step of the paper-literal net (Conv -> ReLU -> LRN -> Pool per conv layer) vs the oracle
+    step with decision replay (GPU pooling codes and pre-LRN ReLU map)."""
+    from paper_1712_02546_b200.net import PartitionedNet, plan_even
+    m = math_id(math)
+    net = synth.NetSpec(kernels=(24, 40), in_hw=20, name="small")
+    B = 40
+    params = synth.params(net, seed=12, std=0.05, bias_std=0.01)
+    x, y = synth.images(B, 3, 20, 20, step=2)
+    pn = PartitionedNet(net.kernels, B, plan_even(net.kernels, 1), math=m, in_hw=20, lrn=LRN_T)
+    pn.load_params(params)
+    pn.set_batch(dev(x), dev(y, torch.int32))
+    pn.forward()
+    torch.cuda.synchronize()
+    rep = []
+    for i, K in enumerate(net.kernels):
+        ho = pn.buf[i]["hw"]
+        rep.append({"a": unpack(pn.buf[i]["yp"], B, K, ho // 2, pn.parts[i]),
+                    "argmax": np.rint(unpack(pn.buf[i]["codes"].float(), B, K, ho // 2, pn.parts[i])).astype(np.uint8),
+                    "pre": unpack(pn.buf[i]["y"], B, K, ho, pn.parts[i])})
+    pn.backward()
+    pn.sgd(0.01)
+    new = pn.export_params()
+    p64 = {k: v.astype(np.float64) for k, v in params.items()}
+    layers = [dict(L, lrn=LRN_T) for L in net.layers()]
+    tr = orc.net_step(p64, x.astype(np.float64), y, 0.01, layers, replay=rep)
+    assert abs(pn.loss() - tr["loss"]) <= TOL[m] * abs(tr["loss"])
+    for k in p64:
+        assert_close(new[k] - params[k], tr["new_params"][k] - p64[k], max(TOL[m], 1e-4), f"LRN update of {k} ({math})")
+    pn.close()
