@@ -1099,103 +1099,99 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
 // per-launch channel table (shared memory) holds each channel's block offset and row stride, so
 // the window crosses rank blocks transparently.
 constexpr int kLrnMaxC = 2048;
-__device__ __forceinline__ float lrn_pow(float s, float e) { return exp2f(e * __log2f(s)); }
 
+// Forward: one CTA per pooled (i, j, b): the four pre-pool pixel rows of all C channels are loaded
+// once into shared memory (per rank block, contiguous), then thread = channel computes the window
+// sums, n = a s^-beta for the four window positions, the max with first-max ties, and writes the
+// pooled value and code into the channel's rank block (padding slots / images are written as 0).
 __global__ void __launch_bounds__(256) lrn_pool_fwd_kernel(const float* __restrict__ a, float* __restrict__ y,
                                                            uint8_t* __restrict__ codes, Blocks gi, Blocks go,
                                                            int C, int B, int W, int half, float alpha,
                                                            float beta, float bias, int round) {
-  __shared__ long long coff[kLrnMaxC];   // start of channel c's block + slot
-  __shared__ int cstr[kLrnMaxC];         // its row stride (block width)
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    int r = 0;
-    while (r + 1 < gi.n && c >= gi.kb[r + 1]) ++r;
-    coff[c] = gi.start[r] + (c - gi.kb[r]);
-    cstr[c] = gi.kw[r];
-  }
+  __shared__ float av[4][kLrnMaxC];
+  const int Wp = go.W, Bp = go.Bp;
+  const int b = blockIdx.x % Bp, ij = blockIdx.x / Bp, j = ij % Wp, i = ij / Wp;
+  const int64_t prow = (int64_t)ij * Bp + b;                    // pooled pixel row
+  const bool real = b < B;
+  if (real)
+    for (int q = 0; q < 4; ++q) {
+      const int64_t row = ((int64_t)(2 * i + (q >> 1)) * W + 2 * j + (q & 1)) * Bp + b;
+      for (int r = 0; r < gi.n; ++r)
+        for (int cc = threadIdx.x; cc < gi.kc[r]; cc += blockDim.x)
+          av[q][gi.kb[r] + cc] = a[gi.start[r] + row * gi.kw[r] + cc];
+    }
   __syncthreads();
-  const int64_t total = go.start[go.n];
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int r = 0;
-    while (r + 1 < go.n && e >= go.start[r + 1]) ++r;
-    const int64_t l = e - go.start[r];
-    const int kw = go.kw[r];
-    const int slot = (int)(l % kw);
-    const int64_t rowp = l / kw;                  // (i*Wp + j)*Bp + b of the pooled grid
-    const int b = (int)(rowp % go.Bp);
-    const int ij = (int)(rowp / go.Bp), j = ij % go.W, i = ij / go.W;
-    float best = 0.f;
-    uint32_t code = 0;
-    if (slot < go.kc[r] && b < B) {
-      const int c = go.kb[r] + slot;
-      const int j0 = max(0, c - half), j1 = min(C - 1, c + half);
-      for (int q = 0; q < 4; ++q) {
-        const int64_t row = ((int64_t)(2 * i + (q >> 1)) * W + 2 * j + (q & 1)) * gi.Bp + b;   // pre-pool pixel row
-        float acc = 0.f;
-        for (int jj = j0; jj <= j1; ++jj) {
-          const float v = a[coff[jj] + row * cstr[jj]];
-          acc = fmaf(v, v, acc);
-        }
-        const float n = a[coff[c] + row * cstr[c]] * lrn_pow(bias + alpha * acc, -beta);
-        if (q == 0 || n > best) {
-          best = n;
-          code = q;
+  for (int r = 0; r < go.n; ++r)
+    for (int cc = threadIdx.x; cc < go.kw[r]; cc += blockDim.x) {
+      float best = 0.f;
+      uint32_t code = 0;
+      if (real && cc < go.kc[r]) {
+        const int c = go.kb[r] + cc;
+        const int j0 = max(0, c - half), j1 = min(C - 1, c + half);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float acc = 0.f;
+          for (int jj = j0; jj <= j1; ++jj) acc = fmaf(av[q][jj], av[q][jj], acc);
+          const float n = av[q][c] * powf(fmaf(alpha, acc, bias), -beta);
+          if (q == 0 || n > best) {
+            best = n;
+            code = q;
+          }
         }
       }
+      const int64_t o = go.start[r] + prow * go.kw[r] + cc;
+      y[o] = round ? tf32_rna(best) : best;
+      codes[o] = (uint8_t)code;
     }
-    y[e] = round ? tf32_rna(best) : best;
-    codes[e] = (uint8_t)code;
-  }
 }
 
-// Backward for this rank's own channels: dn_j = dy routed through the pooling decision, then
+// Backward for this rank's own channels, one CTA per pre-pool (h, w, b) row: a and the routed
+// pooled gradient dn (dy where the pooling code selected this position, else 0) of all channels
+// are staged in shared memory; the scales s_j are computed once for j in own range +- n/2:
 //   da_c = dn_c s_c^(-beta) - 2 alpha beta a_c sum_{|j-c|<=n/2} dn_j a_j s_j^(-beta-1)
-// (needs dy and the decisions of channels c +- n/2 and a over c +- n: the full gathered maps).
 __global__ void __launch_bounds__(256) lrn_pool_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ a,
                                                            const uint8_t* __restrict__ codes, float* __restrict__ da,
                                                            Blocks gi, Blocks go, int rank, int C, int B, int W,
                                                            int half, float alpha, float beta, float bias) {
-  __shared__ long long coff[kLrnMaxC], poff[kLrnMaxC];   // pre-pool / pooled channel offsets
-  __shared__ int cstr[kLrnMaxC];
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    int r = 0;
-    while (r + 1 < gi.n && c >= gi.kb[r + 1]) ++r;
-    coff[c] = gi.start[r] + (c - gi.kb[r]);
-    poff[c] = go.start[r] + (c - go.kb[r]);
-    cstr[c] = gi.kw[r];
+  __shared__ float av[kLrnMaxC], dn[kLrnMaxC], tj[kLrnMaxC], pw[kLrnMaxC];
+  const int Bp = gi.Bp;
+  const int b = blockIdx.x % Bp, hw = blockIdx.x / Bp, w = hw % W, h = hw / W;
+  const int64_t row = (int64_t)hw * Bp + b;
+  const int kb = gi.kb[rank], kc = gi.kc[rank], kw = gi.kw[rank];
+  float* out = da + gi.start[rank] + row * kw;
+  if (b >= B) {
+    for (int cc = threadIdx.x; cc < kw; cc += blockDim.x) out[cc] = 0.f;
+    return;
+  }
+  const int64_t prow = ((int64_t)(h >> 1) * go.W + (w >> 1)) * Bp + b;
+  const uint8_t pos = (uint8_t)(2 * (h & 1) + (w & 1));
+  for (int r = 0; r < gi.n; ++r)
+    for (int cc = threadIdx.x; cc < gi.kc[r]; cc += blockDim.x) {
+      const int c = gi.kb[r] + cc;
+      av[c] = a[gi.start[r] + row * gi.kw[r] + cc];
+      const int64_t po = go.start[r] + prow * go.kw[r] + cc;
+      dn[c] = codes[po] == pos ? dy[po] : 0.f;
+    }
+  __syncthreads();
+  const int lo = max(0, kb - half), hi = min(C - 1, kb + kc - 1 + half);
+  for (int jj = lo + threadIdx.x; jj <= hi; jj += blockDim.x) {
+    float acc = 0.f;
+    for (int i2 = max(0, jj - half); i2 <= min(C - 1, jj + half); ++i2) acc = fmaf(av[i2], av[i2], acc);
+    const float sj = fmaf(alpha, acc, bias);
+    const float p = powf(sj, -beta);
+    pw[jj] = p;
+    tj[jj] = dn[jj] * av[jj] * p / sj;
   }
   __syncthreads();
-  const int64_t n_own = gi.start[rank + 1] - gi.start[rank];
-  const int kw = gi.kw[rank];
-  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_own; l += (int64_t)gridDim.x * blockDim.x) {
-    const int slot = (int)(l % kw);
-    const int64_t row = l / kw;                   // (h*W + w)*Bp + b of the pre-pool grid
-    const int b = (int)(row % gi.Bp);
-    const int hw = (int)(row / gi.Bp), w = hw % W, h = hw / W;
-    float out = 0.f;
-    if (slot < gi.kc[rank] && b < B) {
-      const int c = gi.kb[rank] + slot;
-      const int64_t prow = ((int64_t)(h >> 1) * go.W + (w >> 1)) * go.Bp + b;   // pooled row
-      const uint32_t pos = 2 * (h & 1) + (w & 1);
-      const float ac = a[coff[c] + row * cstr[c]];
-      float sum = 0.f, own = 0.f;
-      for (int j = max(0, c - half); j <= min(C - 1, c + half); ++j) {
-        const int64_t pj = poff[j] + prow * cstr[j];
-        if (codes[pj] != pos) continue;             // dn_j = 0 unless the pool routed here
-        const float dn = dy[pj];
-        float acc = 0.f;
-        for (int i = max(0, j - half); i <= min(C - 1, j + half); ++i) {
-          const float v = a[coff[i] + row * cstr[i]];
-          acc = fmaf(v, v, acc);
-        }
-        const float sj = bias + alpha * acc;
-        const float p = lrn_pow(sj, -beta);
-        if (j == c) own = dn * p;
-        sum = fmaf(dn * a[coff[j] + row * cstr[j]], p / sj, sum);
-      }
-      out = own - 2.f * alpha * beta * ac * sum;
+  for (int cc = threadIdx.x; cc < kw; cc += blockDim.x) {
+    float v = 0.f;
+    if (cc < kc) {
+      const int c = kb + cc;
+      float sum = 0.f;
+      for (int jj = max(0, c - half); jj <= min(C - 1, c + half); ++jj) sum += tj[jj];
+      v = dn[c] * pw[c] - 2.f * alpha * beta * av[c] * sum;
     }
-    da[gi.start[rank] + l] = out;
+    out[cc] = v;
   }
 }
 
@@ -1243,10 +1239,8 @@ int cp_lrn_pool_forward(const float* a_g, int32_t B, int32_t H, int32_t W, const
   CP_TRY(launch_lrn_check(part->num_k, depth, bias));
   const int Bp = roundup(B, 32);
   const Blocks gi = make_blocks(*part, H, W, Bp), go = make_blocks(*part, H / 2, W / 2, Bp);
-  const int64_t total = go.start[go.n];
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  lrn_pool_fwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(a_g, y_g, codes_g, gi, go, part->num_k, B, W,
-                                                                depth / 2, alpha, beta, bias, round_tf32 ? 1 : 0);
+  lrn_pool_fwd_kernel<<<(H / 2) * (W / 2) * Bp, 256, 0, (cudaStream_t)stream>>>(
+      a_g, y_g, codes_g, gi, go, part->num_k, B, W, depth / 2, alpha, beta, bias, round_tf32 ? 1 : 0);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -1261,11 +1255,9 @@ int cp_lrn_pool_backward(const float* dy_g, const float* a_g, const uint8_t* cod
   CP_TRY(launch_lrn_check(part->num_k, depth, bias));
   const int Bp = roundup(B, 32);
   const Blocks gi = make_blocks(*part, H, W, Bp), go = make_blocks(*part, H / 2, W / 2, Bp);
-  const int64_t n = gi.start[rank + 1] - gi.start[rank];
-  if (n == 0) return CP_OK;
-  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  lrn_pool_bwd_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(dy_g, a_g, codes_g, da_g, gi, go, rank, part->num_k,
-                                                                B, W, depth / 2, alpha, beta, bias);
+  if (gi.kw[rank] == 0) return CP_OK;
+  lrn_pool_bwd_kernel<<<H * W * Bp, 256, 0, (cudaStream_t)stream>>>(dy_g, a_g, codes_g, da_g, gi, go, rank,
+                                                                  part->num_k, B, W, depth / 2, alpha, beta, bias);
   CP_LAUNCHED();
   return CP_OK;
 }
