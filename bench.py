@@ -33,6 +33,10 @@ sys.path.insert(0, ROOT)
 NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense peaks (tf32 1.1, bf16 2.25 PF)
 
 
+
+# the same metric string on both arms (the driver divides one by the other)
+METRIC = "conv-layer train images/sec (whole-network SGD step, kernel-partitioned)"
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -167,7 +171,7 @@ def run_reference(args):
         if k >= args.warmup:
             vals.append(v)
     v = statistics.median(vals)
-    line = {"impl": "reference", "metric": "conv-layer train images/sec", "value": v, "unit": "images/s",
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.batch / v * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"paper net {args.net}, CIFAR-10-shaped 32x32x3, batch "
@@ -451,7 +455,7 @@ def main():
         per_img = 2.0 * (2 * k1 * c1 * 25 * o1 * o1 + 3 * k2 * c2 * 25 * o2 * o2)
         step_flop = per_img * B
         line = {
-            "metric": "conv-layer train images/sec (whole-network SGD step, kernel-partitioned)",
+            "metric": METRIC,
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "tf32" if math == cp.CP_MATH_TF32 else "f32", "data": "synthetic",
