@@ -21,7 +21,6 @@
 // (CUDA IPC over NVLink) to all the others, so kernels can store directly into peers' copies.
 struct SymBuf {
   size_t bytes, flag_off;
-  cudaEvent_t ev;             // (unused placeholder for copy-stream joins)
   int64_t own_off = -1, own_elems = 0;   // this rank's block (floats), recorded by its producer
   void* peers[CP_MAX_RANKS];  // peers[rank] = own pointer
 };
@@ -93,7 +92,6 @@ extern "C" int cp_symmetric_alloc(cp_comm c, size_t bytes, void** local_out) {
   }
   SymBuf sb{};
   CP_TRY(sym_map(c, bytes, local_out, sb));
-  CP_CUDA(cudaEventCreateWithFlags(&sb.ev, cudaEventDisableTiming));
   c->sym[*local_out] = sb;
   return CP_OK;
 }
@@ -146,7 +144,6 @@ static void sym_release(cp_comm c, void* local, SymBuf& sb) {
                              ncclSuccess)
     cudaDeviceSynchronize();
   cudaFree(local);
-  if (sb.ev) cudaEventDestroy(sb.ev);
 }
 
 extern "C" int cp_symmetric_free(cp_comm c, void* local) {
@@ -313,12 +310,6 @@ int comm_check_plan(cp_comm c, const Layer& L) {
 }
 
 // Peer pointers of a symmetric buffer (nullptr if `local` is not one).
-cudaEvent_t comm_symmetric_event(cp_comm c, const void* local) {
-  if (!c) return nullptr;
-  auto it = c->sym.find(const_cast<void*>(local));
-  return it == c->sym.end() ? nullptr : it->second.ev;
-}
-
 void comm_symmetric_set_own(cp_comm c, const void* local, int64_t off, int64_t elems) {
   auto it = c->sym.find(const_cast<void*>(local));
   if (it == c->sym.end()) return;

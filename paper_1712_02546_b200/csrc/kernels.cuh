@@ -63,7 +63,6 @@ int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s
 // symmetric (peer-mapped) buffer lookup: peers[r] = rank r's copy; flags[r] = rank r's arrival-flag
 // array (CP_MAX_RANKS u32, indexed by sender rank).  False if `local` is not a symmetric buffer.
 bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags = nullptr);
-cudaEvent_t comm_symmetric_event(cp_comm c, const void* local);
 // producer records its block of a symmetric gathered buffer (for copy-engine distribution)
 void comm_symmetric_set_own(cp_comm c, const void* local, int64_t off, int64_t elems);
 int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks = false);
