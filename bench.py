@@ -136,6 +136,26 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
+def host_cores():
+    """Cores this process may run on (the oracle's OpenMP team is sized to them)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_threads(n):
+    """Size the oracle's OpenMP team: torchrun exports OMP_NUM_THREADS=1 to every rank, but the
+    reference leg runs on rank 0 alone and may use the host's cores (libgomp is shared with the
+    oracle's library)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+        return int(n)
+    except OSError:
+        return int(os.environ.get("OMP_NUM_THREADS", n))
+
+
 def oracle_images_per_s(net, target_s, step=0):
     """Time the oracle's full training step on a bounded sample of the same workload."""
     import numpy as np
@@ -143,6 +163,7 @@ def oracle_images_per_s(net, target_s, step=0):
     import oracle
     import synth
     oracle.build()
+    cores = oracle_threads(host_cores())
     params = {k: v.astype(np.float64) for k, v in synth.params(net, seed=42).items()}
     b, elapsed, done = 1, 0.0, 0
     while True:
@@ -155,7 +176,6 @@ def oracle_images_per_s(net, target_s, step=0):
         if elapsed >= target_s * 0.5 or dt * 2 > target_s:
             break
         b = max(1, min(64, int(b * max(2.0, (target_s - elapsed) / max(dt, 1e-3) * 0.5))))
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return done / elapsed, cores, f"{done} images of the B=128 step's workload ({net.name}), fp64 oracle net_step, {elapsed:.1f} s"
 
 
