@@ -74,7 +74,12 @@ enum {
 
 typedef enum {
   CP_MATH_TF32 = 0,      /* tcgen05 kind::tf32 implicit GEMMs, fp32 accumulate */
-  CP_MATH_FP32_SIMT = 1  /* FP32 CUDA-core reference kernels                  */
+  CP_MATH_FP32_SIMT = 1, /* FP32 CUDA-core reference kernels                  */
+  CP_MATH_BF16 = 2       /* NEXT row f4, report-only: the GEMM operands (weights, layer input, dY)
+                            are rounded to bf16 copies inside the library, tcgen05 kind::f16,
+                            fp32 accumulate and fp32 outputs.  Needs partition widths in multiples
+                            of 64 (cp_partition_plan align 64) and a batch padded to a multiple of
+                            64; error ~1e-2 of max|ref|, outside the 2e-3 TF32 bar */
 } cp_math;
 
 typedef enum {

@@ -16,7 +16,7 @@ CP_MAX_RANKS = 16
 CP_OK = 0
 ERRORS = {-1: "CP_ERR_ARG", -2: "CP_ERR_SHAPE", -3: "CP_ERR_CONFIG", -4: "CP_ERR_DATA", -5: "CP_ERR_CUDA",
           -6: "CP_ERR_NCCL", -7: "CP_ERR_STATE", -8: "CP_ERR_UNSUPPORTED"}
-CP_MATH_TF32, CP_MATH_FP32_SIMT = 0, 1
+CP_MATH_TF32, CP_MATH_FP32_SIMT, CP_MATH_BF16 = 0, 1, 2
 CP_DX_ALLREDUCE, CP_DX_REDUCE_SCATTER, CP_DX_LOCAL, CP_DX_ASYNC, CP_DX_ORDERED = 0, 1, 2, 16, 64
 CP_INPUT_IMAGES, CP_INPUT_GATHER = 0, 1
 

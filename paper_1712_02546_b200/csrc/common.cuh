@@ -151,6 +151,7 @@ struct Layer {
   // workspace carve-up (bytes)
   size_t ws_xcol, ws_z, ws_dy, ws_split, ws_dbpart, ws_total;
   size_t off_xcol, off_z, off_dy, off_split, off_dbpart;
+  size_t off_x16, off_w16, off_dy16;   // bf16 operand copies (CP_MATH_BF16 only)
   int dy_ready;           // epilogue-backward already computed for this step
   const void* dy_key[3];
   cudaEvent_t ev_compute, ev_comm;

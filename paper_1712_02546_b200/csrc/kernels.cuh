@@ -24,6 +24,8 @@ int launch_dgrad_simt(const Layer& L, const float* dY, const float* w, float* dx
 int launch_wgrad_simt(const Layer& L, const float* dY, const float* x, const float* xcol, float* dw,
                       cudaStream_t s);
 int launch_fill(float* p, float v, int64_t n, cudaStream_t s);
+// fp32 -> bf16 (round to nearest even) copy of n elements (CP_MATH_BF16 operand copies)
+int launch_to_bf16(const float* src, void* dst, int64_t n, cudaStream_t s);
 int launch_random_fill(float* p, int64_t n, uint32_t seed, float scale, cudaStream_t s);
 // cross-GPU arrival flags (fused AllGather): set slot `slot` of every peer's flag array / wait for
 // every slot of the own array except `self` (for consumers outside the tensor-core forward)

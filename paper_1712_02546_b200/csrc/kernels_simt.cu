@@ -9,6 +9,8 @@
 // S:L98-115); SGD.
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "kernels.cuh"
 
 namespace cp {
@@ -464,6 +466,26 @@ __global__ void __launch_bounds__(256) bias_grad_final(const float* __restrict__
 int launch_bias_grad(const Layer& L, float* db, const float* part, cudaStream_t s) {
   if (L.Kr == 0) return CP_OK;
   bias_grad_final<<<cdiv(L.Kr, 32), dim3(32, 8), 0, s>>>(part, db, unpool_splits(L), L.Kr, L.Kc);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
+__global__ void to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t n) {
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += (int64_t)gridDim.x * blockDim.x * 4) {
+    if (i + 3 < n) {
+      const float4 v = *reinterpret_cast<const float4*>(src + i);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      reinterpret_cast<__nv_bfloat162*>(dst + i)[0] = lo;
+      reinterpret_cast<__nv_bfloat162*>(dst + i)[1] = hi;
+    } else {
+      for (int64_t j = i; j < n; ++j) dst[j] = __float2bfloat16_rn(src[j]);
+    }
+  }
+}
+int launch_to_bf16(const float* src, void* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return CP_OK;
+  const int blocks = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 16);
+  to_bf16_kernel<<<blocks, 256, 0, s>>>(src, reinterpret_cast<__nv_bfloat16*>(dst), n);
   CP_LAUNCHED();
   return CP_OK;
 }

@@ -28,6 +28,9 @@ using namespace tc;
 namespace {
 
 enum { PASS_FWD = 0, PASS_DGRAD = 1, PASS_WGRAD = 2 };
+// operand element size / elements per 128-byte K-chunk of a layer (bf16 mode: 2 / 64, else 4 / 32)
+inline int op_bytes(const Layer& L) { return L.d.math == CP_MATH_BF16 ? 2 : 4; }
+inline int op_elems(const Layer& L) { return 128 / op_bytes(L); }
 constexpr int BM = 128, BN = 256, BK = 32;
 constexpr int A_BYTES = BM * BK * 4;          // 16 KB: this CTA's 128 rows x 32 k
 constexpr int NUM_THREADS = 384;             // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-w11 epilogue
@@ -85,6 +88,7 @@ struct TcParams {
   int nsched;          // >0: per-group unit lists (host LPT schedule); 0: static round-robin
   short sched_off[MAX_GROUPS + 1];
   short sched[MAX_SCHED];
+  int bke;             // operand elements per K-chunk (one 128-byte row): 32 tf32, 64 bf16
   int pix;             // dgrad pixel mode: a CTA's 128 rows = 128 images of ONE input pixel, a pair = two
                        // horizontally adjacent pixels (exact valid rows, s-union only at borders)
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
@@ -228,8 +232,11 @@ __device__ __forceinline__ void dgrad_taps(const TcParams& p, const Unit& t, int
 // Visit the K-chunks of split `t.sp` of a unit, in order.  A unit's chunk sequence is
 // FWD: (tap, input block, 32-channel chunk); DGRAD: (32-kernel chunk, valid tap);
 // WGRAD: (position, 32-image chunk).  Split sp covers [sp*per, (sp+1)*per) of it.
-template <int PASS, class F>
+// DT: operand type (0 tf32, 1 bf16): a K-chunk is one 128-byte row of elements (BKE = 32 / 64),
+// four MMA K-steps of KSE = 8 / 16 elements.
+template <int PASS, int DT, class F>
 __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t, F f) {
+  constexpr int BKE = DT ? 64 : 32, KSE = DT ? 16 : 8;
   if (PASS == PASS_FWD) {
     const int RS = p.R * p.S;
     const int total = RS * p.cpt;
@@ -241,17 +248,17 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     if (p.arrive) {
       // overlapped gather: input blocks outermost (own block first), then tap, then channel chunk
       int rb = p.self_blk, rem = lo;
-      int nc = (p.kw[rb] + BK - 1) / BK;
+      int nc = (p.kw[rb] + BKE - 1) / BKE;
       while (rem >= nc * RS) {
         rem -= nc * RS;
         rb = rb + 1 == p.nblk ? 0 : rb + 1;
-        nc = (p.kw[rb] + BK - 1) / BK;
+        nc = (p.kw[rb] + BKE - 1) / BKE;
       }
       int tap = rem / nc, c = rem - tap * nc;
       int r = tap / p.S, sx = tap - r * p.S;
       int kw = p.kw[rb];
       for (int idx = lo; idx < hi; ++idx) {
-        f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
+        f(Chunk{tap, rb, c, min(BKE, kw - c * BKE) / KSE, r, sx, 0, 0, 0});
         if (++c == nc) {
           c = 0;
           ++tap;
@@ -263,7 +270,7 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
             tap = r = sx = 0;
             do {
               rb = rb + 1 == p.nblk ? 0 : rb + 1;
-              nc = (p.kw[rb] + BK - 1) / BK;
+              nc = (p.kw[rb] + BKE - 1) / BKE;
             } while (nc == 0);
             kw = p.kw[rb];
           }
@@ -273,16 +280,16 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     }
     // tap outermost, then input block, then channel chunk
     int tap = lo / p.cpt, rem = lo - tap * p.cpt;
-    int rb = 0, nc = (p.kw[0] + BK - 1) / BK;
+    int rb = 0, nc = (p.kw[0] + BKE - 1) / BKE;
     while (rem >= nc) {
       rem -= nc;
       ++rb;
-      nc = (p.kw[rb] + BK - 1) / BK;
+      nc = (p.kw[rb] + BKE - 1) / BKE;
     }
     int c = rem, r = tap / p.S, sx = tap - r * p.S;
     int kw = p.kw[rb];
     for (int idx = lo; idx < hi; ++idx) {
-      f(Chunk{tap, rb, c, min(BK, kw - c * BK) / 8, r, sx, 0, 0, 0});
+      f(Chunk{tap, rb, c, min(BKE, kw - c * BKE) / KSE, r, sx, 0, 0, 0});
       if (++c == nc) {
         c = 0;
         do {
@@ -294,7 +301,7 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
               ++r;
             }
           }
-          nc = (p.kw[rb] + BK - 1) / BK;
+          nc = (p.kw[rb] + BKE - 1) / BKE;
         } while (nc == 0 && tap < RS);
         kw = p.kw[rb];
       }
@@ -302,7 +309,7 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
   } else if (PASS == PASS_DGRAD) {
     int r_lo, nr, s_lo, ns;
     dgrad_taps(p, t, r_lo, nr, s_lo, ns);
-    const int kc = (p.Kc + BK - 1) / BK;
+    const int kc = (p.Kc + BKE - 1) / BKE;
     const int total = nr * ns * kc;
     const int per = (total + p.split - 1) / p.split;
     const int lo = t.sp * per, hi = min(total, lo + per);
@@ -314,7 +321,7 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     int c = lo / nt, rem = lo - c * nt;
     int r = r_lo + rem / ns, sx = s_lo + rem % ns;
     for (int idx = lo; idx < hi; ++idx) {
-      f(Chunk{r * p.S + sx, 0, c, min(BK, p.Kc - c * BK) / 8, r, sx, 0, 0, 0});
+      f(Chunk{r * p.S + sx, 0, c, min(BKE, p.Kc - c * BKE) / KSE, r, sx, 0, 0, 0});
       if (++sx == s_lo + ns) {
         sx = s_lo;
         if (++r == r_lo + nr) {
@@ -327,11 +334,11 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     const int c0 = t.tail ? t.piece * p.tail_per : t.sp * p.chunks_per_split;
     const int c1 = min(p.chunks_total, c0 + (t.tail ? p.tail_per : p.chunks_per_split));
     // k-chunk c = (pq, bc): decoded once, then stepped
-    const int nbc = p.Bp / 32;
+    const int nbc = p.Bp / BKE;
     int bc = c0 % nbc, pq = c0 / nbc;
     int q = pq % p.Wo, pp = pq / p.Wo;
     for (int c = c0; c < c1; ++c) {
-      f(Chunk{0, 0, c, BK / 8, 0, 0, bc, q, pp});
+      f(Chunk{0, 0, c, BKE / KSE, 0, 0, bc, q, pp});
       if (++bc == nbc) {
         bc = 0;
         if (++q == p.Wo) {
@@ -346,11 +353,11 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
 // MMA N for a tile of n columns: multiple of 8 (1 CTA) / 16 (pair); with a pair and MN-major B
 // each CTA's half must be whole 32-column atoms, so N is rounded to 64 (extra columns are zero
 // or neighbouring data and are never stored).
-template <int PASS, int CG>
+template <int PASS, int CG, int DT = 0>
 __host__ __device__ __forceinline__ int mma_n(int n) {
   if (CG == 1) return (n + 7) / 8 * 8;
   if (PASS == PASS_FWD) return (n + 15) / 16 * 16;
-  return (n + 63) / 64 * 64;
+  return DT ? (n + 127) / 128 * 128 : (n + 63) / 64 * 64;   // whole MN-major groups per CTA half
 }
 
 __device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], int n) {
@@ -365,8 +372,12 @@ __device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], i
   }
 }
 
-template <int PASS, int CG>
+template <int PASS, int CG, int DT>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
+  // DT = 1: bf16 operands (kind::f16), a K-chunk = 64 elements; MN-major 64-element groups ("atoms")
+  constexpr int BKE = DT ? 64 : 32;          // elements per 128-byte row = per K-chunk
+  constexpr int ASH = DT ? 6 : 5;            // log2 of the MN-major group width
+  constexpr int GBYTES = BKE * 128;          // bytes of one MN-major group (BKE rows x 128 B)
   using C = Cfg<CG, PASS>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned base (128B swizzle atoms); offsetting the __shared__ array keeps the
@@ -415,7 +426,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int u = unit_at(p, group, ngroups, k);
         if (u < 0) break;
         const Unit t = decode_unit<PASS, CG>(p, u, rank);
-        const int n_mma = mma_n<PASS, CG>(t.n);
+        const int n_mma = mma_n<PASS, CG, DT>(t.n);
         const int nb_own = CG == 2 ? n_mma / 2 : n_mma;          // B columns staged by this CTA
         const int nb0 = t.n0 + (int)rank * nb_own;                // first B column of this CTA
         const int nboxes = p.wide ? (CG == 2 ? 4 : 8) : (nb_own + 31) / 32;  // MN-major B: 32-column atoms
@@ -424,16 +435,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         int wb_n = 0, wb_rb[8], wb_atom[8];
         const int wg_r = PASS == PASS_WGRAD ? t.tap / p.S : 0, wg_s = PASS == PASS_WGRAD ? t.tap % p.S : 0;
         if (PASS == PASS_WGRAD && p.span) {
-          for (int jb = 0; jb * p.apb * 32 < (CG == 2 ? BN / 2 : BN) && jb < 8; ++jb) {
-            const int sl = nb0 + jb * p.apb * 32;   // concatenated slot of this box
+          for (int jb = 0; jb * p.apb * BKE < (CG == 2 ? BN / 2 : BN) && jb < 8; ++jb) {
+            const int sl = nb0 + jb * p.apb * BKE;  // concatenated slot of this box
             int rb = 0;
             while (rb + 1 < p.nblk && sl >= p.coff[rb + 1]) ++rb;
             wb_rb[jb] = rb;
-            wb_atom[jb] = (sl - p.coff[rb]) >> 5;
+            wb_atom[jb] = (sl - p.coff[rb]) >> ASH;
             wb_n = jb + 1;
           }
         }
-        for_each_chunk<PASS>(p, t, [&](const Chunk& ch) {
+        for_each_chunk<PASS, DT>(p, t, [&](const Chunk& ch) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
@@ -461,36 +472,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               arrived |= 1u << ch.rb;
             }
             if (p.unified)
-              ld5(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
+              ld5(a, &p.maps[0], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
             else
-              ld4(a, &p.maps[ch.rb], ch.c * BK, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
-            ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BK, nb0);
+              ld4(a, &p.maps[ch.rb], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
+            ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.r, s = ch.s;
             if (p.pix)
-              ld4(a, &p.maps[0], ch.c * BK, t.bc * 128, 2 * t.j + (int)rank - s, t.i - r);
+              ld4(a, &p.maps[0], ch.c * BKE, t.bc * 128, 2 * t.j + (int)rank - s, t.i - r);
             else
-              ld4(a, &p.maps[0], ch.c * BK, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
+              ld4(a, &p.maps[0], ch.c * BKE, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
             if (p.wide) {
-              ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BK, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> 5, ch.tap);
+              ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BKE, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> ASH, ch.tap);
             } else {
               for (int q = 0; q < nboxes; ++q)
-                ld3(b + q * 4096, &p.maps[CP_MAX_RANKS], p.coff[t.rb] + nb0 + 32 * q, ch.c * BK, ch.tap);
+                ld3(b + q * 4096, &p.maps[CP_MAX_RANKS], p.coff[t.rb] + nb0 + 32 * q, ch.c * BKE, ch.tap);
             }
           } else {
             const int bc = ch.bc, q = ch.q, pp = ch.pp;
             const int r = wg_r, s = wg_s;
             if (p.span) {
-              ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
+              ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * BKE, t.mt * (BM >> ASH), q, pp);
               for (int jb = 0; jb < wb_n; ++jb) {   // boxes of this unit (block / atom hoisted per unit)
                 if (p.unified)
-                  ld5(b + jb * p.apb * 4096, &p.maps[0], 0, bc * 32, wb_atom[jb], (pp + r) * p.Win + q + s, wb_rb[jb]);
+                  ld5(b + jb * p.apb * GBYTES, &p.maps[0], 0, bc * BKE, wb_atom[jb], (pp + r) * p.Win + q + s, wb_rb[jb]);
                 else
-                  ld5(b + jb * p.apb * 4096, &p.maps[wb_rb[jb]], 0, bc * 32, wb_atom[jb], q + s, pp + r);
+                  ld5(b + jb * p.apb * GBYTES, &p.maps[wb_rb[jb]], 0, bc * BKE, wb_atom[jb], q + s, pp + r);
               }
             } else if (p.wide) {
-              ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * 32, t.mt * 4, q, pp);
-              ld5(b, &p.maps[t.rb], 0, bc * 32, nb0 >> 5, q + s, pp + r);
+              ld5(a, &p.maps[CP_MAX_RANKS], 0, bc * BKE, t.mt * (BM >> ASH), q, pp);
+              ld5(b, &p.maps[t.rb], 0, bc * BKE, nb0 >> ASH, q + s, pp + r);
             } else {
               for (int m = 0; m < 4; ++m)
                 ld4(a + m * 4096, &p.maps[CP_MAX_RANKS], t.mt * BM + 32 * m, bc * 32, q, pp);
@@ -520,33 +531,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int n_mma = mma_n<PASS, CG>(t.n);
+        const int n_mma = mma_n<PASS, CG, DT>(t.n);
         const int a_mn = PASS == PASS_WGRAD, b_mn = PASS != PASS_FWD;
-        const uint32_t idesc = idesc_tf32(BM * CG, n_mma, a_mn, b_mn);
+        const uint32_t idesc = DT ? idesc_bf16(BM * CG, n_mma, a_mn, b_mn) : idesc_tf32(BM * CG, n_mma, a_mn, b_mn);
         uint32_t accumulate = 0;
-        for_each_chunk<PASS>(p, t, [&](const Chunk& ch) {
+        for_each_chunk<PASS, DT>(p, t, [&](const Chunk& ch) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
           // descriptors built once per chunk; a K-step only advances the start-address field
           // (16-byte units: +32 B K-major, +1024 B MN-major)
-          const uint64_t ad0 = a_mn ? sdesc_mn(a_addr, 0) : sdesc_k(a_addr, 0);
-          const uint64_t bd0 = b_mn ? sdesc_mn(b_addr, 0) : sdesc_k(b_addr, 0);
-          const uint64_t astep = a_mn ? 64 : 2, bstep = b_mn ? 64 : 2;
-          if (ch.ksteps == BK / 8) {
+          // (bf16 MN-major: 64-element groups of BKE K-rows, +2048 B per K=16 step)
+          const uint64_t ad0 = a_mn ? (DT ? sdesc_mn16(a_addr, 0, BKE) : sdesc_mn(a_addr, 0)) : sdesc_k(a_addr, 0);
+          const uint64_t bd0 = b_mn ? (DT ? sdesc_mn16(b_addr, 0, BKE) : sdesc_mn(b_addr, 0)) : sdesc_k(b_addr, 0);
+          const uint64_t mnstep = DT ? 128 : 64;
+          const uint64_t astep = a_mn ? mnstep : 2, bstep = b_mn ? mnstep : 2;
+          auto mma = [&](int k) {
+            if (DT) {
+              if (CG == 2) mma_bf16_cg2(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+              else mma_bf16(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+            } else {
+              if (CG == 2) mma_tf32_cg2(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+              else mma_tf32(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
+            }
+            accumulate = 1;
+          };
+          if (ch.ksteps == 4) {
 #pragma unroll
-            for (int k = 0; k < BK / 8; ++k) {
-              if (CG == 2) mma_tf32_cg2(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
-              else mma_tf32(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
-              accumulate = 1;
-            }
+            for (int k = 0; k < 4; ++k) mma(k);
           } else {
-            for (int k = 0; k < ch.ksteps; ++k) {
-              if (CG == 2) mma_tf32_cg2(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
-              else mma_tf32(d_tmem, ad0 + k * astep, bd0 + k * bstep, idesc, accumulate);
-              accumulate = 1;
-            }
+            for (int k = 0; k < ch.ksteps; ++k) mma(k);
           }
           if (CG == 2) mma_commit_cg2(&empty[stage]); else mma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
@@ -976,33 +991,35 @@ int get_encoder(EncodeTiledFn* fn) {
 
 // fp32 tensor map, zero OOB fill.  dims innermost first; strides in bytes for dims 1..
 // K-major operand tiles: SWIZZLE_128B; MN-major tiles: SWIZZLE_128B_ATOM_32B (see tc_common.cuh).
+// es: element size (4 = fp32 / tf32 operands, 2 = bf16 operands)
 int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-             const uint32_t* box, bool mn_major = false) {
+             const uint32_t* box, bool mn_major = false, int es = 4) {
   EncodeTiledFn enc;
   CP_TRY(get_encoder(&enc));
   cuuint64_t gd[5], gs[4];
-  cuuint32_t bx[5], es[5];
+  cuuint32_t bx[5], est[5];
   for (int i = 0; i < rank; ++i) {
     gd[i] = dims[i];
     bx[i] = box[i];
-    es[i] = 1;
+    est[i] = 1;
     if (i + 1 < rank) gs[i] = strides[i];
   }
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), gd, gs, bx, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = enc(m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
+                   const_cast<void*>(base), gd, gs, bx, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   (mn_major && es == 4) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) CP_FAIL(CP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return CP_OK;
 }
 
-// 4-D map over an activation block [H][W][Bp][kw] with box {32, 32, bw, bh}
-int map_act(CUtensorMap* m, const float* base, int kw, int Bp, int W, int H, int bw, int bh, bool mn_major) {
+// 4-D map over an activation block [H][W][Bp][kw] with box {one 128-byte row, 32, bw, bh}
+int map_act(CUtensorMap* m, const void* base, int kw, int Bp, int W, int H, int bw, int bh, bool mn_major,
+            int es = 4) {
   const uint64_t dims[4] = {(uint64_t)kw, (uint64_t)Bp, (uint64_t)W, (uint64_t)H};
-  const uint64_t str[3] = {(uint64_t)kw * 4, (uint64_t)kw * Bp * 4, (uint64_t)kw * Bp * W * 4};
-  const uint32_t box[4] = {32, 32, (uint32_t)bw, (uint32_t)bh};
-  return make_map(m, base, 4, dims, str, box, mn_major);
+  const uint64_t str[3] = {(uint64_t)kw * es, (uint64_t)kw * Bp * es, (uint64_t)kw * Bp * W * es};
+  const uint32_t box[4] = {(uint32_t)(128 / es), 32, (uint32_t)bw, (uint32_t)bh};
+  return make_map(m, base, 4, dims, str, box, mn_major, es);
 }
 
 int env_int(const char* name, int dflt) {
@@ -1014,11 +1031,13 @@ int env_int(const char* name, int dflt) {
 // {32, 32, natoms, 1, 1} lands as natoms stacked MN-major 32x32 atoms (the canonical layout).
 // Slots past kw inside the last atom read neighbouring data: they only feed output columns/rows
 // that are never stored, and every buffer carries read slack (conv_part_query).
-int map_act_wide(CUtensorMap* m, const float* base, int kw, int Bp, int W, int H, int natoms) {
-  const uint64_t dims[5] = {32, (uint64_t)Bp, (uint64_t)((kw + 31) / 32), (uint64_t)W, (uint64_t)H};
-  const uint64_t str[4] = {(uint64_t)kw * 4, 128, (uint64_t)kw * Bp * 4, (uint64_t)kw * Bp * W * 4};
-  const uint32_t box[5] = {32, 32, (uint32_t)natoms, 1, 1};
-  return make_map(m, base, 5, dims, str, box, true);
+// (bf16, es = 2: 64-element groups of 64 K-rows, the SWIZZLE_128B canonical MN-major layout)
+int map_act_wide(CUtensorMap* m, const void* base, int kw, int Bp, int W, int H, int natoms, int es = 4) {
+  const int E = 128 / es;
+  const uint64_t dims[5] = {(uint64_t)E, (uint64_t)Bp, (uint64_t)((kw + E - 1) / E), (uint64_t)W, (uint64_t)H};
+  const uint64_t str[4] = {(uint64_t)kw * es, 128, (uint64_t)kw * Bp * es, (uint64_t)kw * Bp * W * es};
+  const uint32_t box[5] = {(uint32_t)E, (uint32_t)E, (uint32_t)natoms, 1, 1};
+  return make_map(m, base, 5, dims, str, box, true, es);
 }
 
 // all input rank blocks have the same (nonzero) width and there are several of them
@@ -1040,12 +1059,12 @@ int num_sms() {
   return n;
 }
 
-template <int PASS, int CG>
+template <int PASS, int CG, int DT = 0>
 int launch_cg(const TcParams& p, cudaStream_t s) {
   if (p.units <= 0) return CP_OK;
   static bool attr = false;
   if (!attr) {
-    CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS, CG, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Cfg<CG, PASS>::SMEM));
     attr = true;
   }
@@ -1067,7 +1086,7 @@ int launch_cg(const TcParams& p, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CP_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<PASS, CG>, p));
+  CP_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<PASS, CG, DT>, p));
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -1102,6 +1121,7 @@ void fill_blocks(TcParams& p, const Layer& L) {
 
 void fill_common(TcParams& p, const Layer& L) {
   fill_blocks(p, L);
+  p.bke = op_elems(L);
   p.epi_groups = env_int("CP_TC_EPI_GROUPS", 0);  // 0: decided per launch from the K-loop length
   p.R = L.images ? 1 : L.R;
   p.S = L.images ? 1 : L.S;
@@ -1145,7 +1165,7 @@ int choose_split(int units, int groups, double chunks, double out_bytes, int max
 bool span_ok(const TcParams& p) {
   if (p.images || p.nblk < 2 || !env_int("CP_TC_SPAN", 1)) return false;
   for (int r = 0; r < p.nblk; ++r)
-    if (p.kw[r] % 32) return false;
+    if (p.kw[r] % p.bke) return false;
   return true;
 }
 
@@ -1193,7 +1213,7 @@ static Plan fwd_plan(const Layer& L, TcParams& p) {
   w.pair = use_pairs() && (L.Bp / 32) % 2 == 0;
   const int CG = w.pair ? 2 : 1;
   int cpt = 0;
-  for (int r = 0; r < p.nblk; ++r) cpt += (p.kw[r] + BK - 1) / BK;
+  for (int r = 0; r < p.nblk; ++r) cpt += (p.kw[r] + op_elems(L) - 1) / op_elems(L);
   p.cpt = cpt;
   w.numM = (L.Ho / 2) * (L.Wo / 2) * (L.Bp / 32) / CG;
   // Balanced N tiles: Kc split into T equal tiles (width a multiple of 16 / 8).  Choose T by
@@ -1250,7 +1270,7 @@ static Plan dgrad_plan(const Layer& L, TcParams& p) {
       t += std::min(R - 1, rows * i + rows - 1) - std::max(0, rows * i - Ho + 1) + 1;
     return t / n;
   };
-  const double kc = (L.Kc + BK - 1) / BK;
+  const double kc = (L.Kc + op_elems(L) - 1) / op_elems(L);
   w.chunks = (int)(avg_valid(L.H, L.Ho, L.R, p.pix ? 1 : 2) * avg_valid(L.W, L.Wo, L.S, 2) * kc + 0.5);
   w.S = env_int("CP_TC_SPLIT_DGRAD", 0);
   if (w.S <= 0) w.S = choose_split(w.numM * w.numN, num_sms() / CG, w.chunks, (double)L.in.start[L.in.n] * 4, 16);
@@ -1268,7 +1288,7 @@ static Plan wgrad_plan(const Layer& L, TcParams& p) {
   const int per_tap = build_ntiles(p);
   w.numM = ((L.Kc + BM - 1) / BM + CG - 1) / CG;
   w.numN = per_tap < 0 ? -1 : per_tap * p.R * p.S;
-  w.chunks = L.Ho * L.Wo * (L.Bp / 32);
+  w.chunks = L.Ho * L.Wo * (L.Bp / op_elems(L));   // K-chunks of op_elems images per position
   w.S = env_int("CP_TC_SPLIT_WGRAD", 0);
   if (w.S <= 0) {
     const int units = std::max(1, w.numM * w.numN), G = num_sms() / CG;
@@ -1289,11 +1309,11 @@ static Plan wgrad_plan(const Layer& L, TcParams& p) {
   w.per = (w.chunks + w.S - 1) / w.S;
   w.S = (w.chunks + w.per - 1) / w.per;
   // atoms per B box: every block holds whole boxes
-  const int own_atoms = (CG == 2 ? BN / 2 : BN) / 32;
+  const int own_atoms = (CG == 2 ? BN / 2 : BN) / op_elems(L);
   w.apb = own_atoms;
   if (p.span)
     for (int r = 0; r < p.nblk; ++r)
-      while (w.apb > 1 && (p.kw[r] / 32) % w.apb) w.apb >>= 1;
+      while (w.apb > 1 && (p.kw[r] / op_elems(L)) % w.apb) w.apb >>= 1;
   return w;
 }
 
@@ -1340,28 +1360,30 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   TcParams p{};
   fill_common(p, L);
   const Plan pl = fwd_plan(L, p);
+  const int es = op_bytes(L), E = 128 / es;
   if (L.images) {
-    CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 2, 2, false));
+    CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 2, 2, false, es));
   } else if (equal_blocks(L)) {
     // one 5-D map over all rank blocks: (slot, b, w, h, block)
     const int kw = L.in.kw[0];
     const uint64_t dims[5] = {(uint64_t)kw, (uint64_t)L.Bp, (uint64_t)L.W, (uint64_t)L.H, (uint64_t)L.in.n};
-    const uint64_t str[4] = {(uint64_t)kw * 4, (uint64_t)kw * L.Bp * 4, (uint64_t)kw * L.Bp * L.W * 4,
-                             (uint64_t)kw * L.Bp * L.W * L.H * 4};
-    const uint32_t box[5] = {32, 32, 2, 2, 1};
-    CP_TRY(make_map(&p.maps[0], xin, 5, dims, str, box, false));
+    const uint64_t str[4] = {(uint64_t)kw * es, (uint64_t)kw * L.Bp * es, (uint64_t)kw * L.Bp * L.W * es,
+                             (uint64_t)kw * L.Bp * L.W * L.H * es};
+    const uint32_t box[5] = {(uint32_t)E, 32, 2, 2, 1};
+    CP_TRY(make_map(&p.maps[0], xin, 5, dims, str, box, false, es));
     p.unified = 1;
   } else {
     for (int r = 0; r < L.in.n; ++r)
-      if (L.in.kw[r] > 0) CP_TRY(map_act(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false));
+      if (L.in.kw[r] > 0)
+        CP_TRY(map_act(&p.maps[r], (const char*)xin + L.in.start[r] * es, L.in.kw[r], L.Bp, L.W, L.H, 2, 2, false, es));
   }
   p.bn_box = pl.pair ? p.nw / 2 : std::min(p.nw, L.Kc);
 
   {
     const uint64_t dims[2] = {(uint64_t)L.Ktot, (uint64_t)std::max(L.Kr, 1)};
-    const uint64_t str[1] = {(uint64_t)L.Ktot * 4};
-    const uint32_t box[2] = {32, (uint32_t)p.bn_box};
-    CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 2, dims, str, box));
+    const uint64_t str[1] = {(uint64_t)L.Ktot * es};
+    const uint32_t box[2] = {(uint32_t)E, (uint32_t)p.bn_box};
+    CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 2, dims, str, box, false, es));
   }
   p.numM = pl.numM;
   p.numN = pl.numN;
@@ -1424,7 +1446,8 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     }
   }
   CP_TRY(tc_time_mark(L, PASS_FWD, 0, s));
-  CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
+  if (es == 2) CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2, 1>(p, s) : launch_cg<PASS_FWD, 1, 1>(p, s)));
+  else CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
   CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
   if (p.tail_st > 0) {
     fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
@@ -1459,24 +1482,26 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     p.fused_dx = 1;
     for (int r = 0; r < L.in.n; ++r) p.dst[r] = dst_blocks[r];
   }
+  const int es = op_bytes(L), E = 128 / es;
   if (p.pix) {
-    // A = dY rows of one pixel: box {32 kernels, 128 images, 1, 1}
+    // A = dY rows of one pixel: box {one 128-byte row of kernels, 128 images, 1, 1}
     const uint64_t dims[4] = {(uint64_t)L.Kc, (uint64_t)L.Bp, (uint64_t)L.Wo, (uint64_t)L.Ho};
-    const uint64_t str[3] = {(uint64_t)L.Kc * 4, (uint64_t)L.Kc * L.Bp * 4, (uint64_t)L.Kc * L.Bp * L.Wo * 4};
-    const uint32_t box[4] = {32, 128, 1, 1};
-    CP_TRY(make_map(&p.maps[0], dY, 4, dims, str, box, false));
+    const uint64_t str[3] = {(uint64_t)L.Kc * es, (uint64_t)L.Kc * L.Bp * es, (uint64_t)L.Kc * L.Bp * L.Wo * es};
+    const uint32_t box[4] = {(uint32_t)E, 128, 1, 1};
+    CP_TRY(make_map(&p.maps[0], dY, 4, dims, str, box, false, es));
   } else {
-    CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false));
+    CP_TRY(map_act(&p.maps[0], dY, L.Kc, L.Bp, L.Wo, L.Ho, 2, 2, false, es));
   }
   p.wide = 1;
   for (int r = 0; r < L.in.n; ++r)
-    if (L.in.coff[r] % 32) p.wide = 0;
+    if (L.in.coff[r] % E) p.wide = 0;
+  if (es == 2 && !p.wide) CP_FAIL(CP_ERR_UNSUPPORTED, "bf16 dgrad needs input block offsets in multiples of 64");
   if (p.wide) {
-    // W [Kr][RS][Cg] viewed as (c' lane, k, c' atom, tap): one box {32, 32, natoms, 1}
-    const uint64_t dims[4] = {32, (uint64_t)L.Kr, (uint64_t)((L.in.Cg + 31) / 32), (uint64_t)(L.R * L.S)};
-    const uint64_t str[3] = {(uint64_t)L.Ktot * 4, 128, (uint64_t)L.in.Cg * 4};
-    const uint32_t box[4] = {32, 32, (uint32_t)(pl.pair ? 4 : 8), 1};
-    CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 4, dims, str, box, true));
+    // W [Kr][RS][Cg] viewed as (c' lane, k, c' group, tap): one box {E, E, groups, 1}
+    const uint64_t dims[4] = {(uint64_t)E, (uint64_t)L.Kr, (uint64_t)((L.in.Cg + E - 1) / E), (uint64_t)(L.R * L.S)};
+    const uint64_t str[3] = {(uint64_t)L.Ktot * es, 128, (uint64_t)L.in.Cg * es};
+    const uint32_t box[4] = {(uint32_t)E, (uint32_t)E, (uint32_t)((pl.pair ? BN / 2 : BN) / E), 1};
+    CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 4, dims, str, box, true, es));
   } else {
     // W [Kr][RS][Cg] viewed as (c', k, tap): MN-major boxes {32 c', 32 k, 1}
     const uint64_t dims[3] = {(uint64_t)L.in.Cg, (uint64_t)L.Kr, (uint64_t)(L.R * L.S)};
@@ -1518,7 +1543,7 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     // in natural order (keeps the spatial L2 locality of neighbouring windows).
     const int CG = pl.pair ? 2 : 1, G = std::min(p.units, num_sms() / CG);
     if (p.nwin_order == 0 && p.units <= MAX_SCHED && G <= MAX_GROUPS && env_int("CP_TC_DGRAD_SCHED", 1)) {
-      const int nbcg = p.pix ? L.Bp / 128 : L.Bp / 32 / CG, W2 = L.W / 2, kc = (L.Kc + BK - 1) / BK;
+      const int nbcg = p.pix ? L.Bp / 128 : L.Bp / 32 / CG, W2 = L.W / 2, kc = (L.Kc + op_elems(L) - 1) / op_elems(L);
       std::vector<std::pair<long long, int>> wk(p.units);
       for (int u = 0; u < p.units; ++u) {
         const int mg = u % p.numM;
@@ -1550,7 +1575,8 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
     }
   }
   CP_TRY(tc_time_mark(L, PASS_DGRAD, 0, s));
-  CP_TRY((pl.pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s)));
+  if (es == 2) CP_TRY((pl.pair ? launch_cg<PASS_DGRAD, 2, 1>(p, s) : launch_cg<PASS_DGRAD, 1, 1>(p, s)));
+  else CP_TRY((pl.pair ? launch_cg<PASS_DGRAD, 2>(p, s) : launch_cg<PASS_DGRAD, 1>(p, s)));
   CP_TRY(tc_time_mark(L, PASS_DGRAD, 1, s));
   if (pl.S > 1) {
     const int64_t n = L.in.start[L.in.n];
@@ -1567,22 +1593,24 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   if (w.numN <= 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many wgrad N tiles");
   p.wide = 1;
   p.apb = w.apb;
-  const int nat = p.span ? w.apb : (w.pair ? 4 : 8);
+  const int es = op_bytes(L), E = 128 / es;
+  const int nat = p.span ? w.apb : (w.pair ? BN / 2 : BN) / E;
   if (L.images) {
-    CP_TRY(map_act_wide(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, nat));
+    CP_TRY(map_act_wide(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, nat, es));
   } else if (p.span && equal_blocks(L)) {
-    // one 5-D map over all rank blocks: (slot lane, b, 32-slot atom, h*W + w, block)
+    // one 5-D map over all rank blocks: (slot lane, b, slot group, h*W + w, block)
     const int kw = L.in.kw[0];
-    const uint64_t dims[5] = {32, (uint64_t)L.Bp, (uint64_t)(kw / 32), (uint64_t)L.H * L.W, (uint64_t)L.in.n};
-    const uint64_t str[4] = {(uint64_t)kw * 4, 128, (uint64_t)kw * L.Bp * 4, (uint64_t)kw * L.Bp * L.W * L.H * 4};
-    const uint32_t box[5] = {32, 32, (uint32_t)nat, 1, 1};
-    CP_TRY(make_map(&p.maps[0], xin, 5, dims, str, box, true));
+    const uint64_t dims[5] = {(uint64_t)E, (uint64_t)L.Bp, (uint64_t)(kw / E), (uint64_t)L.H * L.W, (uint64_t)L.in.n};
+    const uint64_t str[4] = {(uint64_t)kw * es, 128, (uint64_t)kw * L.Bp * es, (uint64_t)kw * L.Bp * L.W * L.H * es};
+    const uint32_t box[5] = {(uint32_t)E, (uint32_t)E, (uint32_t)nat, 1, 1};
+    CP_TRY(make_map(&p.maps[0], xin, 5, dims, str, box, true, es));
     p.unified = 1;
   } else {
     for (int r = 0; r < L.in.n; ++r)
-      if (L.in.kw[r] > 0) CP_TRY(map_act_wide(&p.maps[r], xin + L.in.start[r], L.in.kw[r], L.Bp, L.W, L.H, nat));
+      if (L.in.kw[r] > 0)
+        CP_TRY(map_act_wide(&p.maps[r], (const char*)xin + L.in.start[r] * es, L.in.kw[r], L.Bp, L.W, L.H, nat, es));
   }
-  CP_TRY(map_act_wide(&p.maps[CP_MAX_RANKS], dY, L.Kc, L.Bp, L.Wo, L.Ho, 4));
+  CP_TRY(map_act_wide(&p.maps[CP_MAX_RANKS], dY, L.Kc, L.Bp, L.Wo, L.Ho, BM / E, es));
   p.numM = w.numM;
   p.numN = w.numN;
   p.chunks_total = w.chunks;
@@ -1624,7 +1652,8 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
     p.units = p.tail_full + T * st;
   }
   CP_TRY(tc_time_mark(L, PASS_WGRAD, 0, s));
-  CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2>(p, s) : launch_cg<PASS_WGRAD, 1>(p, s)));
+  if (es == 2) CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2, 1>(p, s) : launch_cg<PASS_WGRAD, 1, 1>(p, s)));
+  else CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2>(p, s) : launch_cg<PASS_WGRAD, 1>(p, s)));
   CP_TRY(tc_time_mark(L, PASS_WGRAD, 1, s));
   if (p.tail_st > 0) {
     wgrad_tail_reduce<<<dim3(BM, CG, ti.n), BN, 0, s>>>(p.tail_buf, dw, ti);

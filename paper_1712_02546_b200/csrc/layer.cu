@@ -52,7 +52,8 @@ static int derive(Layer& L, const cp_conv_desc& d) {
   if (d.in_h < d.k_h || d.in_w < d.k_w)
     CP_FAIL(CP_ERR_SHAPE, "dimension error: input " + shp({d.batch, d.in_c, d.in_h, d.in_w}) + " vs kernels " +
                               shp({d.num_k, d.in_c, d.k_h, d.k_w}));
-  if (d.math != CP_MATH_TF32 && d.math != CP_MATH_FP32_SIMT) CP_FAIL(CP_ERR_CONFIG, "unknown math mode");
+  if (d.math != CP_MATH_TF32 && d.math != CP_MATH_FP32_SIMT && d.math != CP_MATH_BF16)
+    CP_FAIL(CP_ERR_CONFIG, "unknown math mode");
   if (d.input_kind != CP_INPUT_IMAGES && d.input_kind != CP_INPUT_GATHER) CP_FAIL(CP_ERR_CONFIG, "unknown input kind");
   CP_TRY(validate_part(d.out_part, "out_part"));
   if (d.out_part.num_k != d.num_k)
@@ -85,13 +86,28 @@ static int derive(Layer& L, const cp_conv_desc& d) {
     L.Ktot = L.R * L.S * L.in.Cg;
   }
   L.out = make_blocks(d.out_part, L.Hp, L.Wp, L.Bp);
+  if (d.math == CP_MATH_BF16) {   // 64-element K-chunks: whole chunks of slots and of images
+    if (L.Bp % 64) CP_FAIL(CP_ERR_UNSUPPORTED, "bf16 mode: batch padded to 32 must be a multiple of 64");
+    for (int r = 0; r < d.out_part.n_ranks; ++r)
+      if (d.out_part.k_width[r] % 64) CP_FAIL(CP_ERR_CONFIG, "bf16 mode: out_part widths must be multiples of 64");
+    if (!L.images)
+      for (int r = 0; r < d.in_part.n_ranks; ++r)
+        if (d.in_part.k_width[r] % 64) CP_FAIL(CP_ERR_CONFIG, "bf16 mode: in_part widths must be multiples of 64");
+  }
   // workspace carve-up
   size_t off = 0;
   L.off_xcol = off; L.ws_xcol = L.images ? al256((size_t)L.Ho * L.Wo * L.Bp * L.Kcol * 4) : 0; off += L.ws_xcol;
   L.off_z = off; L.ws_z = d.math == CP_MATH_FP32_SIMT ? al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 4) : 0; off += L.ws_z;
   L.off_dy = off; L.ws_dy = al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 4); off += L.ws_dy;
   L.off_dbpart = off; L.ws_dbpart = al256((size_t)kBiasSplitMax * std::max(L.Kc, 8) * 4); off += L.ws_dbpart;
-  L.off_split = off; L.ws_split = d.math == CP_MATH_TF32 ? al256(tc_workspace_bytes(L)) : 0; off += L.ws_split;
+  L.off_split = off; L.ws_split = d.math != CP_MATH_FP32_SIMT ? al256(tc_workspace_bytes(L)) : 0; off += L.ws_split;
+  L.off_x16 = L.off_w16 = L.off_dy16 = 0;
+  if (d.math == CP_MATH_BF16) {
+    const int64_t nx = L.images ? (int64_t)L.Ho * L.Wo * L.Bp * L.Kcol : L.in.start[L.in.n];
+    L.off_x16 = off; off += al256((size_t)nx * 2 + 256);
+    L.off_w16 = off; off += al256((size_t)L.Kr * L.Ktot * 2 + 256);
+    L.off_dy16 = off; off += al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 2 + 256);
+  }
   L.ws_total = off + 256;
   L.dy_ready = 0;
   return CP_OK;
@@ -113,6 +129,8 @@ static int ensure_dy(Layer& L, const float* dy_g, const uint8_t* saved, const fl
   const int64_t o = L.out.start[L.d.rank];
   CP_TRY(launch_unpool(L, dy_g + o, saved, y_g + o, (float*)WS(ws, L.off_dy), (float*)WS(ws, L.off_dbpart),
                        L.d.math == CP_MATH_TF32, s));
+  if (L.d.math == CP_MATH_BF16)
+    CP_TRY(launch_to_bf16((const float*)WS(ws, L.off_dy), WS(ws, L.off_dy16), (int64_t)L.Ho * L.Wo * L.Bp * L.Kc, s));
   L.dy_ready = 1;
   L.dy_key[0] = dy_g; L.dy_key[1] = saved; L.dy_key[2] = y_g;
   return CP_OK;
@@ -275,6 +293,15 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
     if (tf32) {
       CP_TRY(tc_fwd(*L, xin, w, b, yb, saved, ws, s, push_in_epilogue ? peer_blocks : nullptr,
                     push_in_epilogue ? npeers : 0, arrive, kernel_push ? &gp : nullptr));
+    } else if (L->d.math == CP_MATH_BF16) {
+      // report-only bf16 mode: the GEMM reads bf16 copies of its input and weights (fp32 outputs);
+      // the gathered input is complete here (copy-engine distribution + flags above)
+      const int64_t nx = L->images ? (int64_t)L->Ho * L->Wo * L->Bp * L->Kcol : L->in.start[L->in.n];
+      float* x16 = (float*)WS(ws, L->off_x16);
+      float* w16 = (float*)WS(ws, L->off_w16);
+      CP_TRY(launch_to_bf16(xin, x16, nx, s));
+      CP_TRY(launch_to_bf16(w, w16, (int64_t)L->Kr * L->Ktot, s));
+      CP_TRY(tc_fwd(*L, x16, w16, b, yb, saved, ws, s, nullptr, 0, nullptr, nullptr));
     } else {
       float* z = (float*)WS(ws, L->off_z);
       CP_TRY(launch_fwd_simt(*L, x, xin, w, b, z, s));
@@ -309,7 +336,15 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
   // gather layout; the dgrad epilogue stores block q's partial into rank q's slot [this rank].
   void* peers[CP_MAX_RANKS];
   uint32_t* pflags[CP_MAX_RANKS];
-  const bool fused = L->d.math == CP_MATH_TF32 && !L->images && L->comm && L->d.world > 1 &&
+  // GEMM operands: fp32 (tf32 mode) or the bf16 copies (bf16 mode; weights re-rounded here)
+  const bool bf16 = L->d.math == CP_MATH_BF16;
+  const float* dYg = bf16 ? (const float*)WS(ws, L->off_dy16) : dY;
+  const float* wg = w;
+  if (bf16) {
+    CP_TRY(launch_to_bf16(w, WS(ws, L->off_w16), (int64_t)L->Kr * L->Ktot, s));
+    wg = (const float*)WS(ws, L->off_w16);
+  }
+  const bool fused = L->d.math != CP_MATH_FP32_SIMT && !L->images && L->comm && L->d.world > 1 &&
                      dx_mode == CP_DX_REDUCE_SCATTER && comm_symmetric_peers(L->comm, dx, peers, pflags);
   if (fused) {
     int64_t mb = 0;
@@ -325,7 +360,7 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
     }
     if (!ordered) CP_TRY(comm_barrier(L->comm, s));   // no rank still sums last call's slots
     if (L->Kr > 0 && L->Kc > 0) {
-      CP_TRY(tc_dgrad(*L, dY, w, dx, ws, s, dst));
+      CP_TRY(tc_dgrad(*L, dYg, wg, dx, ws, s, dst));
     } else {   // no own kernels: a zero partial for every block (peers still expect the signal)
       for (int q = 0; q < L->in.n; ++q) CP_TRY(launch_fill(dst[q], 0.f, L->in.start[q + 1] - L->in.start[q], s));
     }
@@ -342,8 +377,8 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
     }
     return CP_OK;
   }
-  if (L->d.math == CP_MATH_TF32 && !L->images) {
-    CP_TRY(tc_dgrad(*L, dY, w, dx, ws, s));
+  if (L->d.math != CP_MATH_FP32_SIMT && !L->images) {
+    CP_TRY(tc_dgrad(*L, dYg, wg, dx, ws, s));
   } else {
     CP_TRY(launch_dgrad_simt(*L, dY, w, dx, s));
   }
@@ -379,6 +414,8 @@ int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* save
   const float* xcol = L->images ? (const float*)WS(ws, L->off_xcol) : nullptr;
   if (L->d.math == CP_MATH_TF32) {
     CP_TRY(tc_wgrad(*L, dY, L->images ? xcol : x, dw, ws, s));
+  } else if (L->d.math == CP_MATH_BF16) {   // bf16 copies of dY (ensure_dy) and of the input (forward)
+    CP_TRY(tc_wgrad(*L, (const float*)WS(ws, L->off_dy16), (const float*)WS(ws, L->off_x16), dw, ws, s));
   } else {
     CP_TRY(launch_wgrad_simt(*L, dY, x, xcol, dw, s));
   }

@@ -162,6 +162,29 @@ __device__ __forceinline__ void mma_tf32_cg2(uint32_t d_tmem, uint64_t adesc, ui
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// the same for kind::f16 with bf16 operands (f4, report-only BF16 mode)
+__device__ __forceinline__ void mma_bf16_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // commit the leader's MMAs to the same mbarrier offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
   asm volatile(
@@ -240,6 +263,17 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t tile_addr, int kstep) {
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// kind::f16 with bf16 A/B (format 1), fp32 accumulator
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// MN-major 16-bit operand, SWIZZLE_128B: 64-element (128 B) MN groups of rows_k K-rows each
+// (LBO = rows_k * 128 B between MN groups), 8-row swizzle atoms (SBO = 1 KB); a K=16 MMA step is
+// two atoms (+2 KB).
+__device__ __forceinline__ uint64_t sdesc_mn16(uint32_t tile_addr, int kstep, int rows_k) {
+  return sdesc(tile_addr + kstep * 2048, rows_k * 128, 1024, kLayoutSW128);
 }
 
 }  // namespace tc

@@ -23,12 +23,13 @@ ap.add_argument("--math", default="tf32")
 a = ap.parse_args()
 
 B, P = a.B, a.P
-p1 = cp.cp_partition_plan([1.0] * P, a.K1, a.align)
-p2 = cp.cp_partition_plan([1.0] * P, a.K2, a.align)
+align = 64 if a.math == "bf16" else a.align
+p1 = cp.cp_partition_plan([1.0] * P, a.K1, align)
+p2 = cp.cp_partition_plan([1.0] * P, a.K2, align)
 d = cp.cp_conv_desc()
 d.batch, d.in_c, d.in_h, d.in_w, d.num_k, d.k_h, d.k_w = B, a.K1, 14, 14, a.K2, 5, 5
 d.bias, d.relu, d.pool = 1, 1, a.pool
-d.math = cp.CP_MATH_TF32 if a.math == "tf32" else cp.CP_MATH_FP32_SIMT
+d.math = {"tf32": cp.CP_MATH_TF32, "simt": cp.CP_MATH_FP32_SIMT, "bf16": cp.CP_MATH_BF16}[a.math]
 d.input_kind = cp.CP_INPUT_GATHER
 d.in_part, d.out_part, d.rank, d.world = p1, p2, 0, P
 h = cp.conv_part_create(d, None)

@@ -7,7 +7,8 @@ import torch
 
 from paper_1712_02546_b200 import convpart as cp
 
-TOL = {cp.CP_MATH_FP32_SIMT: 1e-5, cp.CP_MATH_TF32: 2e-3}   # north_star tolerances (max-abs / max|ref|)
+TOL = {cp.CP_MATH_FP32_SIMT: 1e-5, cp.CP_MATH_TF32: 2e-3,   # north_star tolerances (max-abs / max|ref|)
+       cp.CP_MATH_BF16: 1.5e-2}   # f4 report-only bf16 operands: 8-bit mantissas, K up to 12,800 (App. B)
 
 
 def rel_err(gpu, ref):

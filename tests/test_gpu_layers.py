@@ -287,3 +287,47 @@ def test_full_step_lrn_p1(orc, math):
         floor = 2.0 * 2.0 ** -23 * np.abs(params[k]).max() / max(np.abs(ref).max(), 1e-30)
         assert_close(new[k] - params[k], ref, max(TOL[m], 1e-4) + floor, f"LRN update of {k} ({math})")
     pn.close()
+
+
+# ------------------------------------------------------------------ BF16 operands (NEXT row f4, report-only)
+@pytest.mark.parametrize("P,B", [(1, 40), (2, 40), (3, 40), (2, 128)])
+def test_bf16_passes(orc, P, B):
+    """CP_MATH_BF16: every pass with bf16 operand copies (kind::f16, fp32 accumulate) vs the fp64
+    oracle at the report-only bound; partitions aligned to 64-slot widths."""
+    m = cp.CP_MATH_BF16
+    x, w1, b1, w2, b2 = layer_data(B=B)
+    B, K1, K2 = x.shape[0], w1.shape[0], w2.shape[0]
+    p1, p2 = parts_for(P, K1, 64), parts_for(P, K2, 64)
+    L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
+    L1.load(w1, b1)
+    xd = dev(x)
+    L1.forward(xd)
+    a1, _ = orc.relu_pool_fwd(orc.conv_fwd(x.astype(np.float64), w1.astype(np.float64), b1.astype(np.float64)))
+    y1 = L1.y_nchw()
+    assert_close(y1, a1, TOL[m], f"bf16 conv1 fwd (P={P})")
+    L2 = LocalLayer(B, K1, 8, K2, 5, p2, p1, m)
+    L2.load(w2, b2)
+    L2.forward(L1.y)
+    a2, _ = orc.relu_pool_fwd(orc.conv_fwd(y1, w2.astype(np.float64), b2.astype(np.float64)))
+    y2 = L2.y_nchw()
+    assert_close(y2, a2, TOL[m], f"bf16 conv2 fwd (P={P})")
+    da2 = synth.normal(y2.shape, 99, 1.0).astype(np.float32)
+    dxs, dw2, db2 = L2.backward(pack(da2, p2), L1.y)
+    dy2 = orc.unpool_relu_bwd(da2.astype(np.float64), L2.argmax_nchw(), y2)
+    assert_close(unpack(dxs, B, K1, 8, p1), orc.conv_dgrad(dy2, w2.astype(np.float64)), TOL[m], f"bf16 dgrad (P={P})")
+    assert_close(dw2, orc.conv_wgrad(dy2, y1, 5, 5), TOL[m], f"bf16 wgrad (P={P})")
+    da1 = unpack(dxs, B, K1, 8, p1).astype(np.float32)
+    _, dw1, _ = L1.backward(pack(da1, p1), xd)
+    dy1 = orc.unpool_relu_bwd(da1.astype(np.float64), L1.argmax_nchw(), y1)
+    assert_close(dw1, orc.conv_wgrad(dy1, x.astype(np.float64), 5, 5), TOL[m], f"bf16 conv1 wgrad (P={P})")
+    L1.close(); L2.close()
+
+
+def test_bf16_rejects_unaligned_partition():
+    part = parts_for(1, 300, 8)    # width 304: not a multiple of 64
+    d = cp.cp_conv_desc()
+    d.batch, d.in_c, d.in_h, d.in_w, d.num_k, d.k_h, d.k_w = 40, 3, 20, 20, 300, 5, 5
+    d.bias, d.relu, d.pool, d.math, d.input_kind = 1, 1, 1, cp.CP_MATH_BF16, cp.CP_INPUT_IMAGES
+    d.out_part, d.rank, d.world = part, 0, 1
+    with pytest.raises(cp.ConvPartError):
+        cp.conv_part_create(d, None)
