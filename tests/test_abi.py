@@ -46,6 +46,16 @@ def test_planner_bitexact_vs_oracle(cpm, orc):
         kb, kc, kw = orc.plan(t, k)
         assert p.as_tuple() == (kb.tolist(), kc.tolist(), kw.tolist())
     np.testing.assert_allclose(cpm.cp_eq1_weights([10, 20, 40]), [4 / 7, 2 / 7, 1 / 7], rtol=1e-15)
+    # the alignments the product uses: 32 (spanning N tiles) and 64 (bf16 operand mode, 64-element chunks)
+    for align in (32, 64):
+        for _ in range(100):
+            n = int(g.integers(1, 9))
+            t = g.uniform(0.2, 7.0, n)
+            k = int(g.integers(0, 4000))
+            p = cpm.cp_partition_plan(list(t), k, align)
+            kb, kc, kw = orc.plan(t, k, align)
+            assert p.as_tuple() == (kb.tolist(), kc.tolist(), kw.tolist())
+            assert all(w % align == 0 and w >= c for w, c in zip(kw, kc))
 
 
 def test_planner_errors(cpm):
