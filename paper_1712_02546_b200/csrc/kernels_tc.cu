@@ -89,6 +89,7 @@ struct TcParams {
   short sched_off[MAX_GROUPS + 1];
   short sched[MAX_SCHED];
   int bke;             // operand elements per K-chunk (one 128-byte row): 32 tf32, 64 bf16
+  int l2hint;          // dgrad: L2 evict_last on the weights, evict_first on dY (CP_TC_L2HINT)
   int pix;             // dgrad pixel mode: a CTA's 128 rows = 128 images of ONE input pixel, a pair = two
                        // horizontally adjacent pixels (exact valid rows, s-union only at borders)
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       int stage = 0;
       uint32_t phase = 0;
       uint32_t arrived = PASS == PASS_FWD && p.arrive ? 1u << p.self_blk : ~0u;  // input blocks known present
+      const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
       for (int k = 0;; ++k) {
         const int u = unit_at(p, group, ngroups, k);
         if (u < 0) break;
@@ -460,6 +462,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             if (CG == 2) tma_load_4d_cg2(d, m, lbar, c0, c1, c2, c3);
             else tma_load_4d(d, m, &full[stage], c0, c1, c2, c3);
           };
+          auto ld4h = [&](void* d, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t pol) {
+            if (CG == 2) tma_load_4d_cg2_hint(d, m, lbar, c0, c1, c2, c3, pol);
+            else tma_load_4d_hint(d, m, &full[stage], c0, c1, c2, c3, pol);
+          };
           auto ld5 = [&](void* d, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4) {
             if (CG == 2) tma_load_5d_cg2(d, m, lbar, c0, c1, c2, c3, c4);
             else tma_load_5d(d, m, &full[stage], c0, c1, c2, c3, c4);
@@ -478,12 +484,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.r, s = ch.s;
-            if (p.pix)
+            if (p.l2hint && p.pix)
+              ld4h(a, &p.maps[0], ch.c * BKE, t.bc * 128, 2 * t.j + (int)rank - s, t.i - r, pol_stream);
+            else if (p.pix)
               ld4(a, &p.maps[0], ch.c * BKE, t.bc * 128, 2 * t.j + (int)rank - s, t.i - r);
             else
               ld4(a, &p.maps[0], ch.c * BKE, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
             if (p.wide) {
-              ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BKE, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> ASH, ch.tap);
+              if (p.l2hint)
+                ld4h(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BKE, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> ASH, ch.tap, pol_keep);
+              else
+                ld4(b, &p.maps[CP_MAX_RANKS], 0, ch.c * BKE, ((p.span ? 0 : p.coff[t.rb]) + nb0) >> ASH, ch.tap);
             } else {
               for (int q = 0; q < nboxes; ++q)
                 ld3(b + q * 4096, &p.maps[CP_MAX_RANKS], p.coff[t.rb] + nb0 + 32 * q, ch.c * BKE, ch.tap);
@@ -1122,6 +1133,7 @@ void fill_blocks(TcParams& p, const Layer& L) {
 void fill_common(TcParams& p, const Layer& L) {
   fill_blocks(p, L);
   p.bke = op_elems(L);
+  p.l2hint = env_int("CP_TC_L2HINT", 0);
   p.epi_groups = env_int("CP_TC_EPI_GROUPS", 0);  // 0: decided per launch from the K-loop length
   p.R = L.images ? 1 : L.R;
   p.S = L.images ? 1 : L.S;

@@ -1,4 +1,4 @@
-# conv2 passes at P = 1, 2, 4, 8; wgrad tail piece cap (development aid)
+# dgrad L2 policy hints A/B (development aid)
 cd $GRAFT_REPO_ROOT
-for P in 1 2 4 8; do timeout 60 python scripts/pass_bench.py --reps 10 --P $P 2>&1 | tail -1; done
-for m in 8 32 148; do CP_TC_TAIL_MAX=$m timeout 60 python scripts/pass_bench.py --reps 10 --P 4 2>&1 | tail -1; done
+for rep in 1 2; do for h in 0 1; do for P in 1; do echo -n "hint=$h "; CP_TC_L2HINT=$h timeout 60 python scripts/pass_bench.py --reps 10 --P $P 2>&1 | tail -1; done; done; done
+for P in 2 4; do for h in 0 1; do echo -n "hint=$h "; CP_TC_L2HINT=$h timeout 60 python scripts/pass_bench.py --reps 10 --P $P 2>&1 | tail -1; done; done
