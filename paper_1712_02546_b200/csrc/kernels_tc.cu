@@ -42,6 +42,7 @@ constexpr int MAX_NT = 64;
 constexpr int MAX_WIN = 512;                  // dgrad LPT window table (larger grids: natural order)
 constexpr int MAX_GROUPS = 148;               // CTA groups (one per SM or SM pair)
 constexpr int MAX_SCHED = 1024;               // units in an explicit per-group schedule
+constexpr int MAX_PIECES = 2 * MAX_GROUPS + 8;  // stream-tail pieces (<= one or two per CTA group)
 
 // CG = CTAs per MMA (cta_group::1 or ::2).  With a CTA pair the MMA is M=256 (128 rows per CTA)
 // and each CTA stages only half of B (N/2 columns), so per-SM operand traffic drops by 1/3 and
@@ -83,7 +84,8 @@ struct TcParams {
   int cpt;             // fwd: K-chunks per tap (sum over input blocks)
   long long part_stride;  // split-K: floats between split partial buffers (fwd/dgrad)
   int nt_rb[MAX_NT], nt_n0[MAX_NT], nt_n[MAX_NT];  // dgrad / wgrad N-tile list (per tap for wgrad)
-  int tail_full, tail_st, tail_per;  // wgrad tail split: units >= tail_full are (tail unit, K piece)
+  int tail_full, tail_np;  // stream tail: units >= tail_full are pieces (tail unit, K-chunk range)
+  short tail_tu[MAX_PIECES], tail_lo[MAX_PIECES], tail_hi[MAX_PIECES];
   float* tail_buf;     // wgrad tail partials [tail unit][piece][CTA of pair][128 rows][256 cols]
   int nsched;          // >0: per-group unit lists (host LPT schedule); 0: static round-robin
   short sched_off[MAX_GROUPS + 1];
@@ -129,12 +131,12 @@ template <int PASS, int CG>
 __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) {
   Unit t{};
   int mg;
-  if ((PASS == PASS_WGRAD || PASS == PASS_FWD) && p.tail_st > 0 && u >= p.tail_full) {
-    // the last (partial) round of equal tiles is split along K over every CTA group
+  if ((PASS == PASS_WGRAD || PASS == PASS_FWD) && p.tail_np > 0 && u >= p.tail_full) {
+    // the last (partial) round of equal tiles, its K-chunks shared evenly by every CTA group
     const int v = u - p.tail_full;
     t.tail = 1;
-    t.tu = v / p.tail_st;
-    t.piece = v - t.tu * p.tail_st;
+    t.tu = p.tail_tu[v];
+    t.piece = v;
     u = p.tail_full + t.tu;
   }
   if (PASS == PASS_WGRAD) {
@@ -241,8 +243,9 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
   if (PASS == PASS_FWD) {
     const int RS = p.R * p.S;
     const int total = RS * p.cpt;
-    const int per = t.tail ? p.tail_per : (total + p.split - 1) / p.split;
-    const int lo = (t.tail ? t.piece : t.sp) * per, hi = min(total, lo + per);
+    const int per = (total + p.split - 1) / p.split;
+    const int lo = t.tail ? p.tail_lo[t.piece] : t.sp * per;
+    const int hi = t.tail ? p.tail_hi[t.piece] : min(total, lo + per);
     if (lo >= hi) return;
     // decode chunk `lo` once, then step the coordinates (this loop runs on the single producer and
     // MMA threads, one iteration per ~900 tensor cycles)
@@ -332,8 +335,8 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
       }
     }
   } else {
-    const int c0 = t.tail ? t.piece * p.tail_per : t.sp * p.chunks_per_split;
-    const int c1 = min(p.chunks_total, c0 + (t.tail ? p.tail_per : p.chunks_per_split));
+    const int c0 = t.tail ? p.tail_lo[t.piece] : t.sp * p.chunks_per_split;
+    const int c1 = t.tail ? p.tail_hi[t.piece] : min(p.chunks_total, c0 + p.chunks_per_split);
     // k-chunk c = (pq, bc): decoded once, then stepped
     const int nbc = p.Bp / BKE;
     int bc = c0 % nbc, pq = c0 / nbc;
@@ -645,7 +648,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int ncol = min(32, t.n - cc * 32);
         if ((PASS == PASS_FWD || PASS == PASS_WGRAD) && t.tail) {
           // tail piece: raw partial tile, finished by fwd_tail_finish / wgrad_tail_reduce
-          float* dst = p.tail_buf + ((((int64_t)t.tu * p.tail_st + t.piece) * CG + rank) * BM + row) * BN + cc * 32;
+          float* dst = p.tail_buf + (((int64_t)t.piece * CG + rank) * BM + row) * BN + cc * 32;
           store_f32x32(dst, v, 32);
         } else if (PASS == PASS_FWD && p.split > 1) {
           // split-K partial of the pre-pool tile: [sp][Ho][Wo][Bp][Kc]
@@ -813,7 +816,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 constexpr int MAX_TAIL = 148;
 struct TailInfo {
   int n;                      // tail units
-  int st, cg;                 // pieces per unit, CTAs per tile
+  int cg;                     // CTAs per tile
+  short pbeg[MAX_TAIL + 1];   // pieces of tail unit tu: [pbeg[tu], pbeg[tu+1]) in K order
   int Kr, Ktot;
   int kk0[MAX_TAIL];          // first kernel row of the unit's tile (CTA 0)
   int col0[MAX_TAIL];         // first dW column
@@ -824,15 +828,16 @@ __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restri
   const int c = threadIdx.x;  // 256 columns
   const int kk = ti.kk0[tu] + rank * BM + row;
   if (kk >= ti.Kr || c >= ti.ncol[tu]) return;
-  // four independent accumulators (pieces pc = k mod 4) keep several loads in flight; fixed order
-  const float* src = buf + (((int64_t)tu * ti.st * ti.cg + rank) * BM + row) * BN + c;
+  // the unit's pieces in K order (fixed order); four accumulators keep loads in flight
   const int64_t step = (int64_t)ti.cg * BM * BN;
+  const int np = ti.pbeg[tu + 1] - ti.pbeg[tu];
+  const float* src = buf + (((int64_t)ti.pbeg[tu] * ti.cg + rank) * BM + row) * BN + c;
   float a[4] = {0.f, 0.f, 0.f, 0.f};
   int pc = 0;
-  for (; pc + 4 <= ti.st; pc += 4)
+  for (; pc + 4 <= np; pc += 4)
 #pragma unroll
     for (int k = 0; k < 4; ++k) a[k] += src[(pc + k) * step];
-  for (; pc < ti.st; ++pc) a[pc & 3] += src[pc * step];
+  for (; pc < np; ++pc) a[pc & 3] += src[pc * step];
   dw[(int64_t)kk * ti.Ktot + ti.col0[tu] + c] = (a[0] + a[1]) + (a[2] + a[3]);
 }
 
@@ -840,7 +845,8 @@ __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restri
 // then bias, ReLU, 2x2 max-pool (rows q*32+b of a CTA's tile are window position q, image b),
 // argmax code and RN-tf32 rounding, exactly as the fused epilogue.
 struct FwdTailInfo {
-  int n, st, cg, Wo, Wp, Bp, B, Kr, Kc, relu, pool, npeers;
+  int n, cg, Wo, Wp, Bp, B, Kr, Kc, relu, pool, npeers;
+  short pbeg[MAX_TAIL + 1];   // pieces of tail unit tu: [pbeg[tu], pbeg[tu+1])
   float* peer[CP_MAX_RANKS];  // fused AllGather: own block inside each peer's buffer
   int i[MAX_TAIL], j[MAX_TAIL], bc0[MAX_TAIL], n0[MAX_TAIL], ncol[MAX_TAIL];
 };
@@ -855,10 +861,9 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
   const float bs = (bias && n < ti.Kr) ? bias[n] : 0.f;
   float best = 0.f;
   int code = 0;
-  const int64_t step = (int64_t)ti.cg * BM * BN;
   float zq[4] = {0.f, 0.f, 0.f, 0.f};   // the four window positions: independent load streams
-  for (int pc = 0; pc < ti.st; ++pc) {
-    const float* src = buf + (((int64_t)tu * ti.st + pc) * ti.cg + rank) * BM * BN + (int64_t)b * BN + c;
+  for (int pc = ti.pbeg[tu]; pc < ti.pbeg[tu + 1]; ++pc) {
+    const float* src = buf + ((int64_t)pc * ti.cg + rank) * BM * BN + (int64_t)b * BN + c;
 #pragma unroll
     for (int q = 0; q < 4; ++q) zq[q] += src[q * 32 * BN];
   }
@@ -1336,7 +1341,7 @@ size_t tc_workspace_bytes(const Layer& L) {
     fill_common(p, L);
     const Plan w = fwd_plan(L, p);
     if (w.S > 1) need = std::max(need, (size_t)w.S * L.Ho * L.Wo * L.Bp * L.Kc * 4);
-    need = std::max(need, (size_t)num_sms() * BM * BN * 4);   // forward tail-split partials
+    need = std::max(need, (size_t)MAX_PIECES * BM * BN * 4);   // stream-tail partials (pieces x CG x tile)
   }
   if (!L.images && L.Kr > 0) {
     TcParams p{};
@@ -1350,9 +1355,60 @@ size_t tc_workspace_bytes(const Layer& L) {
     const Plan w = wgrad_plan(L, p);
     if (w.numN > 0 && w.S > 1) need = std::max(need, (size_t)w.S * L.Kr * L.Ktot * 4);
     // tail-split partials: at most one round of CTA groups x CG tiles of 128 x 256 floats
-    if (w.numN > 0 && w.S == 1) need = std::max(need, (size_t)num_sms() * BM * BN * 4);
+    if (w.numN > 0 && w.S == 1) need = std::max(need, (size_t)MAX_PIECES * BM * BN * 4);
   }
   return need;
+}
+
+// Stream tail: the last partial round of T equal units (C K-chunks each) is shared evenly by all G
+// CTA groups - group g takes chunks [g q, (g+1) q) of the T*C tail chunks (q = ceil(T*C / G)), cut at
+// unit boundaries into one or two pieces.  Pieces are numbered in chunk order, so a unit's pieces
+// are consecutive (pbeg) and its finish kernel sums them in K order (deterministic).  Each group's
+// explicit list: its full-round units (round-robin order), then its pieces.  Applied when the last
+// round is at most 90 % full (covers a single under-filled round, e.g. 50 units on 74 groups).
+static bool plan_stream_tail(TcParams& p, int G, int chunks, int min_chunks, short* pbeg, int* T_out) {
+  if (!env_int("CP_TC_STREAM_TAIL", 1)) return false;
+  const int units = p.units;
+  if (units <= 0 || chunks < min_chunks) return false;
+  const int rounds = (units + G - 1) / G, T = units - (rounds - 1) * G, full = (rounds - 1) * G;
+  if (T <= 0 || T > MAX_TAIL || 10 * T > 9 * G || G > MAX_GROUPS) return false;
+  const long long W = (long long)T * chunks, q = (W + G - 1) / G;
+  std::vector<std::vector<int>> lists(G);
+  for (int g = 0; g < G; ++g)
+    for (int u = g; u < full; u += G) lists[g].push_back(u);
+  int np = 0;
+  for (int g = 0; g < G; ++g) {
+    long long st = (long long)g * q;
+    const long long en = std::min(W, (long long)(g + 1) * q);
+    while (st < en) {
+      const int tu = (int)(st / chunks), lo = (int)(st - (long long)tu * chunks);
+      const int hi = (int)std::min<long long>(chunks, lo + (en - st));
+      if (np >= MAX_PIECES) return false;
+      p.tail_tu[np] = (short)tu;
+      p.tail_lo[np] = (short)lo;
+      p.tail_hi[np] = (short)hi;
+      lists[g].push_back(full + np);
+      ++np;
+      st += hi - lo;
+    }
+  }
+  if (full + np > MAX_SCHED || chunks > 32767) return false;
+  for (int tu = 0, v = 0; tu <= T; ++tu) {
+    while (v < np && p.tail_tu[v] < tu) ++v;
+    pbeg[tu] = (short)v;
+  }
+  int off = 0;
+  for (int g = 0; g < G; ++g) {
+    p.sched_off[g] = (short)off;
+    for (int u : lists[g]) p.sched[off++] = (short)u;
+  }
+  p.sched_off[G] = (short)off;
+  p.nsched = 1;
+  p.tail_full = full;
+  p.tail_np = np;
+  p.units = full + np;
+  *T_out = T;
+  return true;
 }
 
 int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s) {
@@ -1423,23 +1479,15 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = (long long)L.Ho * L.Wo * L.Bp * L.Kc;
   p.out = pl.S > 1 ? part : y_block;
-  // Tail split of the last partial round of equal tiles (see tc_wgrad); the pooled epilogue of
-  // those tiles runs in fwd_tail_finish after the deterministic sum of the pieces.
+  // Stream tail of the last partial round (plan_stream_tail); the pooled epilogue of those tiles
+  // runs in fwd_tail_finish after the deterministic sum of their pieces.
   FwdTailInfo ti{};
   {
     const int CG = pl.pair ? 2 : 1, G = num_sms() / CG;
-    const int rounds = (p.units + G - 1) / G, T = p.units - (rounds - 1) * G;
-    const int chunks = p.R * p.S * p.cpt;
-    if (pl.S == 1 && rounds > 1 && T > 0 && 2 * T <= G && T <= MAX_TAIL && chunks >= 16 &&
-        env_int("CP_TC_FWD_TAIL", 1)) {
-      int st = std::max(1, std::min(G / T, chunks / 8));
-      const int per = (chunks + st - 1) / st;
-      st = (chunks + per - 1) / per;
-      p.tail_full = (rounds - 1) * G;
-      p.tail_st = st;
-      p.tail_per = per;
+    int T = 0;
+    if (pl.S == 1 && env_int("CP_TC_FWD_TAIL", 1) && plan_stream_tail(p, G, p.R * p.S * p.cpt, 16, ti.pbeg, &T)) {
       p.tail_buf = part;
-      ti.n = T; ti.st = st; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B;
+      ti.n = T; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B;
       ti.Kr = L.Kr; ti.Kc = L.Kc; ti.relu = L.d.relu; ti.pool = L.d.pool;
       ti.npeers = npeers;
       for (int k = 0; k < npeers; ++k) ti.peer[k] = peer_blocks[k];
@@ -1454,14 +1502,13 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
         ti.n0[k] = nt * p.nw;
         ti.ncol[k] = std::min(p.nw, L.Kc - ti.n0[k]);
       }
-      p.units = p.tail_full + T * st;
     }
   }
   CP_TRY(tc_time_mark(L, PASS_FWD, 0, s));
   if (es == 2) CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2, 1>(p, s) : launch_cg<PASS_FWD, 1, 1>(p, s)));
   else CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
   CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
-  if (p.tail_st > 0) {
+  if (p.tail_np > 0) {
     fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
     CP_LAUNCHED();
   }
@@ -1636,19 +1683,10 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   // along K over all CTA groups (their partials are tiny; everything else is written directly).
   TailInfo ti{};
   const int CG = w.pair ? 2 : 1, G = num_sms() / CG;
-  const int rounds = (p.units + G - 1) / G, T = p.units - (rounds - 1) * G;
-  if (w.S == 1 && rounds > 1 && T > 0 && 2 * T <= G && T <= MAX_TAIL && env_int("CP_TC_WGRAD_TAIL", 1)) {
-    // pieces per tail unit: <= 16 - a few leftover units split 74 ways cost more in partial-tile
-    // traffic and reduce latency than the shorter pieces save (measured P=4, T=2)
-    int st = std::max(1, std::min(std::min(G / T, env_int("CP_TC_TAIL_MAX", 16)), w.chunks));
-    const int per = (w.chunks + st - 1) / st;
-    st = (w.chunks + per - 1) / per;                   // every piece non-empty
-    p.tail_full = (rounds - 1) * G;
-    p.tail_st = st;
-    p.tail_per = per;
+  int T = 0;
+  if (w.S == 1 && env_int("CP_TC_WGRAD_TAIL", 1) && plan_stream_tail(p, G, w.chunks, 8, ti.pbeg, &T)) {
     p.tail_buf = (float*)((char*)ws + L.off_split);
     ti.n = T;
-    ti.st = st;
     ti.cg = CG;
     ti.Kr = L.Kr;
     ti.Ktot = L.Ktot;
@@ -1661,13 +1699,12 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
       ti.col0[k] = tap * p.Cg + (p.span ? 0 : p.coff[p.nt_rb[e]]) + p.nt_n0[e];
       ti.ncol[k] = p.nt_n[e];
     }
-    p.units = p.tail_full + T * st;
   }
   CP_TRY(tc_time_mark(L, PASS_WGRAD, 0, s));
   if (es == 2) CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2, 1>(p, s) : launch_cg<PASS_WGRAD, 1, 1>(p, s)));
   else CP_TRY((w.pair ? launch_cg<PASS_WGRAD, 2>(p, s) : launch_cg<PASS_WGRAD, 1>(p, s)));
   CP_TRY(tc_time_mark(L, PASS_WGRAD, 1, s));
-  if (p.tail_st > 0) {
+  if (p.tail_np > 0) {
     wgrad_tail_reduce<<<dim3(BM, CG, ti.n), BN, 0, s>>>(p.tail_buf, dw, ti);
     CP_LAUNCHED();
   }
