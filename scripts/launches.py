@@ -1,13 +1,41 @@
-"""Summarise an ncu --csv launch list (gpu__time_duration.sum per launch) by kernel."""
-import csv, sys
+"""Summarise an ncu --csv launch list (gpu__time_duration.sum per launch).
+
+Prints (1) one step's launches -- the window between the last two conv1 im2col launches (each
+training step starts with exactly one) -- grouped by kernel with its share of that step, then
+(2) the full per-launch list.  ncu serialises launches and runs them cold, so the shares, not the
+absolute times, are what compare with the live bench timing.
+"""
+import csv
+import sys
+from collections import OrderedDict
+
 rows = list(csv.reader(open(sys.argv[1])))
-hdr = None; out = []
+hdr = None
+out = []
 for r in rows:
-    if 'Kernel Name' in r: hdr = r; continue
+    if 'Kernel Name' in r:
+        hdr = r
+        continue
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
         if d.get('Metric Name') == 'gpu__time_duration.sum':
             out.append((d['Kernel Name'][:70], float(d['Metric Value'].replace(',', ''))))
+
+starts = [i for i, (n, _) in enumerate(out) if 'im2col_kernel' in n]
+if len(starts) >= 2:
+    a, b = starts[-2], starts[-1]
+    step = out[a:b]
+    tot = sum(v for _, v in step)
+    agg = OrderedDict()
+    for n, v in step:
+        c, t = agg.get(n, (0, 0.0))
+        agg[n] = (c + 1, t + v)
+    print(f"one step (launches {a}..{b - 1}): {len(step)} launches, {tot / 1e3:.1f} us serialised")
+    for n, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"  {t / 1e3:9.1f} us {100 * t / tot:5.1f}%  x{c:<3d} {n}")
+    print()
+
 tot = sum(v for _, v in out)
-print(f"{len(out)} launches, total {tot/1e3:.1f} us")
-for n, v in out: print(f"{v/1e3:9.1f} us {100*v/tot:5.1f}%  {n}")
+print(f"all: {len(out)} launches, total {tot / 1e3:.1f} us")
+for n, v in out:
+    print(f"{v / 1e3:9.1f} us {100 * v / tot:5.1f}%  {n}")
