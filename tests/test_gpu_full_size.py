@@ -1,0 +1,34 @@
+"""Sampled parity at BASELINE.json's full size on 1 GPU (configs[1]: paper net 500:1500, batch 128),
+in the launch configuration bench.py times at N=1 (-m gpu).  See tests/full_size.py."""
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def test_paper_net_full_size_sampled(orc):
+    from full_size import check_step, paper_setup
+    dev = torch.device("cuda", 0)
+    net, parts, pn, params, x, y = paper_setup(1, 0, None, dev, head="partitioned", fused=True)
+    try:
+        fails = check_step(pn, net, parts, params, x, y, 0, 1, lambda o: [o])
+    finally:
+        pn.close()
+    assert not fails, "\n".join(fails)
+
+
+def test_full_size_check_is_not_vacuous(orc):
+    """Negative control: the same sampled check against an oracle given conv2 weights 0.5 % off
+    (2.5x the TF32 tolerance) must flag the passes that read them, and only those."""
+    from full_size import check_step, paper_setup
+    dev = torch.device("cuda", 0)
+    net, parts, pn, params, x, y = paper_setup(1, 0, None, dev)
+    bad = dict(params)
+    bad["w1"] = params["w1"] * 1.005
+    try:
+        fails = check_step(pn, net, parts, bad, x, y, 0, 1, lambda o: [o])
+    finally:
+        pn.close()
+    text = "\n".join(fails)
+    assert "conv2 forward" in text and "conv2 dgrad" in text, text
+    assert "wgrad" not in text and "conv1 forward" not in text, text
