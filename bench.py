@@ -476,6 +476,16 @@ def main():
         (c1, _, k1, o1, _), (c2, _, k2, o2, _) = net.shapes()
         per_img = 2.0 * (2 * k1 * c1 * 25 * o1 * o1 + 3 * k2 * c2 * 25 * o2 * o2)
         step_flop = per_img * B
+        # burst peak for a timed window of tens of ms; the sustained figure (MEASURED_PEAKS' 4 s
+        # back-to-back run) once the timed steps themselves last a second or more (scaled net)
+        window_s = args.steps * ms_per_step / 1e3
+        if window_s >= 1.0:
+            peak = pk["tf32_sustained"]
+            peak_note = (f" (sustained: the timed window is {window_s:.1f} s; burst = {pk['tf32_burst']:.0f})")
+        else:
+            peak = pk["tf32_burst"]
+            peak_note = (f" (burst: the timed window is {window_s * 1e3:.0f} ms, not the 4 s back-to-back run "
+                         f"behind the sustained figure; sustained = {pk['tf32_sustained']:.0f})")
         line = {
             "metric": METRIC,
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -497,20 +507,18 @@ def main():
                                if world > 1 else "none (N=1)",
                 "parallelism": f"kernel-split x{world}",
                 "l2": "flushed between timed steps (256 MiB write outside the step events)" if flush is not None
-                      else "not flushed (step working set ~700 MB > 126 MB L2)"},
+                      else "not flushed (step working set > 126 MB L2)"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "kernel": f"conv2 {dom} (tcgen05 kind::tf32 implicit GEMM)",
-                         "achieved": achieved, "peak": pk["tf32_burst"], "unit": "TFLOP/s",
-                         "frac": achieved / pk["tf32_burst"], "traffic": ncu_traffic(dom) if world == 1 else None,
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(dom) if world == 1 else None,
                          "traffic_source": "profiles/r01_ncu_conv_tc.json (ncu --set full, same kernel, P=1)",
                          "flop_per_launch": flop_pass, "launch_ms": live_ms[dom],
                          "launch_ms_source": "CUDA events around the GEMM launch inside the timed graph "
                                              "replays (conv_part_timing), mean over the timed steps, max over ranks",
                          "kernel_ms_live": live_ms,
-                         "peak_source": pk["source"] + " (burst: the timed window is ~tens of ms, not the 4 s "
-                                        "back-to-back run behind the sustained figure; sustained = "
-                                        f"{pk['tf32_sustained']:.0f})",
+                         "peak_source": pk["source"] + peak_note,
                          "conv2_pass_ms_alone": per, "conv2_pass_tflops_alone": conv2_tflops},
             "tc_frac_whole_step": step_flop / (ms_per_step / 1e3) / 1e12 / pk["tf32_sustained"],
             "clocks": clk, "loss": loss,

@@ -95,6 +95,7 @@ struct TcParams {
   int pix;             // dgrad pixel mode: a CTA's 128 rows = 128 images of ONE input pixel, a pair = two
                        // horizontally adjacent pixels (exact valid rows, s-union only at borders)
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
+  int wg_taps_slow;    // wgrad unit order: 0 = N (tap, slot tile) fastest; 1 = slot tile, kernel tile, tap
   short win_order[MAX_WIN];
   const float* bias;
   float* out;          // fwd: y block ; dgrad: dx (full gather) ; wgrad: dW or split partials
@@ -139,7 +140,17 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     t.piece = v;
     u = p.tail_full + t.tu;
   }
-  if (PASS == PASS_WGRAD) {
+  if (PASS == PASS_WGRAD && p.wg_taps_slow) {
+    // taps slowest: a wave covers every kernel tile x a few adjacent taps, so the activation rows
+    // it reads span one tap row (large maps: R rows of activations exceed L2, see wgrad_plan)
+    const int per_tap = p.numN / (p.R * p.S);
+    const int e = u % per_tap;
+    const int rest = u / per_tap;
+    mg = rest % p.numM;
+    const int rest2 = rest / p.numM;
+    t.nt = (rest2 % (p.R * p.S)) * per_tap + e;
+    t.sp = rest2 / (p.R * p.S);
+  } else if (PASS == PASS_WGRAD) {
     // N fastest: a wave covers few kernel tiles x many (tap, slot) tiles, so it streams one
     // kernel slice of dY and the (shared, shifted) activations once per position
     t.nt = u % p.numN;
@@ -1109,12 +1120,8 @@ int launch_cg(const TcParams& p, cudaStream_t s) {
 
 // 2-CTA pairs unless disabled (CP_TC_CTA_GROUP=1) or the pass cannot pair its M tiles.
 bool use_pairs() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CP_TC_CTA_GROUP");
-    v = (e && atoi(e) == 1) ? 0 : 1;
-  }
-  return v == 1;
+  const char* e = getenv("CP_TC_CTA_GROUP");   // read per plan (tests switch it between layers)
+  return !(e && atoi(e) == 1);
 }
 
 void fill_blocks(TcParams& p, const Layer& L) {
@@ -1322,7 +1329,25 @@ static Plan wgrad_plan(const Layer& L, TcParams& p) {
       if (t_tail < t_split) w.S = 1;
     }
   }
+  // Accuracy cap on the reduction length per TMEM accumulator.  The wgrad K (= B*Ho*Wo) grows with
+  // batch and image size, and the tensor core's fp32 accumulation error grows linearly with the
+  // number of MMAs accumulated (measured, scripts/wgrad_longk.py: scaled net conv2, 2.9 M terms ->
+  // 6.0e-3 of max|dW|, 4x shorter -> 1.7e-3, 44x -> 1.6e-4).  At most kAccTerms terms per split
+  // keep it near 2.5e-4 (north_star's TF32 bound is 2e-3); splits are summed in fp32 in order.
+  {
+    const int acc_terms = env_int("CP_TC_ACC_TERMS", 1 << 17);
+    const int max_chunks = std::max(1, acc_terms / op_elems(L));
+    w.S = std::max(w.S, (w.chunks + max_chunks - 1) / max_chunks);
+  }
   w.S = std::max(1, std::min(w.S, w.chunks));
+  // Unit order.  N fastest lets a wave share one kernel tile's dY slice, but it reads the
+  // activations of all R tap rows at once; once those rows outgrow L2 (scaled net: 5 rows x 110 x
+  // 256 images x 512 slots = 288 MB) every tap row is re-read from HBM (ncu: 0.9 TB per launch),
+  // so large maps walk the taps slowest instead.
+  {
+    const double rows_bytes = (double)p.R * L.W * L.Bp * (p.images ? 0 : p.Cg) * op_bytes(L);
+    p.wg_taps_slow = env_int("CP_TC_WGRAD_ORDER", rows_bytes > 48e6 ? 1 : 0);
+  }
   w.per = (w.chunks + w.S - 1) / w.S;
   w.S = (w.chunks + w.per - 1) / w.per;
   // atoms per B box: every block holds whole boxes

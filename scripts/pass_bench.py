@@ -20,6 +20,7 @@ ap.add_argument("--K1", type=int, default=500)
 ap.add_argument("--K2", type=int, default=1500)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--math", default="tf32")
+ap.add_argument("--H", type=int, default=14, help="input height/width (scaled net conv2: 110)")
 a = ap.parse_args()
 
 B, P = a.B, a.P
@@ -27,7 +28,7 @@ align = 64 if a.math == "bf16" else a.align
 p1 = cp.cp_partition_plan([1.0] * P, a.K1, align)
 p2 = cp.cp_partition_plan([1.0] * P, a.K2, align)
 d = cp.cp_conv_desc()
-d.batch, d.in_c, d.in_h, d.in_w, d.num_k, d.k_h, d.k_w = B, a.K1, 14, 14, a.K2, 5, 5
+d.batch, d.in_c, d.in_h, d.in_w, d.num_k, d.k_h, d.k_w = B, a.K1, a.H, a.H, a.K2, 5, 5
 d.bias, d.relu, d.pool = 1, 1, a.pool
 d.math = {"tf32": cp.CP_MATH_TF32, "simt": cp.CP_MATH_FP32_SIMT, "bf16": cp.CP_MATH_BF16}[a.math]
 d.input_kind = cp.CP_INPUT_GATHER
@@ -64,7 +65,7 @@ for r in range(a.reps + 2):
         t["wgrad"].append(e[1].elapsed_time(e[2]))
         t["dgrad"].append(e[2].elapsed_time(e[3]))
 Kr = p2.k_count[0]
-flop = 2.0 * B * Kr * a.K1 * 25 * 100
+flop = 2.0 * B * Kr * a.K1 * 25 * (a.H - 4) ** 2
 med = {k: sorted(v)[len(v) // 2] for k, v in t.items()}
 print(json.dumps({"variant": vars(a), "cta_group": os.environ.get("CP_TC_CTA_GROUP", "2"),
                   "ms": med, "tflops": {k: flop / (v / 1e3) / 1e12 for k, v in med.items()}}))

@@ -7,7 +7,8 @@ Checks (north_star invariants):
   * summed partial dX (ReduceScatter / AllReduce) equals the oracle's unsplit dgrad;
   * each rank's dW / db slice equals the oracle's rows (decision replay);
   * the replicated head (loss, FC update) is bitwise identical on all ranks;
-  * the paper net at full size (BASELINE configs[2]) on sampled outputs of every pass.
+  * the paper net (BASELINE configs[2]) and the scaled net (configs[4]) at full size, sampled
+    outputs of every pass.
 """
 import os
 import sys
@@ -234,20 +235,22 @@ def main():
     if not np.all(np.abs(a - b) <= 2e-3 * np.abs(a)):
         failures.append(f"fused vs NCCL collectives over 8 steps: losses {b.tolist()} vs {a.tolist()}")
 
-    # BASELINE configs[2] at full size in bench.py's launch configuration (paper net 500:1500, batch
-    # 128, even partition, fused collectives), sampled parity per pass (tests/full_size.py)
-    from full_size import check_step, paper_setup
+    # BASELINE configs[2] / configs[4] at full size in bench.py's launch configuration (even partition,
+    # fused collectives), sampled parity per pass (tests/full_size.py)
+    from full_size import bench_setup, check_step
 
     def allgather(o):
         out = [None] * world
         dist.all_gather_object(out, o)
         return out
 
-    for head in ("partitioned", "replicated"):
-        net, parts, pn, params, x, y = paper_setup(world, rank, comm, dev, head=head, fused=True)
-        failures += [f"paper net, {head} head: {m}" for m in check_step(pn, net, parts, params, x, y, rank, world,
-                                                                        allgather)]
+    for name, head, net, B in [("paper net", "partitioned", None, 128), ("paper net", "replicated", None, 128),
+                               ("scaled net (configs[4])", "partitioned", synth.scaled_net(), 256)]:
+        net, parts, pn, params, x, y = bench_setup(world, rank, comm, dev, net=net, B=B, head=head)
+        failures += [f"{name}, {head} head: {m}" for m in check_step(pn, net, parts, params, x, y, rank, world,
+                                                                     allgather, n=256)]
         pn.close()
+        torch.cuda.empty_cache()
     cp.cp_comm_destroy(comm)
     allf = [None] * world
     dist.all_gather_object(allf, failures)

@@ -331,3 +331,19 @@ def test_bf16_rejects_unaligned_partition():
     d.out_part, d.rank, d.world = part, 0, 1
     with pytest.raises(cp.ConvPartError):
         cp.conv_part_create(d, None)
+
+
+# Planner variants the default sizes do not reach (the environment overrides are read per call):
+# wgrad tap-slowest unit order (large maps), the wgrad accumulation-length cap forcing split-K (long
+# reductions), forward / dgrad split-K, single-CTA tiles.
+VARIANTS = [{"CP_TC_WGRAD_ORDER": "1"}, {"CP_TC_ACC_TERMS": "1024"}, {"CP_TC_SPLIT_FWD": "3"},
+            {"CP_TC_SPLIT_DGRAD": "2"}, {"CP_TC_CTA_GROUP": "1"}]
+
+
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("P,B,align", [(1, 128, 8), (2, 40, 32), (3, 40, 8)])
+def test_planner_variants(orc, monkeypatch, env, P, B, align):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    test_forward_parity(orc, "tf32", P, B, align)
+    test_backward_parity(orc, "tf32", P, B, align)
