@@ -1718,8 +1718,17 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
     const int per_tap = p.numN / (p.R * p.S);
     for (int k = 0; k < T; ++k) {                      // host mirror of decode_unit<WGRAD>
       const int u = p.tail_full + k;
-      const int nt = u % p.numN, mg = (u / p.numN) % p.numM;
-      const int tap = nt / per_tap, e = nt % per_tap;
+      int tap, e, mg;
+      if (p.wg_taps_slow) {
+        e = u % per_tap;
+        mg = (u / per_tap) % p.numM;
+        tap = (u / per_tap / p.numM) % (p.R * p.S);
+      } else {
+        const int nt = u % p.numN;
+        mg = (u / p.numN) % p.numM;
+        tap = nt / per_tap;
+        e = nt % per_tap;
+      }
       ti.kk0[k] = mg * CG * BM;
       ti.col0[k] = tap * p.Cg + (p.span ? 0 : p.coff[p.nt_rb[e]]) + p.nt_n0[e];
       ti.ncol[k] = p.nt_n[e];

@@ -2,6 +2,7 @@
 (PartitionedNet with bench.py's params, images, partition and flags, so the planner takes the same
 decisions: CTA pairs, pixel-mode dgrad, stream tails, fused collectives at N>1):
   * configs[1]/[2]: the paper net 500:1500 on 32x32x3, batch 128, 1 GPU / N ranks;
+  * configs[3] at its largest batch: the paper net, batch 1024, uneven (Eq. 1) partition, N ranks;
   * configs[4]: the scaled variant 512:2048 on 224x224x3, batch 256, N ranks.
 
 The oracle cannot redo such a step element by element in seconds, so every pass is checked on
@@ -24,10 +25,11 @@ from gpu_util import TOL, rel_err
 from paper_1712_02546_b200 import convpart as cp
 
 
-def bench_setup(world, rank, comm, dev, net=None, B=128, head="partitioned", fused=True):
-    """bench.py's N-GPU workload: even partition, params seed 42, images step 0."""
+def bench_setup(world, rank, comm, dev, net=None, B=128, head="partitioned", fused=True, times=None):
+    """bench.py's N-GPU workload: even partition (or Eq. 1 from per-rank `times`, as
+    `bench.py --partition probe`), params seed 42, images step 0."""
     net = net or synth.paper_net("500:1500")
-    parts = [cp.cp_partition_plan([1.0] * world, K, 8) for K in net.kernels]
+    parts = [cp.cp_partition_plan(times or [1.0] * world, K, 8) for K in net.kernels]
     from paper_1712_02546_b200.net import PartitionedNet
     pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=cp.CP_MATH_TF32, device=dev, head=head,
                         in_hw=net.in_hw, fused=fused)

@@ -7,8 +7,8 @@ Checks (north_star invariants):
   * summed partial dX (ReduceScatter / AllReduce) equals the oracle's unsplit dgrad;
   * each rank's dW / db slice equals the oracle's rows (decision replay);
   * the replicated head (loss, FC update) is bitwise identical on all ranks;
-  * the paper net (BASELINE configs[2]) and the scaled net (configs[4]) at full size, sampled
-    outputs of every pass.
+  * the paper net (BASELINE configs[2], and configs[3]'s batch 1024 with an Eq. 1 partition) and
+    the scaled net (configs[4]) at full size, sampled outputs of every pass.
 """
 import os
 import sys
@@ -244,9 +244,11 @@ def main():
         dist.all_gather_object(out, o)
         return out
 
-    for name, head, net, B in [("paper net", "partitioned", None, 128), ("paper net", "replicated", None, 128),
-                               ("scaled net (configs[4])", "partitioned", synth.scaled_net(), 256)]:
-        net, parts, pn, params, x, y = bench_setup(world, rank, comm, dev, net=net, B=B, head=head)
+    for name, head, net, B, times in [
+            ("paper net", "partitioned", None, 128, None), ("paper net", "replicated", None, 128, None),
+            ("paper net B=1024, Eq. 1 partition (configs[3])", "partitioned", None, 1024, uneven),
+            ("scaled net (configs[4])", "partitioned", synth.scaled_net(), 256, None)]:
+        net, parts, pn, params, x, y = bench_setup(world, rank, comm, dev, net=net, B=B, head=head, times=times)
         failures += [f"{name}, {head} head: {m}" for m in check_step(pn, net, parts, params, x, y, rank, world,
                                                                      allgather, n=256)]
         pn.close()
