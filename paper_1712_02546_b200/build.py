@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                   "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
+                   "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o,
+                   *os.environ.get("CP_NVCC_EXTRA", "").split()]   # experiment builds (-D...), use force
             if src.endswith(".cpp"):
                 cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include"),
                        "-x", "cu", "-c", s, "-o", o]

@@ -52,7 +52,10 @@ struct Cfg {
   static constexpr int B_BYTES = CG == 1 ? BN * BK * 4 : (BN / 2) * BK * 4;
   // forward: pooling exchange; dgrad: per-warp transpose for full-line (NVLink) peer stores
   static constexpr int POOL = PASS != 2 ? EPI_GROUPS * POOL_BYTES : 0;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
+#ifndef CP_TC_STAGES_CG2
+#define CP_TC_STAGES_CG2 6   // experiment hook (-D via CP_NVCC_EXTRA)
+#endif
+  static constexpr int STAGES = CG == 1 ? 4 : CP_TC_STAGES_CG2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + POOL + 256;
 };
