@@ -99,6 +99,9 @@ struct TcParams {
                        // horizontally adjacent pixels (exact valid rows, s-union only at borders)
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
   int wg_taps_slow;    // wgrad unit order: 0 = N (tap, slot tile) fastest; 1 = slot tile, kernel tile, tap
+  int halo;            // fwd (CTA pairs, tf32): one A box per (input block, tap row, channel chunk) holds the
+                       // window's 2 x (S+1) input pixels; the S column taps are 8 KB offsets into it
+                       // (accumulator rows ordered (dw, dh, image) instead of (dh, dw, image))
   short win_order[MAX_WIN];
   const float* bias;
   float* out;          // fwd: y block ; dgrad: dx (full gather) ; wgrad: dW or split partials
@@ -131,6 +134,10 @@ struct Unit {
 // Unit u of this CTA group -> the tile of CTA `rank` (rank = 0 for CG=1).  With CG=2 the pair's
 // two M tiles are two consecutive 32-image chunks of the same 2x2 window (FWD/DGRAD: identical
 // tap lists, so both CTAs run the same K loop) or two consecutive 128-kernel tiles (WGRAD).
+// forward accumulator quadrant (32-row group) <-> row-major 2x2 window position (dh*2 + dw): the
+// identity, or (halo rows ordered (dw, dh, image)) the swap of the two bits - an involution
+__host__ __device__ __forceinline__ int win_pos(int q, int halo) { return halo ? ((q & 1) << 1) | (q >> 1) : q; }
+
 template <int PASS, int CG>
 __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) {
   Unit t{};
@@ -230,6 +237,7 @@ struct Chunk {
   int ksteps;
   int r, s;           // fwd / dgrad: the tap's row and column
   int bc, q, pp;      // wgrad: 32-image chunk and output position of k-chunk c
+  int first, last;    // fwd halo: first / last chunk of its (block, tap row, channel chunk) group in this walk
 };
 // (coordinates are produced by the loops themselves: the single TMA producer thread issues one
 // chunk per ~900 cycles of MMA, so integer divisions on its path cost tensor-pipe time)
@@ -263,6 +271,43 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     if (lo >= hi) return;
     // decode chunk `lo` once, then step the coordinates (this loop runs on the single producer and
     // MMA threads, one iteration per ~900 tensor cycles)
+    if (p.halo) {
+      // input blocks outermost (own block first when gathering), then tap row, channel chunk, and the
+      // tap column innermost: the S column taps of a group share one A halo box
+      const int S = p.S, R = p.R;
+      int rb = p.arrive ? p.self_blk : 0, rem = lo;
+      int nc = (p.kw[rb] + BKE - 1) / BKE;
+      while (rem >= nc * R * S) {
+        rem -= nc * R * S;
+        rb = rb + 1 == p.nblk ? 0 : rb + 1;
+        nc = (p.kw[rb] + BKE - 1) / BKE;
+      }
+      int r = rem / (nc * S);
+      rem -= r * nc * S;
+      int c = rem / S, sx = rem - c * S;
+      int kw = p.kw[rb];
+      for (int idx = lo; idx < hi; ++idx) {
+        Chunk ch{r * S + sx, rb, c, min(BKE, kw - c * BKE) / KSE, r, sx, 0, 0, 0};
+        ch.first = sx == 0 || idx == lo;
+        ch.last = sx == S - 1 || idx == hi - 1;
+        f(ch);
+        if (++sx == S) {
+          sx = 0;
+          if (++c == nc) {
+            c = 0;
+            if (++r == R) {
+              r = 0;
+              do {
+                rb = rb + 1 == p.nblk ? 0 : rb + 1;
+                nc = (p.kw[rb] + BKE - 1) / BKE;
+              } while (nc == 0);
+              kw = p.kw[rb];
+            }
+          }
+        }
+      }
+      return;
+    }
     if (p.arrive) {
       // overlapped gather: input blocks outermost (own block first), then tap, then channel chunk
       int rb = p.self_blk, rem = lo;
@@ -410,7 +455,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = bars + 2 * C::STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  uint64_t* afull = bars + 2 * C::STAGES + 4;    // fwd halo ring (2 stages in the A region)
+  uint64_t* aempty = bars + 2 * C::STAGES + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 8);
+  const int halo_bytes = (p.S + 1) * 8192;       // 2 rows x (S+1) columns x 32 images x 128 B
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -423,6 +471,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * p.epi_groups * CG);
+      mbar_init(&afull[a], 1);
+      mbar_init(&aempty[a], 1);
     }
     fence_barrier_init();
     for (int m = 0; m < (p.unified ? 1 : p.nblk); ++m) tma_prefetch(&p.maps[m]);
@@ -439,6 +489,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int ast = 0;                                   // fwd halo ring stage / phase
+      uint32_t aph = 0;
       uint32_t arrived = PASS == PASS_FWD && p.arrive ? 1u << p.self_blk : ~0u;  // input blocks known present
       const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
       for (int k = 0;; ++k) {
@@ -464,6 +516,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           }
         }
         for_each_chunk<PASS, DT>(p, t, [&](const Chunk& ch) {
+          if (PASS == PASS_FWD && !DT && p.halo) {
+            if (ch.first) {
+              if (!((arrived >> ch.rb) & 1u)) {
+                wait_flag_sys(p.arrive + ch.rb, p.arrive_target);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                arrived |= 1u << ch.rb;
+              }
+              mbar_wait(&aempty[ast], aph ^ 1);
+              if (rank == 0) mbar_arrive_expect_tx(&afull[ast], (uint32_t)halo_bytes * CG);
+              uint8_t* ah = sA + ast * halo_bytes;
+              // box (32 slots, 32 images, 2 rows, S+1 columns): rows land as (column, row, image)
+              if (CG == 2) {
+                const uint32_t abar = mapa(smem_u32(&afull[ast]), 0);
+                if (p.unified) tma_load_5d_cg2(ah, &p.maps[0], abar, ch.c * BKE, t.bc * 32, 2 * t.i + ch.r, 2 * t.j, ch.rb);
+                else tma_load_4d_cg2(ah, &p.maps[ch.rb], abar, ch.c * BKE, t.bc * 32, 2 * t.i + ch.r, 2 * t.j);
+              } else {
+                if (p.unified) tma_load_5d(ah, &p.maps[0], &afull[ast], ch.c * BKE, t.bc * 32, 2 * t.i + ch.r, 2 * t.j, ch.rb);
+                else tma_load_4d(ah, &p.maps[ch.rb], &afull[ast], ch.c * BKE, t.bc * 32, 2 * t.i + ch.r, 2 * t.j);
+              }
+            }
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], (uint32_t)(p.bn_box * BK * 4) * CG);
+            uint8_t* bh = sB + stage * C::B_BYTES;
+            if (CG == 2)
+              tma_load_2d_cg2(bh, &p.maps[CP_MAX_RANKS], mapa(smem_u32(&full[stage]), 0),
+                              ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
+            else
+              tma_load_2d(bh, &p.maps[CP_MAX_RANKS], &full[stage], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
+            if (ch.last && ++ast == 2) {
+              ast = 0;
+              aph ^= 1;
+            }
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            return;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
@@ -549,6 +639,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int ast = 0;
+      uint32_t aph = 0;
       int local = 0;
       for (int k = 0;; ++k, ++local) {
         const int u = unit_at(p, group, ngroups, k);
@@ -563,10 +655,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int a_mn = PASS == PASS_WGRAD, b_mn = PASS != PASS_FWD;
         const uint32_t idesc = DT ? idesc_bf16(BM * CG, n_mma, a_mn, b_mn) : idesc_tf32(BM * CG, n_mma, a_mn, b_mn);
         uint32_t accumulate = 0;
+        const bool halo = PASS == PASS_FWD && !DT && p.halo;
         for_each_chunk<PASS, DT>(p, t, [&](const Chunk& ch) {
+          if (halo && ch.first) {
+            mbar_wait(&afull[ast], aph);
+            tc_fence_after();
+          }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
+          const uint32_t a_addr = halo ? smem_u32(sA + ast * halo_bytes + ch.s * 8192) : smem_u32(sA + stage * A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
           // descriptors built once per chunk; a K-step only advances the start-address field
           // (16-byte units: +32 B K-major, +1024 B MN-major)
@@ -592,6 +689,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             for (int k = 0; k < ch.ksteps; ++k) mma(k);
           }
           if (CG == 2) mma_commit_cg2(&empty[stage]); else mma_commit(&empty[stage]);
+          if (halo && ch.last) {
+            if (CG == 2) mma_commit_cg2(&aempty[ast]); else mma_commit(&aempty[ast]);
+            if (++ast == 2) {
+              ast = 0;
+              aph ^= 1;
+            }
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -666,7 +770,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           store_f32x32(dst, v, 32);
         } else if (PASS == PASS_FWD && p.split > 1) {
           // split-K partial of the pre-pool tile: [sp][Ho][Wo][Bp][Kc]
-          const int dh = quad >> 1, dw = quad & 1;
+          const int pos = win_pos(quad, p.halo);
+          const int dh = pos >> 1, dw = pos & 1;
           const int bb = t.bc * 32 + lane;
           const int64_t o = (int64_t)t.sp * p.part_stride +
                             ((int64_t)((2 * t.i + dh) * p.Wo + 2 * t.j + dw) * p.Bp + bb) * p.Kc + t.n0 + cc * 32;
@@ -707,10 +812,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                 code[q] = 0;
               }
 #pragma unroll
-              for (int w4 = 1; w4 < 4; ++w4)
+              for (int w4 = 1; w4 < 4; ++w4)      // window positions in row-major order (first-max ties)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  const float x = pool_buf[(w4 * 32 + b) * POOL_LD + c4 + q];
+                  const float x = pool_buf[(win_pos(w4, p.halo) * 32 + b) * POOL_LD + c4 + q];
                   if (x > best[q]) {
                     best[q] = x;
                     code[q] = w4;
@@ -743,7 +848,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             }
             asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
           } else {
-            const int dh = quad >> 1, dw = quad & 1;
+            const int pos = win_pos(quad, p.halo);
+            const int dh = pos >> 1, dw = pos & 1;
             const int bb = t.bc * 32 + lane;
             const int64_t o = ((int64_t)((2 * t.i + dh) * p.Wo + 2 * t.j + dw) * p.Bp + bb) * p.Kc + nbase;
             const bool real_b = bb < p.B;
@@ -859,6 +965,7 @@ __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restri
 // then bias, ReLU, 2x2 max-pool (rows q*32+b of a CTA's tile are window position q, image b),
 // argmax code and RN-tf32 rounding, exactly as the fused epilogue.
 struct FwdTailInfo {
+  int halo;   // accumulator quadrants in halo order (win_pos)
   int n, cg, Wo, Wp, Bp, B, Kr, Kc, relu, pool, npeers;
   short pbeg[MAX_TAIL + 1];   // pieces of tail unit tu: [pbeg[tu], pbeg[tu+1])
   float* peer[CP_MAX_RANKS];  // fused AllGather: own block inside each peer's buffer
@@ -881,8 +988,8 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
 #pragma unroll
     for (int q = 0; q < 4; ++q) zq[q] += src[q * 32 * BN];
   }
-  for (int q = 0; q < 4; ++q) {
-    float z = zq[q] + bs;
+  for (int q = 0; q < 4; ++q) {             // q: row-major window position
+    float z = zq[win_pos(q, ti.halo)] + bs;
     if (ti.relu && !(z > 0.f)) z = 0.f;
     if (ti.pool) {
       if (q == 0 || z > best) {
@@ -1457,8 +1564,29 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   fill_common(p, L);
   const Plan pl = fwd_plan(L, p);
   const int es = op_bytes(L), E = 128 / es;
+  // halo A boxes (see TcParams::halo): CTA pairs (the 2-stage halo ring fills the 6-stage A region),
+  // tf32, S <= 5 (2 x (S+1) x 8 KB <= 96 KB).  Measured 5-8 % SLOWER than one box per tap at P = 1/2/4
+  // although it moves 40 % fewer A bytes (profiles/r01_fwd_p4/halo.txt), so it is off unless
+  // CP_TC_FWD_HALO=1 (kept: parity-tested in tests/test_gpu_layers.py::test_planner_variants)
+  p.halo = (pl.pair && es == 4 && !L.images && 2 * (p.S + 1) * 8192 <= Cfg<2, PASS_FWD>::STAGES * A_BYTES &&
+            env_int("CP_TC_FWD_HALO", 0)) ? 1 : 0;
   if (L.images) {
     CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 2, 2, false, es));
+  } else if (p.halo) {
+    // dims (slot, b, h, w[, block]) - h before w, so a box lands as rows (w, h, b) and the 128 rows of
+    // column tap s are the contiguous rows [64 s, 64 s + 128)
+    const int n = equal_blocks(L) ? 1 : L.in.n;
+    for (int r = 0; r < n; ++r) {
+      const int kw = L.in.kw[r];
+      if (kw <= 0) continue;
+      const uint64_t dims[5] = {(uint64_t)kw, (uint64_t)L.Bp, (uint64_t)L.H, (uint64_t)L.W, (uint64_t)L.in.n};
+      const uint64_t str[4] = {(uint64_t)kw * es, (uint64_t)kw * L.Bp * L.W * es, (uint64_t)kw * L.Bp * es,
+                               (uint64_t)kw * L.Bp * L.W * L.H * es};
+      const uint32_t box[5] = {(uint32_t)E, 32, 2, (uint32_t)(p.S + 1), 1};
+      CP_TRY(make_map(&p.maps[r], (const char*)xin + (n == 1 ? 0 : L.in.start[r] * es), n == 1 ? 5 : 4, dims, str,
+                      box, false, es));
+    }
+    p.unified = n == 1 ? 1 : 0;
   } else if (equal_blocks(L)) {
     // one 5-D map over all rank blocks: (slot, b, w, h, block)
     const int kw = L.in.kw[0];
@@ -1515,7 +1643,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     int T = 0;
     if (pl.S == 1 && env_int("CP_TC_FWD_TAIL", 1) && plan_stream_tail(p, G, p.R * p.S * p.cpt, 16, ti.pbeg, &T)) {
       p.tail_buf = part;
-      ti.n = T; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B;
+      ti.n = T; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B; ti.halo = p.halo;
       ti.Kr = L.Kr; ti.Kc = L.Kc; ti.relu = L.d.relu; ti.pool = L.d.pool;
       ti.npeers = npeers;
       for (int k = 0; k < npeers; ++k) ti.peer[k] = peer_blocks[k];
