@@ -99,6 +99,8 @@ struct TcParams {
                        // horizontally adjacent pixels (exact valid rows, s-union only at borders)
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
   int wg_taps_slow;    // wgrad unit order: 0 = N (tap, slot tile) fastest; 1 = slot tile, kernel tile, tap
+  int diag;            // fwd timing diagnostics (CP_TC_DIAG; results are wrong): 1 no MMAs, 2 no A loads,
+                       // 4 no B loads
   int halo;            // fwd (CTA pairs, tf32): one A box per (input block, tap row, channel chunk) holds the
                        // window's 2 x (S+1) input pixels; the S column taps are 8 KB offsets into it
                        // (accumulator rows ordered (dw, dh, image) instead of (dh, dw, image))
@@ -501,7 +503,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int nb_own = CG == 2 ? n_mma / 2 : n_mma;          // B columns staged by this CTA
         const int nb0 = t.n0 + (int)rank * nb_own;                // first B column of this CTA
         const int nboxes = p.wide ? (CG == 2 ? 4 : 8) : (nb_own + 31) / 32;  // MN-major B: 32-column atoms
-        const uint32_t tx_cta = PASS == PASS_FWD ? A_BYTES + p.bn_box * BK * 4 : A_BYTES + nboxes * 4096;
+        const uint32_t tx_cta = PASS == PASS_FWD ? ((p.diag & 2) ? 0 : A_BYTES) + ((p.diag & 4) ? 0 : p.bn_box * BK * 4)
+                                                 : A_BYTES + nboxes * 4096;
         // wgrad span: input block and atom of every B box of this unit, once per unit
         int wb_n = 0, wb_rb[8], wb_atom[8];
         const int wg_r = PASS == PASS_WGRAD ? t.tap / p.S : 0, wg_s = PASS == PASS_WGRAD ? t.tap % p.S : 0;
@@ -584,11 +587,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written data -> TMA reads
               arrived |= 1u << ch.rb;
             }
-            if (p.unified)
+            if (p.diag & 2) {
+            } else if (p.unified)
               ld5(a, &p.maps[0], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
             else
               ld4(a, &p.maps[ch.rb], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
-            ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
+            if (!(p.diag & 4)) ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.r, s = ch.s;
             if (p.l2hint && p.pix)
@@ -682,7 +686,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             }
             accumulate = 1;
           };
-          if (ch.ksteps == 4) {
+          if (PASS == PASS_FWD && (p.diag & 1)) {
+          } else if (ch.ksteps == 4) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma(k);
           } else {
@@ -1568,6 +1573,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   // tf32, S <= 5 (2 x (S+1) x 8 KB <= 96 KB).  Measured 5-8 % SLOWER than one box per tap at P = 1/2/4
   // although it moves 40 % fewer A bytes (profiles/r01_fwd_p4/halo.txt), so it is off unless
   // CP_TC_FWD_HALO=1 (kept: parity-tested in tests/test_gpu_layers.py::test_planner_variants)
+  p.diag = env_int("CP_TC_DIAG", 0);
   p.halo = (pl.pair && es == 4 && !L.images && 2 * (p.S + 1) * 8192 <= Cfg<2, PASS_FWD>::STAGES * A_BYTES &&
             env_int("CP_TC_FWD_HALO", 0)) ? 1 : 0;
   if (L.images) {
