@@ -101,6 +101,8 @@ struct TcParams {
   int wg_taps_slow;    // wgrad unit order: 0 = N (tap, slot tile) fastest; 1 = slot tile, kernel tile, tap
   int diag;            // fwd timing diagnostics (CP_TC_DIAG; results are wrong): 1 no MMAs, 2 no A loads,
                        // 4 no B loads
+  int fwdT;            // transposed forward (CTA-local, tf32): own kernels on M (128-row tiles), the 2x2
+                       // window x 64 images on N = 256; the pool runs in each thread's registers
   int halo;            // fwd (CTA pairs, tf32): one A box per (input block, tap row, channel chunk) holds the
                        // window's 2 x (S+1) input pixels; the S column taps are 8 KB offsets into it
                        // (accumulator rows ordered (dw, dh, image) instead of (dh, dw, image))
@@ -151,6 +153,18 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     t.tu = p.tail_tu[v];
     t.piece = v;
     u = p.tail_full + t.tu;
+  }
+  if (PASS == PASS_FWD && p.fwdT) {
+    // kernel tile fastest (the units of a wave share the window's activation tile), then image chunk
+    t.mt = u % p.numM;
+    const int rest = u / p.numM, nb = p.Bp / 64;
+    t.bc = rest % nb;
+    const int ij = rest / nb;
+    t.j = ij % p.Wp;
+    t.i = ij / p.Wp;
+    t.n0 = t.mt * BM;
+    t.n = BN;
+    return t;
   }
   if (PASS == PASS_WGRAD && p.wg_taps_slow) {
     // taps slowest: a wave covers every kernel tile x a few adjacent taps, so the activation rows
@@ -503,7 +517,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int nb_own = CG == 2 ? n_mma / 2 : n_mma;          // B columns staged by this CTA
         const int nb0 = t.n0 + (int)rank * nb_own;                // first B column of this CTA
         const int nboxes = p.wide ? (CG == 2 ? 4 : 8) : (nb_own + 31) / 32;  // MN-major B: 32-column atoms
-        const uint32_t tx_cta = PASS == PASS_FWD ? ((p.diag & 2) ? 0 : A_BYTES) + ((p.diag & 4) ? 0 : p.bn_box * BK * 4)
+        const uint32_t tx_cta = PASS == PASS_FWD ? (p.fwdT ? A_BYTES + BN * BK * 4
+                                                           : ((p.diag & 2) ? 0 : A_BYTES) + ((p.diag & 4) ? 0 : p.bn_box * BK * 4))
                                                  : A_BYTES + nboxes * 4096;
         // wgrad span: input block and atom of every B box of this unit, once per unit
         int wb_n = 0, wb_rb[8], wb_atom[8];
@@ -587,12 +602,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written data -> TMA reads
               arrived |= 1u << ch.rb;
             }
-            if (p.diag & 2) {
+            if (p.fwdT) {
+              // A = the own kernels' weight rows (K-major), B = 4 window pixels x 64 images (K-major)
+              ld2(a, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, t.n0);
+              if (p.unified) ld5(b, &p.maps[0], ch.c * BKE, t.bc * 64, 2 * t.j + s, 2 * t.i + r, ch.rb);
+              else ld4(b, &p.maps[ch.rb], ch.c * BKE, t.bc * 64, 2 * t.j + s, 2 * t.i + r);
+            } else if (p.diag & 2) {
             } else if (p.unified)
               ld5(a, &p.maps[0], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
             else
               ld4(a, &p.maps[ch.rb], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
-            if (!(p.diag & 4)) ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
+            if (!(p.diag & 4) && !p.fwdT) ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.r, s = ch.s;
             if (p.l2hint && p.pix)
@@ -765,6 +785,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       if (grp >= p.epi_groups) break;
+      if (PASS == PASS_FWD && p.fwdT) {
+        // transposed forward: TMEM lane = own kernel slot, columns = (window position, image); group
+        // grp takes images [32 grp, 32 grp + 32) of the unit's 64; bias + ReLU + first-max pool over
+        // the four positions in registers, then one coalesced 128 B store per image (lanes = slots)
+        const int kk = t.n0 + row;
+        for (int h2 = grp; h2 < 2; h2 += p.epi_groups) {
+          if (t.tail) {
+            for (int pp = 0; pp < 4; ++pp) {
+              float v[32];
+              tmem_ld_32x32b_x32(tbase + (pp * 2 + h2) * 32, v);
+              store_f32x32(p.tail_buf + ((int64_t)t.piece * BM + row) * BN + (pp * 2 + h2) * 32, v, 32);
+            }
+            continue;
+          }
+          const float bs = (p.bias && kk < p.Kr) ? __ldg(p.bias + kk) : 0.f;
+          float best[32];
+          uint32_t code[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) code[q] = 0;
+#pragma unroll 1
+          for (int pp = 0; pp < 4; ++pp) {
+            float v[32];
+            tmem_ld_32x32b_x32(tbase + (pp * 2 + h2) * 32, v);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              float x = v[q] + bs;
+              if (p.relu && !(x > 0.f)) x = 0.f;
+              if (pp == 0) {
+                best[q] = x;
+              } else if (x > best[q]) {
+                best[q] = x;
+                code[q >> 2] = (code[q >> 2] & ~(0xffu << (8 * (q & 3)))) | ((uint32_t)pp << (8 * (q & 3)));
+              }
+            }
+          }
+          if (kk < p.Kc) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const int bb = t.bc * 64 + h2 * 32 + q;
+              const int64_t o = ((int64_t)(t.i * p.Wp + t.j) * p.Bp + bb) * p.Kc + kk;
+              const bool ok = bb < p.B && kk < p.Kr;
+              const float ov = ok ? tf32_rna(best[q]) : 0.f;
+              p.out[o] = ov;
+              p.saved[o] = ok ? (uint8_t)((code[q >> 2] >> (8 * (q & 3))) & 0xffu) : (uint8_t)0;
+              for (int k = 0; k < p.npeers; ++k) p.peer_out[k][o] = ov;
+            }
+          }
+        }
+      } else
       for (int cc = grp, jb = 0; cc < nchunk; cc += p.epi_groups, ++jb) {
         float v[32];
         tmem_ld_32x32b_x32(tbase + cc * 32, v);
@@ -1013,6 +1082,40 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
     saved[o] = ok ? (uint8_t)code : 0;
     for (int k = 0; k < ti.npeers; ++k) ti.peer[k][o] = ok ? tf32_rna(best) : 0.f;
   }
+  if (ti.npeers) __threadfence_system();
+}
+
+// stream-tail finish of the transposed forward: tile rows = own kernel slots, columns = (window
+// position, image of 64); pieces summed in K order, then bias + ReLU + first-max pool.  One block
+// per (tile row, tail unit), one thread per image.
+__global__ void fwd_tail_finish_t(const float* __restrict__ buf, const float* __restrict__ bias, float* __restrict__ y,
+                                  uint8_t* __restrict__ saved, const __grid_constant__ FwdTailInfo ti) {
+  const int tu = blockIdx.y, row = blockIdx.x, b = threadIdx.x;
+  const int kk = ti.n0[tu] + row;
+  if (kk >= ti.Kc) return;
+  const int bb = ti.bc0[tu] + b;
+  const bool ok = bb < ti.B && kk < ti.Kr;
+  const float bs = (bias && kk < ti.Kr) ? bias[kk] : 0.f;
+  float zq[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int pc = ti.pbeg[tu]; pc < ti.pbeg[tu + 1]; ++pc) {
+    const float* src = buf + ((int64_t)pc * BM + row) * BN + b;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) zq[q] += src[q * 64];
+  }
+  float best = 0.f;
+  int code = 0;
+  for (int q = 0; q < 4; ++q) {
+    float z = zq[q] + bs;
+    if (ti.relu && !(z > 0.f)) z = 0.f;
+    if (q == 0 || z > best) {
+      best = z;
+      code = q;
+    }
+  }
+  const int64_t o = ((int64_t)(ti.i[tu] * ti.Wp + ti.j[tu]) * ti.Bp + bb) * ti.Kc + kk;
+  y[o] = ok ? tf32_rna(best) : 0.f;
+  saved[o] = ok ? (uint8_t)code : 0;
+  for (int k = 0; k < ti.npeers; ++k) ti.peer[k][o] = ok ? tf32_rna(best) : 0.f;
   if (ti.npeers) __threadfence_system();
 }
 
@@ -1574,9 +1677,35 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   // although it moves 40 % fewer A bytes (profiles/r01_fwd_p4/halo.txt), so it is off unless
   // CP_TC_FWD_HALO=1 (kept: parity-tested in tests/test_gpu_layers.py::test_planner_variants)
   p.diag = env_int("CP_TC_DIAG", 0);
+  // transposed forward (TcParams::fwdT): tf32, gathered input, pooled, 64-image chunks.  A TF32 MMA
+  // costs the same for any N <= 256, so own-kernel N tiles narrower than 256 waste tensor
+  // time; the transposed CTA-local kernel pads the own kernels to 128 instead but moves 1.5x the
+  // operand bytes per MAC (L2-bound, ~0.5 us per K-chunk).  Measured (P = 1/2/4/8, paper net): it
+  // wins only where 256-wide tiles pad by > 30 % and 128-row tiles by < 10 % (P=4: 375 kernels,
+  // -8 %); CP_TC_FWD_T=0/1 forces it.
+  {
+    const double pad256 = (double)roundup(L.Kc, 256) / std::max(L.Kc, 1);
+    const double pad128 = (double)roundup(L.Kc, 128) / std::max(L.Kc, 1);
+    const int dflt = (pad256 > 1.3 && pad128 < 1.1) ? 1 : 0;
+    p.fwdT = (!L.images && es == 4 && L.d.pool && L.Bp % 64 == 0 && env_int("CP_TC_FWD_T", dflt)) ? 1 : 0;
+  }
   p.halo = (pl.pair && es == 4 && !L.images && 2 * (p.S + 1) * 8192 <= Cfg<2, PASS_FWD>::STAGES * A_BYTES &&
             env_int("CP_TC_FWD_HALO", 0)) ? 1 : 0;
-  if (L.images) {
+  if (p.fwdT) {
+    p.halo = 0;
+    const int n = equal_blocks(L) ? 1 : L.in.n;
+    for (int r = 0; r < n; ++r) {
+      const int kw = L.in.kw[r];
+      if (kw <= 0) continue;
+      const uint64_t dims[5] = {(uint64_t)kw, (uint64_t)L.Bp, (uint64_t)L.W, (uint64_t)L.H, (uint64_t)L.in.n};
+      const uint64_t str[4] = {(uint64_t)kw * es, (uint64_t)kw * L.Bp * es, (uint64_t)kw * L.Bp * L.W * es,
+                               (uint64_t)kw * L.Bp * L.W * L.H * es};
+      const uint32_t box[5] = {(uint32_t)E, 64, 2, 2, 1};
+      CP_TRY(make_map(&p.maps[r], (const char*)xin + (n == 1 ? 0 : L.in.start[r] * es), n == 1 ? 5 : 4, dims, str,
+                      box, false, es));
+    }
+    p.unified = n == 1 ? 1 : 0;
+  } else if (L.images) {
     CP_TRY(map_act(&p.maps[0], xin, L.Kcol, L.Bp, L.Wo, L.Ho, 2, 2, false, es));
   } else if (p.halo) {
     // dims (slot, b, h, w[, block]) - h before w, so a box lands as rows (w, h, b) and the 128 rows of
@@ -1612,7 +1741,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   {
     const uint64_t dims[2] = {(uint64_t)L.Ktot, (uint64_t)std::max(L.Kr, 1)};
     const uint64_t str[1] = {(uint64_t)L.Ktot * es};
-    const uint32_t box[2] = {(uint32_t)E, (uint32_t)p.bn_box};
+    const uint32_t box[2] = {(uint32_t)E, (uint32_t)(p.fwdT ? BM : p.bn_box)};
     CP_TRY(make_map(&p.maps[CP_MAX_RANKS], w, 2, dims, str, box, false, es));
   }
   p.numM = pl.numM;
@@ -1620,6 +1749,13 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   p.split = pl.S;
   p.units = p.numM * p.numN * pl.S;
   p.max_chunks = (pl.chunks + pl.S - 1) / pl.S;
+  if (p.fwdT) {
+    p.numM = (L.Kc + BM - 1) / BM;
+    p.numN = L.Hp * L.Wp * (L.Bp / 64);
+    p.split = 1;
+    p.units = p.numM * p.numN;
+    p.max_chunks = pl.chunks;
+  }
   p.bias = L.d.bias ? b : nullptr;
   p.saved = saved;
   p.npeers = npeers;
@@ -1640,21 +1776,31 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   }
   float* part = (float*)((char*)ws + L.off_split);
   p.part_stride = (long long)L.Ho * L.Wo * L.Bp * L.Kc;
-  p.out = pl.S > 1 ? part : y_block;
+  p.out = (pl.S > 1 && !p.fwdT) ? part : y_block;
   // Stream tail of the last partial round (plan_stream_tail); the pooled epilogue of those tiles
   // runs in fwd_tail_finish after the deterministic sum of their pieces.
   FwdTailInfo ti{};
   {
-    const int CG = pl.pair ? 2 : 1, G = num_sms() / CG;
+    const int CG = (pl.pair && !p.fwdT) ? 2 : 1, G = num_sms() / CG;
     int T = 0;
-    if (pl.S == 1 && env_int("CP_TC_FWD_TAIL", 1) && plan_stream_tail(p, G, p.R * p.S * p.cpt, 16, ti.pbeg, &T)) {
+    if ((pl.S == 1 || p.fwdT) && env_int("CP_TC_FWD_TAIL", 1) && plan_stream_tail(p, G, p.R * p.S * p.cpt, 16, ti.pbeg, &T)) {
       p.tail_buf = part;
       ti.n = T; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B; ti.halo = p.halo;
       ti.Kr = L.Kr; ti.Kc = L.Kc; ti.relu = L.d.relu; ti.pool = L.d.pool;
       ti.npeers = npeers;
       for (int k = 0; k < npeers; ++k) ti.peer[k] = peer_blocks[k];
       const int nbcg = L.Bp / 32 / CG, W2 = L.Wo / 2;
-      for (int k = 0; k < T; ++k) {                    // host mirror of decode_unit<FWD>
+      for (int k = 0; k < T && p.fwdT; ++k) {          // host mirror of decode_unit<FWD> (transposed)
+        const int u = p.tail_full + k;
+        const int mt = u % p.numM, rest = u / p.numM, nb = L.Bp / 64;
+        const int ij = rest / nb;
+        ti.bc0[k] = (rest % nb) * 64;
+        ti.j[k] = ij % L.Wp;
+        ti.i[k] = ij / L.Wp;
+        ti.n0[k] = mt * BM;
+        ti.ncol[k] = BM;
+      }
+      for (int k = 0; k < T && !p.fwdT; ++k) {         // host mirror of decode_unit<FWD>
         const int u = p.tail_full + k;
         const int mg = u % p.numM, nt = (u / p.numM) % p.numN;
         const int ij = mg / nbcg;
@@ -1668,13 +1814,16 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   }
   CP_TRY(tc_time_mark(L, PASS_FWD, 0, s));
   if (es == 2) CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2, 1>(p, s) : launch_cg<PASS_FWD, 1, 1>(p, s)));
-  else CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
+  else CP_TRY(((pl.pair && !p.fwdT) ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
   CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
-  if (p.tail_np > 0) {
+  if (p.tail_np > 0 && p.fwdT) {
+    fwd_tail_finish_t<<<dim3(BM, ti.n), 64, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
+    CP_LAUNCHED();
+  } else if (p.tail_np > 0) {
     fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
     CP_LAUNCHED();
   }
-  if (pl.S > 1) {
+  if (pl.S > 1 && !p.fwdT) {
     PeerSet ps{};
     ps.n = npeers;
     for (int k = 0; k < npeers; ++k) ps.p[k] = peer_blocks[k];
