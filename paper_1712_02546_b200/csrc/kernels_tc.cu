@@ -60,6 +60,21 @@ struct Cfg {
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + POOL + 256;
 };
 
+// forward timing diagnostics (experiment builds only: CP_NVCC_EXTRA=-DCP_TC_DIAG_HOOK, then
+// CP_TC_DIAG = 1 no MMAs / 2 no A loads / 4 no B loads; results are wrong) - compiled out otherwise
+#ifdef CP_TC_DIAG_HOOK
+#define TC_DIAG(p, bit) ((p).diag & (bit))
+#else
+#define TC_DIAG(p, bit) 0
+#endif
+// forward halo A boxes (negative result): compiled in only with -DCP_TC_HALO_HOOK, because
+// even a never-taken runtime check on the single producer / MMA threads costs ~1 % of the forward
+#ifdef CP_TC_HALO_HOOK
+#define TC_HALO(p) ((p).halo)
+#else
+#define TC_HALO(p) 0
+#endif
+
 struct TcParams {
   CUtensorMap maps[CP_MAX_RANKS + 1];  // per-block input maps [0..nblk) ; maps[16] = W (fwd/dgrad) or dY (wgrad); dgrad A = maps[0]
   int nblk;
@@ -154,7 +169,7 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     t.piece = v;
     u = p.tail_full + t.tu;
   }
-  if (PASS == PASS_FWD && p.fwdT) {
+  if (PASS == PASS_FWD && CG == 1 && p.fwdT) {   // (compiled out of the pair kernels)
     // kernel tile fastest (the units of a wave share the window's activation tile), then image chunk
     t.mt = u % p.numM;
     const int rest = u / p.numM, nb = p.Bp / 64;
@@ -287,7 +302,7 @@ __device__ __forceinline__ void for_each_chunk(const TcParams& p, const Unit& t,
     if (lo >= hi) return;
     // decode chunk `lo` once, then step the coordinates (this loop runs on the single producer and
     // MMA threads, one iteration per ~900 tensor cycles)
-    if (p.halo) {
+    if (TC_HALO(p)) {
       // input blocks outermost (own block first when gathering), then tap row, channel chunk, and the
       // tap column innermost: the S column taps of a group share one A halo box
       const int S = p.S, R = p.R;
@@ -517,8 +532,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int nb_own = CG == 2 ? n_mma / 2 : n_mma;          // B columns staged by this CTA
         const int nb0 = t.n0 + (int)rank * nb_own;                // first B column of this CTA
         const int nboxes = p.wide ? (CG == 2 ? 4 : 8) : (nb_own + 31) / 32;  // MN-major B: 32-column atoms
-        const uint32_t tx_cta = PASS == PASS_FWD ? (p.fwdT ? A_BYTES + BN * BK * 4
-                                                           : ((p.diag & 2) ? 0 : A_BYTES) + ((p.diag & 4) ? 0 : p.bn_box * BK * 4))
+        const uint32_t tx_cta = PASS == PASS_FWD ? ((CG == 1 && !DT && p.fwdT) ? A_BYTES + BN * BK * 4
+                                                           : (TC_DIAG(p, 2) ? 0 : A_BYTES) + (TC_DIAG(p, 4) ? 0 : p.bn_box * BK * 4))
                                                  : A_BYTES + nboxes * 4096;
         // wgrad span: input block and atom of every B box of this unit, once per unit
         int wb_n = 0, wb_rb[8], wb_atom[8];
@@ -534,7 +549,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           }
         }
         for_each_chunk<PASS, DT>(p, t, [&](const Chunk& ch) {
-          if (PASS == PASS_FWD && !DT && p.halo) {
+          if (PASS == PASS_FWD && !DT && TC_HALO(p)) {
             if (ch.first) {
               if (!((arrived >> ch.rb) & 1u)) {
                 wait_flag_sys(p.arrive + ch.rb, p.arrive_target);
@@ -602,17 +617,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written data -> TMA reads
               arrived |= 1u << ch.rb;
             }
-            if (p.fwdT) {
+            if (CG == 1 && !DT && p.fwdT) {
               // A = the own kernels' weight rows (K-major), B = 4 window pixels x 64 images (K-major)
               ld2(a, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, t.n0);
               if (p.unified) ld5(b, &p.maps[0], ch.c * BKE, t.bc * 64, 2 * t.j + s, 2 * t.i + r, ch.rb);
               else ld4(b, &p.maps[ch.rb], ch.c * BKE, t.bc * 64, 2 * t.j + s, 2 * t.i + r);
-            } else if (p.diag & 2) {
+            } else if (TC_DIAG(p, 2)) {
             } else if (p.unified)
               ld5(a, &p.maps[0], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r, ch.rb);
             else
               ld4(a, &p.maps[ch.rb], ch.c * BKE, t.bc * 32, 2 * t.j + s, 2 * t.i + r);
-            if (!(p.diag & 4) && !p.fwdT) ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
+            if (!TC_DIAG(p, 4) && !(CG == 1 && !DT && p.fwdT)) ld2(b, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, nb0);
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.r, s = ch.s;
             if (p.l2hint && p.pix)
@@ -679,7 +694,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int a_mn = PASS == PASS_WGRAD, b_mn = PASS != PASS_FWD;
         const uint32_t idesc = DT ? idesc_bf16(BM * CG, n_mma, a_mn, b_mn) : idesc_tf32(BM * CG, n_mma, a_mn, b_mn);
         uint32_t accumulate = 0;
-        const bool halo = PASS == PASS_FWD && !DT && p.halo;
+        const bool halo = PASS == PASS_FWD && !DT && TC_HALO(p);
         for_each_chunk<PASS, DT>(p, t, [&](const Chunk& ch) {
           if (halo && ch.first) {
             mbar_wait(&afull[ast], aph);
@@ -706,7 +721,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             }
             accumulate = 1;
           };
-          if (PASS == PASS_FWD && (p.diag & 1)) {
+          if (PASS == PASS_FWD && TC_DIAG(p, 1)) {
           } else if (ch.ksteps == 4) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma(k);
@@ -785,7 +800,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       if (grp >= p.epi_groups) break;
-      if (PASS == PASS_FWD && p.fwdT) {
+      if (PASS == PASS_FWD && CG == 1 && !DT && p.fwdT) {
         // transposed forward: TMEM lane = own kernel slot, columns = (window position, image); group
         // grp takes images [32 grp, 32 grp + 32) of the unit's 64; bias + ReLU + first-max pool over
         // the four positions in registers, then one coalesced 128 B store per image (lanes = slots)
@@ -844,7 +859,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           store_f32x32(dst, v, 32);
         } else if (PASS == PASS_FWD && p.split > 1) {
           // split-K partial of the pre-pool tile: [sp][Ho][Wo][Bp][Kc]
-          const int pos = win_pos(quad, p.halo);
+          const int pos = win_pos(quad, TC_HALO(p));
           const int dh = pos >> 1, dw = pos & 1;
           const int bb = t.bc * 32 + lane;
           const int64_t o = (int64_t)t.sp * p.part_stride +
@@ -889,7 +904,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               for (int w4 = 1; w4 < 4; ++w4)      // window positions in row-major order (first-max ties)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  const float x = pool_buf[(win_pos(w4, p.halo) * 32 + b) * POOL_LD + c4 + q];
+                  const float x = pool_buf[(win_pos(w4, TC_HALO(p)) * 32 + b) * POOL_LD + c4 + q];
                   if (x > best[q]) {
                     best[q] = x;
                     code[q] = w4;
@@ -922,7 +937,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             }
             asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
           } else {
-            const int pos = win_pos(quad, p.halo);
+            const int pos = win_pos(quad, TC_HALO(p));
             const int dh = pos >> 1, dw = pos & 1;
             const int bb = t.bc * 32 + lane;
             const int64_t o = ((int64_t)((2 * t.i + dh) * p.Wo + 2 * t.j + dw) * p.Bp + bb) * p.Kc + nbase;
@@ -1680,16 +1695,16 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   // transposed forward (TcParams::fwdT): tf32, gathered input, pooled, 64-image chunks.  A TF32 MMA
   // costs the same for any N <= 256, so own-kernel N tiles narrower than 256 waste tensor
   // time; the transposed CTA-local kernel pads the own kernels to 128 instead but moves 1.5x the
-  // operand bytes per MAC (L2-bound, ~0.5 us per K-chunk).  Measured (P = 1/2/4/8, paper net): it
-  // wins only where 256-wide tiles pad by > 30 % and 128-row tiles by < 10 % (P=4: 375 kernels,
-  // -8 %); CP_TC_FWD_T=0/1 forces it.
-  {
-    const double pad256 = (double)roundup(L.Kc, 256) / std::max(L.Kc, 1);
-    const double pad128 = (double)roundup(L.Kc, 128) / std::max(L.Kc, 1);
-    const int dflt = (pad256 > 1.3 && pad128 < 1.1) ? 1 : 0;
-    p.fwdT = (!L.images && es == 4 && L.d.pool && L.Bp % 64 == 0 && env_int("CP_TC_FWD_T", dflt)) ? 1 : 0;
-  }
-  p.halo = (pl.pair && es == 4 && !L.images && 2 * (p.S + 1) * 8192 <= Cfg<2, PASS_FWD>::STAGES * A_BYTES &&
+  // operand bytes per MAC (L2-bound, ~0.5 us per K-chunk): same-box A/B at P=4 0.206 vs 0.200 ms for
+  // the pair kernel, slower at P=1/2/8 as well -> off unless CP_TC_FWD_T=1 (parity-tested; the base
+  // for a CTA-pair transposed kernel)
+  p.fwdT = (!L.images && es == 4 && L.d.pool && L.Bp % 64 == 0 && env_int("CP_TC_FWD_T", 0)) ? 1 : 0;
+#ifdef CP_TC_HALO_HOOK
+  const bool halo_hook = true;
+#else
+  const bool halo_hook = false;
+#endif
+  p.halo = (halo_hook && pl.pair && es == 4 && !L.images && 2 * (p.S + 1) * 8192 <= Cfg<2, PASS_FWD>::STAGES * A_BYTES &&
             env_int("CP_TC_FWD_HALO", 0)) ? 1 : 0;
   if (p.fwdT) {
     p.halo = 0;
