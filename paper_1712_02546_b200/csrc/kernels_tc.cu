@@ -1698,7 +1698,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   // operand bytes per MAC (L2-bound, ~0.5 us per K-chunk): same-box A/B at P=4 0.206 vs 0.200 ms for
   // the pair kernel, slower at P=1/2/8 as well -> off unless CP_TC_FWD_T=1 (parity-tested; the base
   // for a CTA-pair transposed kernel)
-  p.fwdT = (!L.images && es == 4 && L.d.pool && L.Bp % 64 == 0 && env_int("CP_TC_FWD_T", 0)) ? 1 : 0;
+  p.fwdT = (es == 4 && L.d.pool && L.Bp % 64 == 0 && env_int(L.images ? "CP_TC_FWD_T_IMAGES" : "CP_TC_FWD_T", 0)) ? 1 : 0;
 #ifdef CP_TC_HALO_HOOK
   const bool halo_hook = true;
 #else
@@ -1706,7 +1706,15 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
 #endif
   p.halo = (halo_hook && pl.pair && es == 4 && !L.images && 2 * (p.S + 1) * 8192 <= Cfg<2, PASS_FWD>::STAGES * A_BYTES &&
             env_int("CP_TC_FWD_HALO", 0)) ? 1 : 0;
-  if (p.fwdT) {
+  if (p.fwdT && L.images) {
+    // im2col rows [Ho][Wo][Bp][Kcol]: box (32 columns, 64 images, 2 w, 2 h)
+    p.halo = 0;
+    const uint64_t dims[4] = {(uint64_t)L.Kcol, (uint64_t)L.Bp, (uint64_t)L.Wo, (uint64_t)L.Ho};
+    const uint64_t str[3] = {(uint64_t)L.Kcol * es, (uint64_t)L.Kcol * L.Bp * es, (uint64_t)L.Kcol * L.Bp * L.Wo * es};
+    const uint32_t box[4] = {(uint32_t)E, 64, 2, 2};
+    CP_TRY(make_map(&p.maps[0], xin, 4, dims, str, box, false, es));
+    p.unified = 0;
+  } else if (p.fwdT) {
     p.halo = 0;
     const int n = equal_blocks(L) ? 1 : L.in.n;
     for (int r = 0; r < n; ++r) {

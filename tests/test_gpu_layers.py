@@ -340,7 +340,7 @@ def test_bf16_rejects_unaligned_partition():
 # parity-checked there with CP_TC_FWD_HALO=1, scripts/halo_check.sh.)
 VARIANTS = [{"CP_TC_WGRAD_ORDER": "1"}, {"CP_TC_WGRAD_ORDER": "1", "CP_TC_SPLIT_WGRAD": "1"},
             {"CP_TC_SPLIT_WGRAD": "1"}, {"CP_TC_ACC_TERMS": "1024"}, {"CP_TC_SPLIT_FWD": "3"},
-            {"CP_TC_SPLIT_DGRAD": "2"}, {"CP_TC_CTA_GROUP": "1"}, {"CP_TC_FWD_T": "1"}]
+            {"CP_TC_SPLIT_DGRAD": "2"}, {"CP_TC_CTA_GROUP": "1"}, {"CP_TC_FWD_T": "1"}, {"CP_TC_FWD_T_IMAGES": "1"}]
 
 
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
