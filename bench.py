@@ -84,15 +84,21 @@ def peaks():
             "hbm": 6650.0, "source": "fallback B200_PROFILING.md x nominal tf32/bf16"}
 
 
+NCU_FILES = ["r02_ncu_conv_tc.json", "r01_ncu_conv_tc.json"]   # newest first
+
+
 def ncu_traffic(pass_name):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the conv2 kernel of this pass, from
-    the committed ncu --set full summary (the longest launch of that pass = conv2)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_conv_tc.json")) as f:
-            rows = [r for r in json.load(f) if r.get("pass") == pass_name]
-        return max(rows, key=lambda r: r.get("duration_us", 0))["traffic_bytes"] if rows else None
-    except Exception:
-        return None
+    the newest committed ncu --set full summary (the longest launch of that pass = conv2)."""
+    for fn in NCU_FILES:
+        try:
+            with open(os.path.join(ROOT, "profiles", fn)) as f:
+                rows = [r for r in json.load(f) if r.get("pass") == pass_name]
+            if rows:
+                return max(rows, key=lambda r: r.get("duration_us", 0))["traffic_bytes"], f"profiles/{fn}"
+        except Exception:
+            continue
+    return None, None
 
 
 class ClockSampler:
@@ -181,19 +187,38 @@ def oracle_images_per_s(net, target_s, step=0):
 
 
 def run_reference(args):
+    """The oracle as the reference arm: every step is the fp64 oracle's training step on a bounded
+    sample of the B-image batch (b images, b calibrated once during the warm-up so that the whole run
+    takes about --cpu-seconds); ms_per_step is the measured wall time of one such step."""
+    import numpy as np
+
+    import oracle
     import synth
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    oracle.build()
+    cores = oracle_threads(host_cores())
     net = synth.paper_net(args.net)
-    vals = []
+    params = {k: v.astype(np.float64) for k, v in synth.params(net, seed=42).items()}
+    per_step_s = max(0.5, args.cpu_seconds / max(1, args.steps))
+    b, times = 1, []
     for k in range(args.warmup + args.steps):
-        v, cores, sample = oracle_images_per_s(net, max(1.0, args.cpu_seconds / max(1, args.steps)), step=k)
-        if k >= args.warmup:
-            vals.append(v)
-    v = statistics.median(vals)
+        x, y = synth.images(b, 3, net.in_hw, net.in_hw, step=k)
+        t0 = time.perf_counter()
+        oracle.net_step(params, x.astype(np.float64), y, 0.01, net.layers())
+        dt = time.perf_counter() - t0
+        if k < args.warmup:   # calibrate the sample size: about per_step_s of CPU work per step
+            b = max(1, min(args.batch, int(round(b * per_step_s / max(dt, 1e-3)))))
+        else:
+            times.append(dt)
+    dt = statistics.median(times)
+    v = b / dt
+    sample = (f"{b} of the B={args.batch} step's images per step ({net.name}), fp64 oracle net_step; median of "
+              f"{len(times)} timed steps, {dt:.2f} s each")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.batch / v * 1e3,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "images_per_step": b,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"paper net {args.net}, CIFAR-10-shaped 32x32x3, batch "
                                                         f"{args.batch}, CPU fp64 oracle (bounded sample per step)",
@@ -204,6 +229,87 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+def _graph(step_fn, dev):
+    """CUDA graph of one step (kernels + collectives + stream fork/join); returns (graph, launches)."""
+    import torch
+
+    from paper_1712_02546_b200 import convpart as cp
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    c0 = cp.cp_launch_count()
+    with torch.cuda.graph(g):
+        step_fn()
+    n = cp.cp_launch_count() - c0
+    g.replay()
+    torch.cuda.synchronize(dev)
+    return g, n
+
+
+def _timed(run, steps, s, dev, flush, world, after=None):
+    """Device time (ms) of `steps` calls of run(), each bracketed by CUDA events on `s`, L2 flushed
+    between calls (outside the events); max over ranks of the total.  after(k) runs between steps."""
+    import torch
+    import torch.distributed as dist
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    for k in range(steps):
+        if flush is not None:
+            flush.fill_(k & 0xFF)
+        ev[k][0].record(s)
+        run()
+        ev[k][1].record(s)
+        torch.cuda.synchronize(dev)
+        if after:
+            after(k)
+    total = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    return total / steps
+
+
+def _max_over_ranks(vals, dev, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return vals
+    t = torch.tensor(vals, device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def _nccl_reference(parts, B, net, dev, world, steps=20):
+    """NCCL AllGather / ReduceScatter of the step's A1 bytes over NVLink on their own (torch's NCCL
+    process group, the same links): the collective-alone bandwidth the fused paths are compared with."""
+    import torch
+    import torch.distributed as dist
+    Bp = (B + 31) // 32 * 32
+    _, _, _, _, hp1 = net.shapes()[0]
+    blk = hp1 * hp1 * Bp * max(parts[0].k_width[r] for r in range(world))   # floats per rank (equal blocks)
+    src = torch.zeros(blk, device=dev)
+    dst = torch.zeros(blk * world, device=dev)
+    out = {}
+    for name, fn in (("allgather", lambda: dist.all_gather_into_tensor(dst, src)),
+                     ("reduce_scatter", lambda: dist.reduce_scatter_tensor(src, dst))):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = _max_over_ranks([e0.elapsed_time(e1) / steps], dev, world)[0]
+        moved = blk * 4 * (world - 1)      # bytes received (AG) / sent (RS) per rank
+        out[name] = {"bytes_per_rank": moved, "ms": ms, "gbs_per_rank": moved / (ms / 1e3) / 1e9,
+                     "frac_of_770": moved / (ms / 1e3) / 770e9}
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -280,8 +386,9 @@ def main():
     else:
         parts = [cp.cp_partition_plan([1.0] * world, K, align) for K in net.kernels]
 
+    lrn = cp.LRN_DEFAULT if args.lrn else None
     pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, math=math, device=dev, head=args.head,
-                        in_hw=net.in_hw, fused=args.fused == "on", lrn=cp.LRN_DEFAULT if args.lrn else None)
+                        in_hw=net.in_hw, fused=args.fused == "on", lrn=lrn)
     params = synth.params(net, seed=42)
     pn.load_params(params)
     x, y = synth.images(B, 3, net.in_hw, net.in_hw, step=0)
@@ -294,27 +401,20 @@ def main():
     overlap = not args.no_overlap
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step_eager():
+    def step_eager(head=True):
         # the current stream (torch's capture stream while a CUDA graph is being captured)
-        pn.step(0.01, dx_mode, torch.cuda.current_stream(dev), cs, overlap)
+        pn.step(0.01, dx_mode, torch.cuda.current_stream(dev), cs, overlap, head=head)
 
     for _ in range(args.warmup):
         step_eager()
     torch.cuda.synchronize(dev)
-    # ---- CUDA graph of one whole step (kernels + NCCL collectives + stream fork/join): removes
-    # the host launch path from the step; every kernel in it is one of ours (counted at capture)
-    # live timing of conv2's three GEMM kernels inside the timed steps (external event records on
-    # the launching stream, captured into the graph)
+    # live timing of conv2's three GEMM kernels inside the timed steps (external event records on the
+    # launching stream, captured into the graph), and of the fused gather's push window (N > 1)
     cp.conv_part_timing(pn.layers[1], True)
     graph, launches_per_step = None, None
     if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        c0 = cp.cp_launch_count()
-        with torch.cuda.graph(graph):
-            step_eager()
-        launches_per_step = cp.cp_launch_count() - c0
-        graph.replay()
-        torch.cuda.synchronize(dev)
+        # CUDA graph of one whole step: removes the host launch path; every kernel in it is ours
+        graph, launches_per_step = _graph(step_eager, dev)
 
     def step():
         if graph is not None:
@@ -327,37 +427,25 @@ def main():
     # ---- device-timed region: K steps, L2 flushed between steps (outside the step events)
     clocks = ClockSampler(local)
     clocks.start()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    n0 = cp.cp_launch_count()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    live = {"fwd": [], "dgrad": [], "wgrad": []}
-    for k in range(args.steps):
-        if flush is not None:
-            flush.fill_(k & 0xFF)
-        ev[k][0].record(s)
-        step()
-        ev[k][1].record(s)
-        # read this step's kernel events before the next replay re-records them (device time only:
-        # the host sync sits between steps, next to the L2 flush)
-        torch.cuda.synchronize(dev)
+    live = {"fwd": [], "dgrad": [], "wgrad": [], "push": []}
+    fused_gather = world > 1 and bool(pn.sym) and math == cp.CP_MATH_TF32
+
+    def read_live(k):
+        # this step's kernel events, read before the next replay re-records them (device time only: the
+        # host sync sits between steps, next to the L2 flush)
         for name, ps in (("fwd", 0), ("dgrad", 1), ("wgrad", 2)):
             live[name].append(cp.conv_part_kernel_time(pn.layers[1], ps))
-    torch.cuda.synchronize(dev)
+        if fused_gather:
+            try:
+                live["push"].append(cp.conv_part_kernel_time(pn.layers[1], 3))
+            except cp.ConvPartError:
+                pass
+    n0 = cp.cp_launch_count()
+    ms_per_step = _timed(step, args.steps, s, dev, flush, world, after=read_live)
     launches = cp.cp_launch_count() - n0 if graph is None else launches_per_step * args.steps
-    if world > 1:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
     value = B / (ms_per_step / 1e3)
 
-    # ---- end to end through the public API: pinned host images/labels in, loss out, per step
+    # ---- end to end through the public API: pinned host images/labels in, loss out to the host, per step
     h2d = x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size()
     d2h = 4
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
@@ -367,7 +455,9 @@ def main():
     # input pipeline: step k+1's images/labels travel host -> device on a copy stream (pinned source,
     # two staging buffers) while step k computes, inside step k's timed window; step 0's copy is issued
     # inside its own window.  Each step starts with a device copy staging -> the network's input
-    # buffer and ends with the loss read back to pinned host memory.  L2 flushed between steps.
+    # buffer and ends with the loss read back to pinned host memory, which the host then reads (the
+    # user's per-step loss read: one host sync per step, as in the device-timed loop).  L2 flushed
+    # between steps.
     cpy = torch.cuda.Stream(dev)
     stage = [(torch.empty_like(pn.x), torch.empty_like(pn.labels)) for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
@@ -383,6 +473,7 @@ def main():
     for j in range(2):
         free[j].record(s)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    host_losses = []
     for k in range(args.steps):
         j = k & 1
         if flush is not None:
@@ -401,22 +492,20 @@ def main():
         step()
         loss_host.copy_(pn.head["loss"][:1], non_blocking=True)
         e2e_ev[k][1].record(s)
+        e2e_ev[k][1].synchronize()
+        host_losses.append(float(loss_host[0]))
     torch.cuda.synchronize(dev)
     # the timed window is tens of ms; keep the same load (identical, untimed steps) until the
-    # sampler has seen >= 1.5 s so the clock record is meaningful
-    # (step count from the max-over-ranks ms_per_step: identical on every rank, the steps hold
-    # collectives)
+    # sampler has seen >= 1.5 s so the clock record is meaningful (step count from the max-over-ranks
+    # ms_per_step: identical on every rank, the steps hold collectives)
     for _ in range(min(2000, int(1500.0 / max(ms_per_step, 0.05)) + 1)):
         step()
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     clk["window"] = "timed steps + e2e steps + identical untimed steps to >= 1.5 s"
-    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = B / (e2e_ms / args.steps / 1e3)
+    e2e_ms = _max_over_ranks([sum(a.elapsed_time(b) for a, b in e2e_ev) / args.steps], dev, world)[0]
+    e2e_value = B / (e2e_ms / 1e3)
+    loss = pn.loss()
 
     # ---- per-pass kernel timing of conv2 (the dominant kernels) on a no-collective clone
     L2d = pn.descs[1]
@@ -430,9 +519,8 @@ def main():
     dx2 = torch.empty_like(b2["dx"])
     a1 = pn.buf[0]["y"]
     da2 = pn.head["da"]
-    reps = 5
     tim = {"fwd": [], "wgrad": [], "dgrad": []}
-    for r in range(reps + 1):
+    for r in range(6):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         if flush is not None:
             flush.fill_(r)
@@ -449,22 +537,63 @@ def main():
             tim["wgrad"].append(e[1].elapsed_time(e[2]))
             tim["dgrad"].append(e[2].elapsed_time(e[3]))
     cp.conv_part_destroy(h2)
+    del ws2, y2, sv2, dw2, db2, dx2
+
+    # ---- conv stage: the same step with the head replaced by the fixed dA2 it produced
+    g_conv, _ = (_graph(lambda: step_eager(head=False), dev) if graph is not None else (None, None))
+    conv_ms = _timed((lambda: g_conv.replay()) if g_conv is not None else (lambda: step_eager(head=False)),
+                     args.steps, s, dev, flush, world)
+    del g_conv
+
+    # ---- N > 1: the same ranks' compute with no cross-rank exchange, the 1-GPU step on this box, and
+    # NCCL's collectives alone on the same bytes (context for the NVLink fraction)
+    compute_ms, one_gpu, nccl_ref = None, None, None
+    if world > 1:
+        pc = PartitionedNet(net.kernels, B, parts, rank=rank, comm=None, math=math, device=dev, head=args.head,
+                            in_hw=net.in_hw, fused=False, lrn=lrn)
+        pc.load_params(params)
+        pc.set_batch(x_host.to(dev), y_host.to(dev))
+        run_c = lambda: pc.step(0.01, cp.CP_DX_LOCAL, torch.cuda.current_stream(dev), cs, overlap)  # noqa: E731
+        for _ in range(2):
+            run_c()
+        gc, _ = _graph(run_c, dev) if graph is not None else (None, None)
+        compute_ms = _timed((lambda: gc.replay()) if gc is not None else run_c, args.steps, s, dev, flush, world)
+        del gc
+        pc.close()
+        del pc
+        torch.cuda.empty_cache()
+        nccl_ref = _nccl_reference(parts, B, net, dev, world)
+        if rank == 0:
+            p1 = [cp.cp_partition_plan([1.0], K, align) for K in net.kernels]
+            po = PartitionedNet(net.kernels, B, p1, rank=0, comm=None, math=math, device=dev, in_hw=net.in_hw, lrn=lrn)
+            po.load_params(params)
+            po.set_batch(x_host.to(dev), y_host.to(dev))
+            run_o = lambda: po.step(0.01, dx_mode, torch.cuda.current_stream(dev), cs, overlap)  # noqa: E731
+            for _ in range(args.warmup):
+                run_o()
+            go, _ = _graph(run_o, dev) if graph is not None else (None, None)
+            one_ms = _timed((lambda: go.replay()) if go is not None else run_o, args.steps, s, dev, flush, 1)
+            del go
+            po.close()
+            del po
+            torch.cuda.empty_cache()
+            one_gpu = {"value": B / (one_ms / 1e3), "ms_per_step": one_ms}
+        dist.barrier()
+
     Kr2 = parts[1].k_count[rank]
     C2, H2o = net.kernels[0], net.shapes()[1][3]
     flop_pass = 2.0 * B * Kr2 * C2 * 25 * H2o * H2o   # algorithmic MACs x2 of one conv2 pass, own slice
     pk = peaks()
     per = {k: statistics.median(v) for k, v in tim.items()}
-    conv2_tflops = {k: flop_pass / (v / 1e3) / 1e12 for k, v in per.items()}
     # roofline: the dominant conv2 GEMM kernel, its average launch duration measured live in the
     # timed steps (max over ranks: the slowest rank sets the step)
-    live_ms = {k: statistics.fmean(v) for k, v in live.items()}
-    if world > 1:
-        t = torch.tensor([live_ms["fwd"], live_ms["dgrad"], live_ms["wgrad"]], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        live_ms = dict(zip(("fwd", "dgrad", "wgrad"), [float(v) for v in t.tolist()]))
+    live_ms = dict(zip(("fwd", "dgrad", "wgrad"), _max_over_ranks(
+        [statistics.fmean(live[k]) for k in ("fwd", "dgrad", "wgrad")], dev, world)))
+    push_ms = None
+    if fused_gather:
+        push_ms = _max_over_ranks([statistics.fmean(live["push"]) if live["push"] else -1.0], dev, world)[0]
     dom = max(live_ms, key=live_ms.get)
     achieved = flop_pass / (live_ms[dom] / 1e3) / 1e12
-    loss = pn.loss()
 
     if rank == 0:
         cpu = None
@@ -473,19 +602,24 @@ def main():
             cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle", "sample": sample}
         # algorithmic training FLOPs per image (11.368 GFLOP for the paper net):
         # conv1 fwd + wgrad, conv2 fwd + dgrad + wgrad, 2 FLOP per MAC (head: negligible)
-        (c1, _, k1, o1, _), (c2, _, k2, o2, _) = net.shapes()
+        (c1, _, k1, o1, hp1), (c2, _, k2, o2, hp2) = net.shapes()
         per_img = 2.0 * (2 * k1 * c1 * 25 * o1 * o1 + 3 * k2 * c2 * 25 * o2 * o2)
         step_flop = per_img * B
-        # burst peak for a timed window of tens of ms; the sustained figure (MEASURED_PEAKS' 4 s
-        # back-to-back run) once the timed steps themselves last a second or more (scaled net)
+        # ONE peak per line: burst for a timed window of tens of ms, the sustained figure (MEASURED_PEAKS'
+        # 4 s back-to-back run) once the timed steps themselves last a second or more (scaled net); the
+        # contraction's own dtype: TF32 = measured bf16 x nominal tf32/bf16, BF16 = measured bf16
         window_s = args.steps * ms_per_step / 1e3
-        if window_s >= 1.0:
-            peak = pk["tf32_sustained"]
-            peak_note = (f" (sustained: the timed window is {window_s:.1f} s; burst = {pk['tf32_burst']:.0f})")
-        else:
-            peak = pk["tf32_burst"]
-            peak_note = (f" (burst: the timed window is {window_s * 1e3:.0f} ms, not the 4 s back-to-back run "
-                         f"behind the sustained figure; sustained = {pk['tf32_sustained']:.0f})")
+        sustained = window_s >= 1.0
+        bf16 = math == cp.CP_MATH_BF16
+        scale = 1.0 / NOMINAL_TF32_OVER_BF16 if bf16 else 1.0
+        peak = (pk["tf32_sustained"] if sustained else pk["tf32_burst"]) * scale
+        other = (pk["tf32_burst"] if sustained else pk["tf32_sustained"]) * scale
+        kind = "kind::f16 (bf16 operands)" if bf16 else "kind::tf32"
+        peak_note = (f" ({'sustained' if sustained else 'burst'}: the timed window is {window_s * 1e3:.0f} ms; "
+                     f"{'burst' if sustained else 'sustained'} = {other:.0f})")
+        if bf16:
+            peak_note = " (bf16: MEASURED_PEAKS.json bf16 as measured)" + peak_note
+        traffic, traffic_src = ncu_traffic(dom) if world == 1 else (None, None)
         line = {
             "metric": METRIC,
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -501,35 +635,87 @@ def main():
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
                 "head": pn.head_mode, "cuda_graph": graph is not None,
                 "lrn": dict(cp.LRN_DEFAULT) if args.lrn else None,
-                "collectives": ("fused into the GEMM epilogues over NVLink peer memory (gather: forward "
-                                "epilogue stores + arrival flags; dX reduce-scatter: dgrad epilogue stores "
-                                "+ slot sum)" if pn.sym else "NCCL AllGather / ReduceScatter")
+                "collectives": ("fused into the GEMMs over NVLink peer memory (gather: the consuming conv2 forward "
+                                "kernel pushes its own input block into every peer's copy while it computes, "
+                                "arrival counters; dX reduce-scatter: dgrad epilogue stores into the owners' receive "
+                                "slots + rank-order slot sum)" if pn.sym else "NCCL AllGather / ReduceScatter")
                                if world > 1 else "none (N=1)",
                 "parallelism": f"kernel-split x{world}",
                 "l2": "flushed between timed steps (256 MiB write outside the step events)" if flush is not None
                       else "not flushed (step working set > 126 MB L2)"},
-            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms,
+                    "note": "pinned H2D of the step's images + labels (prefetched on a copy stream inside the previous "
+                            "step's window), D2D into the net's input, the graph-replayed step, D2H of the loss and "
+                            "its host read every step"},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "tensor", "kernel": f"conv2 {dom} (tcgen05 kind::tf32 implicit GEMM)",
+            "roofline": {"bound": "tensor", "kernel": f"conv2 {dom} (tcgen05 {kind} implicit GEMM)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(dom) if world == 1 else None,
-                         "traffic_source": "profiles/r01_ncu_conv_tc.json (ncu --set full, same kernel, P=1)",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": f"{traffic_src} (ncu --set full, same kernel, P=1)" if traffic_src else None,
                          "flop_per_launch": flop_pass, "launch_ms": live_ms[dom],
                          "launch_ms_source": "CUDA events around the GEMM launch inside the timed graph "
                                              "replays (conv_part_timing), mean over the timed steps, max over ranks",
                          "kernel_ms_live": live_ms,
-                         "peak_source": pk["source"] + peak_note,
-                         "conv2_pass_ms_alone": per, "conv2_pass_tflops_alone": conv2_tflops},
-            "tc_frac_whole_step": step_flop / (ms_per_step / 1e3) / 1e12 / pk["tf32_sustained"],
-            "clocks": clk, "loss": loss,
+                         "peak_source": (pk["source"] if not bf16 else "MEASURED_PEAKS.json bf16") + peak_note,
+                         "conv2_pass_ms_alone": per,
+                         "conv2_pass_tflops_alone": {k: flop_pass / (v / 1e3) / 1e12 for k, v in per.items()}},
+            # whole-step algorithmic FLOP rate over the same peak as roofline.frac
+            "tc_frac_whole_step": step_flop / (ms_per_step / 1e3) / 1e12 / peak,
+            "conv_stage": {"value": B / (conv_ms / 1e3), "unit": "images/s", "ms_per_step": conv_ms,
+                           "what": "the same step with the FC/softmax head replaced by the fixed dA2 it produced "
+                                   "(conv layers, their gathers and dX sums, wgrad, SGD of the conv slices)"},
+            "clocks": clk, "loss": loss, "loss_host_last": host_losses[-1] if host_losses else None,
         }
-        if math == cp.CP_MATH_BF16:
+        if world > 1:
+            Bp = (B + 31) // 32 * 32
+            blk1 = [hp1 * hp1 * Bp * parts[0].k_width[r] * 4 for r in range(world)]
+            blk2 = [hp2 * hp2 * Bp * parts[1].k_width[r] * 4 for r in range(world)]
+            others1 = sum(blk1) - blk1[rank]
+            egress = blk1[rank] * (world - 1) + others1           # gather push + dX partials to the owners
+            if pn.head_mode == "replicated":
+                egress += blk2[rank] * (world - 1)
+            push_bytes = blk1[rank] * (world - 1)
+            exposed = ms_per_step - compute_ms
+            line["speedup_vs_1"] = ({"value": value / one_gpu["value"], "one_gpu_value": one_gpu["value"],
+                                     "one_gpu_ms_per_step": one_gpu["ms_per_step"],
+                                     "measured": "same box, rank 0's GPU, same config at N=1, CUDA graph"}
+                                    if one_gpu else None)
+            line["breakdown_ms"] = {
+                "step": ms_per_step,
+                "compute_only": compute_ms,
+                "exposed_comm": exposed,
+                "head": ms_per_step - conv_ms,
+                "conv_stage": conv_ms,
+                "conv2_gemms_live": sum(live_ms.values()),
+                "note": "compute_only = the same ranks' kernels with no cross-rank exchange (comm=None, LOCAL dX, "
+                        "each rank's slice; CUDA graph); exposed_comm = step - compute_only; head = step - conv_stage "
+                        "(FC fwd/bwd, softmax, logits AllReduce); cf. the paper's Comm/Conv/Comp split, Fig. 8 "
+                        "(P:L408-412)"}
+            line["nvlink"] = {
+                "link_peak_gbs": 770.0,
+                "link_peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
+                "egress_bytes_per_rank": egress,
+                "gather": {"bytes_pushed": push_bytes, "push_window_ms": push_ms if push_ms and push_ms > 0 else None,
+                           "gbs": push_bytes / (push_ms / 1e3) / 1e9 if push_ms and push_ms > 0 else None,
+                           "frac_of_770": push_bytes / (push_ms / 1e3) / 770e9 if push_ms and push_ms > 0 else None,
+                           "how": "globaltimer window inside the conv2 forward kernel: first chunk claimed -> last "
+                                  "chunk's arrival released (warp 3 of every running CTA), mean over timed steps, "
+                                  "max over ranks; overlapped with the forward's own-block MMAs"},
+                "reduce_scatter": {"bytes_sent": others1, "window_ms": live_ms["dgrad"],
+                                   "gbs_lower_bound": others1 / (live_ms["dgrad"] / 1e3) / 1e9,
+                                   "how": "dgrad epilogue peer stores spread over the whole dgrad kernel: bytes / "
+                                          "kernel time is a lower bound of the link rate"},
+                "exposed_comm_ms": exposed,
+                "step_avg_egress_frac_of_770": egress / (ms_per_step / 1e3) / 770e9,
+                "nccl_alone": nccl_ref}
+        if bf16:
             line["report_only"] = ("NEXT row f4: bf16 GEMM operands (kind::f16), fp32 accumulate; parity ~1e-2 "
                                    "of max|ref|, outside the north_star 2e-3 bar - not the headline mode")
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
-    # teardown: the graph holds NCCL work of our communicator -> free it first, sync, then the comm
+    # teardown: the graph holds work of our communicator -> free it first, sync, then the comm
     torch.cuda.synchronize(dev)
     if graph is not None:
         del graph

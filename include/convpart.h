@@ -13,9 +13,12 @@
  * rank runs dgrad and wgrad for its slice, partial dX are summed across ranks,
  * weight gradients stay local.
  *
- * B200 realisation: one process per GPU; the gather is an NCCL AllGather along
- * channels over NVLink, the dX sum an NCCL AllReduce or ReduceScatter.  Conv
- * passes are implicit GEMMs on tcgen05/TMEM (kind::tf32, FP32 accumulation)
+ * B200 realisation: one process per GPU.  With symmetric (peer-mapped) buffers the
+ * channel gather is fused into the consumer GEMM (the next layer's forward pushes its
+ * own input block into every peer's copy over NVLink while it computes) and the dX
+ * reduce-scatter into the dgrad epilogue (partials stored into the owners' receive
+ * slots, summed in rank order); otherwise NCCL AllGather / ReduceScatter / AllReduce.
+ * Conv passes are implicit GEMMs on tcgen05/TMEM (kind::tf32, FP32 accumulation)
  * with TMA-staged tiles and a fused bias+ReLU+2x2 max-pool epilogue, or FP32
  * SIMT kernels in the reference math mode.
  *
@@ -89,11 +92,15 @@ typedef enum {
   CP_DX_ASYNC = 16,          /* OR-flag: do not make `stream` wait for the dX collective;
                                 call conv_part_wait() before reading dx (lets independent
                                 work such as wgrad overlap the reduction, §8(e))        */
-  CP_DX_ORDERED = 64         /* OR-flag (fused reduce-scatter only): the caller guarantees
-                                that a collective on every rank separates consecutive
-                                backward_data calls of this layer (e.g. the forward's
-                                gather or the logits AllReduce), so the overwrite guard
-                                barrier is skipped                                      */
+  CP_DX_ORDERED = 64         /* OR-flag (fused reduce-scatter only).  PRECONDITION: between two
+                                consecutive backward_data calls of this layer, every rank
+                                passes a cross-rank synchronising operation that is ordered
+                                after its previous slot sum on every rank (PartitionedNet: the
+                                next forward's gather barrier or logits AllReduce, which all
+                                ranks enter only after joining the dX stream).  Then no rank can
+                                store into a receive slot a peer is still summing, and the
+                                overwrite-guard barrier is skipped.  Without that guarantee the
+                                flag races: omit it.                                      */
 } cp_dx_mode;
 
 typedef enum {
@@ -134,23 +141,43 @@ int cp_comm_unique_id(uint8_t id_out[128]);
 int cp_comm_create(const uint8_t id[128], int32_t rank, int32_t world, cp_comm* out);
 int cp_comm_destroy(cp_comm comm);
 
-/* Symmetric buffers for the fused channel AllGather (the gather is Alg. 1's
+/* cp_comm_create_loopback — `world` simulated ranks in ONE process on the current GPU (tests of
+ * the fused peer-memory paths on a single B200): out[r] is rank r's handle.  Symmetric buffers
+ * are plain allocations (the k-th cp_symmetric_alloc of every handle forms one buffer); the
+ * cross-rank barriers are no-ops; the comm-stream tail of a fused reduce-scatter (wait for the
+ * peers' slots, rank-order sum) is held back until every rank has issued its backward_data
+ * call for that layer and then enqueued behind all of their dgrads, so no kernel waits on a
+ * later launch.  The caller issues the P ranks' calls of a layer back to back in rank order; the
+ * fused gather's arrival counters of ranks that have not run yet must be satisfied by the caller
+ * (cp_symmetric_peer gives the addresses).  NCCL collectives, cp_allreduce_sum and
+ * cp_symmetric_wait return CP_ERR_UNSUPPORTED on a loopback handle.  Destroy every handle. */
+int cp_comm_create_loopback(int32_t world, cp_comm* out);
+
+/* Symmetric buffers for the fused collectives (the gather is Alg. 1's
  * "concatenate the output of all nodes").  cp_symmetric_alloc allocates `bytes` of
  * zeroed device memory on every rank (collective: all ranks, same size, same order), exchanges CUDA
- * IPC handles over the communicator and maps every peer's copy (plus a small arrival-flag line
- * behind the data).  Semantics when a layer's y_gathered is symmetric (conv_part_forward):
- *   producer: after a one-word AllReduce (no rank may overwrite a copy a peer still reads), the TF32
- *     forward epilogue stores this rank's block into every peer's copy over NVLink, then sets this
- *     rank's arrival flag in every peer's flag line (no AllGather kernel);
- *   consumer: conv_part_forward whose x is a symmetric gathered buffer consumes its own block first
- *     and each peer block only after that peer's flag is set (gather overlapped with the GEMM), and
- *     resets the flags.  Any other reader of a symmetric gathered output calls cp_symmetric_wait
- *     (waits for all peers' flags on `stream`, then resets them) before reading it.
- * cp_symmetric_free (collective) or cp_comm_destroy releases the buffers.  Errors: CP_ERR_ARG for a
- * pointer that is not a symmetric buffer of `comm`; CUDA/NCCL errors as CP_ERR_CUDA/CP_ERR_NCCL. */
+ * IPC handles over the communicator and maps every peer's copy, plus a 256-byte flag line behind
+ * the data: u32 word q = arrival counter of sender q; word 32 = the gather's chunk-claim counter.
+ * Semantics when a layer's y_gathered is symmetric (conv_part_forward):
+ *   producer: after a device-side cross-rank barrier (no rank may overwrite a copy a peer still
+ *     reads), the GEMM writes this rank's block into its LOCAL copy only;
+ *   consumer: conv_part_forward whose x is a symmetric gathered buffer pushes this rank's input
+ *     block into every peer's copy from the GEMM kernel itself (CP_GATHER_CHUNKS chunks claimed
+ *     by any running CTA, one release-add on the peer's counter per chunk), consumes its own block
+ *     first and each peer block once that peer's counter reached CP_GATHER_CHUNKS (gather
+ *     overlapped with the GEMM; no AllGather kernel), then resets its flag line.  A rank without
+ *     kernels in the consuming layer distributes its block with copy-engine copies and raises the
+ *     counters to CP_GATHER_CHUNKS the same way.  Any other reader of a symmetric gathered output
+ *     calls cp_symmetric_wait (waits for all peers' flags on `stream`, then resets them) first.
+ * cp_symmetric_peer returns rank `rank`'s copy of the buffer and of its flag line as addressable
+ * from this process (tests; diagnostics).  cp_symmetric_free (collective) or cp_comm_destroy
+ * releases the buffers.  Errors: CP_ERR_ARG for a pointer that is not a symmetric buffer of `comm`;
+ * CUDA/NCCL errors as CP_ERR_CUDA/CP_ERR_NCCL. */
+#define CP_GATHER_CHUNKS 256
 int cp_symmetric_alloc(cp_comm comm, size_t bytes, void** local_out);
 int cp_symmetric_free(cp_comm comm, void* local);
 int cp_symmetric_wait(cp_comm comm, void* local, void* stream);
+int cp_symmetric_peer(cp_comm comm, void* local, int32_t rank, void** data, uint32_t** flags);
 
 /* ---------------------------------------------------------------- conv layer */
 typedef struct {
@@ -238,10 +265,14 @@ int conv_part_backward_filter(cp_layer layer, const float* dy_gathered, const ui
 
 /* conv_part_timing — enable (1) / disable (0) per-pass timing of this layer's tensor-core GEMM
  * launches: CUDA events recorded on the launching stream immediately before and after the GEMM
- * kernel (external records, so they also time inside a captured CUDA graph).
+ * kernel (external records, so they also time inside a captured CUDA graph); with a fused gather
+ * input, the forward kernel also stamps (%globaltimer, in the workspace) the window from its first
+ * push chunk claimed to its last chunk's arrival released.
  * conv_part_kernel_time — duration in ms of the last recorded GEMM of `pass` (0 forward,
- * 1 backward-data, 2 backward-filter); the caller synchronizes first.  CP_ERR_STATE if timing is
- * off; a CUDA error if that pass never ran since enabling.  (bench.py's roofline measurement) */
+ * 1 backward-data, 2 backward-filter), or 3: the last fused gather push window (reads the stamps
+ * from the device: blocking).  The caller synchronizes first.  CP_ERR_STATE if timing is off or
+ * (pass 3) no push was recorded; a CUDA error if that pass never ran since enabling.  (bench.py's
+ * roofline and NVLink measurements) */
 int conv_part_timing(cp_layer layer, int32_t enable);
 int conv_part_kernel_time(cp_layer layer, int32_t pass, float* ms);
 
@@ -322,9 +353,12 @@ int cp_sgd(float* p, const float* g, int64_t n, float lr, void* stream);
 int cp_sgd_multi(float* const* params, const float* const* grads, const int64_t* sizes, int32_t count,
                  float lr, void* stream);
 
-/* In-place sum over all ranks of n floats (NCCL AllReduce on `stream`); the result is identical
- * on every rank.  Used by the partitioned head to sum per-rank partial logits.  comm == NULL or a
- * single rank: no-op. */
+/* In-place sum over all ranks of n floats on `stream`; the result is bitwise identical on every
+ * rank.  Once the communicator holds symmetric memory and n <= 65536, a one-CTA peer-memory kernel:
+ * each rank writes its vector into slot [rank] of every peer's scratch (double-buffered by epoch
+ * parity), raises its epoch flag, waits for all peers' flags and sums the slots in ascending rank
+ * order; otherwise NCCL AllReduce.  Used by the partitioned head to sum per-rank partial logits.
+ * comm == NULL or a single rank: no-op. */
 int cp_allreduce_sum(cp_comm comm, float* buf, int64_t n, void* stream);
 
 #ifdef __cplusplus

@@ -29,8 +29,9 @@ EXPORTS = [
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
     "cp_allreduce_sum", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait", "conv_part_timing", "conv_part_kernel_time",
-    "cp_sgd_multi", "cp_lrn_pool_forward", "cp_lrn_pool_backward",
+    "cp_sgd_multi", "cp_lrn_pool_forward", "cp_lrn_pool_backward", "cp_comm_create_loopback", "cp_symmetric_peer",
 ]
+CP_GATHER_CHUNKS = 256   # convpart.h: a complete gather block raises its arrival counter to this
 
 
 class cp_partition(ctypes.Structure):
@@ -120,6 +121,8 @@ def lib():
             "cp_symmetric_alloc": [P, SZ, ctypes.POINTER(P)],
             "cp_symmetric_free": [P, P],
             "cp_symmetric_wait": [P, P, P],
+            "cp_comm_create_loopback": [I32, ctypes.POINTER(P)],
+            "cp_symmetric_peer": [P, P, I32, ctypes.POINTER(P), ctypes.POINTER(P)],
             "conv_part_timing": [P, I32],
             "cp_sgd_multi": [ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(I64), I32, ctypes.c_float, P],
             "cp_lrn_pool_forward": [P, I32, I32, I32, pp, I32, ctypes.c_float, ctypes.c_float, ctypes.c_float,
@@ -193,6 +196,20 @@ def cp_comm_create(uid: bytes, rank: int, world: int):
 
 def cp_comm_destroy(h):
     _call("cp_comm_destroy", h)
+
+
+def cp_comm_create_loopback(world):
+    """`world` simulated ranks on the current GPU (tests of the fused paths): one handle per rank."""
+    arr = (ctypes.c_void_p * world)()
+    _call("cp_comm_create_loopback", int(world), arr)
+    return [ctypes.c_void_p(arr[r]) for r in range(world)]
+
+
+def cp_symmetric_peer(comm, local_ptr, rank):
+    """(data pointer, flag-line pointer) of rank `rank`'s copy of a symmetric buffer, as ints."""
+    d, f = ctypes.c_void_p(), ctypes.c_void_p()
+    _call("cp_symmetric_peer", comm, ctypes.c_void_p(local_ptr), int(rank), ctypes.byref(d), ctypes.byref(f))
+    return d.value, f.value
 
 
 # ---------------------------------------------------------------- layers

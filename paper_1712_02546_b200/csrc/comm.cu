@@ -15,6 +15,7 @@
 
 #include "kernels.cuh"
 
+#include <functional>
 #include <map>
 
 // A symmetric buffer: the same-sized allocation on every rank, each rank holding peer pointers
@@ -23,6 +24,19 @@ struct SymBuf {
   size_t bytes, flag_off;
   int64_t own_off = -1, own_elems = 0;   // this rank's block (floats), recorded by its producer
   void* peers[CP_MAX_RANKS];  // peers[rank] = own pointer
+  int index = -1;             // loopback: allocation sequence number (peers resolved by it)
+};
+
+// Loopback group (tests on one GPU): `world` simulated ranks in one process, each with its own
+// cp_comm handle.  Symmetric buffers are plain allocations on the current device; the k-th
+// allocation of every handle forms one symmetric buffer (peers resolved by index).  No NCCL.
+struct LoopGroup {
+  int world = 0, alive = 0;
+  std::vector<std::vector<void*>> bufs;   // [allocation index][rank]
+  std::vector<void*> ctl;                  // control line per rank
+  // comm-stream tails of the fused reduce-scatter, enqueued once every rank issued its compute
+  std::vector<cudaEvent_t> done;
+  std::vector<std::function<int(const std::vector<cudaEvent_t>&)>> pending;
 };
 
 struct cp_comm_s {
@@ -37,6 +51,8 @@ struct cp_comm_s {
   // one-shot AllReduce scratch (symmetric): [parity][source rank][kArMax] floats
   float* ar = nullptr;
   float* ar_peer[CP_MAX_RANKS] = {};
+  LoopGroup* loop = nullptr;      // loopback handle (cp_comm_create_loopback), else NCCL
+  int sym_count = 0;              // loopback: symmetric allocations made through this handle
 };
 constexpr int kCtlEpoch = 16, kCtlOne = 17, kCtlChunks = 18, kCtlArFlags = 32, kCtlArEpoch = 48, kCtlWords = 64;
 constexpr int64_t kArMax = 1 << 16;   // one-shot AllReduce capacity (floats)
@@ -77,10 +93,54 @@ extern "C" int cp_comm_create(const uint8_t id[128], int32_t rank, int32_t world
   return CP_OK;
 }
 
+// P simulated ranks of one process on the current GPU (tests of the fused peer-memory paths).
+extern "C" int cp_comm_create_loopback(int32_t world, cp_comm* out) {
+  if (!out) CP_FAIL(CP_ERR_ARG, "cp_comm_create_loopback: null pointer");
+  if (world < 1 || world > CP_MAX_RANKS) CP_FAIL(CP_ERR_CONFIG, "cp_comm_create_loopback: world out of [1,16]");
+  auto* g = new LoopGroup{};
+  g->world = world;
+  g->alive = world;
+  g->ctl.assign(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    auto* c = new cp_comm_s{};
+    c->comm = nullptr;
+    c->rank = r;
+    c->world = world;
+    c->loop = g;
+    out[r] = c;
+  }
+  return CP_OK;
+}
+
 static int sym_map(cp_comm c, size_t bytes, void** local_out, SymBuf& sb);
 
 extern "C" int cp_symmetric_alloc(cp_comm c, size_t bytes, void** local_out) {
   if (!c || !local_out || bytes == 0) CP_FAIL(CP_ERR_ARG, "cp_symmetric_alloc: bad arguments");
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    if (!c->ctl) {
+      void* p = nullptr;
+      CP_CUDA(cudaMalloc(&p, kCtlWords * 4));
+      CP_CUDA(cudaMemset(p, 0, kCtlWords * 4));
+      const uint32_t consts[2] = {1u, (uint32_t)cp::kGatherChunks};
+      CP_CUDA(cudaMemcpy((uint32_t*)p + kCtlOne, consts, 8, cudaMemcpyHostToDevice));
+      c->ctl = (uint32_t*)p;
+      g.ctl[c->rank] = p;
+    }
+    SymBuf sb{};
+    sb.bytes = bytes;
+    sb.flag_off = (bytes + 255) / 256 * 256;
+    void* mine = nullptr;
+    CP_CUDA(cudaMalloc(&mine, sb.flag_off + 256));
+    CP_CUDA(cudaMemset(mine, 0, sb.flag_off + 256));
+    sb.index = c->sym_count++;
+    if ((int)g.bufs.size() <= sb.index) g.bufs.resize(sb.index + 1, std::vector<void*>(g.world, nullptr));
+    g.bufs[sb.index][c->rank] = mine;
+    for (int q = 0; q < c->world; ++q) sb.peers[q] = q == c->rank ? mine : nullptr;   // resolved on use
+    c->sym[mine] = sb;
+    *local_out = mine;
+    return CP_OK;
+  }
   if (!c->ctl) {   // first symmetric allocation (collective): the control line
     SymBuf cb{};
     void* p = nullptr;
@@ -138,6 +198,11 @@ static int sym_map(cp_comm c, size_t bytes, void** local_out, SymBuf& sb) {
 // exported allocation (no rank may still hold a mapping of memory that is being freed).
 static void sym_release(cp_comm c, void* local, SymBuf& sb) {
   cudaDeviceSynchronize();
+  if (c->loop) {   // simulated ranks: no mappings, no cross-rank barrier
+    if (sb.index >= 0 && sb.index < (int)c->loop->bufs.size()) c->loop->bufs[sb.index][c->rank] = nullptr;
+    cudaFree(local);
+    return;
+  }
   for (int p = 0; p < c->world; ++p)
     if (p != c->rank && sb.peers[p]) cudaIpcCloseMemHandle(sb.peers[p]);
   if (c->barrier_word && ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, 0) ==
@@ -157,6 +222,15 @@ extern "C" int cp_symmetric_free(cp_comm c, void* local) {
 
 extern "C" int cp_comm_destroy(cp_comm c) {
   if (!c) return CP_OK;
+  if (c->loop) {
+    for (auto& kv : c->sym) sym_release(c, kv.first, kv.second);
+    c->sym.clear();
+    if (c->ctl) cudaFree(c->ctl);
+    c->loop->ctl[c->rank] = nullptr;
+    if (--c->loop->alive == 0) delete c->loop;
+    delete c;
+    return CP_OK;
+  }
   // every rank holds the same number of symmetric buffers, so the per-buffer barriers pair up
   for (auto& kv : c->sym) sym_release(c, kv.first, kv.second);
   c->sym.clear();
@@ -177,8 +251,29 @@ extern "C" int cp_comm_destroy(cp_comm c) {
   return CP_OK;
 }
 
+// Rank `rank`'s copy of a symmetric buffer and its arrival-flag line, as addressable from this
+// process (the local copy, a CUDA-IPC mapping of a peer's, or a simulated rank's allocation).
+extern "C" int cp_symmetric_peer(cp_comm c, void* local, int32_t rank, void** data, uint32_t** flags) {
+  if (!c || !local || !data || rank < 0 || rank >= c->world) CP_FAIL(CP_ERR_ARG, "cp_symmetric_peer: bad arguments");
+  void* peers[CP_MAX_RANKS];
+  uint32_t* fl[CP_MAX_RANKS];
+  if (c->world == 1) {
+    auto it = c->sym.find(local);
+    if (it == c->sym.end()) CP_FAIL(CP_ERR_ARG, "cp_symmetric_peer: not a symmetric buffer");
+    *data = local;
+    if (flags) *flags = (uint32_t*)((char*)local + it->second.flag_off);
+    return CP_OK;
+  }
+  if (!cp::comm_symmetric_peers(c, local, peers, fl))
+    CP_FAIL(CP_ERR_ARG, "cp_symmetric_peer: not a symmetric buffer (or a simulated rank has not allocated it yet)");
+  *data = peers[rank];
+  if (flags) *flags = fl[rank];
+  return CP_OK;
+}
+
 extern "C" int cp_symmetric_wait(cp_comm c, void* local, void* stream) {
   if (!c || c->world == 1) return CP_OK;
+  if (c->loop) CP_FAIL(CP_ERR_UNSUPPORTED, "cp_symmetric_wait: not available on a loopback communicator");
   void* peers[CP_MAX_RANKS];
   uint32_t* flags[CP_MAX_RANKS];
   if (!cp::comm_symmetric_peers(c, local, peers, flags)) CP_FAIL(CP_ERR_ARG, "cp_symmetric_wait: not a symmetric buffer");
@@ -235,6 +330,7 @@ __global__ void __launch_bounds__(512) oneshot_allreduce_kernel(float* buf, int 
 extern "C" int cp_allreduce_sum(cp_comm c, float* buf, int64_t n, void* stream) {
   if (!c || c->world == 1 || n == 0) return CP_OK;
   if (!buf || n < 0) CP_FAIL(CP_ERR_ARG, "cp_allreduce_sum: bad arguments");
+  if (c->loop) CP_FAIL(CP_ERR_UNSUPPORTED, "cp_allreduce_sum: not available on a loopback communicator");
   if (c->ctl && n <= kArMax) {
     if (!c->ar) {   // collective lazy allocation - not while a graph is being captured
       cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
@@ -278,6 +374,7 @@ int comm_check_plan(cp_comm c, const Layer& L) {
     CP_FAIL(CP_ERR_CONFIG, "conv_part_create: desc rank/world " + std::to_string(L.d.rank) + "/" +
                                std::to_string(L.d.world) + " vs communicator " + std::to_string(c->rank) +
                                "/" + std::to_string(c->world));
+  if (c->loop) return CP_OK;   // simulated ranks: the caller builds every rank's map itself
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](int64_t v) { h = (h ^ (uint64_t)v) * 1099511628211ull; };
   const cp_partition* ps[2] = {&L.d.out_part, &L.d.in_part};
@@ -335,10 +432,37 @@ int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks
   return CP_OK;
 }
 
+bool comm_is_loopback(cp_comm c) { return c && c->loop; }
+
+// Loopback: the comm-stream tail of rank r's fused reduce-scatter waits for the slots every
+// simulated rank stores - on one GPU those are later launches of the same process, so the tails
+// are held back until every rank issued its compute (`done` recorded after its dgrad + signal),
+// then enqueued in rank order behind all of them: no kernel ever waits on a later launch.
+int comm_loopback_defer(cp_comm c, cudaEvent_t done, std::function<int(const std::vector<cudaEvent_t>&)> tail) {
+  LoopGroup& g = *c->loop;
+  g.done.push_back(done);
+  g.pending.push_back(std::move(tail));
+  if ((int)g.pending.size() < g.world) return CP_OK;
+  std::vector<cudaEvent_t> all;
+  all.swap(g.done);
+  auto fns = std::move(g.pending);
+  g.pending.clear();
+  for (auto& f : fns) CP_TRY(f(all));
+  return CP_OK;
+}
+
 bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags) {
   if (!c || c->world == 1) return false;
   auto it = c->sym.find(const_cast<void*>(local));
   if (it == c->sym.end()) return false;
+  if (c->loop) {   // resolve the other simulated ranks' copies of this allocation
+    const int k = it->second.index;
+    if (k < 0 || k >= (int)c->loop->bufs.size()) return false;
+    for (int q = 0; q < c->world; ++q) {
+      if (!c->loop->bufs[k][q]) return false;
+      it->second.peers[q] = c->loop->bufs[k][q];
+    }
+  }
   for (int p = 0; p < c->world; ++p) {
     peers[p] = it->second.peers[p];
     if (flags) flags[p] = (uint32_t*)((char*)it->second.peers[p] + it->second.flag_off);
@@ -370,6 +494,7 @@ __global__ void flag_barrier_kernel(CtlPtrs peer, uint32_t* mine, int me, int wo
 
 int comm_barrier(cp_comm c, cudaStream_t s) {
   if (!c || c->world == 1) return CP_OK;
+  if (c->loop) return CP_OK;   // simulated ranks share one GPU and the caller's stream order
   if (!c->ctl) {
     CP_NCCL(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
     return CP_OK;
@@ -398,6 +523,7 @@ static bool equal_widths(const Blocks& g) {
 
 int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s) {
   if (!c || c->world == 1) return CP_OK;
+  if (c->loop) CP_FAIL(CP_ERR_UNSUPPORTED, "loopback communicator: NCCL collectives unavailable (fused paths only)");
   CP_TRY(async_error(c));
   if (equal_widths(g)) {
     const size_t cnt = (size_t)(g.start[1] - g.start[0]);
@@ -421,6 +547,7 @@ int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s
 
 int comm_sum_blocks(cp_comm c, float* buf, const Blocks& g, int dx_mode, cudaStream_t s) {
   if (!c || c->world == 1 || dx_mode == CP_DX_LOCAL) return CP_OK;
+  if (c->loop) CP_FAIL(CP_ERR_UNSUPPORTED, "loopback communicator: NCCL collectives unavailable (fused paths only)");
   CP_TRY(async_error(c));
   if (dx_mode == CP_DX_ALLREDUCE) {
     CP_NCCL(ncclAllReduce(buf, buf, (size_t)g.start[g.n], ncclFloat, ncclSum, c->comm, s));

@@ -130,6 +130,11 @@ __device__ __forceinline__ void wait_flag_sys(const uint32_t* p, uint32_t target
     if (clock64() - t0 > (1ll << 35)) __trap();
   }
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -152,6 +157,8 @@ struct Layer {
   size_t ws_xcol, ws_z, ws_dy, ws_split, ws_dbpart, ws_total;
   size_t off_xcol, off_z, off_dy, off_split, off_dbpart;
   size_t off_x16, off_w16, off_dy16;   // bf16 operand copies (CP_MATH_BF16 only)
+  size_t off_stamp;                    // 2 x u64 globaltimer stamps of the fused gather push (timing only)
+  void* ws_last;                       // workspace of the last forward that recorded push stamps
   int dy_ready;           // epilogue-backward already computed for this step
   const void* dy_key[3];
   cudaEvent_t ev_compute, ev_comm;

@@ -1,10 +1,13 @@
 // kernels.cuh — internal launchers (namespace cp).  All enqueue on `s` and count launches.
 #pragma once
+#include <functional>
+#include <vector>
+
 #include "common.cuh"
 
 namespace cp {
 
-constexpr int kGatherChunks = 256;   // pieces of a kernel-pushed gather block (= the receivers' target)
+constexpr int kGatherChunks = CP_GATHER_CHUNKS;   // pieces of a kernel-pushed gather block (= the receivers' target)
 
 // ---- layout / elementwise (kernels_simt.cu)
 int launch_im2col(const Layer& L, const float* x, float* xcol, bool round_tf32, cudaStream_t s);
@@ -34,6 +37,8 @@ int launch_wait_flags(const uint32_t* flags, int n, int self, cudaStream_t s, bo
 
 // ---- tcgen05 / TMA tensor-core convolutions (kernels_tc.cu)
 size_t tc_workspace_bytes(const Layer& L);
+// create-time validation of the tensor-core plans (every launch-time rejection, checked up front)
+int tc_validate(const Layer& L);
 // fused all-gather -> GEMM (forward over a symmetric gathered input): the kernel's warp 3 pushes
 // this rank's input block (src, n4 float4) into each peer's copy dst[k] in `chunks` pieces, one
 // release-add on the peer's arrival counter cnt[k] per piece; the GEMM waits for `chunks` arrivals
@@ -42,9 +47,12 @@ struct GatherPush {
   const float* src;
   float* dst[CP_MAX_RANKS];
   uint32_t* cnt[CP_MAX_RANKS];
+  uint32_t* claim;   // chunk claim counter, zero at launch (own flag line word kClaimWord)
+  unsigned long long* stamp = nullptr;  // timing: [0] min start, [1] max end (globaltimer ns) of the push
   int n, chunks;
   long long n4;
 };
+constexpr int kClaimWord = 32;   // flag-line word of a symmetric gathered input: the push claim counter
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved,
            void* ws, cudaStream_t s, float* const* peer_blocks = nullptr, int npeers = 0,
            const uint32_t* arrive = nullptr, const GatherPush* gp = nullptr);
@@ -76,5 +84,10 @@ int comm_barrier(cp_comm c, cudaStream_t s);
 // (value 1, or kGatherChunks when `chunks`: stands in for a kernel push of zero bytes)
 int comm_signal_ce(cp_comm c, uint32_t* const* flags, int n, int slot, cudaStream_t s, bool chunks = false);
 int comm_sum_blocks(cp_comm c, float* buf, const Blocks& g, int dx_mode, cudaStream_t s);
+// loopback communicator (P simulated ranks on one GPU, cp_comm_create_loopback)
+bool comm_is_loopback(cp_comm c);
+// hold `tail` (the comm-stream part of a fused reduce-scatter) until every simulated rank issued its
+// compute (`done` recorded after it), then run all tails in rank order with every rank's `done`
+int comm_loopback_defer(cp_comm c, cudaEvent_t done, std::function<int(const std::vector<cudaEvent_t>&)> tail);
 
 }  // namespace cp

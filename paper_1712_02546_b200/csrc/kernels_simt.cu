@@ -1055,6 +1055,7 @@ int cp_pack_fc_weights(const float* wfc, int32_t O, int32_t Hp, int32_t Wp, cons
   // packed per row into gather feature order: reuse the activation pack with B=O, Bp irrelevant.
   Blocks g = make_blocks(*part, Hp, Wp, 32);
   const int64_t total = (int64_t)O * Hp * Wp * g.Cg;
+  if (total == 0) return CP_OK;   // a rank without channels in the last layer (partitioned head)
   pack_fc_kernel<<<grid1d(total, 256), 256, 0, (cudaStream_t)stream>>>(wfc, out, g, O, part->num_k, total);
   CP_LAUNCHED();
   return CP_OK;
@@ -1067,6 +1068,7 @@ int cp_unpack_fc_weights(const float* wg, int32_t O, int32_t Hp, int32_t Wp, con
   Blocks g = make_blocks(*part, Hp, Wp, 32);
   const int64_t PW = (int64_t)Hp * Wp;
   const int64_t total = (int64_t)O * part->num_k * PW;
+  if (total == 0) return CP_OK;
   unpack_fc_kernel<<<grid1d(total, 256), 256, 0, (cudaStream_t)stream>>>(wg, out, g, part->num_k, total);
   CP_LAUNCHED();
   return CP_OK;
@@ -1081,8 +1083,10 @@ int cp_fc_forward(const float* x, int32_t B, int32_t Hp, int32_t Wp, const cp_pa
   const int PW = Hp * Wp, nsc = fc_nsc(g), U = g.n * PW * nsc;
   float* part_buf = (float*)ws;
   cudaStream_t s = (cudaStream_t)stream;
-  fc_fwd_partial<<<dim3(U, (g.Bp + 127) / 128), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
-  CP_LAUNCHED();
+  if (U > 0) {   // U == 0: no features on this rank (partitioned head) -> logits = bias (or 0)
+    fc_fwd_partial<<<dim3(U, (g.Bp + 127) / 128), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
+    CP_LAUNCHED();
+  }
   fc_fwd_reduce<<<cdiv((int64_t)B * O, 32), dim3(32, 32), 0, s>>>(part_buf, bfc, logits, U, g.Bp, B, O);
   CP_LAUNCHED();
   return CP_OK;
@@ -1106,7 +1110,9 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
   const int PW = Hp * Wp;
   cudaStream_t s = (cudaStream_t)stream;
   if (dx || dwg || dbfc) {
-    fc_bwd_fused<<<g.n * PW * fc_nsc(g), 256, 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, fc_nsc(g));
+    // (no features on this rank: one chunk per position, every CTA returns after CTA 0's dbfc)
+    const int nsc = std::max(1, fc_nsc(g));
+    fc_bwd_fused<<<g.n * PW * nsc, 256, 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, nsc);
     CP_LAUNCHED();
   }
   (void)ws;

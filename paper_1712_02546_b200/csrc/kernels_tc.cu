@@ -138,7 +138,9 @@ struct TcParams {
   const float* push_src;
   float* push_dst[CP_MAX_RANKS];
   uint32_t* push_cnt[CP_MAX_RANKS];
-  int npush, push_chunks;
+  unsigned long long* push_stamp;  // timing only: globaltimer window of the push (atomic min start / max end)
+  uint32_t* push_claim;    // chunk claim counter (zero at launch): any resident CTA's warp 3 takes the next
+  int npush, push_chunks;  // (peer, chunk) pair, so the gather completes as long as one CTA runs per rank
   long long push_n4;
 };
 
@@ -750,12 +752,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     // peers in the order they consume this block (host-sorted: the peer that needs it soonest
     // first), all CTAs on one peer at a time so each peer's block completes as early as possible;
     // 8 float4 loads in flight per lane (the source block is L2-resident: just written)
+    // Chunks are claimed dynamically (one atomic per chunk), not assigned by blockIdx: a peer's GEMM
+    // spins on these arrivals, so the push must not depend on every CTA of this grid being resident
+    // (other streams' kernels, MPS / green-context SM limits) - one running CTA finishes the gather.
     if (p.npush > 0) {
       const long long per = (p.push_n4 + p.push_chunks - 1) / p.push_chunks;
       const float4* src = reinterpret_cast<const float4*>(p.push_src);
-      for (int k = 0; k < p.npush; ++k) {
+      const int total = p.npush * p.push_chunks;
+      unsigned long long t_first = 0, t_last = 0;
+      for (;;) {
+        int idx = 0;
+        if (lane == 0) idx = (int)atomicAdd(p.push_claim, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= total) break;
+        if (p.push_stamp && !t_first) t_first = globaltimer_ns();
+        const int k = idx / p.push_chunks, c = idx - k * p.push_chunks;
         float4* dst = reinterpret_cast<float4*>(p.push_dst[k]);
-        for (int c = blockIdx.x; c < p.push_chunks; c += gridDim.x) {
+        {
           const long long b = (long long)c * per, e = min(p.push_n4, b + per);
           for (long long i = b + lane; i < e; i += 256) {
             float4 v[8];
@@ -770,6 +783,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           __syncwarp();
           if (lane == 0) red_add_release_sys(p.push_cnt[k], 1u);
         }
+        if (p.push_stamp) t_last = globaltimer_ns();
+      }
+      if (p.push_stamp && t_first && lane == 0) {
+        atomicMin(p.push_stamp, t_first);
+        atomicMax(p.push_stamp + 1, t_last);
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -1011,7 +1029,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         else mbar_arrive(&tempty[acc]);
       }
     }
-    if (PASS == PASS_FWD && p.npeers > 0) __threadfence_system();  // peer stores performed before exit
+    // peer stores (fused gather from the epilogue, fused dX reduce-scatter) performed system-wide before
+    // exit; the flag release that follows in the next launch then orders after them
+    if ((PASS == PASS_FWD && p.npeers > 0) || (PASS == PASS_DGRAD && p.fused_dx)) __threadfence_system();
   }
   tc_fence_before();
   if (CG == 2) cluster_sync(); else __syncthreads();
@@ -1476,7 +1496,10 @@ static Plan fwd_plan(const Layer& L, TcParams& p) {
   // Balanced N tiles: Kc split into T equal tiles (width a multiple of 16 / 8).  Choose T by
   // rounds of CTA groups x per-chunk time, the latter ~ bytes staged per chunk (A 16 KB + B
   // columns): the kernel is bound by operand delivery, not by MMA issue.
-  {
+  if (L.Kc == 0) {   // a rank without kernels in this layer: no forward GEMM units
+    p.nw = BN;
+    w.numN = 0;
+  } else {
     const int gran = CG == 2 ? 16 : 8, groups = num_sms() / CG;
     double best = 1e300;
     int bestT = (L.Kc + BN - 1) / BN;
@@ -1669,6 +1692,30 @@ static bool plan_stream_tail(TcParams& p, int G, int chunks, int min_chunks, sho
   return true;
 }
 
+// Create-time check of every condition the three tensor-core passes would reject at launch, so a
+// plan that cannot run fails in conv_part_create - never after a rank has entered a cross-rank
+// barrier or started pushing its gather block (the peers would wait for it).
+int tc_validate(const Layer& L) {
+  if ((L.Ho & 1) || (L.Wo & 1))
+    CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 forward needs an even conv output grid (2x2 window tiles), got " +
+                                    std::to_string(L.Ho) + "x" + std::to_string(L.Wo));
+  if (!L.images && L.Kr > 0 && L.Kc > 0) {
+    if ((L.H & 1) || (L.W & 1)) CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 dgrad needs an even input grid");
+    TcParams p{};
+    fill_common(p, L);
+    if (dgrad_plan(L, p).numN < 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many dgrad N tiles");
+    if (L.d.math == CP_MATH_BF16)
+      for (int r = 0; r < L.in.n; ++r)
+        if (L.in.coff[r] % op_elems(L)) CP_FAIL(CP_ERR_UNSUPPORTED, "bf16 dgrad needs input block offsets in multiples of 64");
+  }
+  if (L.Kr > 0) {
+    TcParams p{};
+    fill_common(p, L);
+    if (wgrad_plan(L, p).numN <= 0) CP_FAIL(CP_ERR_UNSUPPORTED, "too many wgrad N tiles");
+  }
+  return CP_OK;
+}
+
 int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s) {
   if (!L.timing) return CP_OK;
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
@@ -1795,6 +1842,8 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     }
     p.push_n4 = gp->n4;
     p.push_chunks = gp->chunks;
+    p.push_claim = gp->claim;
+    p.push_stamp = gp->stamp;
     p.arrive_target = (uint32_t)gp->chunks;
   }
   float* part = (float*)((char*)ws + L.off_split);

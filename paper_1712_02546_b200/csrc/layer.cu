@@ -94,6 +94,7 @@ static int derive(Layer& L, const cp_conv_desc& d) {
       for (int r = 0; r < d.in_part.n_ranks; ++r)
         if (d.in_part.k_width[r] % 64) CP_FAIL(CP_ERR_CONFIG, "bf16 mode: in_part widths must be multiples of 64");
   }
+  if (d.math != CP_MATH_FP32_SIMT) CP_TRY(tc_validate(L));
   // workspace carve-up
   size_t off = 0;
   L.off_xcol = off; L.ws_xcol = L.images ? al256((size_t)L.Ho * L.Wo * L.Bp * L.Kcol * 4) : 0; off += L.ws_xcol;
@@ -108,6 +109,7 @@ static int derive(Layer& L, const cp_conv_desc& d) {
     L.off_w16 = off; off += al256((size_t)L.Kr * L.Ktot * 2 + 256);
     L.off_dy16 = off; off += al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 2 + 256);
   }
+  L.off_stamp = off; off += 256;
   L.ws_total = off + 256;
   L.dy_ready = 0;
   return CP_OK;
@@ -276,6 +278,13 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
       gp.src = x + L->in.start[me];
       gp.n4 = n / 4;
       gp.chunks = kGatherChunks;
+      gp.claim = iflags[me] + kClaimWord;
+      if (L->timing) {   // push window: first chunk claimed -> last chunk's arrival released
+        gp.stamp = (unsigned long long*)WS(ws, L->off_stamp);
+        L->ws_last = ws;
+        CP_CUDA(cudaMemsetAsync(gp.stamp, 0xff, 8, s));
+        CP_CUDA(cudaMemsetAsync(gp.stamp + 1, 0, 8, s));
+      }
       // peer q walks its input blocks from its own upwards, so it needs this rank's block after
       // (me - q) mod P blocks: push to the soonest consumer first
       for (int d = 1; d < L->d.world; ++d) {
@@ -308,7 +317,8 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
       CP_TRY(launch_relu_pool(*L, z, yb, saved, false, s));
     }
   }
-  if (sym_in) CP_CUDA(cudaMemsetAsync((void*)arrive, 0, CP_MAX_RANKS * sizeof(uint32_t), s));
+  // reset the arrival counters and the push claim counter (the whole 256 B flag line)
+  if (sym_in) CP_CUDA(cudaMemsetAsync((void*)arrive, 0, 256, s));
   if (push_in_epilogue) {
     CP_TRY(launch_signal_peers(signal, npeers, me, s));
   } else if (gathered_out && !sym_out) {
@@ -365,17 +375,26 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
       for (int q = 0; q < L->in.n; ++q) CP_TRY(launch_fill(dst[q], 0.f, L->in.start[q + 1] - L->in.start[q], s));
     }
     CP_TRY(launch_signal_peers(signal, ns, me, s));
-    CP_TRY(fork_comm(*L, s, cs));
-    CP_TRY(launch_wait_flags(pflags[me], L->d.world, me, cs));
-    CP_TRY(launch_sum_slots(dx + slots0, mb, L->d.world, dx + L->in.start[me],
-                            L->in.start[me + 1] - L->in.start[me], cs));
-    CP_CUDA(cudaMemsetAsync(pflags[me], 0, CP_MAX_RANKS * sizeof(uint32_t), cs));
-    if (async && cs != s) {
-      CP_CUDA(cudaEventRecord(L->ev_comm, cs));
-    } else {
-      CP_TRY(join_comm(*L, s, cs));
-    }
-    return CP_OK;
+    CP_CUDA(cudaEventRecord(L->ev_compute, s));
+    // comm-stream tail: wait for every peer's slot, sum the slots in rank order into the own block
+    uint32_t* own_flags = pflags[me];
+    const int world = L->d.world;
+    const int64_t n_own = L->in.start[me + 1] - L->in.start[me];
+    float* slots = dx + slots0;
+    float* own = dx + L->in.start[me];
+    cp_layer_s* Lp = L;
+    auto tail = [=](const std::vector<cudaEvent_t>& computed) -> int {
+      for (cudaEvent_t e : computed) CP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+      CP_TRY(launch_wait_flags(own_flags, world, me, cs));
+      CP_TRY(launch_sum_slots(slots, mb, world, own, n_own, cs));
+      CP_CUDA(cudaMemsetAsync(own_flags, 0, CP_MAX_RANKS * sizeof(uint32_t), cs));
+      CP_CUDA(cudaEventRecord(Lp->ev_comm, cs));
+      if (!(async && cs != s)) CP_CUDA(cudaStreamWaitEvent(s, Lp->ev_comm, 0));
+      return CP_OK;
+    };
+    // loopback (simulated ranks on one GPU): tails run once every rank issued its dgrad
+    if (comm_is_loopback(L->comm)) return comm_loopback_defer(L->comm, L->ev_compute, tail);
+    return tail(std::vector<cudaEvent_t>{L->ev_compute});
   }
   if (L->d.math != CP_MATH_FP32_SIMT && !L->images) {
     CP_TRY(tc_dgrad(*L, dYg, wg, dx, ws, s));
@@ -433,8 +452,16 @@ int conv_part_timing(cp_layer L, int32_t enable) {
 }
 
 int conv_part_kernel_time(cp_layer L, int32_t pass, float* ms) {
-  if (!L || !ms || pass < 0 || pass > 2) CP_FAIL(CP_ERR_ARG, "conv_part_kernel_time: bad arguments");
+  if (!L || !ms || pass < 0 || pass > 3) CP_FAIL(CP_ERR_ARG, "conv_part_kernel_time: bad arguments");
   if (!L->timing) CP_FAIL(CP_ERR_STATE, "conv_part_kernel_time: timing not enabled");
+  if (pass == 3) {   // fused gather push window (globaltimer stamps in the workspace; blocking read)
+    if (!L->ws_last) CP_FAIL(CP_ERR_STATE, "conv_part_kernel_time: no forward with a fused gather push yet");
+    unsigned long long t[2];
+    CP_CUDA(cudaMemcpy(t, (char*)L->ws_last + L->off_stamp, sizeof(t), cudaMemcpyDeviceToHost));
+    if (t[0] == ~0ull || t[1] < t[0]) CP_FAIL(CP_ERR_STATE, "conv_part_kernel_time: no push recorded");
+    *ms = (float)((double)(t[1] - t[0]) * 1e-6);
+    return CP_OK;
+  }
   CP_CUDA(cudaEventElapsedTime(ms, L->ev_t[pass][0], L->ev_t[pass][1]));
   return CP_OK;
 }

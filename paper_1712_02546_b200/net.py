@@ -41,10 +41,11 @@ class PartitionedNet:
         rank-local, each rank owns the FC columns of its channels, partial logits are summed with
         one AllReduce (identical logits/loss on every rank; no AllGather of the last layer).
         fused: B200 collective fusion - every all-gathered conv output and every dX is a
-        symmetric (peer-mapped) buffer: the TF32 forward epilogue stores its output block into all ranks'
-        copies over NVLink (the next layer's GEMM consumes its own block first and each peer block when
-        its arrival flag is set) and the dgrad epilogue stores each input block's partial dX into its
-        owner's receive slot (reduce-scatter without an NCCL kernel).
+        symmetric (peer-mapped) buffer: the producer writes its block locally, the consuming layer's TF32
+        forward kernel pushes that block into every peer's copy over NVLink while it computes on its own
+        block first (each peer block is consumed once its arrival counter is complete), and the dgrad
+        epilogue stores each input block's partial dX into its owner's receive slot (reduce-scatter
+        without an NCCL kernel; the owner sums the slots in rank order).
         lrn: None, or LRN parameters {depth, alpha, beta, bias} (convpart.LRN_DEFAULT): every conv layer
         becomes Conv -> bias -> ReLU -> LRN -> Pool (NEXT row f2): the conv runs without
         pooling, its pre-pool output is gathered, every rank runs cp_lrn_pool_forward over all
@@ -115,8 +116,9 @@ class PartitionedNet:
         last = self.head_part
         Fg = h * h * sum(last.k_width[: last.n_ranks])
         self.head = {
-            "wfc": torch.zeros(classes * Fg, device=self.device), "bfc": torch.zeros(classes, device=self.device),
-            "dwfc": torch.zeros(classes * Fg, device=self.device), "dbfc": torch.zeros(classes, device=self.device),
+            # (max(.., 4): a rank without channels in the last layer still holds valid, empty head buffers)
+            "wfc": torch.zeros(max(classes * Fg, 4), device=self.device), "bfc": torch.zeros(classes, device=self.device),
+            "dwfc": torch.zeros(max(classes * Fg, 4), device=self.device), "dbfc": torch.zeros(classes, device=self.device),
             "logits": torch.zeros(batch * classes, device=self.device),
             "dlogits": torch.zeros(batch * classes, device=self.device),
             "loss": torch.zeros(4, device=self.device),
@@ -150,7 +152,8 @@ class PartitionedNet:
             k0, kr = self.parts[-1].k_begin[self.rank], self.parts[-1].k_count[self.rank]
             wfc_np = np.ascontiguousarray(wfc_np.reshape(self.O, -1, self.Hp * self.Wp)[:, k0:k0 + kr])
         wfc = torch.from_numpy(wfc_np.reshape(self.O, -1)).to(self.device)
-        cp.cp_pack_fc_weights(wfc, self.O, self.Hp, self.Wp, self.head_part, self.head["wfc"], stream)
+        if wfc.numel():
+            cp.cp_pack_fc_weights(wfc, self.O, self.Hp, self.Wp, self.head_part, self.head["wfc"], stream)
         self.head["bfc"].copy_(torch.from_numpy(np.ascontiguousarray(params["bfc"], np.float32)))
         torch.cuda.synchronize(self.device)
 
@@ -178,7 +181,9 @@ class PartitionedNet:
         self.labels.copy_(labels.reshape(-1), non_blocking=True)
 
     # ------------------------------------------------------------ one training step
-    def forward(self, stream=None, comm_stream=None):
+    def forward(self, stream=None, comm_stream=None, head=True):
+        """head=False: the conv stage only (every conv layer and its gather; no FC / loss) - bench.py's
+        conv-stage images/s, with backward(head=False) starting from the fixed dA2 in head["da"]."""
         inp = self.x
         for i, L in enumerate(self.layers):
             b = self.buf[i]
@@ -195,6 +200,8 @@ class PartitionedNet:
         last = next((m for m in self.sym if m.tensor.data_ptr() == self.buf[-1]["y"].data_ptr()), None)
         if last is not None and not self.lrn:
             last.wait(stream)   # replicated head reads the gathered last output
+        if not head:
+            return
         bias = hd["bfc"] if (self.head_mode == "replicated" or self.rank == 0) else None
         cp.cp_fc_forward(self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], bias, self.O, hd["logits"],
                          hd["ws"], stream)
@@ -202,10 +209,11 @@ class PartitionedNet:
             cp.cp_allreduce_sum(self.comm, hd["logits"], stream)
         cp.cp_softmax_xent(hd["logits"], self.labels, self.B, self.O, hd["loss"], hd["dlogits"], stream)
 
-    def backward(self, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True):
+    def backward(self, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True, head=True):
         hd = self.head
-        cp.cp_fc_backward(hd["dlogits"], self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], self.O,
-                          self.head_da, hd["dwfc"], hd["dbfc"], hd["ws"], stream)
+        if head:
+            cp.cp_fc_backward(hd["dlogits"], self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"],
+                              self.O, self.head_da, hd["dwfc"], hd["dbfc"], hd["ws"], stream)
         da = hd["da"]
         n = len(self.layers)
         for i in reversed(range(n)):
@@ -231,7 +239,7 @@ class PartitionedNet:
                     cp.conv_part_wait(L, stream)
                 da = b["dx"]
 
-    def sgd(self, lr, stream=None):
+    def sgd(self, lr, stream=None, head=True):
         """SGD on the own conv slices and the head, one fused launch (cp_sgd_multi)."""
         pairs = []
         for i, b in enumerate(self.buf):
@@ -239,14 +247,17 @@ class PartitionedNet:
             ktot = (self.sizes[i].w - 256) // 4 // max(kr, 1) if kr else 0
             pairs.append((b["w"], b["dw"], kr * ktot))
             pairs.append((b["b"], b["db"], kr))
-        pairs.append((self.head["wfc"], self.head["dwfc"]))
-        pairs.append((self.head["bfc"], self.head["dbfc"]))
+        if head:
+            pairs.append((self.head["wfc"], self.head["dwfc"]))
+            pairs.append((self.head["bfc"], self.head["dbfc"]))
         cp.cp_sgd_multi(pairs, lr, stream)
 
-    def step(self, lr=0.01, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True):
-        self.forward(stream, comm_stream)
-        self.backward(dx_mode, stream, comm_stream, overlap)
-        self.sgd(lr, stream)
+    def step(self, lr=0.01, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True, head=True):
+        """One SGD step; head=False: the conv stage with the head replaced by the fixed dA2 in head["da"]
+        (SURVEY §8(d) conv-stage images/s)."""
+        self.forward(stream, comm_stream, head)
+        self.backward(dx_mode, stream, comm_stream, overlap, head)
+        self.sgd(lr, stream, head)
 
     def loss(self):
         return float(self.head["loss"][0].item())

@@ -49,10 +49,21 @@ def main():
             ("eq1+RS+fused+partitioned-head", cp.CP_DX_REDUCE_SCATTER, uneven, "partitioned", True),
             ("skewed+RS+fused+partitioned-head", cp.CP_DX_REDUCE_SCATTER, [1.0] + [12.0] * (world - 1),
              "partitioned", True),
-            ("eq1+AR+fused-gather+partitioned-head", cp.CP_DX_ALLREDUCE, uneven, "partitioned", True)]:
+            ("eq1+AR+fused-gather+partitioned-head", cp.CP_DX_ALLREDUCE, uneven, "partitioned", True),
+            # ranks with zero kernels in a layer: the last rank owns no conv1 kernel (an empty
+            # input block of conv2: empty push, zero partial), rank 0 no conv2 kernel (copy-engine gather)
+            ("zero-kernel-ranks+RS+fused+partitioned-head", cp.CP_DX_REDUCE_SCATTER, "zero", "partitioned", True),
+            ("zero-kernel-ranks+RS+fused+replicated-head", cp.CP_DX_REDUCE_SCATTER, "zero", "replicated", True)]:
         net = synth.NetSpec(kernels=(36, 72), in_hw=20, name="multi")
         B = 40
-        parts = [cp.cp_partition_plan(times, K) for K in net.kernels]
+        if times == "zero":
+            c1 = [36 // (world - 1)] * (world - 1)
+            c1[0] += 36 - sum(c1)
+            c2 = [0] + [72 // (world - 1)] * (world - 1)
+            c2[1] += 72 - sum(c2)
+            parts = [cp.cp_partition.from_counts(c1 + [0]), cp.cp_partition.from_counts(c2)]
+        else:
+            parts = [cp.cp_partition_plan(times, K) for K in net.kernels]
         params = synth.params(net, seed=21, std=0.05, bias_std=0.01)
         x, y = synth.images(B, 3, 20, 20, step=3)
         pn = PartitionedNet(net.kernels, B, parts, rank=rank, comm=comm, device=dev, in_hw=20, head=head,

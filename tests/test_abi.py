@@ -104,3 +104,29 @@ def test_product_path_has_no_oracle_dependency():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", src).replace("oracle/", ""), f
+
+
+def test_create_zero_kernel_ranks_host_side():
+    """conv_part_create's host-side planning (validation, workspace sizing of all three passes) on
+    partitions where a rank owns no kernels of a layer or an input block is empty: it must return a
+    status (CP_OK on a GPU box, CP_ERR_CUDA where no device exists), never crash (a zero-width
+    forward once divided by zero in the N-tile planner)."""
+    from paper_1712_02546_b200 import convpart as cp
+    for c1, c2 in [([36, 0], [40, 32]), ([12, 12, 12], [0, 72, 0]), ([0, 36], [72, 0])]:
+        P = len(c1)
+        p1, p2 = cp.cp_partition.from_counts(c1), cp.cp_partition.from_counts(c2)
+        for r in range(P):
+            for C, H, K, part, inp in [(3, 20, 36, p1, None), (36, 8, 72, p2, p1)]:
+                for math in (cp.CP_MATH_TF32, cp.CP_MATH_FP32_SIMT):
+                    d = cp.cp_conv_desc()
+                    d.batch, d.in_c, d.in_h, d.in_w, d.num_k, d.k_h, d.k_w = 40, C, H, H, K, 5, 5
+                    d.bias, d.relu, d.pool, d.math = 1, 1, 1, math
+                    d.input_kind = cp.CP_INPUT_IMAGES if inp is None else cp.CP_INPUT_GATHER
+                    d.out_part = part
+                    if inp is not None:
+                        d.in_part = inp
+                    d.rank, d.world = r, P
+                    try:
+                        cp.conv_part_destroy(cp.conv_part_create(d, None))
+                    except cp.ConvPartError as e:
+                        assert e.rc == -5, str(e)     # CP_ERR_CUDA: no device here

@@ -127,6 +127,38 @@ def test_backward_parity(orc, math, P, B, align):
     L1.close(); L2.close()
 
 
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("P,B", [(1, 40), (2, 40), (3, 20), (2, 128)])
+def test_image_dgrad_parity(orc, math, P, B):
+    """Row a14: conv_part_backward_data on an image layer (dX of the images, NCHW; S:L62-70 gradInput)
+    vs orc_conv_dgrad, each rank's partial over its own kernels summed in rank order (LOCAL mode
+    stands in for the all-reduce), with decision replay of the GPU's pooling codes."""
+    m = math_id(math)
+    x, w1, b1, _, _ = layer_data(B=B)
+    B, K1 = x.shape[0], w1.shape[0]
+    p1 = parts_for(P, K1)
+    L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
+    L1.load(w1, b1)
+    xd = dev(x)
+    L1.forward(xd)
+    y1, am1 = L1.y_nchw(), L1.argmax_nchw()
+    da1 = synth.normal(y1.shape, 98, 1.0).astype(np.float32)
+    dag = pack(da1, p1)
+    total = None
+    for r in range(P):
+        dx = torch.full((L1.sz[r].dx // 4,), float("nan"), device="cuda")
+        cp.conv_part_backward_data(L1.h[r], dag, L1.saved[r], L1.y, L1.w[r], dx, cp.CP_DX_LOCAL, L1.ws[r])
+        part = dx[: B * 3 * 20 * 20].reshape(B, 3, 20, 20).cpu().numpy().astype(np.float64)
+        if p1.k_count[r] == 0:
+            assert np.all(part == 0)
+        total = part if total is None else total + part
+    dy1 = orc.unpool_relu_bwd(da1.astype(np.float64), am1, y1)
+    ref = orc.conv_dgrad(dy1, w1.astype(np.float64))
+    # TF32 mode rounds dY to tf32 (the tensor-core operand precision) before the fp32 SIMT dgrad
+    assert_close(total, ref, TOL[m], f"conv1 dgrad onto images ({math}, P={P})")
+    L1.close()
+
+
 def test_pack_roundtrip_bitexact(orc):
     g = np.random.default_rng(5)
     for P, counts in [(1, [13]), (3, [5, 0, 9]), (4, [8, 8, 8, 7])]:

@@ -9,6 +9,8 @@
 * the whole training step == torch float64 autograd of the same network
   (an independent library composition), and training makes progress
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -79,6 +81,36 @@ def test_gather_index_map(orc):
     xr = synth.normal((B, C, H, W), 9).astype(np.float64)
     gr = orc.pack_gather(xr, Bp, kb, kc, kw)
     assert np.sort(gr[gr != 0]).tolist() == np.sort(xr.ravel()).tolist()
+
+
+def _read_gather_golden():
+    """tests/golden/gather_layout_example.txt: the hand-written flat gather array."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "gather_layout_example.txt")
+    kv, flat = {}, []
+    with open(path) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if not line:
+                continue
+            if line.startswith("r"):
+                flat += [float(v) for v in line.split(":", 1)[1].split()]
+            else:
+                for tok in line.split():
+                    k, v = tok.split("=")
+                    kv[k] = [int(u) for u in v.split(",")] if "," in v else int(v)
+    return kv, np.array(flat)
+
+
+def test_gather_layout_golden(orc):
+    """Pins orc_pack_gather's (h, w, b, slot) order to a literal, hand-derived array (§8(c)
+    item 9): with H != W and distinct values, an h<->w, b<->w or slot<->b swap changes it."""
+    kv, expected = _read_gather_golden()
+    B, C, H, W, Bp = kv["B"], kv["C"], kv["H"], kv["W"], kv["Bp"]
+    b, c, h, w = np.meshgrid(np.arange(B), np.arange(C), np.arange(H), np.arange(W), indexing="ij")
+    x = (1000 * b + 100 * c + 10 * h + w + 1).astype(np.float64)
+    g = orc.pack_gather(x, Bp, kv["k_begin"], kv["k_count"], kv["k_width"])
+    assert g.size == expected.size == sum(H * W * Bp * kw for kw in kv["k_width"])
+    assert np.array_equal(g, expected)
 
 
 def torch_step(params, x, y, net):
