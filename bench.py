@@ -660,8 +660,8 @@ def main():
                          "peak_source": (pk["source"] if not bf16 else "MEASURED_PEAKS.json bf16") + peak_note,
                          "conv2_pass_ms_alone": per,
                          "conv2_pass_tflops_alone": {k: flop_pass / (v / 1e3) / 1e12 for k, v in per.items()}},
-            # whole-step algorithmic FLOP rate over the same peak as roofline.frac
-            "tc_frac_whole_step": step_flop / (ms_per_step / 1e3) / 1e12 / peak,
+            # whole-step algorithmic FLOP rate over the same peak as roofline.frac, times the N GPUs
+            "tc_frac_whole_step": step_flop / (ms_per_step / 1e3) / 1e12 / (peak * world),
             "conv_stage": {"value": B / (conv_ms / 1e3), "unit": "images/s", "ms_per_step": conv_ms,
                            "what": "the same step with the FC/softmax head replaced by the fixed dA2 it produced "
                                    "(conv layers, their gathers and dX sums, wgrad, SGD of the conv slices)"},
