@@ -440,24 +440,17 @@ def main():
                 live["push"].append(cp.conv_part_kernel_time(pn.layers[1], 3))
             except cp.ConvPartError:
                 pass
-    n0 = cp.cp_launch_count()
-    ms_per_step = _timed(step, args.steps, s, dev, flush, world, after=read_live)
-    launches = cp.cp_launch_count() - n0 if graph is None else launches_per_step * args.steps
-    value = B / (ms_per_step / 1e3)
-
-    # ---- end to end through the public API: pinned host images/labels in, loss out to the host, per step
+    # ---- the timed steps, device-timed (value) and end to end through the public API (e2e) interleaved
+    # step by step, so both see the same clocks / power state (measured one loop after the other, the
+    # later loop ran on a hotter, more power-capped GPU: scripts/e2e_probe.py).
+    # e2e: pinned host images/labels in, loss out to the host, per step.  Input pipeline: step k+1's
+    # images/labels travel host -> device on a copy stream (pinned source, two staging buffers) while
+    # step k computes, inside step k's timed window; step 0's copy is issued inside its own window.
+    # Each e2e step starts with a device copy staging -> the network's input buffer and ends with the
+    # loss read back to pinned host memory, which the host then reads.  L2 flushed before every step.
     h2d = x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size()
     d2h = 4
     loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    # input pipeline: step k+1's images/labels travel host -> device on a copy stream (pinned source,
-    # two staging buffers) while step k computes, inside step k's timed window; step 0's copy is issued
-    # inside its own window.  Each step starts with a device copy staging -> the network's input
-    # buffer and ends with the loss read back to pinned host memory, which the host then reads (the
-    # user's per-step loss read: one host sync per step, as in the device-timed loop).  L2 flushed
-    # between steps.
     cpy = torch.cuda.Stream(dev)
     stage = [(torch.empty_like(pn.x), torch.empty_like(pn.labels)) for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
@@ -472,9 +465,23 @@ def main():
             ready[j].record(cpy)
     for j in range(2):
         free[j].record(s)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     host_losses = []
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    n0 = cp.cp_launch_count()
     for k in range(args.steps):
+        # device-timed step
+        if flush is not None:
+            flush.fill_(k & 0xFF)
+        ev[k][0].record(s)
+        step()
+        ev[k][1].record(s)
+        torch.cuda.synchronize(dev)
+        read_live(k)
+        # end-to-end step
         j = k & 1
         if flush is not None:
             flush.fill_(k & 0xFF)
@@ -495,6 +502,9 @@ def main():
         e2e_ev[k][1].synchronize()
         host_losses.append(float(loss_host[0]))
     torch.cuda.synchronize(dev)
+    launches = (cp.cp_launch_count() - n0) // 2 if graph is None else launches_per_step * args.steps
+    ms_per_step = _max_over_ranks([sum(a.elapsed_time(b) for a, b in ev) / args.steps], dev, world)[0]
+    value = B / (ms_per_step / 1e3)
     # the timed window is tens of ms; keep the same load (identical, untimed steps) until the
     # sampler has seen >= 1.5 s so the clock record is meaningful (step count from the max-over-ranks
     # ms_per_step: identical on every rank, the steps hold collectives)

@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libconvpart.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["plan.cpp", "layer.cu", "comm.cu", "kernels_simt.cu", "kernels_tc.cu"]
+SOURCES = ["plan.cpp", "layer.cu", "comm.cu", "kernels_simt.cu", "kernels_tc.cu", "kernels_conv1.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "tc_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

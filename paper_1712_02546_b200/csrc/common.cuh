@@ -158,7 +158,9 @@ struct Layer {
   size_t off_xcol, off_z, off_dy, off_split, off_dbpart;
   size_t off_x16, off_w16, off_dy16;   // bf16 operand copies (CP_MATH_BF16 only)
   size_t off_stamp;                    // 2 x u64 globaltimer stamps of the fused gather push (timing only)
+  size_t off_c1w;                      // fused image-layer wgrad: per-CTA partial dW / db
   void* ws_last;                       // workspace of the last forward that recorded push stamps
+  const void* xcol_key;                // images whose im2col rows the workspace holds (null: none)
   int dy_ready;           // epilogue-backward already computed for this step
   const void* dy_key[3];
   cudaEvent_t ev_compute, ev_comm;

@@ -3,6 +3,8 @@
 #include <functional>
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace cp {
@@ -63,6 +65,23 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
 int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float* out, int64_t n, cudaStream_t s);
 int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s);
 void tc_release(Layer& L);
+// helpers of kernels_tc.cu shared with kernels_conv1.cu
+int tc_make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                const uint32_t* box, bool mn_major, int es);
+int tc_num_sms();
+int tc_make_map_plain(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                      const uint32_t* box);
+int tc_env_int(const char* name, int dflt);
+// dedicated image-layer (conv1) forward: transposed tcgen05 GEMM with the im2col rows built in shared
+// memory from the NCHW images and the 2x2 pool in registers (kernels_conv1.cu); false = use tc_fwd
+bool c1_fwd_supported(const Layer& L);
+int c1_fwd(Layer& L, const float* x, const float* w, const float* b, float* y_block, uint8_t* saved, cudaStream_t s);
+// fused image-layer backward-filter: unpool + ReLU' + wgrad + db in one split-K tcgen05 kernel + a
+// deterministic reduce (kernels_conv1.cu); da/codes/y are the own pooled block; part = workspace
+bool c1_wgrad_supported(const Layer& L);
+size_t c1_wgrad_workspace(const Layer& L);
+int c1_wgrad(Layer& L, const float* x, const float* da, const uint8_t* codes, const float* y, float* dw, float* db,
+             float* part, cudaStream_t s);
 // timing events around a pass's GEMM launch (no-ops unless L.timing): external records, so they
 // also time when the launch is captured into a CUDA graph
 int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s);

@@ -451,8 +451,18 @@ __global__ void __launch_bounds__(256) bias_grad_final(const float* __restrict__
   const int per = (ns + 7) / 8;
   const int s0 = threadIdx.y * per, s1 = min(ns, s0 + per);
   float t = 0.f;
-  if (slot < Kr)
-    for (int i = s0; i < s1; ++i) t += part[(int64_t)i * Kc + slot];
+  if (slot < Kr) {
+    // loads batched 8 at a time (independent, in flight together), added in the same ascending order
+    int i = s0;
+    for (; i + 8 <= s1; i += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(int64_t)(i + u) * Kc + slot];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t += v[u];
+    }
+    for (; i < s1; ++i) t += part[(int64_t)i * Kc + slot];
+  }
   red[threadIdx.y][threadIdx.x] = t;
   __syncthreads();
   if (threadIdx.y == 0 && slot < Kr) {
@@ -752,8 +762,17 @@ __global__ void __launch_bounds__(1024) fc_fwd_reduce(const float* __restrict__ 
   const int per = (U + 31) / 32;
   const int u0 = threadIdx.y * per, u1 = min(U, u0 + per);
   float t = 0.f;
-  if (e < B * O)
-    for (int u = u0; u < u1; ++u) t += part[(int64_t)u * Bp * O + e];
+  if (e < B * O) {
+    int u = u0;   // loads batched 8 at a time, added in ascending unit order
+    for (; u + 8 <= u1; u += 8) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = part[(int64_t)(u + q) * Bp * O + e];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += v[q];
+    }
+    for (; u < u1; ++u) t += part[(int64_t)u * Bp * O + e];
+  }
   red[threadIdx.y][threadIdx.x] = t;
   __syncthreads();
   if (threadIdx.y == 0 && e < B * O) {
@@ -770,19 +789,32 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
   __shared__ float wsum[8];
   float part = 0.f;
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    const float* l = logits + (int64_t)b * O;
-    float m = l[0];
-    for (int o = 1; o < O; ++o) m = fmaxf(m, l[o]);
-    float se = 0.f;
-    for (int o = 0; o < O; ++o) se += expf(l[o] - m);
-    const float lse = m + logf(se);
+    // the row's logits in registers (one pass over global memory, O <= kMaxO)
+    const float* lp = logits + (int64_t)b * O;
+    float l[kMaxO];
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o) l[o] = o < O ? lp[o] : -INFINITY;
     const int lab = y[b];
+    float m = l[0];
+#pragma unroll
+    for (int o = 1; o < kMaxO; ++o) m = fmaxf(m, l[o]);
+    float se = 0.f;
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o)
+      if (o < O) se += expf(l[o] - m);
+    const float lse = m + logf(se);
     if (lab < 0 || lab >= O) {
       part += __int_as_float(0x7fc00000);  // NaN loss flags an out-of-range label
       continue;
     }
-    part += lse - l[lab];
-    for (int o = 0; o < O; ++o) dl[(int64_t)b * O + o] = (expf(l[o] - lse) - (o == lab ? 1.f : 0.f)) / (float)B;
+    float ll = 0.f;
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o)
+      if (o == lab) ll = l[o];
+    part += lse - ll;
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o)
+      if (o < O) dl[(int64_t)b * O + o] = (expf(l[o] - lse) - (o == lab ? 1.f : 0.f)) / (float)B;
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
@@ -897,6 +929,83 @@ __global__ void __launch_bounds__(256) fc_bwd_fused(const float* __restrict__ dl
                     red[(3 * kMaxO + o) * 64 + sx];
     dwg[o * F + foff + sx] = t;
   }
+}
+
+// FC backward, one thread per gather-layout feature f = (rank block r, position pos, slot) (S:L98-115,
+// chain rule through logits = W x + b):
+//   dx[b][f] = sum_o dlogits[b][o] * W[o][f]      (stored in the gathered input's layout), and
+//   dW[o][f] = sum_b dlogits[b][o] * x[b][f]      (images ascending: fixed order, identical on all ranks);
+// the thread's W column sits in registers, dlogits rows in shared memory (broadcast reads), x / dx
+// rows are coalesced over the feature slots of a position.  CTA 0 also writes dbfc = sum_b dlogits.
+constexpr int kFcCols = 128;   // features per CTA
+constexpr int kFcRows = 256;   // images per shared-memory dlogits chunk
+__global__ void __launch_bounds__(kFcCols) fc_bwd_cols(const float* __restrict__ dl, const float* __restrict__ x,
+                                                      const float* __restrict__ wg, float* __restrict__ dx,
+                                                      float* __restrict__ dwg, float* __restrict__ dbfc, Blocks g,
+                                                      int B, int O, int PW, int64_t F) {
+  __shared__ __align__(16) float dls[kFcRows][kMaxO];
+  const int64_t f = (int64_t)blockIdx.x * kFcCols + threadIdx.x;
+  if (dbfc && blockIdx.x == 0) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int o = w; o < O; o += kFcCols / 32) {
+      float t = 0.f;
+      for (int b = lane; b < B; b += 32) t += dl[(int64_t)b * O + o];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+      if (lane == 0) dbfc[o] = t;
+    }
+  }
+  // feature f -> (block r, position, slot)
+  const bool valid = f < F;
+  int r = 0;
+  while (r + 1 < g.n && f >= (int64_t)PW * g.coff[r + 1]) ++r;
+  const int64_t rem = valid ? f - (int64_t)PW * g.coff[r] : 0;
+  const int kw = g.kw[r] > 0 ? g.kw[r] : 1;
+  const int pos = (int)(rem / kw), slot = (int)(rem - (int64_t)pos * kw);
+  const int64_t xo = g.start[r] + (int64_t)pos * g.Bp * kw + slot;
+  float w[kMaxO], acc[kMaxO];
+#pragma unroll
+  for (int o = 0; o < kMaxO; ++o) {
+    w[o] = (valid && o < O) ? __ldg(wg + o * F + f) : 0.f;
+    acc[o] = 0.f;
+  }
+  for (int b0 = 0; b0 < g.Bp; b0 += kFcRows) {
+    const int nb = min(kFcRows, g.Bp - b0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb * kMaxO; i += kFcCols) {
+      const int row = i / kMaxO, o = i - row * kMaxO;
+      dls[row][o] = (b0 + row < B && o < O) ? __ldg(dl + (int64_t)(b0 + row) * O + o) : 0.f;
+    }
+    __syncthreads();
+    if (!valid) continue;
+    for (int bb = 0; bb < nb; bb += 4) {
+      float xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = (bb + u < nb) ? __ldg(x + xo + (int64_t)(b0 + bb + u) * kw) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (bb + u >= nb) break;
+        const float4* d4 = reinterpret_cast<const float4*>(dls[bb + u]);
+        float d[kMaxO];
+#pragma unroll
+        for (int q = 0; q < kMaxO / 4; ++q) {
+          const float4 v = d4[q];
+          d[4 * q] = v.x; d[4 * q + 1] = v.y; d[4 * q + 2] = v.z; d[4 * q + 3] = v.w;
+        }
+        float dxv = 0.f;
+#pragma unroll
+        for (int o = 0; o < kMaxO; ++o) {
+          dxv = fmaf(d[o], w[o], dxv);
+          acc[o] = fmaf(d[o], xv[u], acc[o]);
+        }
+        if (dx) dx[xo + (int64_t)(b0 + bb + u) * kw] = dxv;
+      }
+    }
+  }
+  if (valid && dwg)
+#pragma unroll
+    for (int o = 0; o < kMaxO; ++o)
+      if (o < O) dwg[o * F + f] = acc[o];
 }
 
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
@@ -1110,9 +1219,9 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
   const int PW = Hp * Wp;
   cudaStream_t s = (cudaStream_t)stream;
   if (dx || dwg || dbfc) {
-    // (no features on this rank: one chunk per position, every CTA returns after CTA 0's dbfc)
-    const int nsc = std::max(1, fc_nsc(g));
-    fc_bwd_fused<<<g.n * PW * nsc, 256, 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, nsc);
+    const int64_t F = (int64_t)PW * g.Cg;   // (0 features on this rank: one CTA computes dbfc only)
+    fc_bwd_cols<<<(unsigned)std::max<int64_t>(1, (F + kFcCols - 1) / kFcCols), kFcCols, 0, s>>>(
+        dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
     CP_LAUNCHED();
   }
   (void)ws;

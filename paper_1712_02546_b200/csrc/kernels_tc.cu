@@ -1092,7 +1092,23 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
   float best = 0.f;
   int code = 0;
   float zq[4] = {0.f, 0.f, 0.f, 0.f};   // the four window positions: independent load streams
-  for (int pc = ti.pbeg[tu]; pc < ti.pbeg[tu + 1]; ++pc) {
+  // pieces in K order; loads of 4 pieces batched (16 in flight), added in the same order
+  int pc = ti.pbeg[tu];
+  const int pe = ti.pbeg[tu + 1];
+  for (; pc + 4 <= pe; pc += 4) {
+    float v[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float* src = buf + ((int64_t)(pc + u) * ti.cg + rank) * BM * BN + (int64_t)b * BN + c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[u][q] = src[q * 32 * BN];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) zq[q] += v[u][q];
+  }
+  for (; pc < pe; ++pc) {
     const float* src = buf + ((int64_t)pc * ti.cg + rank) * BM * BN + (int64_t)b * BN + c;
 #pragma unroll
     for (int q = 0; q < 4; ++q) zq[q] += src[q * 32 * BN];
@@ -1164,11 +1180,22 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
   const int per = (S + 7) / 8;
   const int s0 = threadIdx.y * per, s1 = min(S, s0 + per);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (i4 * 4 < n)
-    for (int s = s0; s < s1; ++s) {
+  if (i4 * 4 < n) {
+    int s = s0;   // loads batched 4 at a time, added in ascending split order
+    for (; s + 4 <= s1; s += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = reinterpret_cast<const float4*>(part + (int64_t)(s + u) * n)[i4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += x[u].x; acc.y += x[u].y; acc.z += x[u].z; acc.w += x[u].w;
+      }
+    }
+    for (; s < s1; ++s) {
       const float4 x = reinterpret_cast<const float4*>(part + (int64_t)s * n)[i4];
       acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
     }
+  }
   red[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && i4 * 4 < n) {
@@ -1715,6 +1742,33 @@ int tc_validate(const Layer& L) {
   }
   return CP_OK;
 }
+
+// exported helpers (shared with kernels_conv1.cu)
+int tc_make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                const uint32_t* box, bool mn_major, int es) {
+  return make_map(m, base, rank, dims, strides, box, mn_major, es);
+}
+int tc_num_sms() { return num_sms(); }
+// fp32 tensor map without swizzle (dense boxes, e.g. an input patch read by CUDA-core threads)
+int tc_make_map_plain(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                      const uint32_t* box) {
+  EncodeTiledFn enc;
+  CP_TRY(get_encoder(&enc));
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], est[5];
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    est[i] = 1;
+    if (i + 1 < rank) gs[i] = strides[i];
+  }
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), gd, gs, bx, est,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) CP_FAIL(CP_ERR_CUDA, "cuTensorMapEncodeTiled (plain) failed (" + std::to_string((int)r) + ")");
+  return CP_OK;
+}
+int tc_env_int(const char* name, int dflt) { return env_int(name, dflt); }
 
 int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s) {
   if (!L.timing) return CP_OK;

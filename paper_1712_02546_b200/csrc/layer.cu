@@ -110,6 +110,7 @@ static int derive(Layer& L, const cp_conv_desc& d) {
     L.off_dy16 = off; off += al256((size_t)L.Ho * L.Wo * L.Bp * L.Kc * 2 + 256);
   }
   L.off_stamp = off; off += 256;
+  L.off_c1w = off; off += al256(L.images ? c1_wgrad_workspace(L) : 0);
   L.ws_total = off + 256;
   L.dy_ready = 0;
   return CP_OK;
@@ -230,9 +231,13 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
   float* yb = y + L->out.start[L->d.rank];
   const bool tf32 = L->d.math == CP_MATH_TF32;
   const float* xin = x;
-  if (L->images) {
+  // image layer on the tensor cores: the dedicated kernel builds its im2col rows in shared memory
+  const bool c1 = L->images && tf32 && c1_fwd_supported(*L) && !gather_push_in_epilogue();
+  L->xcol_key = nullptr;
+  if (L->images && !c1) {
     float* xcol = (float*)WS(ws, L->off_xcol);
     CP_TRY(launch_im2col(*L, x, xcol, tf32, s));
+    L->xcol_key = x;
     xin = xcol;
   }
   // Channel AllGather over NVLink peer memory (B200 path), fused into the consumer
@@ -299,7 +304,9 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
   }
   if (sym_in && !(tf32 && has_gemm)) CP_TRY(launch_wait_flags(arrive, L->d.world, me, s, tf32 && !epi_push));
   if (has_gemm) {
-    if (tf32) {
+    if (c1) {
+      CP_TRY(c1_fwd(*L, x, w, b, yb, saved, s));
+    } else if (tf32) {
       CP_TRY(tc_fwd(*L, xin, w, b, yb, saved, ws, s, push_in_epilogue ? peer_blocks : nullptr,
                     push_in_epilogue ? npeers : 0, arrive, kernel_push ? &gp : nullptr));
     } else if (L->d.math == CP_MATH_BF16) {
@@ -426,11 +433,20 @@ int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* save
   if (!L || !dy_g || !y_g || !x || !dw || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: null pointer");
   if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: pooling needs saved");
   cudaStream_t s = (cudaStream_t)stream;
-  CP_TRY(ensure_dy(*L, dy_g, saved, y_g, ws, s));
-  if (db && L->Kr > 0) CP_TRY(launch_bias_grad(*L, db, (const float*)WS(ws, L->off_dbpart), s));
   if (L->Kr == 0) return CP_OK;
+  if (L->images && L->d.math == CP_MATH_TF32 && c1_wgrad_supported(*L)) {
+    // image layer: unpool + ReLU' + wgrad + db fused (no dY, no im2col rows in HBM)
+    const int64_t o = L->out.start[L->d.rank];
+    return c1_wgrad(*L, x, dy_g + o, saved, y_g + o, dw, db, (float*)WS(ws, L->off_c1w), s);
+  }
+  CP_TRY(ensure_dy(*L, dy_g, saved, y_g, ws, s));
+  if (db) CP_TRY(launch_bias_grad(*L, db, (const float*)WS(ws, L->off_dbpart), s));
   const float* dY = (const float*)WS(ws, L->off_dy);
   const float* xcol = L->images ? (const float*)WS(ws, L->off_xcol) : nullptr;
+  if (L->images && L->xcol_key != x) {   // the forward built its rows on chip: im2col for wgrad here
+    CP_TRY(launch_im2col(*L, x, (float*)WS(ws, L->off_xcol), L->d.math == CP_MATH_TF32, s));
+    L->xcol_key = x;
+  }
   if (L->d.math == CP_MATH_TF32) {
     CP_TRY(tc_wgrad(*L, dY, L->images ? xcol : x, dw, ws, s));
   } else if (L->d.math == CP_MATH_BF16) {   // bf16 copies of dY (ensure_dy) and of the input (forward)
