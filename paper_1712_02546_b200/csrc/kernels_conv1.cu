@@ -13,9 +13,9 @@
 //     and read it back).  A B-set is built once and reused by every 128-kernel M tile.
 //   * The A operand (the own kernels' weights [Kr][Kcol], K-major) streams through a TMA ring.
 //   * Two TMEM accumulators (2 x 256 columns): the epilogue of one M tile overlaps the MMAs of the next.
-// Warp roles (768 threads): w0 TMA producer (weights), w1 MMA issuer (one thread), w2 TMEM allocator,
-// w3 input-patch TMA, w4-w7 B builders, w8-w23 epilogue (four groups of four, one TMEM lane quadrant per
-// warp: the epilogue is ALU-bound, ~20 instructions per pooled output, and needs the warps for latency).
+// Warp roles (896 threads): w0 TMA producer (weights), w1 MMA issuer (one thread), w2 TMEM allocator,
+// w3 input-patch TMA, w4-w11 B builders, w12-w27 epilogue (four groups of four, one TMEM lane quadrant per
+// warp: the epilogue is TMEM-read and ALU bound, ~20 instructions per pooled output, and needs the warps).
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -28,8 +28,8 @@ namespace {
 
 constexpr int C1_BM = 128;            // own kernels per M tile (TMEM lanes)
 constexpr int C1_NMAX = 224;          // pixels per B-set (MMA N), <= 224 so a 32-column load stays in 256
-constexpr int C1_THREADS = 768;
-constexpr int C1_BUILD_WARP0 = 4, C1_EPI_WARP0 = 8, C1_EPI_WARPS = 16;   // 4 epilogue groups of 4 warps
+constexpr int C1_THREADS = 896;
+constexpr int C1_BUILD_WARP0 = 4, C1_BUILD_THREADS = 256, C1_EPI_WARP0 = 12, C1_EPI_WARPS = 16;   // 4 epi groups
 constexpr int C1_EPI_GROUPS = C1_EPI_WARPS / 4;
 constexpr int C1_MAXK = 256;          // Kcol limit (R*S*C padded to 8)
 constexpr int C1_ABYTES = C1_BM * 128;   // one 32-wide K chunk of a 128-kernel A tile
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
     // ======================= B builders: im2col rows of the set, straight from the NCHW images into
     // the 128B-swizzled K-major layout (row n = pixel, 32 tf32 per 128 B row, 16 B chunk j of row n at
     // chunk position j ^ (n & 7))
-    const int t = threadIdx.x - C1_BUILD_WARP0 * 32;   // 0..127
+    const int t = threadIdx.x - C1_BUILD_WARP0 * 32;   // 0..C1_BUILD_THREADS-1
     const int grp = t & 7;                              // 16 B chunk (4 K columns) of the row
     // this thread's patch offsets (K columns grp*4 .. +3 of every 32-wide chunk), in registers
     int offr[C1_MAXK / 32][4];
@@ -234,8 +234,9 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
       const float* patch = sP + buf * (p.patch_bytes / 4);
       const int rows_per_img = 2 * g.ws;
       const int nreal = p.nb * rows_per_img;
+      constexpr int RSTEP = C1_BUILD_THREADS / 8;     // rows per builder pass (8 threads per 128 B row)
       int n = t >> 3, bl = n / rows_per_img, rem = n - bl * rows_per_img;   // (image, row, column) of row n,
-      for (; n < g.n; n += 16) {                                             // stepped (no division per row)
+      for (; n < g.n; n += RSTEP) {                                          // stepped (no division per row)
         const int dh = rem >= g.ws ? 1 : 0, cc = rem - dh * g.ws;
         const bool real = n < nreal;                   // padded images read zeros from the patch (OOB fill)
         const float* src = patch + bl * p.pimg + dh * p.pw + cc;
@@ -252,14 +253,14 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
           }
           *reinterpret_cast<float4*>(drow + c * (C1_NMAX * 128)) = make_float4(v[0], v[1], v[2], v[3]);
         }
-        rem += 16;
+        rem += RSTEP;
         while (rem >= rows_per_img) {
           rem -= rows_per_img;
           ++bl;
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(C1_BUILD_THREADS) : "memory");
       if (t == 0) {
         mbar_arrive(&bfull[buf]);
         mbar_arrive(&pempty[buf]);
