@@ -43,6 +43,7 @@ constexpr int MAX_WIN = 512;                  // dgrad LPT window table (larger 
 constexpr int MAX_GROUPS = 148;               // CTA groups (one per SM or SM pair)
 constexpr int MAX_SCHED = 1024;               // units in an explicit per-group schedule
 constexpr int MAX_PIECES = 2 * MAX_GROUPS + 8;  // stream-tail pieces (<= one or two per CTA group)
+constexpr int MAX_PAIRS = 1024;               // dgrad pixel-pair table entries (input grids up to 2048 pixels)
 
 // CG = CTAs per MMA (cta_group::1 or ::2).  With a CTA pair the MMA is M=256 (128 rows per CTA)
 // and each CTA stages only half of B (N/2 columns), so per-SM operand traffic drops by 1/3 and
@@ -113,6 +114,9 @@ struct TcParams {
   int pix;             // dgrad pixel mode: a CTA's 128 rows = 128 images of ONE input pixel, a pair = two
                        // horizontally adjacent pixels (exact valid rows, s-union only at borders)
   int nwin_order;      // dgrad: windows listed in win_order (0: natural order)
+  int npairs;          // dgrad pixel mode: >0 = the pair table below (pixels paired by tap class), 0 = adjacent
+                       // columns (2j, 2j+1); entry = i0 | w0 << 8 | i1 << 16 | w1 << 24 (CTA 0 / CTA 1 pixel)
+  uint32_t pair_tab[MAX_PAIRS];
   int wg_taps_slow;    // wgrad unit order: 0 = N (tap, slot tile) fastest; 1 = slot tile, kernel tile, tap
   int diag;            // fwd timing diagnostics (CP_TC_DIAG; results are wrong): 1 no MMAs, 2 no A loads,
                        // 4 no B loads
@@ -144,8 +148,11 @@ struct TcParams {
   long long push_n4;
 };
 
+static_assert(sizeof(TcParams) <= 32000, "TcParams exceeds the kernel parameter limit");
+
 struct Unit {
   int mt, nt, sp;
+  uint32_t pix2;       // dgrad pixel mode: both CTAs' pixels, i0 | w0 << 8 | i1 << 16 | w1 << 24
   int tail, tu, piece; // wgrad: K-piece `piece` of tail unit `tu` (last-round units split over all groups)
   int i, j, bc;        // spatial window / batch chunk (fwd, dgrad)
   int n0, n;           // N origin (within own slots or block) and width
@@ -219,8 +226,14 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     const int nbc = p.Bp / 128, W2 = p.Win / 2;
     t.bc = mg % nbc;                  // 128-image chunk
     const int ij = mg / nbc;
-    t.j = ij % W2;                    // pixel pair: columns 2j (CTA 0), 2j+1 (CTA 1)
-    t.i = ij / W2;                    // input row
+    if (p.npairs > 0) {               // pixels paired by tap class (host table)
+      t.pix2 = p.pair_tab[ij];
+    } else {                          // adjacent columns 2j (CTA 0), 2j+1 (CTA 1) of input row i
+      const int i = ij / W2, w = 2 * (ij - i * W2);
+      t.pix2 = (uint32_t)i | ((uint32_t)w << 8) | ((uint32_t)i << 16) | ((uint32_t)(w + 1) << 24);
+    }
+    t.i = rank ? (t.pix2 >> 16) & 0xff : t.pix2 & 0xff;          // this CTA's input pixel (row, column)
+    t.j = rank ? t.pix2 >> 24 : (t.pix2 >> 8) & 0xff;
     t.mt = mg;
   } else if (PASS == PASS_FWD || PASS == PASS_DGRAD) {
     const int nbcg = p.Bp / 32 / CG;
@@ -277,12 +290,21 @@ struct Chunk {
 
 // dgrad: taps (r,s) whose shifted 2x2 window hits the dY grid: r in [r_lo, r_hi], s in [s_lo, s_hi]
 __device__ __forceinline__ void dgrad_taps(const TcParams& p, const Unit& t, int& r_lo, int& nr, int& s_lo, int& ns) {
-  // window mode: input rows 2i, 2i+1; pixel mode: the single input row i
-  const int h0 = p.pix ? t.i : 2 * t.i, h1 = p.pix ? t.i : 2 * t.i + 1;
-  r_lo = max(0, h0 - p.Ho + 1);
-  const int r_hi = min(p.R - 1, h1);
-  s_lo = max(0, 2 * t.j - p.Wo + 1);
-  const int s_hi = min(p.S - 1, 2 * t.j + 1);
+  int r_hi, s_hi;
+  if (p.pix) {
+    // pixel mode: the union of the pair's two pixels' valid tap boxes (both CTAs run one K loop)
+    const int i0 = t.pix2 & 0xff, w0 = (t.pix2 >> 8) & 0xff, i1 = (t.pix2 >> 16) & 0xff, w1 = t.pix2 >> 24;
+    r_lo = max(0, min(i0, i1) - p.Ho + 1);
+    r_hi = min(p.R - 1, max(i0, i1));
+    s_lo = max(0, min(w0, w1) - p.Wo + 1);
+    s_hi = min(p.S - 1, max(w0, w1));
+  } else {
+    // window mode: input rows 2i, 2i+1 and columns 2j, 2j+1
+    r_lo = max(0, 2 * t.i - p.Ho + 1);
+    r_hi = min(p.R - 1, 2 * t.i + 1);
+    s_lo = max(0, 2 * t.j - p.Wo + 1);
+    s_hi = min(p.S - 1, 2 * t.j + 1);
+  }
   nr = r_hi - r_lo + 1;
   ns = s_hi - s_lo + 1;
 }
@@ -633,9 +655,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           } else if (PASS == PASS_DGRAD) {
             const int r = ch.r, s = ch.s;
             if (p.l2hint && p.pix)
-              ld4h(a, &p.maps[0], ch.c * BKE, t.bc * 128, 2 * t.j + (int)rank - s, t.i - r, pol_stream);
+              ld4h(a, &p.maps[0], ch.c * BKE, t.bc * 128, t.j - s, t.i - r, pol_stream);
             else if (p.pix)
-              ld4(a, &p.maps[0], ch.c * BKE, t.bc * 128, 2 * t.j + (int)rank - s, t.i - r);
+              ld4(a, &p.maps[0], ch.c * BKE, t.bc * 128, t.j - s, t.i - r);
             else
               ld4(a, &p.maps[0], ch.c * BKE, t.bc * 32, 2 * t.j - s, 2 * t.i - r);
             if (p.wide) {
@@ -986,7 +1008,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             if (chunk_ok) {
               const int kw = p.kw[rb];
               const int c4 = (lane & 7) * 4;
-              float* base = p.dst[rb] + (p.pix ? ((int64_t)(t.i * p.Win + 2 * t.j + (int)rank) * p.Bp + t.bc * 128 + quad * 32)
+              float* base = p.dst[rb] + (p.pix ? ((int64_t)(t.i * p.Win + t.j) * p.Bp + t.bc * 128 + quad * 32)
                                                 : ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + t.bc * 32)) * kw + slot;
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
@@ -1009,7 +1031,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           } else if (!p.span || slot < p.kw[rb]) {
             const int kw = p.kw[rb];
             const int64_t o = (int64_t)t.sp * p.part_stride + p.start[rb] +
-                              (p.pix ? ((int64_t)(t.i * p.Win + 2 * t.j + (int)rank) * p.Bp + t.bc * 128 + row)
+                              (p.pix ? ((int64_t)(t.i * p.Win + t.j) * p.Bp + t.bc * 128 + row)
                                      : ((int64_t)((2 * t.i + dh) * p.Win + 2 * t.j + dw) * p.Bp + bb)) * kw + slot;
             store_f32x32(p.out + o, v, ncol);
           }
@@ -1559,6 +1581,79 @@ static Plan fwd_plan(const Layer& L, TcParams& p) {
   return w;
 }
 
+// Pixel-mode dgrad pairs two input pixels per CTA pair; both run the K loop over the UNION of their valid
+// tap boxes, so pairing columns 2j, 2j+1 wastes MACs at every border column (paper net: 1.08x the exact
+// work).  Pixels with the same (row tap range, column tap range) class need no union: pair them within
+// their class (row-major), then the <= 1 leftover per class greedily by the fewest added MACs (paper net:
+// 1.027x).  Entries sorted by the first pixel (spatial locality of the unit order).
+static int build_pixel_pairs(const Layer& L, TcParams& p) {
+  const int H = L.H, W = L.W;
+  if (H * W / 2 > MAX_PAIRS || H > 255 || W > 255 || (W & 1) || !env_int("CP_TC_DGRAD_PAIRS", 1)) return 0;
+  auto rlo = [&](int i) { return std::max(0, i - L.Ho + 1); };
+  auto rhi = [&](int i) { return std::min(L.R - 1, i); };
+  auto slo = [&](int w) { return std::max(0, w - L.Wo + 1); };
+  auto shi = [&](int w) { return std::min(L.S - 1, w); };
+  auto box = [&](int i0, int w0, int i1, int w1) {
+    const int nr = std::max(rhi(i0), rhi(i1)) - std::min(rlo(i0), rlo(i1)) + 1;
+    const int ns = std::max(shi(w0), shi(w1)) - std::min(slo(w0), slo(w1)) + 1;
+    return nr * ns;
+  };
+  std::vector<std::pair<long long, int>> keyed;   // (class key, pixel) in row-major order
+  for (int i = 0; i < H; ++i)
+    for (int w = 0; w < W; ++w)
+      keyed.push_back({((long long)(rlo(i) * 64 + rhi(i)) * 64 + slo(w)) * 64 + shi(w), i * W + w});
+  std::stable_sort(keyed.begin(), keyed.end(),
+                   [](const std::pair<long long, int>& a, const std::pair<long long, int>& b) { return a.first < b.first; });
+  std::vector<std::pair<int, int>> pairs, singles;
+  std::vector<int> left;
+  for (size_t k = 0; k < keyed.size();) {
+    size_t e = k;
+    while (e < keyed.size() && keyed[e].first == keyed[k].first) ++e;
+    size_t m = k;
+    for (; m + 1 < e; m += 2) pairs.push_back({keyed[m].second, keyed[m + 1].second});
+    if (m < e) left.push_back(keyed[m].second);
+    k = e;
+  }
+  std::sort(left.begin(), left.end());
+  std::vector<char> used(left.size(), 0);
+  for (size_t a = 0; a < left.size(); ++a) {
+    if (used[a]) continue;
+    used[a] = 1;
+    int best = -1, bc = 1 << 30;
+    const int ia = left[a] / W, wa = left[a] % W;
+    for (size_t b = a + 1; b < left.size(); ++b) {
+      if (used[b]) continue;
+      const int ib = left[b] / W, wb = left[b] % W;
+      // the MACs the union adds over the two pixels' own tap boxes
+      const int c = 2 * box(ia, wa, ib, wb) - box(ia, wa, ia, wa) - box(ib, wb, ib, wb);
+      if (c < bc) {
+        bc = c;
+        best = (int)b;
+      }
+    }
+    if (best < 0) return 0;   // (odd leftover: cannot happen for an even pixel count)
+    used[best] = 1;
+    pairs.push_back({left[a], left[best]});
+  }
+  for (auto& pr : pairs)
+    if (pr.first > pr.second) std::swap(pr.first, pr.second);
+  std::sort(pairs.begin(), pairs.end());
+  if ((int)pairs.size() != H * W / 2) return 0;
+  for (size_t k = 0; k < pairs.size(); ++k) {
+    const int a = pairs[k].first, b = pairs[k].second;
+    p.pair_tab[k] = (uint32_t)(a / W) | ((uint32_t)(a % W) << 8) | ((uint32_t)(b / W) << 16) | ((uint32_t)(b % W) << 24);
+  }
+  return (int)pairs.size();
+}
+
+// valid-tap box of pixel-mode pair entry e (host mirror of dgrad_taps)
+static int pair_taps(const Layer& L, uint32_t e) {
+  const int i0 = e & 0xff, w0 = (e >> 8) & 0xff, i1 = (e >> 16) & 0xff, w1 = e >> 24;
+  const int nr = std::min(L.R - 1, std::max(i0, i1)) - std::max(0, std::min(i0, i1) - L.Ho + 1) + 1;
+  const int ns = std::min(L.S - 1, std::max(w0, w1)) - std::max(0, std::min(w0, w1) - L.Wo + 1) + 1;
+  return nr * ns;
+}
+
 static Plan dgrad_plan(const Layer& L, TcParams& p) {
   Plan w{};
   w.pair = use_pairs() && (L.Bp / 32) % 2 == 0;
@@ -1569,6 +1664,7 @@ static Plan dgrad_plan(const Layer& L, TcParams& p) {
   // union wastes only at the borders (paper net: 1.08x the exact MACs vs 1.17x for 2x2 windows)
   p.pix = (w.pair && L.Bp % 128 == 0 && env_int("CP_TC_DGRAD_PIX", 1)) ? 1 : 0;
   w.numM = p.pix ? L.H * (L.W / 2) * (L.Bp / 128) : (L.H / 2) * (L.W / 2) * (L.Bp / 32) / CG;
+  p.npairs = p.pix ? build_pixel_pairs(L, p) : 0;
   // average valid taps of a tile: (sum over tile rows of valid r) * (same for s) / tiles
   auto avg_valid = [](int Hin, int Ho, int R, int rows) {
     double t = 0;
@@ -1579,6 +1675,11 @@ static Plan dgrad_plan(const Layer& L, TcParams& p) {
   };
   const double kc = (L.Kc + op_elems(L) - 1) / op_elems(L);
   w.chunks = (int)(avg_valid(L.H, L.Ho, L.R, p.pix ? 1 : 2) * avg_valid(L.W, L.Wo, L.S, 2) * kc + 0.5);
+  if (p.npairs > 0) {
+    double t = 0;
+    for (int k = 0; k < p.npairs; ++k) t += pair_taps(L, p.pair_tab[k]);
+    w.chunks = (int)(t / p.npairs * kc + 0.5);
+  }
   w.S = env_int("CP_TC_SPLIT_DGRAD", 0);
   if (w.S <= 0) w.S = choose_split(w.numM * w.numN, num_sms() / CG, w.chunks, (double)L.in.start[L.in.n] * 4, 16);
   return w;
@@ -2044,10 +2145,16 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
       for (int u = 0; u < p.units; ++u) {
         const int mg = u % p.numM;
         const int ij = mg / nbcg, i = ij / W2, j = ij % W2;
-        const int h0 = p.pix ? i : 2 * i, h1 = p.pix ? i : 2 * i + 1;
-        const int nr = std::min(L.R - 1, h1) - std::max(0, h0 - L.Ho + 1) + 1;
-        const int ns = std::min(L.S - 1, 2 * j + 1) - std::max(0, 2 * j - L.Wo + 1) + 1;
-        const long long work = ((long long)nr * ns * kc + pl.S - 1) / pl.S;
+        int taps;
+        if (p.pix && p.npairs > 0) {
+          taps = pair_taps(L, p.pair_tab[ij]);
+        } else {
+          const int h0 = p.pix ? i : 2 * i, h1 = p.pix ? i : 2 * i + 1;
+          const int nr = std::min(L.R - 1, h1) - std::max(0, h0 - L.Ho + 1) + 1;
+          const int ns = std::min(L.S - 1, 2 * j + 1) - std::max(0, 2 * j - L.Wo + 1) + 1;
+          taps = nr * ns;
+        }
+        const long long work = ((long long)taps * kc + pl.S - 1) / pl.S;
         wk[u] = {-work, u};
       }
       std::stable_sort(wk.begin(), wk.end());
