@@ -15,6 +15,10 @@
 
 #include "kernels.cuh"
 
+#include <cuda.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <functional>
 #include <map>
 
@@ -25,6 +29,12 @@ struct SymBuf {
   int64_t own_off = -1, own_elems = 0;   // this rank's block (floats), recorded by its producer
   void* peers[CP_MAX_RANKS];  // peers[rank] = own pointer
   int index = -1;             // loopback: allocation sequence number (peers resolved by it)
+  // NVLink multicast (CP_MULTICAST=1): the buffer is a driver VMM allocation bound to a multicast
+  // object; `mc` maps it (a store / reduction through `mc` reaches every rank's copy via NVSwitch)
+  bool vmm = false;
+  size_t map_bytes = 0;
+  void* mc = nullptr;
+  CUmemGenericAllocationHandle h[CP_MAX_RANKS] = {}, h_mc = 0;
 };
 
 // Loopback group (tests on one GPU): `world` simulated ranks in one process, each with its own
@@ -113,6 +123,9 @@ extern "C" int cp_comm_create_loopback(int32_t world, cp_comm* out) {
 }
 
 static int sym_map(cp_comm c, size_t bytes, void** local_out, SymBuf& sb);
+static int sym_map_multicast(cp_comm c, size_t bytes, void** local_out, SymBuf& sb, bool* done);
+namespace cp { bool multicast_requested(); }
+using cp::multicast_requested;
 
 extern "C" int cp_symmetric_alloc(cp_comm c, size_t bytes, void** local_out) {
   if (!c || !local_out || bytes == 0) CP_FAIL(CP_ERR_ARG, "cp_symmetric_alloc: bad arguments");
@@ -151,8 +164,25 @@ extern "C" int cp_symmetric_alloc(cp_comm c, size_t bytes, void** local_out) {
     CP_CUDA(cudaMemcpy(c->ctl + kCtlOne, consts, 8, cudaMemcpyHostToDevice));
   }
   SymBuf sb{};
-  CP_TRY(sym_map(c, bytes, local_out, sb));
+  bool done = false;
+  if (multicast_requested()) CP_TRY(sym_map_multicast(c, bytes, local_out, sb, &done));
+  if (!done) CP_TRY(sym_map(c, bytes, local_out, sb));
   c->sym[*local_out] = sb;
+  return CP_OK;
+}
+
+// All-gather `n` bytes per rank through NCCL (blocking; allocation time only).  Also a barrier.
+static int allgather_bytes(cp_comm c, const void* mine, size_t n, std::vector<uint8_t>& all) {
+  uint8_t* dev = nullptr;
+  CP_CUDA(cudaMalloc(&dev, n * (size_t)(c->world + 1)));
+  CP_CUDA(cudaMemcpy(dev + n * (size_t)c->world, mine, n, cudaMemcpyHostToDevice));
+  ncclResult_t r = ncclAllGather(dev + n * (size_t)c->world, dev, n, ncclUint8, c->comm, 0);
+  all.assign(n * (size_t)c->world, 0);
+  cudaError_t e = cudaSuccess;
+  if (r == ncclSuccess) e = cudaMemcpy(all.data(), dev, all.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dev);
+  if (r != ncclSuccess) CP_FAIL(CP_ERR_NCCL, std::string("symmetric alloc exchange: ") + ncclGetErrorString(r));
+  if (e != cudaSuccess) CP_FAIL(CP_ERR_CUDA, std::string("symmetric alloc exchange: ") + cudaGetErrorString(e));
   return CP_OK;
 }
 
@@ -166,17 +196,8 @@ static int sym_map(cp_comm c, size_t bytes, void** local_out, SymBuf& sb) {
   cudaIpcMemHandle_t h;
   CP_CUDA(cudaIpcGetMemHandle(&h, mine));
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  // exchange the 64-byte handles with an NCCL AllGather (blocking: allocation time only)
-  uint8_t* dev = nullptr;
-  CP_CUDA(cudaMalloc(&dev, 64 * (size_t)(c->world + 1)));
-  CP_CUDA(cudaMemcpy(dev + 64 * (size_t)c->world, &h, 64, cudaMemcpyHostToDevice));
-  ncclResult_t r = ncclAllGather(dev + 64 * (size_t)c->world, dev, 64, ncclUint8, c->comm, 0);
-  std::vector<uint8_t> all(64 * (size_t)c->world);
-  cudaError_t e = cudaSuccess;
-  if (r == ncclSuccess) e = cudaMemcpy(all.data(), dev, all.size(), cudaMemcpyDeviceToHost);
-  cudaFree(dev);
-  if (r != ncclSuccess) CP_FAIL(CP_ERR_NCCL, std::string("symmetric alloc handle exchange: ") + ncclGetErrorString(r));
-  if (e != cudaSuccess) CP_FAIL(CP_ERR_CUDA, std::string("symmetric alloc: ") + cudaGetErrorString(e));
+  std::vector<uint8_t> all;
+  CP_TRY(allgather_bytes(c, &h, 64, all));
   for (int p = 0; p < c->world; ++p) {
     if (p == c->rank) {
       sb.peers[p] = mine;
@@ -194,6 +215,231 @@ static int sym_map(cp_comm c, size_t bytes, void** local_out, SymBuf& sb) {
   return CP_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// NVLink multicast symmetric buffers (CP_MULTICAST=1).  Driver VMM: each rank cuMemCreate's its
+// copy with a POSIX-fd shareable handle; peers obtain the exporter's fd with pidfd_getfd (same node,
+// same user) and map it; rank 0 creates the multicast object, every rank adds its device and binds
+// its copy, and maps the multicast address.  Driver entry points come from cudaGetDriverEntryPoint
+// (no libcuda link).  Any failure on any rank is agreed collectively and the buffer falls back to
+// the CUDA-IPC path above, so every rank always takes the same path.
+struct Drv {
+  bool ok = false;
+  CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+  CUresult (*memRelease)(CUmemGenericAllocationHandle);
+  CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  CUresult (*addrFree)(CUdeviceptr, size_t);
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  CUresult (*unmap)(CUdeviceptr, size_t);
+  CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  CUresult (*exportH)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long);
+  CUresult (*importH)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+  CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+  CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice);
+  CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                        unsigned long long);
+  CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+  CUresult (*mcGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+};
+static Drv& drv() {
+  static Drv d = [] {
+    Drv x{};
+    bool ok = true;
+    auto get = [&](const char* name, auto& fn) {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+          !p)
+        ok = false;
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+    };
+    get("cuMemCreate", x.memCreate);
+    get("cuMemRelease", x.memRelease);
+    get("cuMemGetAllocationGranularity", x.granularity);
+    get("cuMemAddressReserve", x.reserve);
+    get("cuMemAddressFree", x.addrFree);
+    get("cuMemMap", x.map);
+    get("cuMemUnmap", x.unmap);
+    get("cuMemSetAccess", x.setAccess);
+    get("cuMemExportToShareableHandle", x.exportH);
+    get("cuMemImportFromShareableHandle", x.importH);
+    get("cuMulticastCreate", x.mcCreate);
+    get("cuMulticastAddDevice", x.mcAddDevice);
+    get("cuMulticastBindMem", x.mcBindMem);
+    get("cuMulticastUnbind", x.mcUnbind);
+    get("cuMulticastGetGranularity", x.mcGranularity);
+    x.ok = ok;
+    return x;
+  }();
+  return d;
+}
+
+bool cp::multicast_requested() {
+  static const int v = [] {
+    const char* e = getenv("CP_MULTICAST");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+// reserve + map + grant this device read/write access
+static bool vmm_map(CUmemGenericAllocationHandle h, size_t size, size_t align, int dev, void** va_out) {
+  Drv& d = drv();
+  CUdeviceptr va = 0;
+  if (d.reserve(&va, size, align, 0, 0) != CUDA_SUCCESS) return false;
+  if (d.map(va, size, 0, h, 0) != CUDA_SUCCESS) {
+    d.addrFree(va, size);
+    return false;
+  }
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (d.setAccess(va, size, &acc, 1) != CUDA_SUCCESS) {
+    d.unmap(va, size);
+    d.addrFree(va, size);
+    return false;
+  }
+  *va_out = (void*)va;
+  return true;
+}
+
+static void vmm_unmap(void* va, size_t size) {
+  if (!va) return;
+  drv().unmap((CUdeviceptr)va, size);
+  drv().addrFree((CUdeviceptr)va, size);
+}
+
+// a peer process's file descriptor, duplicated into this process (Linux >= 5.6)
+static int fd_from_peer(int pid, int fd) {
+#if defined(SYS_pidfd_open) && defined(SYS_pidfd_getfd)
+  const int pfd = (int)syscall(SYS_pidfd_open, pid, 0);
+  if (pfd < 0) return -1;
+  const int mine = (int)syscall(SYS_pidfd_getfd, pfd, fd, 0);
+  close(pfd);
+  return mine;
+#else
+  (void)pid;
+  (void)fd;
+  return -1;
+#endif
+}
+
+// collective: every rank contributes `ok`; true iff all ranks are ok
+static int agree(cp_comm c, bool ok, bool* all_ok) {
+  const uint8_t v = ok ? 1 : 0;
+  std::vector<uint8_t> all;
+  CP_TRY(allgather_bytes(c, &v, 1, all));
+  *all_ok = true;
+  for (uint8_t a : all) *all_ok = *all_ok && a;
+  return CP_OK;
+}
+
+static void vmm_release(cp_comm c, SymBuf& sb) {
+  Drv& d = drv();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (sb.mc) vmm_unmap(sb.mc, sb.map_bytes);
+  if (sb.h_mc) {
+    if (sb.h[c->rank]) d.mcUnbind(sb.h_mc, dev, 0, sb.map_bytes);
+    d.memRelease(sb.h_mc);
+  }
+  for (int q = 0; q < c->world; ++q) {
+    if (sb.peers[q]) vmm_unmap(sb.peers[q], sb.map_bytes);
+    if (sb.h[q]) d.memRelease(sb.h[q]);
+    sb.peers[q] = nullptr;
+    sb.h[q] = 0;
+  }
+  sb.mc = nullptr;
+  sb.h_mc = 0;
+}
+
+// Returns CP_OK with *done=false (nothing allocated) if any rank could not set the buffer up.
+static int sym_map_multicast(cp_comm c, size_t bytes, void** local_out, SymBuf& sb, bool* done) {
+  *done = false;
+  Drv& d = drv();
+  int dev = 0;
+  CP_CUDA(cudaGetDevice(&dev));
+  sb.bytes = bytes;
+  sb.flag_off = (bytes + 255) / 256 * 256;
+  sb.vmm = true;
+  const int me = c->rank;
+  bool ok = d.ok;
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CUmulticastObjectProp mp{};
+  mp.numDevices = (unsigned)c->world;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g1 = 0, g2 = 0;
+  if (ok) ok = d.granularity(&g1, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS;
+  if (ok) ok = d.mcGranularity(&g2, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS;
+  const size_t gran = std::max<size_t>(std::max(g1, g2), 1);
+  const size_t size = (sb.flag_off + 256 + gran - 1) / gran * gran;
+  sb.map_bytes = size;
+  mp.size = size;
+  int fds[3] = {(int)getpid(), -1, -1};   // pid, fd of this rank's copy, fd of the multicast object (rank 0)
+  if (ok) ok = d.memCreate(&sb.h[me], size, &prop, 0) == CUDA_SUCCESS;
+  if (ok) ok = vmm_map(sb.h[me], size, gran, dev, &sb.peers[me]);
+  if (ok) ok = cudaMemset(sb.peers[me], 0, size) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+  if (ok) ok = d.exportH(&fds[1], sb.h[me], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) == CUDA_SUCCESS;
+  if (ok && me == 0) {
+    ok = d.mcCreate(&sb.h_mc, &mp) == CUDA_SUCCESS;
+    if (ok) ok = d.exportH(&fds[2], sb.h_mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) == CUDA_SUCCESS;
+  }
+  std::vector<uint8_t> all;
+  bool all_ok = false;
+  int rc = agree(c, ok, &all_ok);
+  if (rc == CP_OK && all_ok) rc = allgather_bytes(c, fds, sizeof(fds), all);
+  if (rc == CP_OK && all_ok) {
+    // import the peers' copies and (ranks > 0) the multicast object
+    auto peer_fds = [&](int q, int k) {
+      int v;
+      memcpy(&v, all.data() + sizeof(fds) * (size_t)q + 4 * k, 4);
+      return v;
+    };
+    for (int q = 0; q < c->world && ok; ++q) {
+      if (q == me) continue;
+      const int fd = fd_from_peer(peer_fds(q, 0), peer_fds(q, 1));
+      ok = fd >= 0 && d.importH(&sb.h[q], (void*)(intptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) == CUDA_SUCCESS;
+      if (fd >= 0) close(fd);
+      if (ok) ok = vmm_map(sb.h[q], size, gran, dev, &sb.peers[q]);
+    }
+    if (ok && me != 0) {
+      const int fd = fd_from_peer(peer_fds(0, 0), peer_fds(0, 2));
+      ok = fd >= 0 && d.importH(&sb.h_mc, (void*)(intptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) == CUDA_SUCCESS;
+      if (fd >= 0) close(fd);
+    }
+    if (ok) ok = d.mcAddDevice(sb.h_mc, dev) == CUDA_SUCCESS;
+    rc = agree(c, ok, &all_ok);   // every device added before any bind; exporters may close their fds
+  }
+  if (fds[1] >= 0) close(fds[1]);
+  if (fds[2] >= 0) close(fds[2]);
+  if (rc == CP_OK && all_ok) {
+    ok = d.mcBindMem(sb.h_mc, 0, sb.h[me], 0, size, 0) == CUDA_SUCCESS;
+    rc = agree(c, ok, &all_ok);
+  }
+  if (rc == CP_OK && all_ok) {
+    ok = vmm_map(sb.h_mc, size, gran, dev, &sb.mc);
+    rc = agree(c, ok, &all_ok);
+  }
+  if (rc != CP_OK || !all_ok) {
+    vmm_release(c, sb);
+    sb = SymBuf{};
+    if (rc != CP_OK) return rc;
+    return CP_OK;   // *done = false: the caller falls back to CUDA IPC
+  }
+  if (!c->barrier_word) {
+    CP_CUDA(cudaMalloc(&c->barrier_word, sizeof(float)));
+    CP_CUDA(cudaMemset(c->barrier_word, 0, sizeof(float)));
+  }
+  *local_out = sb.peers[me];
+  *done = true;
+  return CP_OK;
+}
+
 // Unmap every peer's copy, then wait until all ranks have unmapped theirs before freeing the
 // exported allocation (no rank may still hold a mapping of memory that is being freed).
 static void sym_release(cp_comm c, void* local, SymBuf& sb) {
@@ -203,11 +449,30 @@ static void sym_release(cp_comm c, void* local, SymBuf& sb) {
     cudaFree(local);
     return;
   }
-  for (int p = 0; p < c->world; ++p)
-    if (p != c->rank && sb.peers[p]) cudaIpcCloseMemHandle(sb.peers[p]);
+  if (sb.vmm) {   // multicast: unbind + unmap everything, then the barrier, then the own copy
+    Drv& d = drv();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (sb.mc) vmm_unmap(sb.mc, sb.map_bytes);
+    if (sb.h_mc) d.mcUnbind(sb.h_mc, dev, 0, sb.map_bytes);
+    for (int p = 0; p < c->world; ++p)
+      if (p != c->rank) {
+        vmm_unmap(sb.peers[p], sb.map_bytes);
+        if (sb.h[p]) d.memRelease(sb.h[p]);
+      }
+  } else {
+    for (int p = 0; p < c->world; ++p)
+      if (p != c->rank && sb.peers[p]) cudaIpcCloseMemHandle(sb.peers[p]);
+  }
   if (c->barrier_word && ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, 0) ==
                              ncclSuccess)
     cudaDeviceSynchronize();
+  if (sb.vmm) {
+    if (sb.h_mc) drv().memRelease(sb.h_mc);
+    vmm_unmap(local, sb.map_bytes);
+    drv().memRelease(sb.h[c->rank]);
+    return;
+  }
   cudaFree(local);
 }
 
@@ -449,6 +714,13 @@ int comm_loopback_defer(cp_comm c, cudaEvent_t done, std::function<int(const std
   g.pending.clear();
   for (auto& f : fns) CP_TRY(f(all));
   return CP_OK;
+}
+
+// Multicast address of a symmetric buffer (nullptr unless it was set up with CP_MULTICAST=1).
+void* comm_symmetric_mc(cp_comm c, const void* local) {
+  if (!c || c->world == 1 || c->loop) return nullptr;
+  auto it = c->sym.find(const_cast<void*>(local));
+  return it == c->sym.end() ? nullptr : it->second.mc;
 }
 
 bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags) {

@@ -53,6 +53,7 @@ struct GatherPush {
   unsigned long long* stamp = nullptr;  // timing: [0] min start, [1] max end (globaltimer ns) of the push
   int n, chunks;
   long long n4;
+  int mc = 0;   // 1: dst[0] / cnt[0] are multicast addresses (one store reaches every rank)
 };
 constexpr int kClaimWord = 32;   // flag-line word of a symmetric gathered input: the push claim counter
 int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved,
@@ -92,6 +93,9 @@ int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s
 // symmetric (peer-mapped) buffer lookup: peers[r] = rank r's copy; flags[r] = rank r's arrival-flag
 // array (CP_MAX_RANKS u32, indexed by sender rank).  False if `local` is not a symmetric buffer.
 bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags = nullptr);
+// NVLink multicast address of a symmetric buffer (CP_MULTICAST=1), else nullptr
+void* comm_symmetric_mc(cp_comm c, const void* local);
+bool multicast_requested();
 // producer records its block of a symmetric gathered buffer (for copy-engine distribution)
 void comm_symmetric_set_own(cp_comm c, const void* local, int64_t off, int64_t elems);
 int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks = false);

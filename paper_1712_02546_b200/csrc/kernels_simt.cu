@@ -694,6 +694,7 @@ __host__ __device__ inline int fc_nsc(const Blocks& g) {
   return (m + kFcChunk - 1) / kFcChunk;
 }
 
+template <int OO>   // compile-time class bound (10 for CIFAR's 10 classes, else kMaxO)
 __global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
                                                       float* __restrict__ part, Blocks g, int B, int O, int PW,
                                                       int nsc) {
@@ -730,15 +731,15 @@ __global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ 
   }
   __syncthreads();
   const int bl = threadIdx.x >> 1, half = threadIdx.x & 1;
-  float acc[kMaxO];
+  float acc[OO];
 #pragma unroll
-  for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
+  for (int o = 0; o < OO; ++o) acc[o] = 0.f;
 #pragma unroll
   for (int k = 0; k < kFcChunk / 8; ++k) {
     const int q = 2 * k + half;
     const float4 xv = *reinterpret_cast<const float4*>(xs + bl * kFcLd + 4 * q);
 #pragma unroll
-    for (int o = 0; o < kMaxO; ++o) {
+    for (int o = 0; o < OO; ++o) {
       if (o < O) {
         const float4 w = ws[o][q];
         acc[o] = fmaf(xv.x, w.x, fmaf(xv.y, w.y, fmaf(xv.z, w.z, fmaf(xv.w, w.w, acc[o]))));
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ 
     }
   }
 #pragma unroll
-  for (int o = 0; o < kMaxO; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
+  for (int o = 0; o < OO; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
   const int b = b0 + bl;
   if (half == 0 && b < g.Bp)
     for (int o = 0; o < O; ++o) part[((int64_t)u * g.Bp + b) * O + o] = acc[o];
@@ -931,23 +932,29 @@ __global__ void __launch_bounds__(256) fc_bwd_fused(const float* __restrict__ dl
   }
 }
 
-// FC backward, one thread per gather-layout feature f = (rank block r, position pos, slot) (S:L98-115,
+// FC backward, one CTA column per gather-layout feature f = (rank block r, position pos, slot) (S:L98-115,
 // chain rule through logits = W x + b):
 //   dx[b][f] = sum_o dlogits[b][o] * W[o][f]      (stored in the gathered input's layout), and
-//   dW[o][f] = sum_b dlogits[b][o] * x[b][f]      (images ascending: fixed order, identical on all ranks);
-// the thread's W column sits in registers, dlogits rows in shared memory (broadcast reads), x / dx
-// rows are coalesced over the feature slots of a position.  CTA 0 also writes dbfc = sum_b dlogits.
-constexpr int kFcCols = 128;   // features per CTA
-constexpr int kFcRows = 256;   // images per shared-memory dlogits chunk
-__global__ void __launch_bounds__(kFcCols) fc_bwd_cols(const float* __restrict__ dl, const float* __restrict__ x,
-                                                      const float* __restrict__ wg, float* __restrict__ dx,
-                                                      float* __restrict__ dwg, float* __restrict__ dbfc, Blocks g,
-                                                      int B, int O, int PW, int64_t F) {
-  __shared__ __align__(16) float dls[kFcRows][kMaxO];
-  const int64_t f = (int64_t)blockIdx.x * kFcCols + threadIdx.x;
+//   dW[o][f] = sum_b dlogits[b][o] * x[b][f]      (fixed order: image groups ascending, within a group
+//                                                  images ascending; identical on all ranks).
+// CTA = 64 features x 8 image groups (512 threads): thread (f, g) handles images g, g+8, ... with 8 loads
+// of x in flight (the load latency, not bandwidth, bounded the one-thread-per-feature version); its W
+// column sits in registers, dlogits rows in shared memory (broadcast reads); the 8 groups' dW partials
+// combine through shared memory.  CTA 0 also writes dbfc = sum_b dlogits.
+constexpr int kFcF = 64, kFcG = 8;   // features x image groups per CTA
+constexpr int kFcRows = 256;         // images per shared-memory dlogits chunk
+template <int OO>
+__global__ void __launch_bounds__(kFcF * kFcG) fc_bwd_cols(const float* __restrict__ dl, const float* __restrict__ x,
+                                                          const float* __restrict__ wg, float* __restrict__ dx,
+                                                          float* __restrict__ dwg, float* __restrict__ dbfc, Blocks g,
+                                                          int B, int O, int PW, int64_t F) {
+  __shared__ __align__(16) float dls[kFcRows][OO];
+  __shared__ float red[kFcG][OO][kFcF];
+  const int tx = threadIdx.x, ig = threadIdx.y, tid = ig * kFcF + tx;
+  const int64_t f = (int64_t)blockIdx.x * kFcF + tx;
   if (dbfc && blockIdx.x == 0) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int o = w; o < O; o += kFcCols / 32) {
+    const int w = tid >> 5, lane = tid & 31;
+    for (int o = w; o < O; o += kFcF * kFcG / 32) {
       float t = 0.f;
       for (int b = lane; b < B; b += 32) t += dl[(int64_t)b * O + o];
 #pragma unroll
@@ -963,49 +970,55 @@ __global__ void __launch_bounds__(kFcCols) fc_bwd_cols(const float* __restrict__
   const int kw = g.kw[r] > 0 ? g.kw[r] : 1;
   const int pos = (int)(rem / kw), slot = (int)(rem - (int64_t)pos * kw);
   const int64_t xo = g.start[r] + (int64_t)pos * g.Bp * kw + slot;
-  float w[kMaxO], acc[kMaxO];
+  float w[OO], acc[OO];
 #pragma unroll
-  for (int o = 0; o < kMaxO; ++o) {
+  for (int o = 0; o < OO; ++o) {
     w[o] = (valid && o < O) ? __ldg(wg + o * F + f) : 0.f;
     acc[o] = 0.f;
   }
   for (int b0 = 0; b0 < g.Bp; b0 += kFcRows) {
     const int nb = min(kFcRows, g.Bp - b0);
     __syncthreads();
-    for (int i = threadIdx.x; i < nb * kMaxO; i += kFcCols) {
-      const int row = i / kMaxO, o = i - row * kMaxO;
+    for (int i = tid; i < nb * OO; i += kFcF * kFcG) {
+      const int row = i / OO, o = i - row * OO;
       dls[row][o] = (b0 + row < B && o < O) ? __ldg(dl + (int64_t)(b0 + row) * O + o) : 0.f;
     }
     __syncthreads();
     if (!valid) continue;
-    for (int bb = 0; bb < nb; bb += 4) {
-      float xv[4];
+    for (int bb = ig; bb < nb; bb += 8 * kFcG) {
+      float xv[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = (bb + u < nb) ? __ldg(x + xo + (int64_t)(b0 + bb + u) * kw) : 0.f;
+      for (int u = 0; u < 8; ++u) {
+        const int b = bb + u * kFcG;
+        xv[u] = b < nb ? __ldg(x + xo + (int64_t)(b0 + b) * kw) : 0.f;
+      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (bb + u >= nb) break;
-        const float4* d4 = reinterpret_cast<const float4*>(dls[bb + u]);
-        float d[kMaxO];
-#pragma unroll
-        for (int q = 0; q < kMaxO / 4; ++q) {
-          const float4 v = d4[q];
-          d[4 * q] = v.x; d[4 * q + 1] = v.y; d[4 * q + 2] = v.z; d[4 * q + 3] = v.w;
-        }
+      for (int u = 0; u < 8; ++u) {
+        const int b = bb + u * kFcG;
+        if (b >= nb) break;
         float dxv = 0.f;
 #pragma unroll
-        for (int o = 0; o < kMaxO; ++o) {
-          dxv = fmaf(d[o], w[o], dxv);
-          acc[o] = fmaf(d[o], xv[u], acc[o]);
+        for (int o = 0; o < OO; ++o) {
+          const float d = dls[b][o];
+          dxv = fmaf(d, w[o], dxv);
+          acc[o] = fmaf(d, xv[u], acc[o]);
         }
-        if (dx) dx[xo + (int64_t)(b0 + bb + u) * kw] = dxv;
+        if (dx) dx[xo + (int64_t)(b0 + b) * kw] = dxv;
       }
     }
   }
-  if (valid && dwg)
 #pragma unroll
-    for (int o = 0; o < kMaxO; ++o)
-      if (o < O) dwg[o * F + f] = acc[o];
+  for (int o = 0; o < OO; ++o) red[ig][o][tx] = acc[o];
+  __syncthreads();
+  if (ig == 0 && valid && dwg)
+#pragma unroll
+    for (int o = 0; o < OO; ++o) {
+      if (o >= O) continue;
+      float t = red[0][o][tx];
+#pragma unroll
+      for (int q = 1; q < kFcG; ++q) t += red[q][o][tx];
+      dwg[o * F + f] = t;
+    }
 }
 
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
@@ -1193,7 +1206,8 @@ int cp_fc_forward(const float* x, int32_t B, int32_t Hp, int32_t Wp, const cp_pa
   float* part_buf = (float*)ws;
   cudaStream_t s = (cudaStream_t)stream;
   if (U > 0) {   // U == 0: no features on this rank (partitioned head) -> logits = bias (or 0)
-    fc_fwd_partial<<<dim3(U, (g.Bp + 127) / 128), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
+    if (O <= 10) fc_fwd_partial<10><<<dim3(U, (g.Bp + 127) / 128), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
+    else fc_fwd_partial<kMaxO><<<dim3(U, (g.Bp + 127) / 128), 256, 0, s>>>(x, wg, part_buf, g, B, O, PW, nsc);
     CP_LAUNCHED();
   }
   fc_fwd_reduce<<<cdiv((int64_t)B * O, 32), dim3(32, 32), 0, s>>>(part_buf, bfc, logits, U, g.Bp, B, O);
@@ -1220,8 +1234,9 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
   cudaStream_t s = (cudaStream_t)stream;
   if (dx || dwg || dbfc) {
     const int64_t F = (int64_t)PW * g.Cg;   // (0 features on this rank: one CTA computes dbfc only)
-    fc_bwd_cols<<<(unsigned)std::max<int64_t>(1, (F + kFcCols - 1) / kFcCols), kFcCols, 0, s>>>(
-        dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
+    const unsigned nblk = (unsigned)std::max<int64_t>(1, (F + kFcF - 1) / kFcF);
+    if (O <= 10) fc_bwd_cols<10><<<nblk, dim3(kFcF, kFcG), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
+    else fc_bwd_cols<kMaxO><<<nblk, dim3(kFcF, kFcG), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
     CP_LAUNCHED();
   }
   (void)ws;

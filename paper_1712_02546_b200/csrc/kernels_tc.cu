@@ -143,6 +143,8 @@ struct TcParams {
   float* push_dst[CP_MAX_RANKS];
   uint32_t* push_cnt[CP_MAX_RANKS];
   unsigned long long* push_stamp;  // timing only: globaltimer window of the push (atomic min start / max end)
+  int push_mc;             // 1: push_dst[0] / push_cnt[0] are NVLink multicast addresses (multimem)
+  int push_warps;          // warps per CTA pushing (1: warp 3; 2: warps 2 and 3), CP_TC_PUSH_WARPS
   uint32_t* push_claim;    // chunk claim counter (zero at launch): any resident CTA's warp 3 takes the next
   int npush, push_chunks;  // (peer, chunk) pair, so the gather completes as long as one CTA runs per rank
   long long push_n4;
@@ -768,8 +770,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         if (CG == 2) mma_commit_cg2(&tfull[acc]); else mma_commit(&tfull[acc]);
       }
     }
-  } else if (PASS == PASS_FWD && warp == 3) {
-    // ======================= gather pusher (otherwise idle warp): this rank's input block -> peers,
+  } else if (PASS == PASS_FWD && (warp == 3 || (warp == 2 && p.push_warps > 1))) {
+    // ======================= gather pushers (otherwise idle warps 3 and 2 - the latter after its TMEM
+    // allocation): this rank's input block -> peers,
     // full 512 B per warp store instruction, while the MMA warps consume the own block
     // peers in the order they consume this block (host-sorted: the peer that needs it soonest
     // first), all CTAs on one peer at a time so each peer's block completes as early as possible;
@@ -797,13 +800,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 #pragma unroll
             for (int u = 0; u < 8; ++u)
               if (i + 32 * u < e) v[u] = __ldg(src + i + 32 * u);
+            if (p.push_mc) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (i + 32 * u < e) dst[i + 32 * u] = v[u];
+              for (int u = 0; u < 8; ++u)
+                if (i + 32 * u < e)
+                  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                               :: "l"(dst + i + 32 * u), "f"(v[u].x), "f"(v[u].y), "f"(v[u].z), "f"(v[u].w)
+                               : "memory");
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (i + 32 * u < e) dst[i + 32 * u] = v[u];
+            }
           }
           __threadfence_system();
           __syncwarp();
-          if (lane == 0) red_add_release_sys(p.push_cnt[k], 1u);
+          if (lane == 0) {
+            if (p.push_mc)
+              asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" :: "l"(p.push_cnt[k]), "n"(1) : "memory");
+            else
+              red_add_release_sys(p.push_cnt[k], 1u);
+          }
         }
         if (p.push_stamp) t_last = globaltimer_ns();
       }
@@ -1998,6 +2015,8 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     p.push_n4 = gp->n4;
     p.push_chunks = gp->chunks;
     p.push_claim = gp->claim;
+    p.push_mc = gp->mc;
+    p.push_warps = env_int("CP_TC_PUSH_WARPS", 1);
     p.push_stamp = gp->stamp;
     p.arrive_target = (uint32_t)gp->chunks;
   }

@@ -290,9 +290,18 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
         CP_CUDA(cudaMemsetAsync(gp.stamp, 0xff, 8, s));
         CP_CUDA(cudaMemsetAsync(gp.stamp + 1, 0, 8, s));
       }
+      // NVLink multicast (CP_MULTICAST=1): one multimem store per 16 B reaches every rank's copy
+      // through the NVSwitch (and rewrites the own block with itself); the arrival counter [me] is
+      // raised on every rank by one multimem reduction per chunk
+      char* mc = (char*)comm_symmetric_mc(L->comm, x);
+      if (mc) {
+        gp.mc = 1;
+        gp.dst[gp.n] = (float*)mc + L->in.start[me];
+        gp.cnt[gp.n++] = (uint32_t*)(mc + ((char*)iflags[me] - (char*)x)) + me;
+      }
       // peer q walks its input blocks from its own upwards, so it needs this rank's block after
       // (me - q) mod P blocks: push to the soonest consumer first
-      for (int d = 1; d < L->d.world; ++d) {
+      for (int d = 1; d < L->d.world && !mc; ++d) {
         const int q = (me - d + L->d.world) % L->d.world;
         gp.dst[gp.n] = (float*)ipeers[q] + L->in.start[me];
         gp.cnt[gp.n++] = iflags[q] + me;
