@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libconvpart.so")
+LIB_PATH = os.environ.get("CP_LIB") or os.path.join(HERE, "libconvpart.so")   # CP_LIB: experiment builds
 
 CP_MAX_RANKS = 16
 CP_OK = 0

@@ -31,6 +31,7 @@ struct SymBuf {
   int index = -1;             // loopback: allocation sequence number (peers resolved by it)
   // NVLink multicast (CP_MULTICAST=1): the buffer is a driver VMM allocation bound to a multicast
   // object; `mc` maps it (a store / reduction through `mc` reaches every rank's copy via NVSwitch)
+  cudaEvent_t pending = nullptr;   // producer's deferred barrier, waited for by the consumer
   bool vmm = false;
   size_t map_bytes = 0;
   void* mc = nullptr;
@@ -543,6 +544,7 @@ extern "C" int cp_symmetric_wait(cp_comm c, void* local, void* stream) {
   uint32_t* flags[CP_MAX_RANKS];
   if (!cp::comm_symmetric_peers(c, local, peers, flags)) CP_FAIL(CP_ERR_ARG, "cp_symmetric_wait: not a symmetric buffer");
   cudaStream_t s = (cudaStream_t)stream;
+  if (cudaEvent_t pe = cp::comm_symmetric_take_pending(c, local)) CP_CUDA(cudaStreamWaitEvent(s, pe, 0));
   if (!cp::gather_push_in_epilogue()) CP_TRY(cp::comm_ce_distribute(c, local, s));
   CP_TRY(cp::launch_wait_flags(flags[c->rank], c->world, c->rank, s));
   CP_CUDA(cudaMemsetAsync(flags[c->rank], 0, CP_MAX_RANKS * sizeof(uint32_t), s));
@@ -714,6 +716,20 @@ int comm_loopback_defer(cp_comm c, cudaEvent_t done, std::function<int(const std
   g.pending.clear();
   for (auto& f : fns) CP_TRY(f(all));
   return CP_OK;
+}
+
+void comm_symmetric_set_pending(cp_comm c, const void* local, cudaEvent_t ev) {
+  auto it = c->sym.find(const_cast<void*>(local));
+  if (it != c->sym.end()) it->second.pending = ev;
+}
+
+cudaEvent_t comm_symmetric_take_pending(cp_comm c, const void* local) {
+  if (!c) return nullptr;
+  auto it = c->sym.find(const_cast<void*>(local));
+  if (it == c->sym.end()) return nullptr;
+  cudaEvent_t e = it->second.pending;
+  it->second.pending = nullptr;
+  return e;
 }
 
 // Multicast address of a symmetric buffer (nullptr unless it was set up with CP_MULTICAST=1).

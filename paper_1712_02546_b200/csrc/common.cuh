@@ -164,6 +164,7 @@ struct Layer {
   int dy_ready;           // epilogue-backward already computed for this step
   const void* dy_key[3];
   cudaEvent_t ev_compute, ev_comm;
+  cudaEvent_t ev_bar_fork = nullptr, ev_bar = nullptr;   // deferred gather barrier (comm stream)
   // optional per-pass GEMM timing (conv_part_timing): events around the tensor-core kernel launch
   int timing;
   cudaEvent_t ev_t[3][2];

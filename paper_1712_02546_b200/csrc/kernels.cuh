@@ -93,6 +93,10 @@ int comm_allgather_blocks(cp_comm c, float* buf, const Blocks& g, cudaStream_t s
 // symmetric (peer-mapped) buffer lookup: peers[r] = rank r's copy; flags[r] = rank r's arrival-flag
 // array (CP_MAX_RANKS u32, indexed by sender rank).  False if `local` is not a symmetric buffer.
 bool comm_symmetric_peers(cp_comm c, const void* local, void** peers, uint32_t** flags = nullptr);
+// deferred producer barrier of a symmetric gathered buffer: recorded by the producer's forward on the
+// comm stream, waited for (once) by the consumer's forward before it distributes its block
+void comm_symmetric_set_pending(cp_comm c, const void* local, cudaEvent_t ev);
+cudaEvent_t comm_symmetric_take_pending(cp_comm c, const void* local);
 // NVLink multicast address of a symmetric buffer (CP_MULTICAST=1), else nullptr
 void* comm_symmetric_mc(cp_comm c, const void* local);
 bool multicast_requested();

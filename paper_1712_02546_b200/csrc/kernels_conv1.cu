@@ -230,6 +230,16 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
       const uint32_t bph = p.nbuf == 2 ? ((ls >> 1) & 1) : (ls & 1);
       mbar_wait(&pfull[buf], bph);
       mbar_wait(&bempty[buf], bph ^ 1);
+#if defined(C1_EXP) && C1_EXP == 3
+      if (true) {   // experiment: no B build (timing only)
+        asm volatile("bar.sync 1, %0;" ::"n"(C1_BUILD_THREADS) : "memory");
+        if (t == 0) {
+          mbar_arrive(&bfull[buf]);
+          mbar_arrive(&pempty[buf]);
+        }
+        continue;
+      }
+#endif
       uint8_t* base = sB + buf * p.bset_bytes;
       const float* patch = sP + buf * (p.patch_bytes / 4);
       const int rows_per_img = 2 * g.ws;
@@ -288,9 +298,16 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
           const int cs = (cb == nblk - 1) ? max(0, g.ws - 16) : cb * 16;
           const int col0 = bl * 2 * g.ws + cs;
           uint32_t r0[16], r1[16];
+#if defined(C1_EXP) && C1_EXP == 2
+          continue;   // experiment: no TMEM reads, no epilogue
+#endif
           tmem_ld_x16_nowait(tb + col0, r0);
           tmem_ld_x16_nowait(tb + col0 + g.ws, r1);
           tmem_wait_ld();
+#if defined(C1_EXP) && C1_EXP == 1
+          if (r0[0] == 0x7fffffffu && r1[3] == 0x7fffffffu) p.out[0] = 1.f;   // experiment: loads only
+          continue;
+#endif
           const int bb = g.b0 + bl;
           if (kk >= p.Kc) continue;                    // rows past the own block (last M tile)
           const bool ok = bb < p.B && kk < p.Kr;       // padded image / padded kernel slot -> exact 0
@@ -313,6 +330,10 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
             if (z1 > best) { best = z1; code = 1; }
             if (z2 > best) { best = z2; code = 2; }
             if (z3 > best) { best = z3; code = 3; }
+#if defined(C1_EXP) && C1_EXP == 4
+            if (__float_as_uint(best) == 0x7fffffffu && code == 7) op[0] = 0.f;   // experiment: no stores
+            continue;
+#endif
             if (q >= q_lo && q < q_hi) {
               op[q * st] = ok ? tf32_round(best) : 0.f;
               sp[q * st] = ok ? (uint8_t)code : (uint8_t)0;

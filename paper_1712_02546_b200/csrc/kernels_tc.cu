@@ -93,6 +93,8 @@ struct TcParams {
   int numM, numN, split, units, chunks_per_split, chunks_total;  // numM counts M tiles per CTA group
   int bn_box;          // fwd: B box rows
   int nw;              // fwd: N tile width (balanced: Kc split into equal tiles)
+  int nlim;            // fwd (kernels on N): this launch computes own slots [0, nlim) (split forward: < Kc)
+  int m_off;           // fwd transposed: first own slot of M tile 0 (split forward: the remainder)
   int epi_groups;      // 1 or 2 epilogue warp groups (blockDim = 128 + 128*groups; CP_TC_EPI_GROUPS)
   int max_chunks;      // longest K loop of a unit (after split), for the launch heuristics
   int wide;            // MN-major operands loaded as one 5-D box of 32-column atoms (else per-atom boxes)
@@ -188,7 +190,7 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     const int ij = rest / nb;
     t.j = ij % p.Wp;
     t.i = ij / p.Wp;
-    t.n0 = t.mt * BM;
+    t.n0 = p.m_off + t.mt * BM;
     t.n = BN;
     return t;
   }
@@ -250,7 +252,7 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
   }
   if (PASS == PASS_FWD) {
     t.n0 = t.nt * p.nw;
-    t.n = min(p.nw, p.Kc - t.n0);
+    t.n = min(p.nw, p.nlim - t.n0);
   } else if (PASS == PASS_DGRAD) {
     t.rb = p.nt_rb[t.nt];
     t.n0 = p.nt_n0[t.nt];
@@ -1551,8 +1553,9 @@ struct Plan {
   int apb;                         // wgrad span: atoms per B box
 };
 
-static Plan fwd_plan(const Layer& L, TcParams& p) {
+static Plan fwd_plan(const Layer& L, TcParams& p, int kc = -1) {
   Plan w{};
+  if (kc < 0) kc = L.Kc;   // own slots computed on N by this launch (split forward: the 256-multiple part)
   w.pair = use_pairs() && (L.Bp / 32) % 2 == 0;
   const int CG = w.pair ? 2 : 1;
   int cpt = 0;
@@ -1562,17 +1565,17 @@ static Plan fwd_plan(const Layer& L, TcParams& p) {
   // Balanced N tiles: Kc split into T equal tiles (width a multiple of 16 / 8).  Choose T by
   // rounds of CTA groups x per-chunk time, the latter ~ bytes staged per chunk (A 16 KB + B
   // columns): the kernel is bound by operand delivery, not by MMA issue.
-  if (L.Kc == 0) {   // a rank without kernels in this layer: no forward GEMM units
+  if (kc == 0) {   // a rank without kernels in this layer: no forward GEMM units
     p.nw = BN;
     w.numN = 0;
   } else {
     const int gran = CG == 2 ? 16 : 8, groups = num_sms() / CG;
     double best = 1e300;
-    int bestT = (L.Kc + BN - 1) / BN;
-    for (int T = (L.Kc + BN - 1) / BN; T <= (L.Kc + BN - 1) / BN + 4; ++T) {
-      const int nw = ((L.Kc + T - 1) / T + gran - 1) / gran * gran;
+    int bestT = (kc + BN - 1) / BN;
+    for (int T = (kc + BN - 1) / BN; T <= (kc + BN - 1) / BN + 4; ++T) {
+      const int nw = ((kc + T - 1) / T + gran - 1) / gran * gran;
       if (nw > BN || nw <= 0) continue;
-      const int tiles = (L.Kc + nw - 1) / nw;
+      const int tiles = (kc + nw - 1) / nw;
       const int units = w.numM * tiles;
       double rounds = std::ceil((double)units / groups);
       const int last = units - ((int)rounds - 1) * groups;    // tiles in the last round
@@ -1588,7 +1591,7 @@ static Plan fwd_plan(const Layer& L, TcParams& p) {
     if (env_int("CP_TC_FWD_NW", 0) > 0) p.nw = env_int("CP_TC_FWD_NW", 0);
     if (p.nw <= 0) p.nw = BN;
     (void)bestT;
-    w.numN = (L.Kc + p.nw - 1) / p.nw;
+    w.numN = (kc + p.nw - 1) / p.nw;
   }
   w.chunks = p.R * p.S * cpt;
   // forward split-K re-reads the whole pre-pool tile from HBM; measured slower at every P, so it
@@ -1897,14 +1900,18 @@ int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s) {
   return CP_OK;
 }
 
-int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
-           cudaStream_t s, float* const* peer_blocks, int npeers, const uint32_t* arrive, const GatherPush* gp) {
-  if (L.Kc == 0) return CP_OK;
+// One forward GEMM launch over own slots [0, kc) on N (kernels-on-N kernels) or, transposed, over
+// [m_off, Kc) on M; force_T: -1 = CP_TC_FWD_T, 0/1 = off/on.  `push`: this launch runs the gather push.
+static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved,
+                       void* ws, cudaStream_t s, float* const* peer_blocks, int npeers, const uint32_t* arrive,
+                       const GatherPush* gp, int kc, int m_off, int force_T, bool push, bool mark0, bool mark1) {
   if ((L.Ho & 1) || (L.Wo & 1))
     CP_FAIL(CP_ERR_UNSUPPORTED, "tcgen05 forward needs an even conv output grid (2x2 window tiles)");
   TcParams p{};
   fill_common(p, L);
-  const Plan pl = fwd_plan(L, p);
+  const Plan pl = fwd_plan(L, p, kc);
+  p.nlim = kc;
+  p.m_off = m_off;
   const int es = op_bytes(L), E = 128 / es;
   // halo A boxes (see TcParams::halo): CTA pairs (the 2-stage halo ring fills the 6-stage A region),
   // tf32, S <= 5 (2 x (S+1) x 8 KB <= 96 KB).  Measured 5-8 % SLOWER than one box per tap at P = 1/2/4
@@ -1917,7 +1924,8 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   // operand bytes per MAC (L2-bound, ~0.5 us per K-chunk): same-box A/B at P=4 0.206 vs 0.200 ms for
   // the pair kernel, slower at P=1/2/8 as well -> off unless CP_TC_FWD_T=1 (parity-tested; the base
   // for a CTA-pair transposed kernel)
-  p.fwdT = (es == 4 && L.d.pool && L.Bp % 64 == 0 && env_int(L.images ? "CP_TC_FWD_T_IMAGES" : "CP_TC_FWD_T", 0)) ? 1 : 0;
+  p.fwdT = (es == 4 && L.d.pool && L.Bp % 64 == 0 &&
+            (force_T >= 0 ? force_T : env_int(L.images ? "CP_TC_FWD_T_IMAGES" : "CP_TC_FWD_T", 0))) ? 1 : 0;
 #ifdef CP_TC_HALO_HOOK
   const bool halo_hook = true;
 #else
@@ -1992,7 +2000,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   p.units = p.numM * p.numN * pl.S;
   p.max_chunks = (pl.chunks + pl.S - 1) / pl.S;
   if (p.fwdT) {
-    p.numM = (L.Kc + BM - 1) / BM;
+    p.numM = (L.Kc - p.m_off + BM - 1) / BM;
     p.numN = L.Hp * L.Wp * (L.Bp / 64);
     p.split = 1;
     p.units = p.numM * p.numN;
@@ -2007,7 +2015,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
   p.arrive_target = 1;
   if (gp && !L.images) {
     p.push_src = gp->src;
-    p.npush = gp->n;
+    p.npush = push ? gp->n : 0;
     for (int k = 0; k < gp->n; ++k) {
       p.push_dst[k] = gp->dst[k];
       p.push_cnt[k] = gp->cnt[k];
@@ -2017,7 +2025,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     p.push_claim = gp->claim;
     p.push_mc = gp->mc;
     p.push_warps = env_int("CP_TC_PUSH_WARPS", 1);
-    p.push_stamp = gp->stamp;
+    p.push_stamp = push ? gp->stamp : nullptr;
     p.arrive_target = (uint32_t)gp->chunks;
   }
   float* part = (float*)((char*)ws + L.off_split);
@@ -2043,7 +2051,7 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
         ti.bc0[k] = (rest % nb) * 64;
         ti.j[k] = ij % L.Wp;
         ti.i[k] = ij / L.Wp;
-        ti.n0[k] = mt * BM;
+        ti.n0[k] = p.m_off + mt * BM;
         ti.ncol[k] = BM;
       }
       for (int k = 0; k < T && !p.fwdT; ++k) {         // host mirror of decode_unit<FWD>
@@ -2054,14 +2062,14 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
         ti.j[k] = ij % W2;
         ti.i[k] = ij / W2;
         ti.n0[k] = nt * p.nw;
-        ti.ncol[k] = std::min(p.nw, L.Kc - ti.n0[k]);
+        ti.ncol[k] = std::min(p.nw, kc - ti.n0[k]);
       }
     }
   }
-  CP_TRY(tc_time_mark(L, PASS_FWD, 0, s));
+  if (mark0) CP_TRY(tc_time_mark(L, PASS_FWD, 0, s));
   if (es == 2) CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2, 1>(p, s) : launch_cg<PASS_FWD, 1, 1>(p, s)));
   else CP_TRY(((pl.pair && !p.fwdT) ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
-  CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
+  if (mark1) CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
   if (p.tail_np > 0 && p.fwdT) {
     fwd_tail_finish_t<<<dim3(BM, ti.n), 64, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
     CP_LAUNCHED();
@@ -2080,6 +2088,30 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
     CP_LAUNCHED();
   }
   return CP_OK;
+}
+
+// Split forward (CP_TC_FWD_SPLIT=1; off by default - measured no faster at P=4 on one GPU, 0.194 ->
+// 0.192 ms, and 70 us slower inside the fused 4-GPU step, profiles/r02_fwd_split.txt): a TF32 MMA costs the same for any N <= 256,
+// so an own-slot count just above a multiple of 256 (P=4 of the paper net: 375 = 256 + 119) wastes a
+// whole N tile.  Then the CTA-pair kernel computes the 256-multiple part with full 256-wide N tiles
+// and the transposed CTA-local kernel the remainder on M (119 of 128 TMEM lanes used, N = 256
+// pixels x images): 375 slots cost 256 + 128 MMA columns instead of 2 x 256.  Both launches write
+// disjoint slots of the same output block; the first runs the gather push, both wait for arrivals.
+int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved, void* ws,
+           cudaStream_t s, float* const* peer_blocks, int npeers, const uint32_t* arrive, const GatherPush* gp) {
+  if (L.Kc == 0) return CP_OK;
+  const int rem = L.Kc % BN;
+  const bool split = op_bytes(L) == 4 && !L.images && L.d.pool && L.Bp % 64 == 0 && use_pairs() &&
+                     (L.Bp / 32) % 2 == 0 && L.Kc > BN && rem >= 64 && rem <= BM &&
+                     env_int("CP_TC_FWD_SPLIT", 0) && !env_int("CP_TC_FWD_T", 0) && env_int("CP_TC_SPLIT_FWD", 1) == 1 &&
+                     env_int("CP_TC_FWD_NW", 0) == 0 && !env_int("CP_TC_FWD_HALO", 0);
+  if (!split)
+    return tc_fwd_part(L, xin, w, b, y_block, saved, ws, s, peer_blocks, npeers, arrive, gp, L.Kc, 0, -1, true, true,
+                       true);
+  const int k1 = L.Kc - rem;
+  CP_TRY(tc_fwd_part(L, xin, w, b, y_block, saved, ws, s, peer_blocks, npeers, arrive, gp, k1, 0, 0, true, true, false));
+  return tc_fwd_part(L, xin, w, b, y_block, saved, ws, s, peer_blocks, npeers, arrive, gp, L.Kc, k1, 1, false, false,
+                     true);
 }
 
 int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s, float* const* dst_blocks) {

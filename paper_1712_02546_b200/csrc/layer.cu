@@ -216,6 +216,8 @@ int conv_part_destroy(cp_layer L) {
       if (L->ev_t[p][e]) cudaEventDestroy(L->ev_t[p][e]);
   if (L->ev_compute) cudaEventDestroy(L->ev_compute);
   if (L->ev_comm) cudaEventDestroy(L->ev_comm);
+  if (L->ev_bar_fork) cudaEventDestroy(L->ev_bar_fork);
+  if (L->ev_bar) cudaEventDestroy(L->ev_bar);
 
   delete L;
   return CP_OK;
@@ -267,12 +269,32 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
         peer_blocks[npeers++] = (float*)peers[r] + L->out.start[me];
       }
     comm_symmetric_set_own(L->comm, y, L->out.start[me], L->out.start[me + 1] - L->out.start[me]);
-    CP_TRY(comm_barrier(L->comm, s));
+    if (!epi_push && cs != s && !comm_is_loopback(L->comm)) {
+      // Nothing but this rank writes its own copy's own block, so only the consumer's distribution
+      // (the push into the peers' copies, or their copy-engine copies) must wait for the barrier: it
+      // runs on the comm stream, overlapped with this layer's GEMM, and the consumer's forward waits
+      // for it (comm_symmetric_take_pending) - rank skew and the barrier latency hide behind conv1.
+      if (!L->ev_bar) {
+        CP_CUDA(cudaEventCreateWithFlags(&L->ev_bar_fork, cudaEventDisableTiming));
+        CP_CUDA(cudaEventCreateWithFlags(&L->ev_bar, cudaEventDisableTiming));
+      }
+      CP_CUDA(cudaEventRecord(L->ev_bar_fork, s));
+      CP_CUDA(cudaStreamWaitEvent(cs, L->ev_bar_fork, 0));
+      CP_TRY(comm_barrier(L->comm, cs));
+      CP_CUDA(cudaEventRecord(L->ev_bar, cs));
+      comm_symmetric_set_pending(L->comm, y, L->ev_bar);
+    } else {
+      CP_TRY(comm_barrier(L->comm, s));
+    }
   }
   void* ipeers[CP_MAX_RANKS];
   uint32_t* iflags[CP_MAX_RANKS];
   const bool sym_in = !L->images && L->comm && L->d.world > 1 && comm_symmetric_peers(L->comm, x, ipeers, iflags);
   const uint32_t* arrive = sym_in ? iflags[me] : nullptr;
+  if (sym_in) {   // the producer's deferred barrier: no peer still reads its copy of the previous step
+    cudaEvent_t pe = comm_symmetric_take_pending(L->comm, x);
+    if (pe) CP_CUDA(cudaStreamWaitEvent(s, pe, 0));
+  }
   const bool has_gemm = L->Kr > 0 || L->Kc > 0;
   GatherPush gp{};
   bool kernel_push = false;
@@ -380,8 +402,10 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
     float* dst[CP_MAX_RANKS];
     uint32_t* signal[CP_MAX_RANKS];
     int ns = 0;
+    // CP_RS_LOCAL_DIAG=1 (timing diagnostic, WRONG results): every partial into the own copy's slots
+    static const int rs_local_diag = tc_env_int("CP_RS_LOCAL_DIAG", 0);
     for (int q = 0; q < L->in.n; ++q) {
-      dst[q] = (float*)peers[q] + slots0 + (int64_t)me * mb;
+      dst[q] = (float*)peers[rs_local_diag ? me : q] + slots0 + (int64_t)(rs_local_diag ? q : me) * mb;
       if (q != me) signal[ns++] = pflags[q];
     }
     if (!ordered) CP_TRY(comm_barrier(L->comm, s));   // no rank still sums last call's slots

@@ -49,6 +49,8 @@ dx = torch.zeros(sz.dx // 4, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 s = torch.cuda.current_stream()
 t = {"fwd": [], "wgrad": [], "dgrad": []}
+g = {"fwd": [], "dgrad": [], "wgrad": []}   # the tcgen05 GEMM launch alone (conv_part_timing events)
+cp.conv_part_timing(h, True)
 for r in range(a.reps + 2):
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     flush.fill_(r)
@@ -64,9 +66,15 @@ for r in range(a.reps + 2):
         t["fwd"].append(e[0].elapsed_time(e[1]))
         t["wgrad"].append(e[1].elapsed_time(e[2]))
         t["dgrad"].append(e[2].elapsed_time(e[3]))
+        for k, pss in (("fwd", 0), ("dgrad", 1), ("wgrad", 2)):
+            g[k].append(cp.conv_part_kernel_time(h, pss))
 Kr = p2.k_count[0]
 flop = 2.0 * B * Kr * a.K1 * 25 * (a.H - 4) ** 2
 med = {k: sorted(v)[len(v) // 2] for k, v in t.items()}
-print(json.dumps({"variant": vars(a), "cta_group": os.environ.get("CP_TC_CTA_GROUP", "2"),
-                  "ms": med, "tflops": {k: flop / (v / 1e3) / 1e12 for k, v in med.items()}}))
+gm = {k: sorted(v)[len(v) // 2] for k, v in g.items()}
+peak = 1651.7 * 1.1 / 2.25
+print(json.dumps({"variant": vars(a), "cta_group": os.environ.get("CP_TC_CTA_GROUP", "2"), "own_kernels": Kr,
+                  "ms": med, "tflops": {k: flop / (v / 1e3) / 1e12 for k, v in med.items()},
+                  "gemm_ms": gm, "gemm_tflops": {k: flop / (v / 1e3) / 1e12 for k, v in gm.items() if v > 0},
+                  "gemm_frac_of_807": {k: flop / (v / 1e3) / 1e12 / peak for k, v in gm.items() if v > 0}}))
 cp.conv_part_destroy(h)

@@ -63,8 +63,22 @@ PB = [(1, 40, 8), (2, 40, 8), (3, 40, 8), (1, 20, 8), (2, 40, 32), (4, 40, 32), 
 @pytest.mark.parametrize("math", MATHS)
 @pytest.mark.parametrize("P,B,align", PB)
 def test_forward_parity(orc, math, P, B, align):
+    _forward_parity(orc, math, P, B, align)
+
+
+# Split forward (tc_fwd): own-slot counts just above a multiple of 256 run as a CTA-pair launch over the
+# 256-multiple part + a transposed launch over the remainder (rank 0 of P=4 in the paper net: 375 slots).
+# K2 = 330 at P=1 -> 336 slots (256 + 80); K2 = 750 at P=2 -> 376 (256 + 120); B = 64 / 128 (pair chunks)
+@pytest.mark.parametrize("split", ["1", "0"])
+@pytest.mark.parametrize("P,B,K2", [(1, 64, 330), (2, 64, 750), (2, 128, 750)])
+def test_split_forward_parity(orc, monkeypatch, split, P, B, K2):
+    monkeypatch.setenv("CP_TC_FWD_SPLIT", split)
+    _forward_parity(orc, "tf32", P, B, 8, K2=K2, K1=40)
+
+
+def _forward_parity(orc, math, P, B, align, K2=300, K1=70):
     m = math_id(math)
-    x, w1, b1, w2, b2 = layer_data(B=B)
+    x, w1, b1, w2, b2 = layer_data(B=B, K1=K1, K2=K2)
     B, K1, K2 = x.shape[0], w1.shape[0], w2.shape[0]
     p1, p2 = parts_for(P, K1, align), parts_for(P, K2, align)
     L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
