@@ -95,10 +95,10 @@ typedef enum {
   CP_DX_ORDERED = 64         /* OR-flag (fused reduce-scatter only).  PRECONDITION: between two
                                 consecutive backward_data calls of this layer, every rank
                                 passes a cross-rank synchronising operation that is ordered
-                                after its previous slot sum on every rank (PartitionedNet: the
+                                after its previous dX sum on every rank (PartitionedNet: the
                                 next forward's gather barrier or logits AllReduce, which all
                                 ranks enter only after joining the dX stream).  Then no rank can
-                                store into a receive slot a peer is still summing, and the
+                                overwrite partials a peer is still summing, and the
                                 overwrite-guard barrier is skipped.  Without that guarantee the
                                 flag races: omit it.                                      */
 } cp_dx_mode;
@@ -247,12 +247,16 @@ int conv_part_forward(cp_layer layer, const float* x, const float* w, const floa
  * CP_DX_ASYNC flag and comm_stream != stream, `stream` is not made to wait for the
  * collective: call conv_part_wait(layer, stream) before consuming dx.
  * Fused reduce-scatter (SURVEY §8(f) f1, TF32 path): when dx is a symmetric buffer of
- * at least dx_peer bytes (cp_symmetric_alloc) and dx_mode is CP_DX_REDUCE_SCATTER, the
- * dgrad epilogue stores each input block's partial straight into its owner's receive
- * slot (peers over NVLink), sets this rank's arrival flag at every peer, and the sum of
- * the n_ranks slots (ascending rank order) lands in this rank's block of dx on
- * comm_stream - no NCCL collective.  Unless CP_DX_ORDERED is given, a one-word
- * AllReduce first guards the receive slots against overwrite while a peer still sums. */
+ * at least dx_peer bytes (cp_symmetric_alloc) and dx_mode is CP_DX_REDUCE_SCATTER, no
+ * NCCL collective runs.  Default ("push"): the dgrad epilogue stores each input block's
+ * partial straight into its owner's receive slot behind the gather layout (peers over
+ * NVLink), sets this rank's arrival flag at every peer, and on comm_stream the owner sums
+ * the n_ranks slots in ascending rank order into its block of dx.  CP_RS_MODE=pull / ce
+ * (environment): the dgrad writes every partial into this rank's own copy of dx, sets its
+ * ready flag at every peer, and each owner fetches its block's partials from all copies
+ * over NVLink (SM loads / copy-engine copies into its receive slots) and sums them in the
+ * same order - the same bits.  Unless CP_DX_ORDERED is given, a cross-rank barrier first
+ * guards the slots / partials against overwrite while an owner still reads them. */
 int conv_part_backward_data(cp_layer layer, const float* dy_gathered, const uint8_t* saved,
                             const float* y_gathered, const float* w, float* dx, int32_t dx_mode,
                             void* workspace, void* stream, void* comm_stream);

@@ -571,13 +571,11 @@ __global__ void __launch_bounds__(512) oneshot_allreduce_kernel(float* buf, int 
     float* dst = peers.s[q] + ((int64_t)par * world + me) * kArMax;
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = buf[i];
   }
-  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    ctl[kCtlArEpoch] = e;
-    for (int q = 0; q < world; ++q)
-      if (q != me) cp::st_release_sys(peers.c[q] + kCtlArFlags + me, e);
-  }
+  if (threadIdx.x == 0) ctl[kCtlArEpoch] = e;
+  // one release per peer, in parallel (thread q): the barrier orders every thread's slot stores
+  // before thread q's release (fence cumulativity), so no per-thread fence is needed
+  if (threadIdx.x < world && (int)threadIdx.x != me) cp::st_release_sys(peers.c[threadIdx.x] + kCtlArFlags + me, e);
   if (threadIdx.x < world && (int)threadIdx.x != me) {
     const long long t0 = clock64();
     while ((int)(cp::ld_acquire_sys(ctl + kCtlArFlags + threadIdx.x) - e) < 0) {
@@ -688,8 +686,10 @@ int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks
   if (it == c->sym.end()) CP_FAIL(CP_ERR_ARG, "not a symmetric buffer");
   const SymBuf& sb = it->second;
   if (sb.own_off < 0) CP_FAIL(CP_ERR_STATE, "symmetric gather: no producer wrote this buffer yet");
-  for (int q = 0; q < c->world; ++q) {
-    if (q == c->rank) continue;
+  // peers in the order they consume this block (peer q walks its input blocks from its own upwards,
+  // so it needs this rank's block after (rank - q) mod P blocks): the soonest consumer first
+  for (int d = 1; d < c->world; ++d) {
+    const int q = (c->rank - d + c->world) % c->world;
     if (sb.own_elems)
       CP_CUDA(cudaMemcpyAsync((float*)sb.peers[q] + sb.own_off, (const float*)local + sb.own_off,
                               (size_t)sb.own_elems * 4, cudaMemcpyDeviceToDevice, s));

@@ -165,6 +165,7 @@ struct Layer {
   const void* dy_key[3];
   cudaEvent_t ev_compute, ev_comm;
   cudaEvent_t ev_bar_fork = nullptr, ev_bar = nullptr;   // deferred gather barrier (comm stream)
+  cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;     // copy-engine gather on the comm stream
   // optional per-pass GEMM timing (conv_part_timing): events around the tensor-core kernel launch
   int timing;
   cudaEvent_t ev_t[3][2];

@@ -63,6 +63,8 @@ int tc_fwd(Layer& L, const float* xin, const float* w, const float* b, float* y_
 int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cudaStream_t s,
              float* const* dst_blocks = nullptr);
 // dx_own = sum over q (ascending) of the P receive slots (fused reduce-scatter epilogue)
+// pull reduce-scatter: out = sum over r ascending of src[r] (n floats, 16-byte aligned blocks)
+int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64_t n, cudaStream_t s);
 int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float* out, int64_t n, cudaStream_t s);
 int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s);
 void tc_release(Layer& L);

@@ -545,6 +545,40 @@ int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float
   return CP_OK;
 }
 
+// pull reduce-scatter: out[e] = sum_{r ascending} src[r][e] (float4; src[r] = rank r's partial of the
+// own block, read from its copy over NVLink).  Every rank's load of an element is issued before the sum
+// (NVLink read latency); in place when out == src[self] (the same thread reads, then writes).
+struct SrcPtrs {
+  const float* p[CP_MAX_RANKS];
+};
+__global__ void __launch_bounds__(256) sum_peer_blocks_kernel(SrcPtrs src, int n_src, float* out, int64_t n4) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= n4) return;
+  float4 v[CP_MAX_RANKS];
+#pragma unroll
+  for (int r = 0; r < CP_MAX_RANKS; ++r)
+    if (r < n_src) v[r] = reinterpret_cast<const float4*>(src.p[r])[i];
+  float4 a = v[0];
+#pragma unroll
+  for (int r = 1; r < CP_MAX_RANKS; ++r)
+    if (r < n_src) {
+      a.x += v[r].x; a.y += v[r].y; a.z += v[r].z; a.w += v[r].w;
+    }
+  reinterpret_cast<float4*>(out)[i] = a;
+}
+int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return CP_OK;
+  if (n & 3) CP_FAIL(CP_ERR_UNSUPPORTED, "sum_peer_blocks: size not a multiple of 4");
+  SrcPtrs sp{};
+  for (int r = 0; r < n_src; ++r) {
+    if (reinterpret_cast<uintptr_t>(src[r]) & 15) CP_FAIL(CP_ERR_UNSUPPORTED, "sum_peer_blocks: unaligned block");
+    sp.p[r] = src[r];
+  }
+  sum_peer_blocks_kernel<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(sp, n_src, out, n / 4);
+  CP_LAUNCHED();
+  return CP_OK;
+}
+
 struct FlagPtrs {
   uint32_t* f[CP_MAX_RANKS];
 };

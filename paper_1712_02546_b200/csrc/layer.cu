@@ -218,9 +218,26 @@ int conv_part_destroy(cp_layer L) {
   if (L->ev_comm) cudaEventDestroy(L->ev_comm);
   if (L->ev_bar_fork) cudaEventDestroy(L->ev_bar_fork);
   if (L->ev_bar) cudaEventDestroy(L->ev_bar);
+  if (L->ev_gfork) cudaEventDestroy(L->ev_gfork);
+  if (L->ev_gjoin) cudaEventDestroy(L->ev_gjoin);
 
   delete L;
   return CP_OK;
+}
+
+static bool gather_on_copy_engines() {   // CP_GATHER_MODE=ce (A/B; default: in-kernel push)
+  const char* e = getenv("CP_GATHER_MODE");
+  return e && strcmp(e, "ce") == 0;
+}
+
+// fused reduce-scatter variant, read per call (tests switch it between layers): 0 push (default: the dgrad
+// epilogue stores each partial into its owner's receive slot), 1 pull (owners read the partials with SM
+// loads), 2 ce (owners copy the partials into their receive slots with the copy engines)
+static int rs_mode() {
+  const char* e = getenv("CP_RS_MODE");
+  if (e && strcmp(e, "pull") == 0) return 1;
+  if (e && strcmp(e, "ce") == 0) return 2;
+  return 0;
 }
 
 int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b, float* y, uint8_t* saved,
@@ -297,10 +314,23 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
   }
   const bool has_gemm = L->Kr > 0 || L->Kc > 0;
   GatherPush gp{};
-  bool kernel_push = false;
+  bool kernel_push = false, ce_forked = false;
   if (sym_in && !epi_push) {
     const int64_t n = L->in.start[me + 1] - L->in.start[me];
-    if (tf32 && has_gemm) {
+    if (tf32 && has_gemm && gather_on_copy_engines() && cs != s && !comm_is_loopback(L->comm)) {
+      // CP_GATHER_MODE=ce: the copy engines distribute this rank's block (need order, one flag per
+      // peer after its copy) on the comm stream while the GEMM runs and waits for its arrivals; no SM
+      // work for the transfer
+      if (!L->ev_gfork) {
+        CP_CUDA(cudaEventCreateWithFlags(&L->ev_gfork, cudaEventDisableTiming));
+        CP_CUDA(cudaEventCreateWithFlags(&L->ev_gjoin, cudaEventDisableTiming));
+      }
+      CP_CUDA(cudaEventRecord(L->ev_gfork, s));
+      CP_CUDA(cudaStreamWaitEvent(cs, L->ev_gfork, 0));
+      CP_TRY(comm_ce_distribute(L->comm, x, cs, true));
+      CP_CUDA(cudaEventRecord(L->ev_gjoin, cs));
+      ce_forked = true;
+    } else if (tf32 && has_gemm) {
       kernel_push = true;
       gp.src = x + L->in.start[me];
       gp.n4 = n / 4;
@@ -357,6 +387,7 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
   }
   // reset the arrival counters and the push claim counter (the whole 256 B flag line)
   if (sym_in) CP_CUDA(cudaMemsetAsync((void*)arrive, 0, 256, s));
+  if (ce_forked) CP_CUDA(cudaStreamWaitEvent(s, L->ev_gjoin, 0));   // own outgoing copies done
   if (push_in_epilogue) {
     CP_TRY(launch_signal_peers(signal, npeers, me, s));
   } else if (gathered_out && !sym_out) {
@@ -367,6 +398,8 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
   return CP_OK;
 }
 
+// fused reduce-scatter variant: pull (default; owners read the partials) or push (CP_RS_MODE=push: the
+// dgrad epilogue stores each partial into its owner's receive slot)
 int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved, const float* y_g, const float* w,
                             float* dx, int32_t dx_mode, void* ws, void* stream, void* comm_stream) {
   if (!L || !dy_g || !y_g || !w || !dx || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_backward_data: null pointer");
@@ -394,6 +427,56 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
   }
   const bool fused = L->d.math != CP_MATH_FP32_SIMT && !L->images && L->comm && L->d.world > 1 &&
                      dx_mode == CP_DX_REDUCE_SCATTER && comm_symmetric_peers(L->comm, dx, peers, pflags);
+  // Pull variants (CP_RS_MODE=pull / ce): the dgrad writes every partial block into this rank's OWN copy
+  // (plain local epilogue), raises "partials ready" at every peer, and each owner's comm-stream tail
+  // fetches its block's partials from all copies over NVLink - SM loads (pull) or copy-engine copies
+  // into its receive slots (ce) - and sums them in rank order; the transfer overlaps the next GEMM
+  // (wgrad) instead of slowing the dgrad epilogue with peer stores.
+  const int rsm = fused ? rs_mode() : 0;
+  if (rsm != 0) {
+    const int me = L->d.rank, world = L->d.world;
+    uint32_t* signal[CP_MAX_RANKS];
+    int ns = 0;
+    for (int q = 0; q < world; ++q)
+      if (q != me) signal[ns++] = pflags[q];
+    if (!ordered) CP_TRY(comm_barrier(L->comm, s));   // no owner still reads last call's partials
+    if (L->Kr > 0 && L->Kc > 0) {
+      CP_TRY(tc_dgrad(*L, dYg, wg, dx, ws, s));
+    } else {   // no own kernels: zero partials (the owners still read them)
+      CP_TRY(launch_fill(dx, 0.f, L->in.start[L->in.n], s));
+    }
+    CP_TRY(launch_signal_peers(signal, ns, me, s));
+    CP_CUDA(cudaEventRecord(L->ev_compute, s));
+    uint32_t* own_flags = pflags[me];
+    const int64_t off = L->in.start[me], n_own = L->in.start[me + 1] - L->in.start[me];
+    int64_t mb = 0;
+    for (int r = 0; r < L->in.n; ++r) mb = std::max(mb, L->in.start[r + 1] - L->in.start[r]);
+    float* slots = dx + L->in.start[L->in.n];   // receive slots behind the gather layout (ce mode)
+    const float* src[CP_MAX_RANKS];
+    const float* remote[CP_MAX_RANKS];
+    for (int r = 0; r < world; ++r) {
+      remote[r] = (const float*)peers[r] + off;
+      src[r] = (rsm == 2 && r != me) ? slots + (int64_t)r * mb : remote[r];
+    }
+    float* own = dx + off;
+    cp_layer_s* Lp = L;
+    std::vector<const float*> srcv(src, src + world), remv(remote, remote + world);
+    auto tail = [=](const std::vector<cudaEvent_t>& computed) -> int {
+      for (cudaEvent_t e : computed) CP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+      CP_TRY(launch_wait_flags(own_flags, world, me, cs));
+      if (rsm == 2)   // copy engines: every peer's partial of the own block into its local receive slot
+        for (int r = 0; r < world; ++r)
+          if (r != me && n_own)
+            CP_CUDA(cudaMemcpyAsync((void*)srcv[r], remv[r], (size_t)n_own * 4, cudaMemcpyDeviceToDevice, cs));
+      CP_TRY(launch_sum_peer_blocks(srcv.data(), world, own, n_own, cs));
+      CP_CUDA(cudaMemsetAsync(own_flags, 0, CP_MAX_RANKS * sizeof(uint32_t), cs));
+      CP_CUDA(cudaEventRecord(Lp->ev_comm, cs));
+      if (!(async && cs != s)) CP_CUDA(cudaStreamWaitEvent(s, Lp->ev_comm, 0));
+      return CP_OK;
+    };
+    if (comm_is_loopback(L->comm)) return comm_loopback_defer(L->comm, L->ev_compute, tail);
+    return tail(std::vector<cudaEvent_t>{L->ev_compute});
+  }
   if (fused) {
     int64_t mb = 0;
     for (int r = 0; r < L->in.n; ++r) mb = std::max(mb, L->in.start[r + 1] - L->in.start[r]);

@@ -28,6 +28,12 @@ from paper_1712_02546_b200 import convpart as cp  # noqa: E402
 from paper_1712_02546_b200.net import PartitionedNet  # noqa: E402
 
 
+def _log(rank, msg):
+    """progress on stderr (rank 0): locates a failing case in the torchrun log"""
+    if rank == 0:
+        print(f"[multi_gpu_check] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -54,6 +60,7 @@ def main():
             # input block of conv2: empty push, zero partial), rank 0 no conv2 kernel (copy-engine gather)
             ("zero-kernel-ranks+RS+fused+partitioned-head", cp.CP_DX_REDUCE_SCATTER, "zero", "partitioned", True),
             ("zero-kernel-ranks+RS+fused+replicated-head", cp.CP_DX_REDUCE_SCATTER, "zero", "replicated", True)]:
+        _log(rank, mode_name)
         net = synth.NetSpec(kernels=(36, 72), in_hw=20, name="multi")
         B = 40
         if times == "zero":
@@ -259,6 +266,7 @@ def main():
             ("paper net", "partitioned", None, 128, None), ("paper net", "replicated", None, 128, None),
             ("paper net B=1024, Eq. 1 partition (configs[3])", "partitioned", None, 1024, uneven),
             ("scaled net (configs[4])", "partitioned", synth.scaled_net(), 256, None)]:
+        _log(rank, f"full size: {name}, {head} head")
         net, parts, pn, params, x, y = bench_setup(world, rank, comm, dev, net=net, B=B, head=head, times=times)
         failures += [f"{name}, {head} head: {m}" for m in check_step(pn, net, parts, params, x, y, rank, world,
                                                                      allgather, n=256)]

@@ -5,9 +5,9 @@ every rank has its own copy of each symmetric buffer, and the SAME library paths
 conv1's device barrier + local block write, conv2's forward kernel pushing its own input block into
 every peer's copy from its warp 3 (chunk claims, release-adds on the peers' arrival counters) while
 it consumes its own block first (the fused channel AllGather, Alg. 1 L19-22 P:L178-182, "reshapes
-and rearranges" P:L235), and conv2's dgrad epilogue storing each input block's partial into its
-owner's receive slot, the owner summing the P slots in rank order (the fused reduce-scatter of dX,
-north_star).
+and rearranges" P:L235), and conv2's dgrad with the fused reduce-scatter of dX (north_star) in both variants: pull (each rank
+keeps its partials in its own copy, the owner reads and sums them in rank order) and push (the dgrad
+epilogue stores each input block's partial into its owner's receive slot, the owner sums the slots).
 
 No kernel may spin on a later launch of the same process (one GPU, one stream), so:
   * gather: the ranks' conv2 forwards run in rank order; before rank r's kernel, the blocks of the
@@ -20,9 +20,9 @@ No kernel may spin on a later launch of the same process (one GPU, one stream), 
   * reduce-scatter: the library holds each rank's comm-stream tail (wait for the flags, rank-order
     slot sum) until every rank has issued its dgrad (the loopback contract in convpart.h).
 Compared with the fp64 oracle (decision replay of the GPU's pooling codes): the gathered conv1
-output (TF32 bar 2e-3), each rank's conv2 output, every receive slot (rank q's partial dX of block
-r) and the summed dX of each rank's block; the slot sum must equal the fp32 rank-order sum of the
-slots bit for bit.  Cases include uneven Eq. 1 maps and ranks with zero kernels in a layer (the
+output (TF32 bar 2e-3), each rank's conv2 output, every partial (rank q's partial dX of block r: a receive
+slot in push mode, rank q's own copy in pull mode) and the summed dX of each rank's block; in push mode
+the sum must equal the fp32 rank-order sum of the slots bit for bit.  Cases include uneven Eq. 1 maps and ranks with zero kernels in a layer (the
 copy-engine gather and zero-partial paths), and B=128 (pixel-mode dgrad), each over two steps.
 """
 import numpy as np
@@ -75,8 +75,10 @@ def blocks(part, H, W, Bp):
     return out, start
 
 
+@pytest.mark.parametrize("rs_mode", ["push", "pull", "ce"])
 @pytest.mark.parametrize("name,P,B,s1,s2", CASES, ids=[c[0] for c in CASES])
-def test_loopback_fused_collectives(orc, name, P, B, s1, s2):
+def test_loopback_fused_collectives(orc, monkeypatch, name, P, B, s1, s2, rs_mode):
+    monkeypatch.setenv("CP_RS_MODE", rs_mode)
     K1, K2, H0 = 36, 72, 20
     Bp = (B + 31) // 32 * 32
     p1, p2 = make_part(s1, K1), make_part(s2, K2)
@@ -192,18 +194,23 @@ def test_loopback_fused_collectives(orc, name, P, B, s1, s2):
             a, e_ = blk_in2[r]
             k0, kr = p1.k_begin[r], p1.k_count[r]
             nblk = e_ - a
-            slots = [dx2[r].tensor[n1 + q * mb: n1 + q * mb + nblk] for q in range(P)]
-            acc = slots[0].clone()
-            for q in range(1, P):
-                acc += slots[q]
-            if not torch.equal(acc, dx2[r].tensor[a:e_]):
-                failures.append(f"step {step}: rank {r}'s block is not the rank-order fp32 sum of its slots")
+            if rs_mode == "push":   # receive slots behind the gather layout of the owner's copy
+                slots = [dx2[r].tensor[n1 + q * mb: n1 + q * mb + nblk] for q in range(P)]
+                acc = slots[0].clone()
+                for q in range(1, P):
+                    acc += slots[q]
+                if not torch.equal(acc, dx2[r].tensor[a:e_]):
+                    failures.append(f"step {step}: rank {r}'s block is not the rank-order fp32 sum of its slots")
+            else:                   # pull / ce: rank q's partial of block r stays in rank q's own copy (q != r)
+                slots = [None if q == r else dx2[q].tensor[a:e_] for q in range(P)]
             if f_dx[r][:P].any().item():
                 failures.append(f"step {step}: rank {r}'s dX flags not reset: {f_dx[r][:P].tolist()}")
             if not kr:
                 continue
             Kw = p1.k_width[r]
             for q in range(P):
+                if slots[q] is None:   # pull: the owner's own partial was summed in place
+                    continue
                 qk0, qkr = p2.k_begin[q], p2.k_count[q]
                 got_q = slots[q].reshape(8, 8, Bp, Kw)[:, :, :B, :kr].permute(2, 3, 0, 1).cpu().numpy()
                 if not qkr:
