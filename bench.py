@@ -427,8 +427,11 @@ def main():
     # ---- device-timed region: K steps, L2 flushed between steps (outside the step events)
     clocks = ClockSampler(local)
     clocks.start()
-    live = {"fwd": [], "dgrad": [], "wgrad": [], "push": []}
+    live = {"fwd": [], "dgrad": [], "wgrad": [], "push": [], "rs": []}
     fused_gather = world > 1 and bool(pn.sym) and math == cp.CP_MATH_TF32
+    # the library's fused-collective variants (environment, read per call; defaults: copy engines)
+    gather_mode = "push" if os.environ.get("CP_GATHER_MODE") == "push" else "ce"
+    rs_mode = os.environ.get("CP_RS_MODE") if os.environ.get("CP_RS_MODE") in ("push", "pull") else "ce"
 
     def read_live(k):
         # this step's kernel events, read before the next replay re-records them (device time only: the
@@ -436,10 +439,11 @@ def main():
         for name, ps in (("fwd", 0), ("dgrad", 1), ("wgrad", 2)):
             live[name].append(cp.conv_part_kernel_time(pn.layers[1], ps))
         if fused_gather:
-            try:
-                live["push"].append(cp.conv_part_kernel_time(pn.layers[1], 3))
-            except cp.ConvPartError:
-                pass
+            for name, ps in (("push", 3), ("rs", 4)):
+                try:
+                    live[name].append(cp.conv_part_kernel_time(pn.layers[1], ps))
+                except cp.ConvPartError:
+                    pass
     # ---- the timed steps, device-timed (value) and end to end through the public API (e2e) interleaved
     # step by step, so both see the same clocks / power state (measured one loop after the other, the
     # later loop ran on a hotter, more power-capped GPU: scripts/e2e_probe.py).
@@ -611,9 +615,10 @@ def main():
     # timed steps (max over ranks: the slowest rank sets the step)
     live_ms = dict(zip(("fwd", "dgrad", "wgrad"), _max_over_ranks(
         [statistics.fmean(live[k]) for k in ("fwd", "dgrad", "wgrad")], dev, world)))
-    push_ms = None
+    push_ms = rs_ms = None
     if fused_gather:
-        push_ms = _max_over_ranks([statistics.fmean(live["push"]) if live["push"] else -1.0], dev, world)[0]
+        push_ms, rs_ms = _max_over_ranks([statistics.fmean(live[k]) if live[k] else -1.0 for k in ("push", "rs")],
+                                         dev, world)
     dom = max(live_ms, key=live_ms.get)
     achieved = flop_pass / (live_ms[dom] / 1e3) / 1e12
 
@@ -657,10 +662,12 @@ def main():
                 "probe_times_s": probe_times, "dx_collective": args.dx, "overlap_wgrad_with_dx_reduce": overlap,
                 "head": pn.head_mode, "cuda_graph": graph is not None,
                 "lrn": dict(cp.LRN_DEFAULT) if args.lrn else None,
-                "collectives": ("fused into the GEMMs over NVLink peer memory (gather: the consuming conv2 forward "
-                                "kernel pushes its own input block into every peer's copy while it computes, "
-                                "arrival counters; dX reduce-scatter: dgrad epilogue stores into the owners' receive "
-                                "slots + rank-order slot sum)" if pn.sym else "NCCL AllGather / ReduceScatter")
+                "collectives": (f"NVLink peer memory, no NCCL kernels: gather = {gather_mode} (ce: copy engines "
+                                "copy the own block into every peer's copy on the comm stream while conv2 forward "
+                                "computes its own block first, arrival flags; push: the forward kernel's warp 3 "
+                                f"pushes it), dX reduce-scatter = {rs_mode} (ce: owners fetch their block's partials "
+                                "with the copy engines while wgrad runs; push: dgrad epilogue peer stores), "
+                                "rank-order sum" if pn.sym else "NCCL AllGather / ReduceScatter")
                                if world > 1 else "none (N=1)",
                 "parallelism": f"kernel-split x{world}",
                 "l2": "flushed between timed steps (256 MiB write outside the step events)" if flush is not None
@@ -718,16 +725,28 @@ def main():
                 "link_peak_gbs": 770.0,
                 "link_peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
                 "egress_bytes_per_rank": egress,
-                "gather": {"bytes_pushed": push_bytes, "push_window_ms": push_ms if push_ms and push_ms > 0 else None,
+                "gather": {"mode": gather_mode, "bytes_pushed": push_bytes,
+                           "window_ms": push_ms if push_ms and push_ms > 0 else None,
                            "gbs": push_bytes / (push_ms / 1e3) / 1e9 if push_ms and push_ms > 0 else None,
                            "frac_of_770": push_bytes / (push_ms / 1e3) / 770e9 if push_ms and push_ms > 0 else None,
-                           "how": "globaltimer window inside the conv2 forward kernel: first chunk claimed -> last "
-                                  "chunk's arrival released (warp 3 of every running CTA), mean over timed steps, "
-                                  "max over ranks; overlapped with the forward's own-block MMAs"},
-                "reduce_scatter": {"bytes_sent": others1, "window_ms": live_ms["dgrad"],
-                                   "gbs_lower_bound": others1 / (live_ms["dgrad"] / 1e3) / 1e9,
-                                   "how": "dgrad epilogue peer stores spread over the whole dgrad kernel: bytes / "
-                                          "kernel time is a lower bound of the link rate"},
+                           "how": ("CUDA events on the comm stream around the copy-engine copies of the own block "
+                                   "into every peer's copy (+ one flag per peer), mean over timed steps, max over "
+                                   "ranks; overlapped with the conv2 forward's own-block MMAs" if gather_mode == "ce"
+                                   else "globaltimer window inside the conv2 forward kernel: first chunk claimed -> "
+                                   "last chunk's arrival released (warp 3 of every running CTA), mean over timed "
+                                   "steps, max over ranks; overlapped with the forward's own-block MMAs")},
+                "reduce_scatter": ({"mode": "ce", "bytes_received": push_bytes,
+                                    "window_ms": rs_ms if rs_ms and rs_ms > 0 else None,
+                                    "gbs": push_bytes / (rs_ms / 1e3) / 1e9 if rs_ms and rs_ms > 0 else None,
+                                    "frac_of_770": push_bytes / (rs_ms / 1e3) / 770e9 if rs_ms and rs_ms > 0 else None,
+                                    "how": "CUDA events on the comm stream around the owner's copy-engine fetch of "
+                                           "its block's partials from every peer (after all ready flags), mean over "
+                                           "timed steps, max over ranks; overlapped with conv2 wgrad"}
+                                   if rs_mode == "ce" else
+                                   {"mode": rs_mode, "bytes_sent": others1, "window_ms": live_ms["dgrad"],
+                                    "gbs_lower_bound": others1 / (live_ms["dgrad"] / 1e3) / 1e9,
+                                    "how": "dgrad epilogue peer stores spread over the whole dgrad kernel (push) or "
+                                           "SM loads by the owner (pull): bytes / dgrad time is a lower bound"}),
                 "exposed_comm_ms": exposed,
                 "step_avg_egress_frac_of_770": egress / (ms_per_step / 1e3) / 770e9,
                 "nccl_alone": nccl_ref}

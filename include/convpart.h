@@ -14,10 +14,12 @@
  * weight gradients stay local.
  *
  * B200 realisation: one process per GPU.  With symmetric (peer-mapped) buffers the
- * channel gather is fused into the consumer GEMM (the next layer's forward pushes its
- * own input block into every peer's copy over NVLink while it computes) and the dX
- * reduce-scatter into the dgrad epilogue (partials stored into the owners' receive
- * slots, summed in rank order); otherwise NCCL AllGather / ReduceScatter / AllReduce.
+ * channel gather overlaps the consumer GEMM (copy engines distribute each rank's block
+ * over NVLink while the next layer's forward computes its own block first; or the GEMM
+ * kernel pushes it itself) and the dX reduce-scatter overlaps the next GEMM (owners
+ * fetch the partials by copy engine, or the dgrad epilogue stores them into the owners'
+ * receive slots; summed in rank order); otherwise NCCL AllGather / ReduceScatter /
+ * AllReduce.
  * Conv passes are implicit GEMMs on tcgen05/TMEM (kind::tf32, FP32 accumulation)
  * with TMA-staged tiles and a fused bias+ReLU+2x2 max-pool epilogue, or FP32
  * SIMT kernels in the reference math mode.
@@ -159,16 +161,19 @@ int cp_comm_create_loopback(int32_t world, cp_comm* out);
  * IPC handles over the communicator and maps every peer's copy, plus a 256-byte flag line behind
  * the data: u32 word q = arrival counter of sender q; word 32 = the gather's chunk-claim counter.
  * Semantics when a layer's y_gathered is symmetric (conv_part_forward):
- *   producer: after a device-side cross-rank barrier (no rank may overwrite a copy a peer still
- *     reads), the GEMM writes this rank's block into its LOCAL copy only;
- *   consumer: conv_part_forward whose x is a symmetric gathered buffer pushes this rank's input
- *     block into every peer's copy from the GEMM kernel itself (CP_GATHER_CHUNKS chunks claimed
- *     by any running CTA, one release-add on the peer's counter per chunk), consumes its own block
- *     first and each peer block once that peer's counter reached CP_GATHER_CHUNKS (gather
- *     overlapped with the GEMM; no AllGather kernel), then resets its flag line.  A rank without
- *     kernels in the consuming layer distributes its block with copy-engine copies and raises the
- *     counters to CP_GATHER_CHUNKS the same way.  Any other reader of a symmetric gathered output
- *     calls cp_symmetric_wait (waits for all peers' flags on `stream`, then resets them) first.
+ *   producer: the GEMM writes this rank's block into its LOCAL copy only; a device-side
+ *     cross-rank barrier (no rank may overwrite a copy a peer still reads) runs on comm_stream
+ *     (on stream when comm_stream == stream) and the consumer's distribution waits for it;
+ *   consumer: conv_part_forward whose x is a symmetric gathered buffer distributes this rank's
+ *     input block into every peer's copy and consumes its own block first, each peer block once
+ *     that peer's counter is raised (gather overlapped with the GEMM; no AllGather kernel), then
+ *     resets its flag line.  Default (tensor-core consumer, comm_stream != stream): copy-engine
+ *     copies on comm_stream, peers in the order they consume the block, then the counter set to
+ *     CP_GATHER_CHUNKS.  CP_GATHER_MODE=push (environment): the GEMM kernel pushes the block
+ *     itself (CP_GATHER_CHUNKS chunks claimed by any running CTA, one release-add on the peer's
+ *     counter per chunk).  A rank without kernels in the consuming layer uses copy-engine copies
+ *     on stream.  Any other reader of a symmetric gathered output calls cp_symmetric_wait (waits
+ *     for all peers' flags on `stream`, then resets them) first.
  * cp_symmetric_peer returns rank `rank`'s copy of the buffer and of its flag line as addressable
  * from this process (tests; diagnostics).  cp_symmetric_free (collective) or cp_comm_destroy
  * releases the buffers.  Errors: CP_ERR_ARG for a pointer that is not a symmetric buffer of `comm`;
@@ -248,15 +253,16 @@ int conv_part_forward(cp_layer layer, const float* x, const float* w, const floa
  * collective: call conv_part_wait(layer, stream) before consuming dx.
  * Fused reduce-scatter (SURVEY §8(f) f1, TF32 path): when dx is a symmetric buffer of
  * at least dx_peer bytes (cp_symmetric_alloc) and dx_mode is CP_DX_REDUCE_SCATTER, no
- * NCCL collective runs.  Default ("push"): the dgrad epilogue stores each input block's
- * partial straight into its owner's receive slot behind the gather layout (peers over
- * NVLink), sets this rank's arrival flag at every peer, and on comm_stream the owner sums
- * the n_ranks slots in ascending rank order into its block of dx.  CP_RS_MODE=pull / ce
- * (environment): the dgrad writes every partial into this rank's own copy of dx, sets its
- * ready flag at every peer, and each owner fetches its block's partials from all copies
- * over NVLink (SM loads / copy-engine copies into its receive slots) and sums them in the
- * same order - the same bits.  Unless CP_DX_ORDERED is given, a cross-rank barrier first
- * guards the slots / partials against overwrite while an owner still reads them. */
+ * NCCL collective runs.  Default ("ce"): the dgrad writes every input block's partial into
+ * this rank's own copy of dx, sets this rank's ready flag at every peer, and on comm_stream
+ * each owner waits for all flags, copies its block's partials from the peers' copies into
+ * its receive slots behind the gather layout with the copy engines (NVLink, no SM) and
+ * sums the n_ranks partials in ascending rank order into its block of dx.
+ * CP_RS_MODE=pull (environment): the owner reads the partials with SM loads instead;
+ * CP_RS_MODE=push: the dgrad epilogue stores each partial straight into its owner's receive
+ * slot and the owner sums the slots - all three give the same bits.  Unless CP_DX_ORDERED is
+ * given, a cross-rank barrier first guards the slots / partials against overwrite while an
+ * owner still reads them. */
 int conv_part_backward_data(cp_layer layer, const float* dy_gathered, const uint8_t* saved,
                             const float* y_gathered, const float* w, float* dx, int32_t dx_mode,
                             void* workspace, void* stream, void* comm_stream);
@@ -269,14 +275,16 @@ int conv_part_backward_filter(cp_layer layer, const float* dy_gathered, const ui
 
 /* conv_part_timing — enable (1) / disable (0) per-pass timing of this layer's tensor-core GEMM
  * launches: CUDA events recorded on the launching stream immediately before and after the GEMM
- * kernel (external records, so they also time inside a captured CUDA graph); with a fused gather
- * input, the forward kernel also stamps (%globaltimer, in the workspace) the window from its first
- * push chunk claimed to its last chunk's arrival released.
+ * kernel (external records, so they also time inside a captured CUDA graph).  With a fused gather
+ * input, also the gather window: events on comm_stream around the copy-engine distribution, or (in-
+ * kernel push) %globaltimer stamps in the workspace from the first push chunk claimed to the last
+ * chunk's arrival released; with the copy-engine reduce-scatter, events on comm_stream around the
+ * partials' fetch (after all peers' ready flags).
  * conv_part_kernel_time — duration in ms of the last recorded GEMM of `pass` (0 forward,
- * 1 backward-data, 2 backward-filter), or 3: the last fused gather push window (reads the stamps
- * from the device: blocking).  The caller synchronizes first.  CP_ERR_STATE if timing is off or
- * (pass 3) no push was recorded; a CUDA error if that pass never ran since enabling.  (bench.py's
- * roofline and NVLink measurements) */
+ * 1 backward-data, 2 backward-filter), 3: the last gather window (push stamps: a blocking read),
+ * 4: the last reduce-scatter fetch window.  The caller synchronizes first.  CP_ERR_STATE if timing
+ * is off or (pass 3 / 4) no such window was recorded; a CUDA error if that pass never ran since
+ * enabling.  (bench.py's roofline and NVLink measurements) */
 int conv_part_timing(cp_layer layer, int32_t enable);
 int conv_part_kernel_time(cp_layer layer, int32_t pass, float* ms);
 

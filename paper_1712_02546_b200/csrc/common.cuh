@@ -168,7 +168,8 @@ struct Layer {
   cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;     // copy-engine gather on the comm stream
   // optional per-pass GEMM timing (conv_part_timing): events around the tensor-core kernel launch
   int timing;
-  cudaEvent_t ev_t[3][2];
+  cudaEvent_t ev_t[5][2];   // timing: GEMM of pass 0/1/2, 3 copy-engine gather, 4 reduce-scatter transfer
+  int ce_gather_timed = 0, rs_timed = 0;   // a window of kind 3 / 4 was recorded since timing was enabled
 
   // TMA descriptor cache lives in the TC module (opaque)
   void* tc_cache;

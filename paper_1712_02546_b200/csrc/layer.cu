@@ -211,7 +211,7 @@ int conv_part_query(cp_layer L, cp_sizes* o) {
 int conv_part_destroy(cp_layer L) {
   if (!L) return CP_OK;
   tc_release(*L);
-  for (int p = 0; p < 3; ++p)
+  for (int p = 0; p < 5; ++p)
     for (int e = 0; e < 2; ++e)
       if (L->ev_t[p][e]) cudaEventDestroy(L->ev_t[p][e]);
   if (L->ev_compute) cudaEventDestroy(L->ev_compute);
@@ -225,19 +225,21 @@ int conv_part_destroy(cp_layer L) {
   return CP_OK;
 }
 
-static bool gather_on_copy_engines() {   // CP_GATHER_MODE=ce (A/B; default: in-kernel push)
+// gather variant of a tensor-core consumer with a comm stream, read per call: copy engines (default) or
+// CP_GATHER_MODE=push (warp 3 of the consuming GEMM pushes the block over NVLink)
+static bool gather_on_copy_engines() {
   const char* e = getenv("CP_GATHER_MODE");
-  return e && strcmp(e, "ce") == 0;
+  return !(e && strcmp(e, "push") == 0);
 }
 
-// fused reduce-scatter variant, read per call (tests switch it between layers): 0 push (default: the dgrad
-// epilogue stores each partial into its owner's receive slot), 1 pull (owners read the partials with SM
-// loads), 2 ce (owners copy the partials into their receive slots with the copy engines)
+// fused reduce-scatter variant, read per call (tests switch it between layers): 2 ce (default: the owners'
+// copy engines fetch the partials into their receive slots), 1 pull (owners read the partials with SM
+// loads), 0 push (the dgrad epilogue stores each partial into its owner's receive slot)
 static int rs_mode() {
   const char* e = getenv("CP_RS_MODE");
   if (e && strcmp(e, "pull") == 0) return 1;
-  if (e && strcmp(e, "ce") == 0) return 2;
-  return 0;
+  if (e && strcmp(e, "push") == 0) return 0;
+  return 2;
 }
 
 int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b, float* y, uint8_t* saved,
@@ -286,23 +288,6 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
         peer_blocks[npeers++] = (float*)peers[r] + L->out.start[me];
       }
     comm_symmetric_set_own(L->comm, y, L->out.start[me], L->out.start[me + 1] - L->out.start[me]);
-    if (!epi_push && cs != s && !comm_is_loopback(L->comm)) {
-      // Nothing but this rank writes its own copy's own block, so only the consumer's distribution
-      // (the push into the peers' copies, or their copy-engine copies) must wait for the barrier: it
-      // runs on the comm stream, overlapped with this layer's GEMM, and the consumer's forward waits
-      // for it (comm_symmetric_take_pending) - rank skew and the barrier latency hide behind conv1.
-      if (!L->ev_bar) {
-        CP_CUDA(cudaEventCreateWithFlags(&L->ev_bar_fork, cudaEventDisableTiming));
-        CP_CUDA(cudaEventCreateWithFlags(&L->ev_bar, cudaEventDisableTiming));
-      }
-      CP_CUDA(cudaEventRecord(L->ev_bar_fork, s));
-      CP_CUDA(cudaStreamWaitEvent(cs, L->ev_bar_fork, 0));
-      CP_TRY(comm_barrier(L->comm, cs));
-      CP_CUDA(cudaEventRecord(L->ev_bar, cs));
-      comm_symmetric_set_pending(L->comm, y, L->ev_bar);
-    } else {
-      CP_TRY(comm_barrier(L->comm, s));
-    }
   }
   void* ipeers[CP_MAX_RANKS];
   uint32_t* iflags[CP_MAX_RANKS];
@@ -318,16 +303,20 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
   if (sym_in && !epi_push) {
     const int64_t n = L->in.start[me + 1] - L->in.start[me];
     if (tf32 && has_gemm && gather_on_copy_engines() && cs != s && !comm_is_loopback(L->comm)) {
-      // CP_GATHER_MODE=ce: the copy engines distribute this rank's block (need order, one flag per
-      // peer after its copy) on the comm stream while the GEMM runs and waits for its arrivals; no SM
-      // work for the transfer
+      // copy-engine gather (default): the copy engines distribute this rank's block (need order, one
+      // flag per peer after its copy) on the comm stream while the GEMM runs and waits for its
+      // arrivals; no SM does transfer work.  Nothing queued ahead of the copies on the comm stream
+      // waits for a peer (the producer barrier of this layer's own output is enqueued after them)
       if (!L->ev_gfork) {
         CP_CUDA(cudaEventCreateWithFlags(&L->ev_gfork, cudaEventDisableTiming));
         CP_CUDA(cudaEventCreateWithFlags(&L->ev_gjoin, cudaEventDisableTiming));
       }
       CP_CUDA(cudaEventRecord(L->ev_gfork, s));
       CP_CUDA(cudaStreamWaitEvent(cs, L->ev_gfork, 0));
+      CP_TRY(tc_time_mark(*L, 3, 0, cs));   // gather window: first copy issued -> last flag written
       CP_TRY(comm_ce_distribute(L->comm, x, cs, true));
+      CP_TRY(tc_time_mark(*L, 3, 1, cs));
+      if (L->timing) L->ce_gather_timed = 1;
       CP_CUDA(cudaEventRecord(L->ev_gjoin, cs));
       ce_forked = true;
     } else if (tf32 && has_gemm) {
@@ -361,6 +350,28 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
     } else {
       // (a TF32 rank without kernels here signals the chunk count its peers' GEMMs wait for)
       CP_TRY(comm_ce_distribute(L->comm, x, s, tf32));
+    }
+  }
+  // Producer-side barrier of a gathered output (after the input-side distribution above: the comm
+  // stream's copy-engine gather must not queue behind a cross-rank barrier while this rank's GEMM
+  // holds every SM spinning on its peers' copies)
+  if (sym_out) {
+    if (!epi_push && cs != s && !comm_is_loopback(L->comm)) {
+      // Nothing but this rank writes its own copy's own block, so only the consumer's distribution
+      // (the push into the peers' copies, or their copy-engine copies) must wait for the barrier: it
+      // runs on the comm stream, overlapped with this layer's GEMM, and the consumer's forward waits
+      // for it (comm_symmetric_take_pending) - rank skew and the barrier latency hide behind conv1.
+      if (!L->ev_bar) {
+        CP_CUDA(cudaEventCreateWithFlags(&L->ev_bar_fork, cudaEventDisableTiming));
+        CP_CUDA(cudaEventCreateWithFlags(&L->ev_bar, cudaEventDisableTiming));
+      }
+      CP_CUDA(cudaEventRecord(L->ev_bar_fork, s));
+      CP_CUDA(cudaStreamWaitEvent(cs, L->ev_bar_fork, 0));
+      CP_TRY(comm_barrier(L->comm, cs));
+      CP_CUDA(cudaEventRecord(L->ev_bar, cs));
+      comm_symmetric_set_pending(L->comm, y, L->ev_bar);
+    } else {
+      CP_TRY(comm_barrier(L->comm, s));
     }
   }
   if (sym_in && !(tf32 && has_gemm)) CP_TRY(launch_wait_flags(arrive, L->d.world, me, s, tf32 && !epi_push));
@@ -464,10 +475,14 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
     auto tail = [=](const std::vector<cudaEvent_t>& computed) -> int {
       for (cudaEvent_t e : computed) CP_CUDA(cudaStreamWaitEvent(cs, e, 0));
       CP_TRY(launch_wait_flags(own_flags, world, me, cs));
-      if (rsm == 2)   // copy engines: every peer's partial of the own block into its local receive slot
+      if (rsm == 2) {   // copy engines: every peer's partial of the own block into its local receive slot
+        CP_TRY(tc_time_mark(*Lp, 4, 0, cs));   // transfer window: all partials ready -> copies done
         for (int r = 0; r < world; ++r)
           if (r != me && n_own)
             CP_CUDA(cudaMemcpyAsync((void*)srcv[r], remv[r], (size_t)n_own * 4, cudaMemcpyDeviceToDevice, cs));
+        CP_TRY(tc_time_mark(*Lp, 4, 1, cs));
+        if (Lp->timing) Lp->rs_timed = 1;
+      }
       CP_TRY(launch_sum_peer_blocks(srcv.data(), world, own, n_own, cs));
       CP_CUDA(cudaMemsetAsync(own_flags, 0, CP_MAX_RANKS * sizeof(uint32_t), cs));
       CP_CUDA(cudaEventRecord(Lp->ev_comm, cs));
@@ -575,17 +590,28 @@ int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* save
 
 int conv_part_timing(cp_layer L, int32_t enable) {
   if (!L) CP_FAIL(CP_ERR_ARG, "conv_part_timing: null layer");
-  if (enable && !L->timing)
-    for (int p = 0; p < 3; ++p)
+  if (enable && !L->timing) {
+    for (int p = 0; p < 5; ++p)
       for (int e = 0; e < 2; ++e)
         if (!L->ev_t[p][e]) CP_CUDA(cudaEventCreate(&L->ev_t[p][e]));
+    L->ce_gather_timed = L->rs_timed = 0;
+  }
   L->timing = enable ? 1 : 0;
   return CP_OK;
 }
 
 int conv_part_kernel_time(cp_layer L, int32_t pass, float* ms) {
-  if (!L || !ms || pass < 0 || pass > 3) CP_FAIL(CP_ERR_ARG, "conv_part_kernel_time: bad arguments");
+  if (!L || !ms || pass < 0 || pass > 4) CP_FAIL(CP_ERR_ARG, "conv_part_kernel_time: bad arguments");
   if (!L->timing) CP_FAIL(CP_ERR_STATE, "conv_part_kernel_time: timing not enabled");
+  if (pass == 4) {   // reduce-scatter transfer window (copy-engine fetch of the partials, comm stream)
+    if (!L->rs_timed) CP_FAIL(CP_ERR_STATE, "conv_part_kernel_time: no copy-engine reduce-scatter recorded");
+    CP_CUDA(cudaEventElapsedTime(ms, L->ev_t[4][0], L->ev_t[4][1]));
+    return CP_OK;
+  }
+  if (pass == 3 && L->ce_gather_timed) {   // copy-engine gather window (comm stream events)
+    CP_CUDA(cudaEventElapsedTime(ms, L->ev_t[3][0], L->ev_t[3][1]));
+    return CP_OK;
+  }
   if (pass == 3) {   // fused gather push window (globaltimer stamps in the workspace; blocking read)
     if (!L->ws_last) CP_FAIL(CP_ERR_STATE, "conv_part_kernel_time: no forward with a fused gather push yet");
     unsigned long long t[2];

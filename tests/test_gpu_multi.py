@@ -12,14 +12,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("rs_mode", ["push", "ce"])
-def test_multi_gpu_parity(rs_mode):
-    """Fused reduce-scatter variants (CP_RS_MODE): the dgrad pushes the partials (default) / the owners
-    fetch them with the copy engines (the SM-load pull variant runs in the loopback test)."""
+@pytest.mark.parametrize("rs_mode,gather_mode", [("ce", "ce"), ("push", "push")])
+def test_multi_gpu_parity(rs_mode, gather_mode):
+    """Fused collective variants: copy-engine gather + copy-engine reduce-scatter (the defaults) and the
+    in-kernel variants (CP_GATHER_MODE=push: the consuming GEMM pushes its block; CP_RS_MODE=push: the
+    dgrad epilogue stores the partials into the owners' slots).  The SM-load pull variant of the
+    reduce-scatter runs in the loopback test."""
     n = min(torch.cuda.device_count(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29517 if rs_mode == 'push' else 29518}",
+           "--master-addr=127.0.0.1", f"--master-port={29517 if rs_mode == 'ce' else 29518}",
            os.path.join(ROOT, "tests", "multi_gpu_check.py")]
-    env = dict(os.environ, CP_RS_MODE=rs_mode)
+    env = dict(os.environ, CP_RS_MODE=rs_mode, CP_GATHER_MODE=gather_mode)
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
