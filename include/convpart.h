@@ -273,6 +273,17 @@ int conv_part_backward_filter(cp_layer layer, const float* dy_gathered, const ui
                               const float* y_gathered, const float* x, float* dw, float* db,
                               void* workspace, void* stream);
 
+/* conv_part_backward_filter_sgd — conv_part_backward_filter followed by this rank's SGD step
+ * on its own slice: w -= lr*dw, b -= lr*db (b and db both given or both NULL; w, b
+ * must not alias dw, db).  dw and db are still written.  TF32 / BF16 and the image-layer kernels
+ * apply the update where the final dW / db are produced (the wgrad epilogue, its split-K or
+ * stream-tail reduce, the bias reduce, the conv1 reduce) instead of a separate pass over W and dW
+ * (the same fused multiply-add as cp_sgd: bitwise identical to backward_filter + sgd_step); the
+ * FP32 SIMT mode runs the separate update. */
+int conv_part_backward_filter_sgd(cp_layer layer, const float* dy_gathered, const uint8_t* saved,
+                                  const float* y_gathered, const float* x, float* dw, float* db, float* w,
+                                  float* b, float lr, void* workspace, void* stream);
+
 /* conv_part_timing — enable (1) / disable (0) per-pass timing of this layer's tensor-core GEMM
  * launches: CUDA events recorded on the launching stream immediately before and after the GEMM
  * kernel (external records, so they also time inside a captured CUDA graph).  With a fused gather

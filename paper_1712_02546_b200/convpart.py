@@ -24,7 +24,8 @@ CP_INPUT_IMAGES, CP_INPUT_GATHER = 0, 1
 EXPORTS = [
     "cp_partition_plan", "cp_eq1_weights", "cp_comm_unique_id", "cp_comm_create", "cp_comm_destroy",
     "conv_part_create", "conv_part_query", "conv_part_destroy", "conv_part_probe_bytes", "conv_part_probe",
-    "conv_part_forward", "conv_part_backward_data", "conv_part_backward_filter", "conv_part_wait", "conv_part_sgd_step",
+    "conv_part_forward", "conv_part_backward_data", "conv_part_backward_filter", "conv_part_backward_filter_sgd",
+    "conv_part_wait", "conv_part_sgd_step",
     "cp_launch_count", "cp_last_error", "cp_pack_nchw", "cp_unpack_nchw", "cp_unpack_saved",
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
@@ -103,6 +104,7 @@ def lib():
             "conv_part_forward": [P, P, P, P, P, P, P, P, P],
             "conv_part_backward_data": [P, P, P, P, P, P, I32, P, P, P],
             "conv_part_backward_filter": [P, P, P, P, P, P, P, P, P],
+            "conv_part_backward_filter_sgd": [P, P, P, P, P, P, P, P, P, ctypes.c_float, P, P],
             "conv_part_sgd_step": [P, P, P, P, P, ctypes.c_float, P],
             "conv_part_wait": [P, P],
             "cp_pack_nchw": [P, I32, I32, I32, I32, pp, P, P],
@@ -255,6 +257,12 @@ def conv_part_backward_data(h, dy, saved, y, w, dx, dx_mode, ws, stream=None, co
 def conv_part_backward_filter(h, dy, saved, y, x, dw, db, ws, stream=None):
     _call("conv_part_backward_filter", h, _ptr(dy), _ptr(saved), _ptr(y), _ptr(x), _ptr(dw), _ptr(db),
           _ptr(ws), _stream(stream))
+
+
+def conv_part_backward_filter_sgd(h, dy, saved, y, x, dw, db, w, b, lr, ws, stream=None):
+    """backward_filter + the own slice's SGD step (w -= lr*dw, b -= lr*db) fused where dW / db are final."""
+    _call("conv_part_backward_filter_sgd", h, _ptr(dy), _ptr(saved), _ptr(y), _ptr(x), _ptr(dw), _ptr(db), _ptr(w),
+          _ptr(b), float(lr), _ptr(ws), _stream(stream))
 
 
 def conv_part_wait(h, stream=None):

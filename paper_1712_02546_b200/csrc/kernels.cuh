@@ -20,7 +20,8 @@ constexpr int kBiasSplitMax = 256;
 int launch_unpool(const Layer& L, const float* dy_block, const uint8_t* saved, const float* y_block,
                   float* dY, float* bias_part, bool round_tf32, cudaStream_t s);
 // db from the partials launch_unpool wrote
-int launch_bias_grad(const Layer& L, float* db, const float* part, cudaStream_t s);
+int launch_bias_grad(const Layer& L, float* db, const float* part, cudaStream_t s, float* sgd_b = nullptr,
+                     float lr = 0.f);
 
 // ---- FP32 SIMT reference convolutions (kernels_simt.cu)
 int launch_fwd_simt(const Layer& L, const float* x, const float* xcol, const float* w, const float* b,
@@ -66,7 +67,9 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
 // pull reduce-scatter: out = sum over r ascending of src[r] (n floats, 16-byte aligned blocks)
 int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64_t n, cudaStream_t s);
 int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float* out, int64_t n, cudaStream_t s);
-int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s);
+// sgd_w: fused SGD update of the own weights wherever the final dW is produced (w -= sgd_lr * dW)
+int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s, float* sgd_w = nullptr,
+             float sgd_lr = 0.f);
 void tc_release(Layer& L);
 // helpers of kernels_tc.cu shared with kernels_conv1.cu
 int tc_make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
@@ -84,7 +87,7 @@ int c1_fwd(Layer& L, const float* x, const float* w, const float* b, float* y_bl
 bool c1_wgrad_supported(const Layer& L);
 size_t c1_wgrad_workspace(const Layer& L);
 int c1_wgrad(Layer& L, const float* x, const float* da, const uint8_t* codes, const float* y, float* dw, float* db,
-             float* part, cudaStream_t s);
+             float* part, cudaStream_t s, float* sgd_w = nullptr, float* sgd_b = nullptr, float lr = 0.f);
 // timing events around a pass's GEMM launch (no-ops unless L.timing): external records, so they
 // also time when the launch is captured into a CUDA graph
 int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s);

@@ -599,7 +599,8 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
 // sums combine in fixed order (deterministic).
 __global__ void __launch_bounds__(256) conv1_wgrad_reduce(const float* __restrict__ part, const float* __restrict__ dbpart,
                                                           float* __restrict__ dw, float* __restrict__ db, int nkr,
-                                                          int Kr, int Kc, int Kcol) {
+                                                          int Kr, int Kc, int Kcol, float* __restrict__ sgd_w,
+                                                          float* __restrict__ sgd_b, float lr) {
   __shared__ float red[8][33];
   const int e = blockIdx.x * 32 + threadIdx.x;
   const int n = Kr * Kcol;
@@ -636,8 +637,13 @@ __global__ void __launch_bounds__(256) conv1_wgrad_reduce(const float* __restric
     float u = red[0][threadIdx.x];
 #pragma unroll
     for (int k = 1; k < 8; ++k) u += red[k][threadIdx.x];
-    if (is_w) dw[e] = u;
-    else db[e - n] = u;
+    if (is_w) {
+      dw[e] = u;
+      if (sgd_w) sgd_w[e] = fmaf(-lr, u, sgd_w[e]);   // fused SGD (final dW)
+    } else {
+      db[e - n] = u;
+      if (sgd_b) sgd_b[e - n] = fmaf(-lr, u, sgd_b[e - n]);
+    }
   }
 }
 
@@ -786,7 +792,7 @@ size_t c1_wgrad_workspace(const Layer& L) {
 }
 
 int c1_wgrad(Layer& L, const float* x, const float* da, const uint8_t* codes, const float* y, float* dw, float* db,
-             float* part, cudaStream_t s) {
+             float* part, cudaStream_t s, float* sgd_w, float* sgd_b, float lr) {
   W1Params p{};
   size_t smem = 0;
   int grid = 0;
@@ -819,7 +825,8 @@ int c1_wgrad(Layer& L, const float* x, const float* da, const uint8_t* codes, co
   CP_LAUNCHED();
   CP_TRY(tc_time_mark(L, 2, 1, s));
   const int n = L.Kr * L.Kcol + (db ? L.Kr : 0);
-  conv1_wgrad_reduce<<<(n + 31) / 32, dim3(32, 8), 0, s>>>(p.part, p.dbpart, dw, db, p.nkr, L.Kr, L.Kc, L.Kcol);
+  conv1_wgrad_reduce<<<(n + 31) / 32, dim3(32, 8), 0, s>>>(p.part, p.dbpart, dw, db, p.nkr, L.Kr, L.Kc, L.Kcol,
+                                                           sgd_w, db ? sgd_b : nullptr, lr);
   CP_LAUNCHED();
   return CP_OK;
 }

@@ -445,7 +445,7 @@ int launch_unpool(const Layer& L, const float* dy_block, const uint8_t* saved, c
 // db[slot] = sum of the unpool kernel's bias partials, splits added in ascending order:
 // block (32 slots, 8 split lanes), lanes combined in fixed order.
 __global__ void __launch_bounds__(256) bias_grad_final(const float* __restrict__ part, float* db, int ns, int Kr,
-                                                       int Kc) {
+                                                       int Kc, float* sgd_b, float lr) {
   __shared__ float red[8][33];
   const int slot = blockIdx.x * 32 + threadIdx.x;
   const int per = (ns + 7) / 8;
@@ -470,12 +470,13 @@ __global__ void __launch_bounds__(256) bias_grad_final(const float* __restrict__
 #pragma unroll
     for (int k = 1; k < 8; ++k) u += red[k][threadIdx.x];
     db[slot] = u;
+    if (sgd_b) sgd_b[slot] = fmaf(-lr, u, sgd_b[slot]);   // fused SGD of the own biases
   }
 }
 
-int launch_bias_grad(const Layer& L, float* db, const float* part, cudaStream_t s) {
+int launch_bias_grad(const Layer& L, float* db, const float* part, cudaStream_t s, float* sgd_b, float lr) {
   if (L.Kr == 0) return CP_OK;
-  bias_grad_final<<<cdiv(L.Kr, 32), dim3(32, 8), 0, s>>>(part, db, unpool_splits(L), L.Kr, L.Kc);
+  bias_grad_final<<<cdiv(L.Kr, 32), dim3(32, 8), 0, s>>>(part, db, unpool_splits(L), L.Kr, L.Kc, sgd_b, lr);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -1060,10 +1061,10 @@ __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, i
   if (i + 3 < n && ((reinterpret_cast<uintptr_t>(p + i) | reinterpret_cast<uintptr_t>(g + i)) & 15) == 0) {
     float4 a = *reinterpret_cast<float4*>(p + i);
     const float4 b = *reinterpret_cast<const float4*>(g + i);
-    a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
+    a.x = fmaf(-lr, b.x, a.x); a.y = fmaf(-lr, b.y, a.y); a.z = fmaf(-lr, b.z, a.z); a.w = fmaf(-lr, b.w, a.w);
     *reinterpret_cast<float4*>(p + i) = a;
   } else {
-    for (int64_t j = i; j < n && j < i + 4; ++j) p[j] -= lr * g[j];
+    for (int64_t j = i; j < n && j < i + 4; ++j) p[j] = fmaf(-lr, g[j], p[j]);
   }
 }
 
@@ -1408,10 +1409,10 @@ __global__ void sgd_multi_kernel(const __grid_constant__ SgdList L, float lr) {
     if (e + 3 < L.n[t] && ((reinterpret_cast<uintptr_t>(p + e) | reinterpret_cast<uintptr_t>(g + e)) & 15) == 0) {
       float4 a = *reinterpret_cast<float4*>(p + e);
       const float4 b = *reinterpret_cast<const float4*>(g + e);
-      a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
+      a.x = fmaf(-lr, b.x, a.x); a.y = fmaf(-lr, b.y, a.y); a.z = fmaf(-lr, b.z, a.z); a.w = fmaf(-lr, b.w, a.w);
       *reinterpret_cast<float4*>(p + e) = a;
     } else {
-      for (long long j = e; j < L.n[t] && j < e + 4; ++j) p[j] -= lr * g[j];
+      for (long long j = e; j < L.n[t] && j < e + 4; ++j) p[j] = fmaf(-lr, g[j], p[j]);
     }
   }
 }

@@ -94,6 +94,8 @@ struct TcParams {
   int bn_box;          // fwd: B box rows
   int nw;              // fwd: N tile width (balanced: Kc split into equal tiles)
   int nlim;            // fwd (kernels on N): this launch computes own slots [0, nlim) (split forward: < Kc)
+  float* sgd_w;        // wgrad with the fused SGD update: the own weights (w -= sgd_lr * dW where dW is final)
+  float sgd_lr;
   int m_off;           // fwd transposed: first own slot of M tile 0 (split forward: the remainder)
   int epi_groups;      // 1 or 2 epilogue warp groups (blockDim = 128 + 128*groups; CP_TC_EPI_GROUPS)
   int max_chunks;      // longest K loop of a unit (after split), for the launch heuristics
@@ -480,6 +482,27 @@ __host__ __device__ __forceinline__ int mma_n(int n) {
   if (CG == 1) return (n + 7) / 8 * 8;
   if (PASS == PASS_FWD) return (n + 15) / 16 * 16;
   return DT ? (n + 127) / 128 * 128 : (n + 63) / 64 * 64;   // whole MN-major groups per CTA half
+}
+
+// w[q] -= lr * v[q] for q < n (the fused SGD update; same fma as cp_sgd)
+__device__ __forceinline__ void sgd_f32x32(float* w, const float (&v)[32], int n, float lr) {
+  if (n >= 32 && ((reinterpret_cast<uintptr_t>(w) & 15) == 0)) {
+    float4 a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = reinterpret_cast<const float4*>(w)[q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a[q].x = fmaf(-lr, v[4 * q], a[q].x);
+      a[q].y = fmaf(-lr, v[4 * q + 1], a[q].y);
+      a[q].z = fmaf(-lr, v[4 * q + 2], a[q].z);
+      a[q].w = fmaf(-lr, v[4 * q + 3], a[q].w);
+      reinterpret_cast<float4*>(w)[q] = a[q];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < n) w[q] = fmaf(-lr, v[q], w[q]);
+  }
 }
 
 __device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], int n) {
@@ -1060,6 +1083,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             const int64_t col = (int64_t)t.tap * p.Cg + (p.span ? 0 : p.coff[t.rb]) + t.n0 + cc * 32;
             const int64_t o = ((int64_t)t.sp * p.Kr + kk) * p.Ktot + col;
             store_f32x32(p.out + o, v, ncol);
+            if (p.sgd_w) sgd_f32x32(p.sgd_w + o, v, ncol, p.sgd_lr);   // final dW (no split): fused SGD
           }
         }
       }
@@ -1092,6 +1116,8 @@ struct TailInfo {
   int kk0[MAX_TAIL];          // first kernel row of the unit's tile (CTA 0)
   int col0[MAX_TAIL];         // first dW column
   int ncol[MAX_TAIL];         // valid columns
+  float* sgd_w;               // fused SGD: w -= sgd_lr * dW (nullptr: none)
+  float sgd_lr;
 };
 __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restrict__ dw, const __grid_constant__ TailInfo ti) {
   const int tu = blockIdx.z, rank = blockIdx.y, row = blockIdx.x;
@@ -1108,7 +1134,10 @@ __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restri
 #pragma unroll
     for (int k = 0; k < 4; ++k) a[k] += src[(pc + k) * step];
   for (; pc < np; ++pc) a[pc & 3] += src[pc * step];
-  dw[(int64_t)kk * ti.Ktot + ti.col0[tu] + c] = (a[0] + a[1]) + (a[2] + a[3]);
+  const int64_t o = (int64_t)kk * ti.Ktot + ti.col0[tu] + c;
+  const float d = (a[0] + a[1]) + (a[2] + a[3]);
+  dw[o] = d;
+  if (ti.sgd_w) ti.sgd_w[o] = fmaf(-ti.sgd_lr, d, ti.sgd_w[o]);
 }
 
 // forward tail: the tile's pre-pool accumulator = sum over pieces (in order) of the partial tiles;
@@ -1215,7 +1244,7 @@ __global__ void fwd_tail_finish_t(const float* __restrict__ buf, const float* __
 // out = sum_s part[s] (split-K partials).  Block (32 float4, 8 split lanes): lane y adds splits
 // y*per .. in ascending order, the 8 lane sums combine in fixed order (deterministic).  n % 4 == 0.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ out,
-                                                            int64_t n, int S) {
+                                                            int64_t n, int S, float* __restrict__ sgd_w, float lr) {
   __shared__ float4 red[8][32];
   const int64_t i4 = (int64_t)blockIdx.x * 32 + threadIdx.x;
   const int per = (S + 7) / 8;
@@ -1247,11 +1276,17 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
       t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
     }
     reinterpret_cast<float4*>(out)[i4] = t;
+    if (sgd_w) {   // fused SGD on the final dW
+      float4 a = reinterpret_cast<const float4*>(sgd_w)[i4];
+      a.x = fmaf(-lr, t.x, a.x); a.y = fmaf(-lr, t.y, a.y); a.z = fmaf(-lr, t.z, a.z); a.w = fmaf(-lr, t.w, a.w);
+      reinterpret_cast<float4*>(sgd_w)[i4] = a;
+    }
   }
 }
-static int launch_splitk_reduce(const float* part, float* out, int64_t n, int S, cudaStream_t s) {
+static int launch_splitk_reduce(const float* part, float* out, int64_t n, int S, cudaStream_t s,
+                                float* sgd_w = nullptr, float lr = 0.f) {
   if (n % 4) CP_FAIL(CP_ERR_UNSUPPORTED, "split-K reduce: size not a multiple of 4");
-  splitk_reduce_kernel<<<(unsigned)((n / 4 + 31) / 32), dim3(32, 8), 0, s>>>(part, out, n, S);
+  splitk_reduce_kernel<<<(unsigned)((n / 4 + 31) / 32), dim3(32, 8), 0, s>>>(part, out, n, S, sgd_w, lr);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -2239,7 +2274,8 @@ int tc_dgrad(Layer& L, const float* dY, const float* w, float* dx, void* ws, cud
   return CP_OK;
 }
 
-int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s) {
+int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, cudaStream_t s, float* sgd_w,
+             float sgd_lr) {
   if (L.Kr == 0) return CP_OK;
   TcParams p{};
   fill_common(p, L);
@@ -2274,6 +2310,8 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   p.units = p.numM * p.numN * w.S;
   float* part = w.S > 1 ? (float*)((char*)ws + L.off_split) : dw;
   p.out = part;
+  p.sgd_w = w.S == 1 ? sgd_w : nullptr;   // split-K: the update runs in the split reduce
+  p.sgd_lr = sgd_lr;
   // Tail split: when the last round of equal tiles is at most half full, split only those tiles
   // along K over all CTA groups (their partials are tiny; everything else is written directly).
   TailInfo ti{};
@@ -2285,6 +2323,8 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
     ti.cg = CG;
     ti.Kr = L.Kr;
     ti.Ktot = L.Ktot;
+    ti.sgd_w = sgd_w;
+    ti.sgd_lr = sgd_lr;
     const int per_tap = p.numN / (p.R * p.S);
     for (int k = 0; k < T; ++k) {                      // host mirror of decode_unit<WGRAD>
       const int u = p.tail_full + k;
@@ -2314,7 +2354,7 @@ int tc_wgrad(Layer& L, const float* dY, const float* xin, float* dw, void* ws, c
   }
   if (w.S > 1) {
     const int64_t n = (int64_t)L.Kr * L.Ktot;
-    CP_TRY(launch_splitk_reduce(part, dw, n, w.S, s));
+    CP_TRY(launch_splitk_reduce(part, dw, n, w.S, s, sgd_w, sgd_lr));
   }
   return CP_OK;
 }

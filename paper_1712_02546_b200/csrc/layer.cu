@@ -559,19 +559,19 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
   return CP_OK;
 }
 
-int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* saved, const float* y_g, const float* x,
-                              float* dw, float* db, void* ws, void* stream) {
-  if (!L || !dy_g || !y_g || !x || !dw || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: null pointer");
-  if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: pooling needs saved");
-  cudaStream_t s = (cudaStream_t)stream;
+// backward-filter with an optional SGD update of the own slice (w, b non-null): fused into the kernels that
+// produce the final dW / db (wgrad epilogue, its tail / split reduce, the bias reduce, the conv1 reduce);
+// the modes without a fused variant run the separate update after the pass
+static int backward_filter(cp_layer L, const float* dy_g, const uint8_t* saved, const float* y_g, const float* x,
+                           float* dw, float* db, float* w, float* b, float lr, void* ws, cudaStream_t s) {
   if (L->Kr == 0) return CP_OK;
   if (L->images && L->d.math == CP_MATH_TF32 && c1_wgrad_supported(*L)) {
     // image layer: unpool + ReLU' + wgrad + db fused (no dY, no im2col rows in HBM)
     const int64_t o = L->out.start[L->d.rank];
-    return c1_wgrad(*L, x, dy_g + o, saved, y_g + o, dw, db, (float*)WS(ws, L->off_c1w), s);
+    return c1_wgrad(*L, x, dy_g + o, saved, y_g + o, dw, db, (float*)WS(ws, L->off_c1w), s, w, b, lr);
   }
   CP_TRY(ensure_dy(*L, dy_g, saved, y_g, ws, s));
-  if (db) CP_TRY(launch_bias_grad(*L, db, (const float*)WS(ws, L->off_dbpart), s));
+  if (db) CP_TRY(launch_bias_grad(*L, db, (const float*)WS(ws, L->off_dbpart), s, b, lr));
   const float* dY = (const float*)WS(ws, L->off_dy);
   const float* xcol = L->images ? (const float*)WS(ws, L->off_xcol) : nullptr;
   if (L->images && L->xcol_key != x) {   // the forward built its rows on chip: im2col for wgrad here
@@ -579,13 +579,32 @@ int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* save
     L->xcol_key = x;
   }
   if (L->d.math == CP_MATH_TF32) {
-    CP_TRY(tc_wgrad(*L, dY, L->images ? xcol : x, dw, ws, s));
+    CP_TRY(tc_wgrad(*L, dY, L->images ? xcol : x, dw, ws, s, w, lr));
   } else if (L->d.math == CP_MATH_BF16) {   // bf16 copies of dY (ensure_dy) and of the input (forward)
-    CP_TRY(tc_wgrad(*L, (const float*)WS(ws, L->off_dy16), (const float*)WS(ws, L->off_x16), dw, ws, s));
+    CP_TRY(tc_wgrad(*L, (const float*)WS(ws, L->off_dy16), (const float*)WS(ws, L->off_x16), dw, ws, s, w, lr));
   } else {
     CP_TRY(launch_wgrad_simt(*L, dY, x, xcol, dw, s));
+    if (w) CP_TRY(cp_sgd(w, dw, (int64_t)L->Kr * L->Ktot, lr, s));
   }
   return CP_OK;
+}
+
+int conv_part_backward_filter(cp_layer L, const float* dy_g, const uint8_t* saved, const float* y_g, const float* x,
+                              float* dw, float* db, void* ws, void* stream) {
+  if (!L || !dy_g || !y_g || !x || !dw || !ws) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: null pointer");
+  if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter: pooling needs saved");
+  return backward_filter(L, dy_g, saved, y_g, x, dw, db, nullptr, nullptr, 0.f, ws, (cudaStream_t)stream);
+}
+
+int conv_part_backward_filter_sgd(cp_layer L, const float* dy_g, const uint8_t* saved, const float* y_g,
+                                  const float* x, float* dw, float* db, float* w, float* b, float lr, void* ws,
+                                  void* stream) {
+  if (!L || !dy_g || !y_g || !x || !dw || !ws || !w) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter_sgd: null pointer");
+  if (L->d.pool && !saved) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter_sgd: pooling needs saved");
+  if ((b != nullptr) != (db != nullptr))
+    CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter_sgd: b and db must be given together");
+  if (w == dw || (b && b == db)) CP_FAIL(CP_ERR_ARG, "conv_part_backward_filter_sgd: w/b must not alias dw/db");
+  return backward_filter(L, dy_g, saved, y_g, x, dw, db, w, b, lr, ws, (cudaStream_t)stream);
 }
 
 int conv_part_timing(cp_layer L, int32_t enable) {

@@ -209,8 +209,16 @@ class PartitionedNet:
             cp.cp_allreduce_sum(self.comm, hd["logits"], stream)
         cp.cp_softmax_xent(hd["logits"], self.labels, self.B, self.O, hd["loss"], hd["dlogits"], stream)
 
-    def backward(self, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True, head=True):
+    def backward(self, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True, head=True,
+                 lr=None):
+        """lr given: each conv layer's SGD step runs inside the backward pass - for a gather-input layer as a
+        separate update on comm_stream right after its wgrad, overlapped with the next layer's backward
+        (joined before returning); for the image layer fused into its backward-filter kernels
+        (conv_part_backward_filter_sgd).  sgd(..., convs=False) then updates only the head."""
         hd = self.head
+        s_main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        side = comm_stream is not None and comm_stream != s_main
+        joined = True
         if head:
             cp.cp_fc_backward(hd["dlogits"], self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"],
                               self.O, self.head_da, hd["dwfc"], hd["dbfc"], hd["ws"], stream)
@@ -233,16 +241,30 @@ class PartitionedNet:
                 cp.conv_part_backward_data(L, da, b["saved"], b["y"], b["w"], b["dx"], mode, b["ws"], stream,
                                            comm_stream)
             # wgrad needs no communication: it overlaps the dX reduction on the comm stream (§8(e))
-            cp.conv_part_backward_filter(L, da, b["saved"], b["y"], xin, b["dw"], b["db"], b["ws"], stream)
+            if lr is None or (i > 0 and side):
+                cp.conv_part_backward_filter(L, da, b["saved"], b["y"], xin, b["dw"], b["db"], b["ws"], stream)
+            else:
+                cp.conv_part_backward_filter_sgd(L, da, b["saved"], b["y"], xin, b["dw"], b["db"], b["w"], b["b"], lr,
+                                                 b["ws"], stream)
             if i > 0:
                 if overlap:
                     cp.conv_part_wait(L, stream)
+                if lr is not None and side:
+                    # this layer's update (HBM-bound) on the comm stream - behind its dX reduction, which the
+                    # main stream already waited for - while the next layer's backward runs on the SMs
+                    ev = torch.cuda.Event()
+                    ev.record(s_main)
+                    comm_stream.wait_event(ev)
+                    cp.conv_part_sgd_step(L, b["w"], b["b"], b["dw"], b["db"], lr, comm_stream)
+                    joined = False
                 da = b["dx"]
+        if not joined:
+            s_main.wait_stream(comm_stream)
 
-    def sgd(self, lr, stream=None, head=True):
-        """SGD on the own conv slices and the head, one fused launch (cp_sgd_multi)."""
+    def sgd(self, lr, stream=None, head=True, convs=True):
+        """SGD on the own conv slices (convs) and the head, one fused launch (cp_sgd_multi)."""
         pairs = []
-        for i, b in enumerate(self.buf):
+        for i, b in enumerate(self.buf if convs else []):
             d, kr = self.descs[i], self.parts[i].k_count[self.rank]
             ktot = (self.sizes[i].w - 256) // 4 // max(kr, 1) if kr else 0
             pairs.append((b["w"], b["dw"], kr * ktot))
@@ -250,14 +272,18 @@ class PartitionedNet:
         if head:
             pairs.append((self.head["wfc"], self.head["dwfc"]))
             pairs.append((self.head["bfc"], self.head["dbfc"]))
-        cp.cp_sgd_multi(pairs, lr, stream)
+        if pairs:
+            cp.cp_sgd_multi(pairs, lr, stream)
 
-    def step(self, lr=0.01, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True, head=True):
+    def step(self, lr=0.01, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True, head=True,
+             fuse_sgd=False):
         """One SGD step; head=False: the conv stage with the head replaced by the fixed dA2 in head["da"]
-        (SURVEY §8(d) conv-stage images/s)."""
+        (SURVEY §8(d) conv-stage images/s).  fuse_sgd: the conv slices' update runs inside the backward
+        pass (see backward(lr=...)) instead of one cp_sgd_multi launch at the end - measured no faster
+        on B200, so off by default."""
         self.forward(stream, comm_stream, head)
-        self.backward(dx_mode, stream, comm_stream, overlap, head)
-        self.sgd(lr, stream, head)
+        self.backward(dx_mode, stream, comm_stream, overlap, head, lr=lr if fuse_sgd else None)
+        self.sgd(lr, stream, head, convs=not fuse_sgd)
 
     def loss(self):
         return float(self.head["loss"][0].item())

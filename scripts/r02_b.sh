@@ -1,0 +1,5 @@
+# fused SGD in the backward-filter kernels: GPU suite (bitwise test), bench N=1/4/2
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02b_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r02b_pytest.log
+timeout 300 python bench.py > gpurun_out/r02b_n1.json 2> gpurun_out/r02b_n1.err; echo "n1 rc=$?"
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29522 bench.py --gpus 4 > gpurun_out/r02b_n4.json 2> gpurun_out/r02b_n4.err; echo "n4 rc=$?"
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29521 bench.py --gpus 2 > gpurun_out/r02b_n2.json 2> gpurun_out/r02b_n2.err; echo "n2 rc=$?"

@@ -396,3 +396,48 @@ def test_planner_variants(orc, monkeypatch, env, P, B, align):
         monkeypatch.setenv(k, v)
     test_forward_parity(orc, "tf32", P, B, align)
     test_backward_parity(orc, "tf32", P, B, align)
+
+
+# Fused SGD (conv_part_backward_filter_sgd): the update w -= lr*dW, b -= lr*db runs where dW / db are final
+# (wgrad epilogue, stream-tail / split-K reduce, bias reduce, conv1 reduce) and must equal
+# backward_filter + conv_part_sgd_step bit for bit (same fma), with dW / db unchanged.  Cases: the
+# stream tail (P=1, B=128), Eq. 1 maps (P=3), forced split-K (CP_TC_ACC_TERMS), no tail
+# (CP_TC_WGRAD_TAIL=0), both layers (conv1: the image-layer kernel), and the SIMT mode (separate update).
+@pytest.mark.parametrize("env", [{}, {"CP_TC_ACC_TERMS": "1024"}, {"CP_TC_WGRAD_TAIL": "0"}],
+                         ids=["default", "split-K", "no-tail"])
+@pytest.mark.parametrize("math,P,B", [("tf32", 1, 128), ("tf32", 3, 40), ("tf32", 2, 64), ("simt", 2, 40)])
+def test_fused_sgd_bitwise(orc, monkeypatch, env, math, P, B):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    m = math_id(math)
+    x, w1, b1, w2, b2 = layer_data(B=B)
+    K1, K2 = w1.shape[0], w2.shape[0]
+    p1, p2 = parts_for(P, K1), parts_for(P, K2)
+    L1 = LocalLayer(B, 3, 20, K1, 5, p1, None, m)
+    L1.load(w1, b1)
+    xd = dev(x)
+    L1.forward(xd)
+    L2 = LocalLayer(B, K1, 8, K2, 5, p2, p1, m)
+    L2.load(w2, b2)
+    L2.forward(L1.y)
+    lr = 0.0371
+    for L, xin, hp, K in ((L2, L1.y, 2, K2), (L1, xd, 8, K1)):
+        da = pack(synth.normal((B, K, hp, hp), 77, 1.0).astype(np.float32), L.out_part)
+        for r in range(L.P):
+            if not L.out_part.k_count[r]:
+                continue
+            args = (L.h[r], da, L.saved[r], L.y, xin)
+            dw_a, db_a = torch.zeros_like(L.w[r]), torch.zeros_like(L.b[r])
+            w_a, b_a = L.w[r].clone(), L.b[r].clone()
+            cp.conv_part_backward_filter(*args, dw_a, db_a, L.ws[r])
+            cp.conv_part_sgd_step(L.h[r], w_a, b_a, dw_a, db_a, lr)
+            dw_b, db_b = torch.zeros_like(L.w[r]), torch.zeros_like(L.b[r])
+            w_b, b_b = L.w[r].clone(), L.b[r].clone()
+            cp.conv_part_backward_filter_sgd(*args, dw_b, db_b, w_b, b_b, lr, L.ws[r])
+            torch.cuda.synchronize()
+            tag = f"layer K={K} rank {r} ({math}, P={P}, {env})"
+            assert torch.equal(dw_a, dw_b) and torch.equal(db_a, db_b), f"dW/db differ with the fused update: {tag}"
+            assert torch.equal(w_a, w_b), f"fused weight update differs: {tag}"
+            assert torch.equal(b_a, b_b), f"fused bias update differs: {tag}"
+            assert not torch.equal(w_a, L.w[r]), f"no update happened: {tag}"
+    L1.close(); L2.close()
