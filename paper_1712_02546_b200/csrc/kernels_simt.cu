@@ -729,8 +729,11 @@ __host__ __device__ inline int fc_nsc(const Blocks& g) {
   return (m + kFcChunk - 1) / kFcChunk;
 }
 
+#ifndef FC_FWD_MINB
+#define FC_FWD_MINB 1   // experiment builds: minimum resident CTAs per SM for fc_fwd_partial
+#endif
 template <int OO>   // compile-time class bound (10 for CIFAR's 10 classes, else kMaxO)
-__global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
+__global__ void __launch_bounds__(256, FC_FWD_MINB) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
                                                       float* __restrict__ part, Blocks g, int B, int O, int PW,
                                                       int nsc) {
   __shared__ __align__(16) float xs[128 * kFcLd];
@@ -976,10 +979,16 @@ __global__ void __launch_bounds__(256) fc_bwd_fused(const float* __restrict__ dl
 // of x in flight (the load latency, not bandwidth, bounded the one-thread-per-feature version); its W
 // column sits in registers, dlogits rows in shared memory (broadcast reads); the 8 groups' dW partials
 // combine through shared memory.  CTA 0 also writes dbfc = sum_b dlogits.
-constexpr int kFcF = 64, kFcG = 8;   // features x image groups per CTA
+#ifndef FC_KFCG
+#define FC_KFCG 8
+#endif
+#ifndef FC_BWD_MINB
+#define FC_BWD_MINB 1
+#endif
+constexpr int kFcF = 64, kFcG = FC_KFCG;   // features x image groups per CTA
 constexpr int kFcRows = 256;         // images per shared-memory dlogits chunk
 template <int OO>
-__global__ void __launch_bounds__(kFcF * kFcG) fc_bwd_cols(const float* __restrict__ dl, const float* __restrict__ x,
+__global__ void __launch_bounds__(kFcF * kFcG, FC_BWD_MINB) fc_bwd_cols(const float* __restrict__ dl, const float* __restrict__ x,
                                                           const float* __restrict__ wg, float* __restrict__ dx,
                                                           float* __restrict__ dwg, float* __restrict__ dbfc, Blocks g,
                                                           int B, int O, int PW, int64_t F) {

@@ -57,6 +57,8 @@ CASES = [
     ("P2-zero-kernel-conv1", 2, 40, {"counts": [36, 0]}, {"counts": [40, 32]}),
     ("P3-zero-kernel-conv2", 3, 40, {"counts": [12, 12, 12]}, {"counts": [0, 72, 0]}),
     ("P2-B128-pixel-dgrad", 2, 128, {"t": [1.0, 1.0]}, {"t": [1.0, 1.0]}),
+    # 8 ranks (no 8-GPU box in the pool: the 8-way fused paths are exercised here)
+    ("P8-even", 8, 40, {"t": [1.0] * 8}, {"t": [1.0] * 8}),
 ]
 
 
