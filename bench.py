@@ -503,6 +503,9 @@ def main():
             cpy.wait_stream(s)
             prefetch(0)
         s.wait_event(ready[j])
+        if k + 1 < args.steps:   # step k+1's inputs travel while step k computes (other staging buffer)
+            cpy.wait_stream(s)
+            prefetch(k + 1)
         if e2e_graphs is not None:
             e2e_graphs[j].replay()   # staging -> input copies + the step, one graph launch
         else:
@@ -512,9 +515,6 @@ def main():
         free[j].record(s)
         loss_host.copy_(pn.head["loss"][:1], non_blocking=True)
         e2e_ev[k][1].record(s)
-        if k + 1 < args.steps:   # step k+1's inputs travel while step k computes (other staging buffer),
-            cpy.wait_event(e2e_ev[k][0])   # after this window opened; enqueued once the step is (host order)
-            prefetch(k + 1)
         e2e_ev[k][1].synchronize()
         host_losses.append(float(loss_host[0]))
     torch.cuda.synchronize(dev)
