@@ -765,19 +765,20 @@ struct CtlPtrs {
   uint32_t* p[CP_MAX_RANKS];
 };
 __global__ void flag_barrier_kernel(CtlPtrs peer, uint32_t* mine, int me, int world) {
+  // one warp: thread q releases this rank's epoch at peer q and waits for peer q's (in parallel)
+  const int q = threadIdx.x;
   const uint32_t e = mine[kCtlEpoch] + 1;
-  mine[kCtlEpoch] = e;
-  __threadfence_system();
-  for (int q = 0; q < world; ++q)
-    if (q != me) st_release_sys(peer.p[q] + me, e);
-  const long long t0 = clock64();
-  for (int q = 0; q < world; ++q) {
-    if (q == me) continue;
+  __syncwarp();
+  if (q == 0) mine[kCtlEpoch] = e;
+  if (q < world && q != me) {
+    st_release_sys(peer.p[q] + me, e);
+    const long long t0 = clock64();
     while ((int)(ld_acquire_sys(mine + q) - e) < 0) {
       asm volatile("nanosleep.u32 64;");
       if (clock64() - t0 > (1ll << 35)) __trap();
     }
   }
+  __syncwarp();
 }
 
 int comm_barrier(cp_comm c, cudaStream_t s) {
@@ -789,7 +790,7 @@ int comm_barrier(cp_comm c, cudaStream_t s) {
   }
   CtlPtrs cp{};
   for (int q = 0; q < c->world; ++q) cp.p[q] = c->ctl_peer[q];
-  flag_barrier_kernel<<<1, 1, 0, s>>>(cp, c->ctl, c->rank, c->world);
+  flag_barrier_kernel<<<1, 32, 0, s>>>(cp, c->ctl, c->rank, c->world);
   CP_LAUNCHED();
   return CP_OK;
 }

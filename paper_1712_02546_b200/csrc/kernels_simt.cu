@@ -583,11 +583,11 @@ int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64
 struct FlagPtrs {
   uint32_t* f[CP_MAX_RANKS];
 };
-// Runs after the storing kernel (stream order): the fence makes its peer stores visible system-wide
-// before the release store of the flag.
+// Runs after the storing kernel (stream order); thread k releases peer k's flag (a system-scope release
+// orders everything before it, the previous kernel's stores included) - the releases run in parallel
+// instead of one system fence after another.
 __global__ void signal_peers_kernel(FlagPtrs fp, int n, int slot) {
-  __threadfence_system();
-  for (int k = 0; k < n; ++k) st_release_sys(fp.f[k] + slot, 1u);
+  if ((int)threadIdx.x < n) st_release_sys(fp.f[threadIdx.x] + slot, 1u);
 }
 __global__ void wait_flags_kernel(const uint32_t* flags, int n, int self, uint32_t target) {
   for (int r = 0; r < n; ++r)
@@ -598,7 +598,7 @@ int launch_signal_peers(uint32_t* const* peer_flags, int n, int slot, cudaStream
   if (n <= 0) return CP_OK;
   FlagPtrs fp{};
   for (int k = 0; k < n; ++k) fp.f[k] = peer_flags[k];
-  signal_peers_kernel<<<1, 1, 0, s>>>(fp, n, slot);
+  signal_peers_kernel<<<1, 32, 0, s>>>(fp, n, slot);
   CP_LAUNCHED();
   return CP_OK;
 }

@@ -25,7 +25,7 @@ def demangle(name):
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else None
     lines = []
-    for obj in ("kernels_tc.cu.o", "kernels_simt.cu.o", "comm.cu.o"):
+    for obj in ("kernels_tc.cu.o", "kernels_conv1.cu.o", "kernels_simt.cu.o", "comm.cu.o"):
         path = os.path.join(OBJ, obj)
         sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
         cur, counts = None, collections.OrderedDict()
@@ -46,7 +46,7 @@ def main():
                 counts[cur][op] += 1
         for fn, c in counts.items():
             fam = {k: v for k, v in c.items() if k != "instructions"}
-            if obj != "kernels_tc.cu.o" and not fam:
+            if obj not in ("kernels_tc.cu.o", "kernels_conv1.cu.o") and not fam:
                 continue
             short = re.sub(r"cp::\(anonymous namespace\)::|\(anonymous namespace\)::|cp::", "", fn).split("(")[0]
             items = ", ".join(f"{k} {v}" for k, v in sorted(fam.items()))
