@@ -384,6 +384,15 @@ int cp_sgd_multi(float* const* params, const float* const* grads, const int64_t*
  * comm == NULL or a single rank: no-op. */
 int cp_allreduce_sum(cp_comm comm, float* buf, int64_t n, void* stream);
 
+/* cp_allreduce_sum of the [B][O] partial logits followed by cp_softmax_xent on the sum, in ONE
+ * launch when the one-shot peer-memory path applies (the same block sums the slots in rank order,
+ * then computes loss and dlogits: dlogits bitwise the same as the two calls, the loss too for
+ * B <= 256 - beyond that its fixed-order tree runs over twice the threads).  logits is replaced by
+ * the summed logits.  Otherwise (comm NULL / one rank: softmax only; NCCL path) the two calls.
+ * B in [1,8192], O in [1,16]; CP_ERR_ARG otherwise; CP_ERR_UNSUPPORTED on a loopback handle. */
+int cp_allreduce_softmax_xent(cp_comm comm, float* logits, const int32_t* labels, int32_t B, int32_t O,
+                              float* loss, float* dlogits, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

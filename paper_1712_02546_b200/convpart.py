@@ -29,7 +29,7 @@ EXPORTS = [
     "cp_launch_count", "cp_last_error", "cp_pack_nchw", "cp_unpack_nchw", "cp_unpack_saved",
     "cp_pack_conv_weights", "cp_unpack_conv_weights", "cp_head_workspace_bytes", "cp_pack_fc_weights",
     "cp_unpack_fc_weights", "cp_fc_forward", "cp_softmax_xent", "cp_fc_backward", "cp_sgd",
-    "cp_allreduce_sum", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait", "conv_part_timing", "conv_part_kernel_time",
+    "cp_allreduce_sum", "cp_allreduce_softmax_xent", "cp_symmetric_alloc", "cp_symmetric_free", "cp_symmetric_wait", "conv_part_timing", "conv_part_kernel_time",
     "cp_sgd_multi", "cp_lrn_pool_forward", "cp_lrn_pool_backward", "cp_comm_create_loopback", "cp_symmetric_peer",
 ]
 CP_GATHER_CHUNKS = 256   # convpart.h: a complete gather block raises its arrival counter to this
@@ -120,6 +120,7 @@ def lib():
             "cp_fc_backward": [P, P, I32, I32, I32, pp, P, I32, P, P, P, P, P],
             "cp_sgd": [P, P, I64, ctypes.c_float, P],
             "cp_allreduce_sum": [P, P, I64, P],
+            "cp_allreduce_softmax_xent": [P, P, P, I32, I32, P, P, P],
             "cp_symmetric_alloc": [P, SZ, ctypes.POINTER(P)],
             "cp_symmetric_free": [P, P],
             "cp_symmetric_wait": [P, P, P],
@@ -328,6 +329,12 @@ def cp_fc_backward(dl, x, B, Hp, Wp, part, wg, O, dx, dwg, dbfc, ws, stream=None
 
 def cp_allreduce_sum(comm, buf, stream=None):
     _call("cp_allreduce_sum", comm, _ptr(buf), buf.numel(), _stream(stream))
+
+
+def cp_allreduce_softmax_xent(comm, logits, labels, B, O, loss, dlogits, stream=None):
+    """Sum the partial logits over all ranks, then softmax cross-entropy - one launch on the one-shot path."""
+    _call("cp_allreduce_softmax_xent", comm, _ptr(logits), _ptr(labels), int(B), int(O), _ptr(loss), _ptr(dlogits),
+          _stream(stream))
 
 
 class SymmetricBuffer:

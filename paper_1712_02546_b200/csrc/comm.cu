@@ -560,9 +560,18 @@ struct ArPtrs {
   float* s[CP_MAX_RANKS];
   uint32_t* c[CP_MAX_RANKS];
 };
+// Optional softmax-xent epilogue (y != nullptr): the summed vector is the [B][O] logits; the same block
+// then computes loss and dlogits (cp_allreduce_softmax_xent - one launch instead of two).
+struct SoftmaxArgs {
+  const int* y;
+  int B, O;
+  float* loss;
+  float* dl;
+};
 __global__ void __launch_bounds__(512) oneshot_allreduce_kernel(float* buf, int n, ArPtrs peers, float* mine,
-                                                                uint32_t* ctl, int me, int world) {
+                                                                uint32_t* ctl, int me, int world, SoftmaxArgs sm) {
   __shared__ uint32_t e_s;
+  __shared__ float wsum[16];
   if (threadIdx.x == 0) e_s = ctl[kCtlArEpoch] + 1;
   __syncthreads();
   const uint32_t e = e_s;
@@ -590,37 +599,65 @@ __global__ void __launch_bounds__(512) oneshot_allreduce_kernel(float* buf, int 
     for (int q = 1; q < world; ++q) t += src[(int64_t)q * kArMax + i];
     buf[i] = t;
   }
+  if (sm.y) {
+    __syncthreads();   // every summed logit written (block-visible global stores)
+    cp::softmax_xent_block(buf, sm.y, sm.B, sm.O, sm.loss, sm.dl, wsum);
+  }
+}
+
+// the one-shot path (scratch allocated lazily, outside graph capture), or nullptr
+static float* oneshot_scratch(cp_comm c, int64_t n, cudaStream_t s) {
+  if (!c->ctl || n > kArMax) return nullptr;
+  if (!c->ar) {   // collective lazy allocation - not while a graph is being captured
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return nullptr;
+    SymBuf ab{};
+    void* p = nullptr;
+    if (sym_map(c, (size_t)2 * c->world * kArMax * 4, &p, ab) != CP_OK) return nullptr;
+    c->ar = (float*)p;
+    for (int q = 0; q < c->world; ++q) c->ar_peer[q] = (float*)ab.peers[q];
+  }
+  return c->ar;
 }
 
 extern "C" int cp_allreduce_sum(cp_comm c, float* buf, int64_t n, void* stream) {
   if (!c || c->world == 1 || n == 0) return CP_OK;
   if (!buf || n < 0) CP_FAIL(CP_ERR_ARG, "cp_allreduce_sum: bad arguments");
   if (c->loop) CP_FAIL(CP_ERR_UNSUPPORTED, "cp_allreduce_sum: not available on a loopback communicator");
-  if (c->ctl && n <= kArMax) {
-    if (!c->ar) {   // collective lazy allocation - not while a graph is being captured
-      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-      CP_CUDA(cudaStreamIsCapturing((cudaStream_t)stream, &st));
-      if (st == cudaStreamCaptureStatusNone) {
-        SymBuf ab{};
-        void* p = nullptr;
-        CP_TRY(sym_map(c, (size_t)2 * c->world * kArMax * 4, &p, ab));
-        c->ar = (float*)p;
-        for (int q = 0; q < c->world; ++q) c->ar_peer[q] = (float*)ab.peers[q];
-      }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (oneshot_scratch(c, n, s)) {
+    ArPtrs ap{};
+    for (int q = 0; q < c->world; ++q) {
+      ap.s[q] = c->ar_peer[q];
+      ap.c[q] = c->ctl_peer[q];
     }
-    if (c->ar) {
-      ArPtrs ap{};
-      for (int q = 0; q < c->world; ++q) {
-        ap.s[q] = c->ar_peer[q];
-        ap.c[q] = c->ctl_peer[q];
-      }
-      oneshot_allreduce_kernel<<<1, 512, 0, (cudaStream_t)stream>>>(buf, (int)n, ap, c->ar, c->ctl, c->rank, c->world);
-      CP_LAUNCHED();
-      return CP_OK;
-    }
+    oneshot_allreduce_kernel<<<1, 512, 0, s>>>(buf, (int)n, ap, c->ar, c->ctl, c->rank, c->world, SoftmaxArgs{});
+    CP_LAUNCHED();
+    return CP_OK;
   }
-  CP_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclFloat, ncclSum, c->comm, (cudaStream_t)stream));
+  CP_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclFloat, ncclSum, c->comm, s));
   return CP_OK;
+}
+
+extern "C" int cp_allreduce_softmax_xent(cp_comm c, float* logits, const int32_t* labels, int32_t B, int32_t O,
+                                         float* loss, float* dlogits, void* stream) {
+  if (!logits || !labels || !loss || !dlogits || B < 1 || B > 8192 || O < 1 || O > cp::kHeadMaxO)
+    CP_FAIL(CP_ERR_ARG, "cp_allreduce_softmax_xent: bad arguments");
+  const int64_t n = (int64_t)B * O;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c && c->world > 1 && !c->loop && oneshot_scratch(c, n, s)) {
+    ArPtrs ap{};
+    for (int q = 0; q < c->world; ++q) {
+      ap.s[q] = c->ar_peer[q];
+      ap.c[q] = c->ctl_peer[q];
+    }
+    const SoftmaxArgs sm{labels, B, O, loss, dlogits};
+    oneshot_allreduce_kernel<<<1, 512, 0, s>>>(logits, (int)n, ap, c->ar, c->ctl, c->rank, c->world, sm);
+    CP_LAUNCHED();
+    return CP_OK;
+  }
+  CP_TRY(cp_allreduce_sum(c, logits, n, stream));   // world 1: no-op; otherwise NCCL (or unsupported)
+  return cp_softmax_xent(logits, labels, B, O, loss, dlogits, stream);
 }
 
 namespace cp {

@@ -122,6 +122,52 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// softmax cross-entropy over B rows of O <= kHeadMaxO logits by one thread block:
+// loss = mean_b (logsumexp(l_b) - l_b[y_b]), dl = (softmax - onehot) / B; the loss sum is a
+// fixed-order tree (warp shuffles, then the warps in order) - identical wherever it runs.
+// wsum: shared scratch of blockDim/32 floats.
+constexpr int kHeadMaxO = 16;
+__device__ __forceinline__ void softmax_xent_block(const float* logits, const int* y, int B, int O, float* loss,
+                                                   float* dl, float* wsum) {
+  float part = 0.f;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const float* lp = logits + (int64_t)b * O;   // the row's logits in registers (one pass)
+    float l[kHeadMaxO];
+#pragma unroll
+    for (int o = 0; o < kHeadMaxO; ++o) l[o] = o < O ? lp[o] : -INFINITY;
+    const int lab = y[b];
+    float m = l[0];
+#pragma unroll
+    for (int o = 1; o < kHeadMaxO; ++o) m = fmaxf(m, l[o]);
+    float se = 0.f;
+#pragma unroll
+    for (int o = 0; o < kHeadMaxO; ++o)
+      if (o < O) se += expf(l[o] - m);
+    const float lse = m + logf(se);
+    if (lab < 0 || lab >= O) {
+      part += __int_as_float(0x7fc00000);  // NaN loss flags an out-of-range label
+      continue;
+    }
+    float ll = 0.f;
+#pragma unroll
+    for (int o = 0; o < kHeadMaxO; ++o)
+      if (o == lab) ll = l[o];
+    part += lse - ll;
+#pragma unroll
+    for (int o = 0; o < kHeadMaxO; ++o)
+      if (o < O) dl[(int64_t)b * O + o] = (expf(l[o] - lse) - (o == lab ? 1.f : 0.f)) / (float)B;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wsum[w];
+    *loss = t / (float)B;
+  }
+}
+
 // wait until *p >= target (arrival counters / flags)
 __device__ __forceinline__ void wait_flag_sys(const uint32_t* p, uint32_t target = 1) {
   const long long t0 = clock64();

@@ -552,20 +552,22 @@ int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float
 struct SrcPtrs {
   const float* p[CP_MAX_RANKS];
 };
-__global__ void __launch_bounds__(256) sum_peer_blocks_kernel(SrcPtrs src, int n_src, float* out, int64_t n4) {
-  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  if (i >= n4) return;
-  float4 v[CP_MAX_RANKS];
+__global__ void __launch_bounds__(512) sum_peer_blocks_kernel(SrcPtrs src, int n_src, float* out, int64_t n4) {
+  // grid-stride over a small grid: the sum runs beside the next GEMM (wgrad) on a few SMs instead of
+  // flooding every SM with short blocks
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v[CP_MAX_RANKS];
 #pragma unroll
-  for (int r = 0; r < CP_MAX_RANKS; ++r)
-    if (r < n_src) v[r] = reinterpret_cast<const float4*>(src.p[r])[i];
-  float4 a = v[0];
+    for (int r = 0; r < CP_MAX_RANKS; ++r)
+      if (r < n_src) v[r] = reinterpret_cast<const float4*>(src.p[r])[i];
+    float4 a = v[0];
 #pragma unroll
-  for (int r = 1; r < CP_MAX_RANKS; ++r)
-    if (r < n_src) {
-      a.x += v[r].x; a.y += v[r].y; a.z += v[r].z; a.w += v[r].w;
-    }
-  reinterpret_cast<float4*>(out)[i] = a;
+    for (int r = 1; r < CP_MAX_RANKS; ++r)
+      if (r < n_src) {
+        a.x += v[r].x; a.y += v[r].y; a.z += v[r].z; a.w += v[r].w;
+      }
+    reinterpret_cast<float4*>(out)[i] = a;
+  }
 }
 int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64_t n, cudaStream_t s) {
   if (n <= 0) return CP_OK;
@@ -575,7 +577,13 @@ int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64
     if (reinterpret_cast<uintptr_t>(src[r]) & 15) CP_FAIL(CP_ERR_UNSUPPORTED, "sum_peer_blocks: unaligned block");
     sp.p[r] = src[r];
   }
-  sum_peer_blocks_kernel<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(sp, n_src, out, n / 4);
+  static const int blocks = [] {
+    const char* e = getenv("CP_RS_SUM_BLOCKS");   // grid of the rank-order sum (A/B; default 32)
+    return e ? std::max(1, atoi(e)) : 32;
+  }();
+  const int64_t n4 = n / 4;
+  const unsigned grid = (unsigned)std::min<int64_t>(blocks, (n4 + 511) / 512);
+  sum_peer_blocks_kernel<<<grid, 512, 0, s>>>(sp, n_src, out, n4);
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -714,7 +722,7 @@ __global__ void unpack_w_images_kernel(const float* __restrict__ wg, float* __re
 
 // ---------------------------------------------------------------- replicated head
 // FC features in gather order: block r, position pos = h*Wp+w, slot; f' = Hp*Wp*coff[r] + pos*kw[r] + slot.
-constexpr int kMaxO = 16;
+constexpr int kMaxO = kHeadMaxO;
 
 // FC forward over the gather layout (logits = W x + b).  CTA = (rank block r, position pos,
 // 64-slot chunk) x 128-image chunk: the x tile [128 images][64 slots] and the weight slice
@@ -826,44 +834,7 @@ __global__ void __launch_bounds__(1024) fc_fwd_reduce(const float* __restrict__ 
 __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restrict__ logits, const int* __restrict__ y,
                                                            int B, int O, float* loss, float* dl) {
   __shared__ float wsum[8];
-  float part = 0.f;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    // the row's logits in registers (one pass over global memory, O <= kMaxO)
-    const float* lp = logits + (int64_t)b * O;
-    float l[kMaxO];
-#pragma unroll
-    for (int o = 0; o < kMaxO; ++o) l[o] = o < O ? lp[o] : -INFINITY;
-    const int lab = y[b];
-    float m = l[0];
-#pragma unroll
-    for (int o = 1; o < kMaxO; ++o) m = fmaxf(m, l[o]);
-    float se = 0.f;
-#pragma unroll
-    for (int o = 0; o < kMaxO; ++o)
-      if (o < O) se += expf(l[o] - m);
-    const float lse = m + logf(se);
-    if (lab < 0 || lab >= O) {
-      part += __int_as_float(0x7fc00000);  // NaN loss flags an out-of-range label
-      continue;
-    }
-    float ll = 0.f;
-#pragma unroll
-    for (int o = 0; o < kMaxO; ++o)
-      if (o == lab) ll = l[o];
-    part += lse - ll;
-#pragma unroll
-    for (int o = 0; o < kMaxO; ++o)
-      if (o < O) dl[(int64_t)b * O + o] = (expf(l[o] - lse) - (o == lab ? 1.f : 0.f)) / (float)B;
-  }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = part;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wsum[w];
-    *loss = t / (float)B;
-  }
+  softmax_xent_block(logits, y, B, O, loss, dl, wsum);
 }
 
 // FC backward in one launch (S:L98-115 chain rule through logits = W x + b): CTA = (rank block r,

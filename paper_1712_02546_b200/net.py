@@ -205,9 +205,12 @@ class PartitionedNet:
         bias = hd["bfc"] if (self.head_mode == "replicated" or self.rank == 0) else None
         cp.cp_fc_forward(self.head_x, self.B, self.Hp, self.Wp, self.head_part, hd["wfc"], bias, self.O, hd["logits"],
                          hd["ws"], stream)
-        if self.head_mode == "partitioned":
-            cp.cp_allreduce_sum(self.comm, hd["logits"], stream)
-        cp.cp_softmax_xent(hd["logits"], self.labels, self.B, self.O, hd["loss"], hd["dlogits"], stream)
+        if self.head_mode == "partitioned" and self.comm is not None:
+            # the partial logits' AllReduce and the softmax in one launch (one-shot peer-memory path)
+            cp.cp_allreduce_softmax_xent(self.comm, hd["logits"], self.labels, self.B, self.O, hd["loss"], hd["dlogits"],
+                                         stream)
+        else:
+            cp.cp_softmax_xent(hd["logits"], self.labels, self.B, self.O, hd["loss"], hd["dlogits"], stream)
 
     def backward(self, dx_mode=cp.CP_DX_REDUCE_SCATTER, stream=None, comm_stream=None, overlap=True, head=True,
                  lr=None):

@@ -39,12 +39,14 @@ def phases(pn, s, cs):
     bias = hd["bfc"] if pn.rank == 0 else None
     cp.cp_fc_forward(pn.head_x, pn.B, pn.Hp, pn.Wp, pn.head_part, hd["wfc"], bias, pn.O, hd["logits"], hd["ws"], s)
     mark("fc_fwd")
-    cp.cp_allreduce_sum(pn.comm, hd["logits"], s)
-    mark("logits_allreduce")
-    cp.cp_softmax_xent(hd["logits"], pn.labels, pn.B, pn.O, hd["loss"], hd["dlogits"], s)
+    if pn.comm is not None:
+        cp.cp_allreduce_softmax_xent(pn.comm, hd["logits"], pn.labels, pn.B, pn.O, hd["loss"], hd["dlogits"], s)
+    else:
+        cp.cp_softmax_xent(hd["logits"], pn.labels, pn.B, pn.O, hd["loss"], hd["dlogits"], s)
+    mark("logits_allreduce+softmax")
     cp.cp_fc_backward(hd["dlogits"], pn.head_x, pn.B, pn.Hp, pn.Wp, pn.head_part, hd["wfc"], pn.O, pn.head_da,
                       hd["dwfc"], hd["dbfc"], hd["ws"], s)
-    mark("softmax+fc_bwd")
+    mark("fc_bwd")
     da = hd["da"]
     for i in reversed(range(len(pn.layers))):
         L, b = pn.layers[i], pn.buf[i]
