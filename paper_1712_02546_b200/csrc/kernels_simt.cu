@@ -552,22 +552,22 @@ int launch_sum_slots(const float* slots, int64_t slot_stride, int n_slots, float
 struct SrcPtrs {
   const float* p[CP_MAX_RANKS];
 };
-__global__ void __launch_bounds__(512) sum_peer_blocks_kernel(SrcPtrs src, int n_src, float* out, int64_t n4) {
-  // grid-stride over a small grid: the sum runs beside the next GEMM (wgrad) on a few SMs instead of
-  // flooding every SM with short blocks
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    float4 v[CP_MAX_RANKS];
+__global__ void __launch_bounds__(256) sum_peer_blocks_kernel(SrcPtrs src, int n_src, float* out, int64_t n4) {
+  // one float4 per thread over a full grid: beside the concurrent wgrad the sum needs many resident
+  // warps to finish in time (a 32-block grid-stride version left 53-59 us of dX wait at N=2)
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= n4) return;
+  float4 v[CP_MAX_RANKS];
 #pragma unroll
-    for (int r = 0; r < CP_MAX_RANKS; ++r)
-      if (r < n_src) v[r] = reinterpret_cast<const float4*>(src.p[r])[i];
-    float4 a = v[0];
+  for (int r = 0; r < CP_MAX_RANKS; ++r)
+    if (r < n_src) v[r] = reinterpret_cast<const float4*>(src.p[r])[i];
+  float4 a = v[0];
 #pragma unroll
-    for (int r = 1; r < CP_MAX_RANKS; ++r)
-      if (r < n_src) {
-        a.x += v[r].x; a.y += v[r].y; a.z += v[r].z; a.w += v[r].w;
-      }
-    reinterpret_cast<float4*>(out)[i] = a;
-  }
+  for (int r = 1; r < CP_MAX_RANKS; ++r)
+    if (r < n_src) {
+      a.x += v[r].x; a.y += v[r].y; a.z += v[r].z; a.w += v[r].w;
+    }
+  reinterpret_cast<float4*>(out)[i] = a;
 }
 int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64_t n, cudaStream_t s) {
   if (n <= 0) return CP_OK;
@@ -577,13 +577,7 @@ int launch_sum_peer_blocks(const float* const* src, int n_src, float* out, int64
     if (reinterpret_cast<uintptr_t>(src[r]) & 15) CP_FAIL(CP_ERR_UNSUPPORTED, "sum_peer_blocks: unaligned block");
     sp.p[r] = src[r];
   }
-  static const int blocks = [] {
-    const char* e = getenv("CP_RS_SUM_BLOCKS");   // grid of the rank-order sum (A/B; default 32)
-    return e ? std::max(1, atoi(e)) : 32;
-  }();
-  const int64_t n4 = n / 4;
-  const unsigned grid = (unsigned)std::min<int64_t>(blocks, (n4 + 511) / 512);
-  sum_peer_blocks_kernel<<<grid, 512, 0, s>>>(sp, n_src, out, n4);
+  sum_peer_blocks_kernel<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(sp, n_src, out, n / 4);
   CP_LAUNCHED();
   return CP_OK;
 }
