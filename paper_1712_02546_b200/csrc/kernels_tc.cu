@@ -16,6 +16,7 @@
 // Persistent: grid = min(units, #SMs); two TMEM accumulators (2 x 256 columns) let the
 // epilogue of tile t overlap the MMAs of tile t+1.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <vector>
 
@@ -97,6 +98,10 @@ struct TcParams {
   float* sgd_w;        // wgrad with the fused SGD update: the own weights (w -= sgd_lr * dW where dW is final)
   float sgd_lr;
   int m_off;           // fwd transposed: first own slot of M tile 0 (split forward: the remainder)
+  int nsched_groups;   // multicast forward: clusters the host planned for (resident at once)
+  int fcl;             // fwd transposed, multicast cluster (conv_tc_kernel<..., MC = 1>): CTAs per cluster = the
+                       // slice's M tiles; a unit = one position tile for the whole cluster, its activation
+                       // tile loaded once (each CTA a slice, TMA multicast to all), weights per CTA
   int epi_groups;      // 1 or 2 epilogue warp groups (blockDim = 128 + 128*groups; CP_TC_EPI_GROUPS)
   int max_chunks;      // longest K loop of a unit (after split), for the launch heuristics
   int wide;            // MN-major operands loaded as one 5-D box of 32-column atoms (else per-atom boxes)
@@ -185,9 +190,10 @@ __device__ __forceinline__ Unit decode_unit(const TcParams& p, int u, int rank) 
     u = p.tail_full + t.tu;
   }
   if (PASS == PASS_FWD && CG == 1 && p.fwdT) {   // (compiled out of the pair kernels)
-    // kernel tile fastest (the units of a wave share the window's activation tile), then image chunk
-    t.mt = u % p.numM;
-    const int rest = u / p.numM, nb = p.Bp / 64;
+    // kernel tile fastest (the units of a wave share the window's activation tile), then image chunk;
+    // multicast cluster: the unit is the position tile, the kernel tile the CTA's rank in the cluster
+    t.mt = p.fcl ? rank : u % p.numM;
+    const int rest = p.fcl ? u : u / p.numM, nb = p.Bp / 64;
     t.bc = rest % nb;
     const int ij = rest / nb;
     t.j = ij % p.Wp;
@@ -517,8 +523,9 @@ __device__ __forceinline__ void store_f32x32(float* dst, const float (&v)[32], i
   }
 }
 
-template <int PASS, int CG, int DT>
+template <int PASS, int CG, int DT, int MC>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
+  // MC = 1 (PASS_FWD, CG = 1, transposed): clusters of p.fcl CTAs share each activation tile (multicast)
   // DT = 1: bf16 operands (kind::f16), a K-chunk = 64 elements; MN-major 64-element groups ("atoms")
   constexpr int BKE = DT ? 64 : 32;          // elements per 128-byte row = per K-chunk
   constexpr int ASH = DT ? 6 : 5;            // log2 of the MN-major group width
@@ -544,11 +551,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
-  const int group = blockIdx.x / CG, ngroups = gridDim.x / CG;
+  const uint32_t crank = MC ? cluster_ctarank() : rank;   // multicast cluster: this CTA's kernel tile
+  const int CS = MC ? p.fcl : CG;                 // CTAs per unit group
+  const int group = blockIdx.x / CS, ngroups = gridDim.x / CS;
+  const uint16_t mc_mask = (uint16_t)((1u << CS) - 1u);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? CS : 1);          // multicast: every CTA of the cluster releases the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   }
   if (warp == 2) tmem_alloc<CG>(tmem_slot, 512);
   tc_fence_before();
-  if (CG == 2) cluster_sync(); else __syncthreads();
+  if (CG == 2 || MC) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -578,7 +588,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       for (int k = 0;; ++k) {
         const int u = unit_at(p, group, ngroups, k);
         if (u < 0) break;
-        const Unit t = decode_unit<PASS, CG>(p, u, rank);
+        const Unit t = decode_unit<PASS, CG>(p, u, MC ? crank : rank);
         const int n_mma = mma_n<PASS, CG, DT>(t.n);
         const int nb_own = CG == 2 ? n_mma / 2 : n_mma;          // B columns staged by this CTA
         const int nb0 = t.n0 + (int)rank * nb_own;                // first B column of this CTA
@@ -671,7 +681,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             if (CG == 1 && !DT && p.fwdT) {
               // A = the own kernels' weight rows (K-major), B = 4 window pixels x 64 images (K-major)
               ld2(a, &p.maps[CP_MAX_RANKS], ch.tap * p.Cg + p.coff[ch.rb] + ch.c * BKE, t.n0);
-              if (p.unified) ld5(b, &p.maps[0], ch.c * BKE, t.bc * 64, 2 * t.j + s, 2 * t.i + r, ch.rb);
+              if (MC) {
+                // this CTA's slice of the activation tile (rows = image + 64 w + 128 h), multicast to the
+                // cluster: 2 CTAs one h row each (maps[1], 128 rows); 3 CTAs h = 0 (maps[1]) and the two
+                // pixels of h = 1 (maps[2], 64 rows); 4 CTAs one pixel each (maps[2])
+                const int hh = CS == 2 ? (int)crank : CS == 3 ? (crank > 0) : (int)(crank >> 1);
+                const int ww = CS == 2 ? 0 : CS == 3 ? (crank > 0 ? (int)crank - 1 : 0) : (int)(crank & 1);
+                const bool half = CS == 2 || (CS == 3 && crank == 0);
+                tma_load_5d_mc(b + (hh * 128 + ww * 64) * 128, &p.maps[half ? 1 : 2], &full[stage], ch.c * BKE,
+                               t.bc * 64, 2 * t.j + s + ww, 2 * t.i + r + hh, ch.rb, mc_mask);
+              } else if (p.unified) ld5(b, &p.maps[0], ch.c * BKE, t.bc * 64, 2 * t.j + s, 2 * t.i + r, ch.rb);
               else ld4(b, &p.maps[ch.rb], ch.c * BKE, t.bc * 64, 2 * t.j + s, 2 * t.i + r);
             } else if (TC_DIAG(p, 2)) {
             } else if (p.unified)
@@ -722,6 +741,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             phase ^= 1;
           }
         });
+      }
+      if (MC) {   // drain: every CTA of the cluster released every stage this CTA multicast into
+        for (int i = 0; i < C::STAGES; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -779,7 +807,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           } else {
             for (int k = 0; k < ch.ksteps; ++k) mma(k);
           }
-          if (CG == 2) mma_commit_cg2(&empty[stage]); else mma_commit(&empty[stage]);
+          if (CG == 2) mma_commit_cg2(&empty[stage]);
+          else if (MC) mma_commit_mc(&empty[stage], mc_mask);   // every CTA that multicast into the stage
+          else mma_commit(&empty[stage]);
           if (halo && ch.last) {
             if (CG == 2) mma_commit_cg2(&aempty[ast]); else mma_commit(&aempty[ast]);
             if (++ast == 2) {
@@ -864,7 +894,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     for (int k = 0;; ++k, ++local) {
       const int u = unit_at(p, group, ngroups, k);
       if (u < 0) break;
-      const Unit t = decode_unit<PASS, CG>(p, u, rank);
+      const Unit t = decode_unit<PASS, CG>(p, u, MC ? crank : rank);
       const int acc = local & 1;
       const int nchunk = (t.n + 31) / 32;
       // forward bias of this unit's chunks (one column per lane), loaded before the accumulator wait
@@ -889,10 +919,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int kk = t.n0 + row;
         for (int h2 = grp; h2 < 2; h2 += p.epi_groups) {
           if (t.tail) {
+            const int64_t tile = MC ? (int64_t)t.piece * CS + crank : (int64_t)t.piece;   // [piece][cluster rank]
             for (int pp = 0; pp < 4; ++pp) {
               float v[32];
               tmem_ld_32x32b_x32(tbase + (pp * 2 + h2) * 32, v);
-              store_f32x32(p.tail_buf + ((int64_t)t.piece * BM + row) * BN + (pp * 2 + h2) * 32, v, 32);
+              store_f32x32(p.tail_buf + (tile * BM + row) * BN + (pp * 2 + h2) * 32, v, 32);
             }
             continue;
           }
@@ -1099,7 +1130,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     if ((PASS == PASS_FWD && p.npeers > 0) || (PASS == PASS_DGRAD && p.fused_dx)) __threadfence_system();
   }
   tc_fence_before();
-  if (CG == 2) cluster_sync(); else __syncthreads();
+  if (CG == 2 || MC) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, 512);
@@ -1211,15 +1242,16 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
 // per (tile row, tail unit), one thread per image.
 __global__ void fwd_tail_finish_t(const float* __restrict__ buf, const float* __restrict__ bias, float* __restrict__ y,
                                   uint8_t* __restrict__ saved, const __grid_constant__ FwdTailInfo ti) {
-  const int tu = blockIdx.y, row = blockIdx.x, b = threadIdx.x;
-  const int kk = ti.n0[tu] + row;
+  // blockIdx.z: the M tile within a multicast cluster's unit (ti.cg tiles per piece; 1 otherwise)
+  const int tu = blockIdx.y, row = blockIdx.x, b = threadIdx.x, mt = blockIdx.z;
+  const int kk = ti.n0[tu] + mt * BM + row;
   if (kk >= ti.Kc) return;
   const int bb = ti.bc0[tu] + b;
   const bool ok = bb < ti.B && kk < ti.Kr;
   const float bs = (bias && kk < ti.Kr) ? bias[kk] : 0.f;
   float zq[4] = {0.f, 0.f, 0.f, 0.f};
   for (int pc = ti.pbeg[tu]; pc < ti.pbeg[tu + 1]; ++pc) {
-    const float* src = buf + ((int64_t)pc * BM + row) * BN + b;
+    const float* src = buf + (((int64_t)pc * ti.cg + mt) * BM + row) * BN + b;
 #pragma unroll
     for (int q = 0; q < 4; ++q) zq[q] += src[q * 64];
   }
@@ -1442,34 +1474,64 @@ int num_sms() {
   return n;
 }
 
-template <int PASS, int CG, int DT = 0>
-int launch_cg(const TcParams& p, cudaStream_t s) {
-  if (p.units <= 0) return CP_OK;
-  static bool attr = false;
-  if (!attr) {
-    CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS, CG, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Cfg<CG, PASS>::SMEM));
-    attr = true;
-  }
-  const int groups = std::min(p.units, num_sms() / CG);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(groups * CG);
+// launch shape of conv_tc_kernel<PASS, CG, DT, MC>: block size (epilogue groups) and, for the multicast
+// clusters, how many clusters of `cs` CTAs can be resident at once (cluster placement is per GPC)
+template <int PASS, int CG, int DT, int MC>
+static void launch_shape(TcParams& p, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, int cs) {
   // short K loops (conv1: 3 chunks per tile) are epilogue-bound -> two epilogue warp groups;
   // long ones keep one group (fewer warps polling barriers next to the MMA issuer)
-  TcParams* pp = const_cast<TcParams*>(&p);
-  if (pp->epi_groups <= 0) pp->epi_groups = p.max_chunks < 64 ? 2 : 1;
-  pp->epi_groups = std::max(1, std::min(EPI_GROUPS, pp->epi_groups));
-  cfg.blockDim = dim3(128 + 128 * pp->epi_groups);
+  if (p.epi_groups <= 0) p.epi_groups = p.max_chunks < 64 ? 2 : 1;
+  p.epi_groups = std::max(1, std::min(EPI_GROUPS, p.epi_groups));
+  cfg.blockDim = dim3(128 + 128 * p.epi_groups);
   cfg.dynamicSmemBytes = Cfg<CG, PASS>::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.x = cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CP_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<PASS, CG, DT>, p));
+}
+
+template <int PASS, int CG, int DT = 0, int MC = 0>
+static int kernel_attr() {
+  static bool attr = false;
+  if (!attr) {
+    CP_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PASS, CG, DT, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Cfg<CG, PASS>::SMEM));
+    attr = true;
+  }
+  return CP_OK;
+}
+
+// clusters of `cs` CTAs of the multicast transposed forward that fit on the GPU at once
+int fwd_mc_max_clusters(TcParams& p, int cs) {
+  if (kernel_attr<PASS_FWD, 1, 0, 1>() != CP_OK) return 0;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(cs * (num_sms() / cs));
+  launch_shape<PASS_FWD, 1, 0, 1>(p, cfg, at, cs);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, conv_tc_kernel<PASS_FWD, 1, 0, 1>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return std::min(n, num_sms() / cs);
+}
+
+template <int PASS, int CG, int DT = 0, int MC = 0>
+int launch_cg(const TcParams& p, cudaStream_t s) {
+  if (p.units <= 0) return CP_OK;
+  CP_TRY((kernel_attr<PASS, CG, DT, MC>()));
+  TcParams* pp = const_cast<TcParams*>(&p);
+  const int cs = MC ? p.fcl : CG;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  launch_shape<PASS, CG, DT, MC>(*pp, cfg, at, cs);
+  const int max_groups = MC ? p.nsched_groups : num_sms() / CG;   // MC: the host planned this many clusters
+  const int groups = std::min(p.units, max_groups);
+  cfg.gridDim = dim3(groups * cs);
+  cfg.stream = s;
+  CP_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<PASS, CG, DT, MC>, p));
   CP_LAUNCHED();
   return CP_OK;
 }
@@ -1935,6 +1997,14 @@ int tc_time_mark(Layer& L, int pass, int end, cudaStream_t s) {
   return CP_OK;
 }
 
+// multicast-cluster transposed forward (CP_TC_FWD_MC=1, with the transposed forward): 2-4 kernel tiles of
+// 128 share each activation tile, loaded once per cluster (each CTA a slice, TMA multicast)
+static bool fwd_mc_enabled(const Layer& L, int m_off) {
+  const int tiles = (L.Kc - m_off + BM - 1) / BM;
+  return env_int("CP_TC_FWD_MC", 0) && !L.images && op_bytes(L) == 4 && tiles >= 2 && tiles <= 4 &&
+         L.Bp % 64 == 0 && equal_blocks(L);
+}
+
 // One forward GEMM launch over own slots [0, kc) on N (kernels-on-N kernels) or, transposed, over
 // [m_off, Kc) on M; force_T: -1 = CP_TC_FWD_T, 0/1 = off/on.  `push`: this launch runs the gather push.
 static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* b, float* y_block, uint8_t* saved,
@@ -1988,6 +2058,12 @@ static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* 
       const uint32_t box[5] = {(uint32_t)E, 64, 2, 2, 1};
       CP_TRY(make_map(&p.maps[r], (const char*)xin + (n == 1 ? 0 : L.in.start[r] * es), n == 1 ? 5 : 4, dims, str,
                       box, false, es));
+      if (n == 1 && fwd_mc_enabled(L, m_off)) {
+        // multicast-cluster slices of the activation box: one h row (128 rows) / one pixel (64 rows)
+        const uint32_t bh[5] = {(uint32_t)E, 64, 2, 1, 1}, bq[5] = {(uint32_t)E, 64, 1, 1, 1};
+        CP_TRY(make_map(&p.maps[1], xin, 5, dims, str, bh, false, es));
+        CP_TRY(make_map(&p.maps[2], xin, 5, dims, str, bq, false, es));
+      }
     }
     p.unified = n == 1 ? 1 : 0;
   } else if (L.images) {
@@ -2040,6 +2116,15 @@ static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* 
     p.split = 1;
     p.units = p.numM * p.numN;
     p.max_chunks = pl.chunks;
+    if (p.unified && fwd_mc_enabled(L, p.m_off)) {
+      // multicast clusters: one cluster per position tile, its CTAs = the kernel tiles
+      const int g = fwd_mc_max_clusters(p, p.numM);
+      if (g > 0) {
+        p.fcl = p.numM;
+        p.units = p.numN;
+        p.nsched_groups = g;
+      }
+    }
   }
   p.bias = L.d.bias ? b : nullptr;
   p.saved = saved;
@@ -2070,18 +2155,18 @@ static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* 
   // runs in fwd_tail_finish after the deterministic sum of their pieces.
   FwdTailInfo ti{};
   {
-    const int CG = (pl.pair && !p.fwdT) ? 2 : 1, G = num_sms() / CG;
+    const int CG = (pl.pair && !p.fwdT) ? 2 : 1, G = p.fcl ? p.nsched_groups : num_sms() / CG;
     int T = 0;
     if ((pl.S == 1 || p.fwdT) && env_int("CP_TC_FWD_TAIL", 1) && plan_stream_tail(p, G, p.R * p.S * p.cpt, 16, ti.pbeg, &T)) {
       p.tail_buf = part;
-      ti.n = T; ti.cg = CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B; ti.halo = p.halo;
+      ti.n = T; ti.cg = p.fcl ? p.fcl : CG; ti.Wo = L.Wo; ti.Wp = L.Wp; ti.Bp = L.Bp; ti.B = L.B; ti.halo = p.halo;
       ti.Kr = L.Kr; ti.Kc = L.Kc; ti.relu = L.d.relu; ti.pool = L.d.pool;
       ti.npeers = npeers;
       for (int k = 0; k < npeers; ++k) ti.peer[k] = peer_blocks[k];
       const int nbcg = L.Bp / 32 / CG, W2 = L.Wo / 2;
       for (int k = 0; k < T && p.fwdT; ++k) {          // host mirror of decode_unit<FWD> (transposed)
         const int u = p.tail_full + k;
-        const int mt = u % p.numM, rest = u / p.numM, nb = L.Bp / 64;
+        const int mt = p.fcl ? 0 : u % p.numM, rest = p.fcl ? u : u / p.numM, nb = L.Bp / 64;
         const int ij = rest / nb;
         ti.bc0[k] = (rest % nb) * 64;
         ti.j[k] = ij % L.Wp;
@@ -2101,12 +2186,16 @@ static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* 
       }
     }
   }
+  if (env_int("CP_TC_PLAN_LOG", 0))
+    fprintf(stderr, "[tc_fwd] Kc=%d kc=%d m_off=%d fwdT=%d fcl=%d units=%d numM=%d numN=%d groups=%d tail_np=%d nw=%d\n",
+            L.Kc, kc, m_off, p.fwdT, p.fcl, p.units, p.numM, p.numN, p.fcl ? p.nsched_groups : -1, p.tail_np, p.nw);
   if (mark0) CP_TRY(tc_time_mark(L, PASS_FWD, 0, s));
   if (es == 2) CP_TRY((pl.pair ? launch_cg<PASS_FWD, 2, 1>(p, s) : launch_cg<PASS_FWD, 1, 1>(p, s)));
+  else if (p.fcl) CP_TRY((launch_cg<PASS_FWD, 1, 0, 1>(p, s)));
   else CP_TRY(((pl.pair && !p.fwdT) ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
   if (mark1) CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
   if (p.tail_np > 0 && p.fwdT) {
-    fwd_tail_finish_t<<<dim3(BM, ti.n), 64, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
+    fwd_tail_finish_t<<<dim3(BM, ti.n, p.fcl ? p.fcl : 1), 64, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
     CP_LAUNCHED();
   } else if (p.tail_np > 0) {
     fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
