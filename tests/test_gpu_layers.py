@@ -382,11 +382,12 @@ def test_bf16_rejects_unaligned_partition():
 # Planner variants the default sizes do not reach (the environment overrides are read per call):
 # wgrad tap-slowest unit order (large maps), with and without the stream tail (S = 1), the wgrad
 # accumulation-length cap forcing split-K (long reductions), forward / dgrad split-K, single-CTA tiles,
-# the transposed forward.  (The forward halo boxes exist only in -DCP_TC_HALO_HOOK experiment builds:
+# the transposed forward (also with multicast clusters).  (The forward halo boxes exist only in -DCP_TC_HALO_HOOK experiment builds:
 # parity-checked there with CP_TC_FWD_HALO=1, scripts/halo_check.sh.)
 VARIANTS = [{"CP_TC_WGRAD_ORDER": "1"}, {"CP_TC_WGRAD_ORDER": "1", "CP_TC_SPLIT_WGRAD": "1"},
             {"CP_TC_SPLIT_WGRAD": "1"}, {"CP_TC_ACC_TERMS": "1024"}, {"CP_TC_SPLIT_FWD": "3"},
-            {"CP_TC_SPLIT_DGRAD": "2"}, {"CP_TC_CTA_GROUP": "1"}, {"CP_TC_FWD_T": "1"}, {"CP_TC_FWD_T_IMAGES": "1"}]
+            {"CP_TC_SPLIT_DGRAD": "2"}, {"CP_TC_CTA_GROUP": "1"}, {"CP_TC_FWD_T": "1"}, {"CP_TC_FWD_T_IMAGES": "1"},
+            {"CP_TC_FWD_T": "1", "CP_TC_FWD_MC": "1"}]   # the last: multicast clusters (P=2 here: 2 CTAs)
 
 
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
