@@ -16,6 +16,16 @@
 namespace cp {
 
 static inline dim3 grid1d(int64_t n, int t) { return dim3((unsigned)((n + t - 1) / t)); }
+static int num_sms_simt() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 
 // ============================================================== generic SIMT implicit GEMM
 // C[m][n] = sum_k A(m,k) * B(k,n), fp32, k ascending per output (fixed order).
@@ -731,11 +741,8 @@ __host__ __device__ inline int fc_nsc(const Blocks& g) {
   return (m + kFcChunk - 1) / kFcChunk;
 }
 
-#ifndef FC_FWD_MINB
-#define FC_FWD_MINB 1   // experiment builds: minimum resident CTAs per SM for fc_fwd_partial
-#endif
 template <int OO>   // compile-time class bound (10 for CIFAR's 10 classes, else kMaxO)
-__global__ void __launch_bounds__(256, FC_FWD_MINB) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
+__global__ void __launch_bounds__(256) fc_fwd_partial(const float* __restrict__ x, const float* __restrict__ wg,
                                                       float* __restrict__ part, Blocks g, int B, int O, int PW,
                                                       int nsc) {
   __shared__ __align__(16) float xs[128 * kFcLd];
@@ -944,16 +951,13 @@ __global__ void __launch_bounds__(256) fc_bwd_fused(const float* __restrict__ dl
 // of x in flight (the load latency, not bandwidth, bounded the one-thread-per-feature version); its W
 // column sits in registers, dlogits rows in shared memory (broadcast reads); the 8 groups' dW partials
 // combine through shared memory.  CTA 0 also writes dbfc = sum_b dlogits.
-#ifndef FC_KFCG
-#define FC_KFCG 8
-#endif
-#ifndef FC_BWD_MINB
-#define FC_BWD_MINB 1
-#endif
-constexpr int kFcF = 64, kFcG = FC_KFCG;   // features x image groups per CTA
+// features x image groups per CTA: 8 groups (512 threads) when the grid fits on the SMs in one wave,
+// else 4 (256 threads, twice as many resident CTAs: the paper net's 37,600 features at P=1 run in one
+// wave, 28.7 -> 20.5 us; profiles/r02_head_variants.jsonl)
+constexpr int kFcF = 64;
 constexpr int kFcRows = 256;         // images per shared-memory dlogits chunk
-template <int OO>
-__global__ void __launch_bounds__(kFcF * kFcG, FC_BWD_MINB) fc_bwd_cols(const float* __restrict__ dl, const float* __restrict__ x,
+template <int OO, int kFcG>
+__global__ void __launch_bounds__(kFcF * kFcG) fc_bwd_cols(const float* __restrict__ dl, const float* __restrict__ x,
                                                           const float* __restrict__ wg, float* __restrict__ dx,
                                                           float* __restrict__ dwg, float* __restrict__ dbfc, Blocks g,
                                                           int B, int O, int PW, int64_t F) {
@@ -1244,8 +1248,12 @@ int cp_fc_backward(const float* dl, const float* x, int32_t B, int32_t Hp, int32
   if (dx || dwg || dbfc) {
     const int64_t F = (int64_t)PW * g.Cg;   // (0 features on this rank: one CTA computes dbfc only)
     const unsigned nblk = (unsigned)std::max<int64_t>(1, (F + kFcF - 1) / kFcF);
-    if (O <= 10) fc_bwd_cols<10><<<nblk, dim3(kFcF, kFcG), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
-    else fc_bwd_cols<kMaxO><<<nblk, dim3(kFcF, kFcG), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
+    // 512-thread CTAs: 2 resident per SM (64 registers); 256-thread: 4
+    const bool narrow = (int64_t)nblk > 2 * (int64_t)num_sms_simt();
+    if (O <= 10 && narrow) fc_bwd_cols<10, 4><<<nblk, dim3(kFcF, 4), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
+    else if (O <= 10) fc_bwd_cols<10, 8><<<nblk, dim3(kFcF, 8), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
+    else if (narrow) fc_bwd_cols<kMaxO, 4><<<nblk, dim3(kFcF, 4), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
+    else fc_bwd_cols<kMaxO, 8><<<nblk, dim3(kFcF, 8), 0, s>>>(dl, x, wg, dx, dwg, dbfc, g, B, O, PW, F);
     CP_LAUNCHED();
   }
   (void)ws;
