@@ -382,7 +382,9 @@ struct W1Params {
   float* part;               // [nkr][Kc][Kcol] partial dW of every K range
   float* dbpart;             // [nkr][2][Kc] partial db (image halves of a chunk)
   int B, Bp, C, H, W, Hp, Wp, Kc, Kcol, ncolr;   // ncolr = R*S*C real im2col columns
-  int nchunks, ngrp8, ntile, nkr, stages, stage_bytes, tile_bytes, raw_off_y, raw_off_c, raw_off_x, raw_bytes;
+  int nchunks, ngrp8, ntile, nkr, tile_bytes, raw_off_y, raw_off_c, raw_off_x, raw_bytes;
+  int tstages, rstages;      // built-tile ring (released by the MMAs) and raw-input ring (released by the builders)
+  int tstage_bytes, rstage_bytes;
   int xpw, pimg;             // patch row width (>= S + 1, x4) and floats of one image's patch C * (R+1) * xpw
   int relu, round;
   int off[C1_MAXK];          // im2col column -> (ch*(R+1) + r)*8 + s inside an image's patch
@@ -399,27 +401,34 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  // stage s: [A tile 16 KB][B tile <= 256 x 128 B][raw: dA 8 KB | y 8 KB | codes 8 x Kc B | x patch]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * p.stage_bytes);
-  uint64_t* rfull = bars;         // [stages] raw inputs landed (TMA / bulk)
-  uint64_t* full = bars + 8;      // [stages] tiles built
-  uint64_t* empty = bars + 16;    // [stages] MMAs done
-  uint64_t* tfull = bars + 24;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
-  int* off_s = reinterpret_cast<int*>(bars + 26);
+  // tile stage t: [A tile 16 KB][B tile <= 256 x 128 B]; raw stage r: [dA 8 KB | y 8 KB | codes 8 x Kc B |
+  // x patch].  Two rings: the raw inputs run several chunks ahead of the builders (their slots are released
+  // as soon as the builders have read them), the built tiles are released by the MMAs.
+  uint8_t* raws = smem + p.tstages * p.tstage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(raws + p.rstages * p.rstage_bytes);
+  uint64_t* rfull = bars;         // [rstages] raw inputs landed (TMA / bulk)
+  uint64_t* rempty = bars + 8;    // [rstages] raw inputs read by every builder warp
+  uint64_t* full = bars + 16;     // [tstages] tiles built
+  uint64_t* empty = bars + 24;    // [tstages] MMAs done
+  uint64_t* tfull = bars + 32;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 33);
+  int* off_s = reinterpret_cast<int*>(bars + 34);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = blockIdx.x % p.ntile, kr = blockIdx.x / p.ntile;
   const int k0 = nt * 256, nN = min(256, p.Kc - k0);
   for (int k = threadIdx.x; k < C1_MAXK; k += blockDim.x) off_s[k] = p.off[k];
   // A rows >= ncolr stay zero for the whole kernel (columns past R*S*C)
-  for (int st = 0; st < p.stages; ++st)
+  for (int st = 0; st < p.tstages; ++st)
     for (int e = threadIdx.x; e < (128 - p.ncolr) * 32; e += blockDim.x)
-      reinterpret_cast<float*>(smem + st * p.stage_bytes)[p.ncolr * 32 + e] = 0.f;
+      reinterpret_cast<float*>(smem + st * p.tstage_bytes)[p.ncolr * 32 + e] = 0.f;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 0 && lane == 0) {
-    for (int st = 0; st < p.stages; ++st) {
+    for (int st = 0; st < p.rstages; ++st) {
       mbar_init(&rfull[st], 1);
+      mbar_init(&rempty[st], W1_BWARPS + W1_AWARPS);
+    }
+    for (int st = 0; st < p.tstages; ++st) {
       mbar_init(&full[st], W1_BWARPS + W1_AWARPS);
       mbar_init(&empty[st], 1);
     }
@@ -450,8 +459,8 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
         const int win = c / p.ngrp8, b0 = (c - win * p.ngrp8) * 8;
         const int i = win / p.Wp, j = win - i * p.Wp;
         const int row = win * p.Bp + b0;
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* rw = smem + stage * p.stage_bytes + p.tile_bytes;
+        mbar_wait(&rempty[stage], phase ^ 1);
+        uint8_t* rw = raws + stage * p.rstage_bytes;
         mbar_arrive_expect_tx(&rfull[stage], bytes);
         tma_load_2d(rw, &p.damap, &rfull[stage], k0, row);
         tma_load_2d(rw + p.raw_off_y, &p.ymap, &rfull[stage], k0, row);
@@ -459,7 +468,7 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
         // (TMA: the innermost box coordinate must be 16-byte aligned -> start at the 4-float boundary at or
         // below column 2j; the builders add the shift (2j) & 3)
         tma_load_4d(rw + p.raw_off_x, &p.xmap, &rfull[stage], (2 * j) & ~3, 2 * i, 0, b0);
-        if (++stage == p.stages) {
+        if (++stage == p.rstages) {
           stage = 0;
           phase ^= 1;
         }
@@ -474,12 +483,12 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
       for (int c = c_begin; c < c_end; ++c) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t a = smem_u32(smem + stage * p.stage_bytes);
+        const uint32_t a = smem_u32(smem + stage * p.tstage_bytes);
         const uint64_t ad = sdesc_k(a, 0), bd = sdesc_k(a + 128 * 128, 0);
 #pragma unroll
         for (int k = 0; k < 4; ++k) mma_tf32(tmem_base, ad + 2 * k, bd + 2 * k, idesc, (c > c_begin || k > 0) ? 1u : 0u);
         mma_commit(&empty[stage]);
-        if (++stage == p.stages) {
+        if (++stage == p.tstages) {
           stage = 0;
           phase ^= 1;
         }
@@ -494,15 +503,16 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
     const int kl = tb & 255, half = tb >> 8;            // kernel of the tile, images 4*half .. 4*half+3
     const bool active = kl < nN;
     float dbacc = 0.f;
-    int stage = 0;
-    uint32_t phase = 0;
+    int rstage = 0, tstage = 0;
+    uint32_t rphase = 0, tphase = 0;
     for (int c = c_begin; c < c_end; ++c) {
-      mbar_wait(&rfull[stage], phase);
-      uint8_t* st = smem + stage * p.stage_bytes;
-      const float* rda = reinterpret_cast<const float*>(st + p.tile_bytes);
-      const float* ry = reinterpret_cast<const float*>(st + p.tile_bytes + p.raw_off_y);
-      const uint8_t* rc = st + p.tile_bytes + p.raw_off_c + k0;
-      uint8_t* sb = st + 128 * 128;
+      mbar_wait(&rfull[rstage], rphase);
+      mbar_wait(&empty[tstage], tphase ^ 1);          // the tile slot's previous MMAs are done
+      const uint8_t* rw = raws + rstage * p.rstage_bytes;
+      const float* rda = reinterpret_cast<const float*>(rw);
+      const float* ry = reinterpret_cast<const float*>(rw + p.raw_off_y);
+      const uint8_t* rc = rw + p.raw_off_c + k0;
+      uint8_t* sb = smem + tstage * p.tstage_bytes + 128 * 128;
       if (active) {
         float g[4], yv[4];
         uint32_t cd[4];
@@ -526,10 +536,17 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full[stage]);
-      if (++stage == p.stages) {
-        stage = 0;
-        phase ^= 1;
+      if (lane == 0) {
+        mbar_arrive(&full[tstage]);
+        mbar_arrive(&rempty[rstage]);
+      }
+      if (++rstage == p.rstages) {
+        rstage = 0;
+        rphase ^= 1;
+      }
+      if (++tstage == p.tstages) {
+        tstage = 0;
+        tphase ^= 1;
       }
     }
     if (active) p.dbpart[((int64_t)kr * 2 + half) * p.Kc + k0 + kl] = dbacc;   // this K range's db (chunks ascending)
@@ -558,8 +575,8 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
   } else if (warp >= W1_AWARP0) {
     // ======================= A builders: item = (im2col column, image): the window's 4 input pixels
     const int t = threadIdx.x - W1_AWARP0 * 32;        // 0..127
-    int stage = 0;
-    uint32_t phase = 0;
+    int rstage = 0, tstage = 0;
+    uint32_t rphase = 0, tphase = 0;
     int win = c_begin / p.ngrp8, bg = c_begin - win * p.ngrp8, jw = win % p.Wp;   // stepped per chunk
     for (int c = c_begin; c < c_end; ++c) {
       const int jsh = (2 * jw) & 3;                    // column shift of the aligned patch
@@ -567,9 +584,10 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
         bg = 0;
         if (++jw == p.Wp) jw = 0;
       }
-      mbar_wait(&rfull[stage], phase);
-      uint8_t* st = smem + stage * p.stage_bytes;
-      const float* rx = reinterpret_cast<const float*>(st + p.tile_bytes + p.raw_off_x) + jsh;
+      mbar_wait(&rfull[rstage], rphase);
+      mbar_wait(&empty[tstage], tphase ^ 1);
+      uint8_t* st = smem + tstage * p.tstage_bytes;
+      const float* rx = reinterpret_cast<const float*>(raws + rstage * p.rstage_bytes + p.raw_off_x) + jsh;
       for (int it = t; it < p.ncolr * 8; it += 128) {
         const int col = it >> 3, bb = it & 7;
         const float* src = rx + bb * p.pimg + off_s[col];
@@ -579,10 +597,17 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full[stage]);
-      if (++stage == p.stages) {
-        stage = 0;
-        phase ^= 1;
+      if (lane == 0) {
+        mbar_arrive(&full[tstage]);
+        mbar_arrive(&rempty[rstage]);
+      }
+      if (++rstage == p.rstages) {
+        rstage = 0;
+        rphase ^= 1;
+      }
+      if (++tstage == p.tstages) {
+        tstage = 0;
+        tphase ^= 1;
       }
     }
   }
@@ -753,16 +778,21 @@ static bool w1_plan(const Layer& L, W1Params& p, size_t* smem, int* grid) {
   p.raw_off_c = 2 * 8 * 256 * 4;
   p.raw_off_x = (p.raw_off_c + 8 * L.Kc + 127) / 128 * 128;
   p.raw_bytes = p.raw_off_x + 8 * p.pimg * 4;
-  p.stage_bytes = (p.tile_bytes + p.raw_bytes + 1023) / 1024 * 1024;
-  const size_t fixed = 1024 + 256 + 4 * C1_MAXK + 256;
-  p.stages = 0;
-  for (int st = 4; st >= 2; --st)
-    if (fixed + (size_t)st * p.stage_bytes <= 227 * 1024) {
-      p.stages = st;
+  p.tstage_bytes = (p.tile_bytes + 1023) / 1024 * 1024;
+  p.rstage_bytes = (p.raw_bytes + 1023) / 1024 * 1024;
+  const size_t fixed = 1024 + 512 + 4 * C1_MAXK + 256;
+  // two built tiles (the MMA of one overlaps the build of the next); the rest of shared memory holds
+  // raw-input stages so that the TMA loads run several chunks ahead (CP_C1W_RSTAGES caps it, A/B)
+  p.tstages = 2;
+  p.rstages = 0;
+  const int rcap = std::max(2, std::min(8, tc_env_int("CP_C1W_RSTAGES", 8)));
+  for (int st = rcap; st >= 2; --st)
+    if (fixed + (size_t)p.tstages * p.tstage_bytes + (size_t)st * p.rstage_bytes <= 227 * 1024) {
+      p.rstages = st;
       break;
     }
-  if (!p.stages) return false;
-  *smem = fixed + (size_t)p.stages * p.stage_bytes;
+  if (!p.rstages) return false;
+  *smem = fixed + (size_t)p.tstages * p.tstage_bytes + (size_t)p.rstages * p.rstage_bytes;
   *grid = p.ntile * p.nkr;
   for (int kk = 0; kk < C1_MAXK; ++kk) {
     int o = -1;
