@@ -1,6 +1,6 @@
 """Summarise an ncu --csv launch list (gpu__time_duration.sum per launch).
 
-Prints (1) one step's launches -- the window between the last two conv1 im2col launches (each
+Prints (1) one step's launches -- the window between the last two image-layer forward launches (each
 training step starts with exactly one) -- grouped by kernel with its share of that step, then
 (2) the full per-launch list.  ncu serialises launches and runs them cold, so the shares, not the
 absolute times, are what compare with the live bench timing.
@@ -21,7 +21,8 @@ for r in rows:
         if d.get('Metric Name') == 'gpu__time_duration.sum':
             out.append((d['Kernel Name'][:70], float(d['Metric Value'].replace(',', ''))))
 
-starts = [i for i, (n, _) in enumerate(out) if 'im2col_kernel' in n]
+# a training step starts with the image layer's forward (conv1_fwd_kernel; im2col_kernel in other modes)
+starts = [i for i, (n, _) in enumerate(out) if 'im2col_kernel' in n or 'conv1_fwd_kernel' in n]
 if len(starts) >= 2:
     a, b = starts[-2], starts[-1]
     step = out[a:b]
