@@ -718,18 +718,28 @@ void comm_symmetric_set_own(cp_comm c, const void* local, int64_t off, int64_t e
 
 // Copy-engine gather (consumers outside the tensor-core forward): this rank's block into every
 // peer's copy, then the arrival flag (value 1) behind the data at every peer - no SM involved.
-int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks) {
+int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks, cudaStream_t s2,
+                       const cudaEvent_t* evs) {
   auto it = c->sym.find(const_cast<void*>(local));
   if (it == c->sym.end()) CP_FAIL(CP_ERR_ARG, "not a symmetric buffer");
   const SymBuf& sb = it->second;
   if (sb.own_off < 0) CP_FAIL(CP_ERR_STATE, "symmetric gather: no producer wrote this buffer yet");
   // peers in the order they consume this block (peer q walks its input blocks from its own upwards,
-  // so it needs this rank's block after (rank - q) mod P blocks): the soonest consumer first
+  // so it needs this rank's block after (rank - q) mod P blocks): the soonest consumer first.  With a
+  // second stream s2, each peer's copy is split in two halves on two copy engines (the flag follows
+  // both: s waits for evs[d] recorded on s2 after the second half)
+  const int64_t h = s2 ? (sb.own_elems / 2 + 3) / 4 * 4 : sb.own_elems;   // first half, 16-byte multiple
   for (int d = 1; d < c->world; ++d) {
     const int q = (c->rank - d + c->world) % c->world;
-    if (sb.own_elems)
-      CP_CUDA(cudaMemcpyAsync((float*)sb.peers[q] + sb.own_off, (const float*)local + sb.own_off,
-                              (size_t)sb.own_elems * 4, cudaMemcpyDeviceToDevice, s));
+    float* dst = (float*)sb.peers[q] + sb.own_off;
+    const float* src = (const float*)local + sb.own_off;
+    if (h > 0) CP_CUDA(cudaMemcpyAsync(dst, src, (size_t)h * 4, cudaMemcpyDeviceToDevice, s));
+    if (s2) {
+      if (sb.own_elems > h)
+        CP_CUDA(cudaMemcpyAsync(dst + h, src + h, (size_t)(sb.own_elems - h) * 4, cudaMemcpyDeviceToDevice, s2));
+      CP_CUDA(cudaEventRecord(evs[d], s2));
+      CP_CUDA(cudaStreamWaitEvent(s, evs[d], 0));
+    }
     uint32_t* f = (uint32_t*)((char*)sb.peers[q] + sb.flag_off);
     CP_TRY(comm_signal_ce(c, &f, 1, c->rank, s, chunks));
   }

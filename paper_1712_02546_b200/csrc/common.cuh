@@ -212,6 +212,8 @@ struct Layer {
   cudaEvent_t ev_compute, ev_comm;
   cudaEvent_t ev_bar_fork = nullptr, ev_bar = nullptr;   // deferred gather barrier (comm stream)
   cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;     // copy-engine gather on the comm stream
+  cudaStream_t cs2 = nullptr;                              // second copy stream (split gather copies)
+  cudaEvent_t ev_split[CP_MAX_RANKS] = {};
   // optional per-pass GEMM timing (conv_part_timing): events around the tensor-core kernel launch
   int timing;
   cudaEvent_t ev_t[5][2];   // timing: GEMM of pass 0/1/2, 3 copy-engine gather, 4 reduce-scatter transfer

@@ -107,7 +107,8 @@ void* comm_symmetric_mc(cp_comm c, const void* local);
 bool multicast_requested();
 // producer records its block of a symmetric gathered buffer (for copy-engine distribution)
 void comm_symmetric_set_own(cp_comm c, const void* local, int64_t off, int64_t elems);
-int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks = false);
+int comm_ce_distribute(cp_comm c, const void* local, cudaStream_t s, bool chunks = false, cudaStream_t s2 = nullptr,
+                       const cudaEvent_t* evs = nullptr);
 // CP_GATHER_PUSH=epilogue: the producer's GEMM epilogue pushes (A/B experiment), else the consumer
 bool gather_push_in_epilogue();
 // cross-rank barrier on s (device-side epoch flags once symmetric memory exists, else NCCL)

@@ -220,6 +220,9 @@ int conv_part_destroy(cp_layer L) {
   if (L->ev_bar) cudaEventDestroy(L->ev_bar);
   if (L->ev_gfork) cudaEventDestroy(L->ev_gfork);
   if (L->ev_gjoin) cudaEventDestroy(L->ev_gjoin);
+  for (int k = 0; k < CP_MAX_RANKS; ++k)
+    if (L->ev_split[k]) cudaEventDestroy(L->ev_split[k]);
+  if (L->cs2) cudaStreamDestroy(L->cs2);
 
   delete L;
   return CP_OK;
@@ -313,8 +316,15 @@ int conv_part_forward(cp_layer L, const float* x, const float* w, const float* b
       }
       CP_CUDA(cudaEventRecord(L->ev_gfork, s));
       CP_CUDA(cudaStreamWaitEvent(cs, L->ev_gfork, 0));
+      // CP_GATHER_CE_STREAMS=2: each peer's copy in two halves on two copy engines
+      const bool split = tc_env_int("CP_GATHER_CE_STREAMS", 1) >= 2;
+      if (split && !L->cs2) {
+        CP_CUDA(cudaStreamCreateWithFlags(&L->cs2, cudaStreamNonBlocking));
+        for (int k = 0; k < CP_MAX_RANKS; ++k) CP_CUDA(cudaEventCreateWithFlags(&L->ev_split[k], cudaEventDisableTiming));
+      }
+      if (split) CP_CUDA(cudaStreamWaitEvent(L->cs2, L->ev_gfork, 0));
       CP_TRY(tc_time_mark(*L, 3, 0, cs));   // gather window: first copy issued -> last flag written
-      CP_TRY(comm_ce_distribute(L->comm, x, cs, true));
+      CP_TRY(comm_ce_distribute(L->comm, x, cs, true, split ? L->cs2 : nullptr, L->ev_split));
       CP_TRY(tc_time_mark(*L, 3, 1, cs));
       if (L->timing) L->ce_gather_timed = 1;
       CP_CUDA(cudaEventRecord(L->ev_gjoin, cs));
@@ -477,9 +487,29 @@ int conv_part_backward_data(cp_layer L, const float* dy_g, const uint8_t* saved,
       CP_TRY(launch_wait_flags(own_flags, world, me, cs));
       if (rsm == 2) {   // copy engines: every peer's partial of the own block into its local receive slot
         CP_TRY(tc_time_mark(*Lp, 4, 0, cs));   // transfer window: all partials ready -> copies done
+        // CP_RS_CE_STREAMS=2: each copy in two halves, the second on another copy engine (stream cs2)
+        const bool split = tc_env_int("CP_RS_CE_STREAMS", 1) >= 2;
+        if (split && !Lp->cs2) {
+          CP_CUDA(cudaStreamCreateWithFlags(&Lp->cs2, cudaStreamNonBlocking));
+          for (int k = 0; k < CP_MAX_RANKS; ++k)
+            CP_CUDA(cudaEventCreateWithFlags(&Lp->ev_split[k], cudaEventDisableTiming));
+        }
+        const int64_t h = split ? (n_own / 2 + 3) / 4 * 4 : n_own;
+        if (split) {
+          CP_CUDA(cudaEventRecord(Lp->ev_split[0], cs));
+          CP_CUDA(cudaStreamWaitEvent(Lp->cs2, Lp->ev_split[0], 0));
+        }
         for (int r = 0; r < world; ++r)
-          if (r != me && n_own)
-            CP_CUDA(cudaMemcpyAsync((void*)srcv[r], remv[r], (size_t)n_own * 4, cudaMemcpyDeviceToDevice, cs));
+          if (r != me && n_own) {
+            CP_CUDA(cudaMemcpyAsync((void*)srcv[r], remv[r], (size_t)h * 4, cudaMemcpyDeviceToDevice, cs));
+            if (split && n_own > h)
+              CP_CUDA(cudaMemcpyAsync((void*)(srcv[r] + h), remv[r] + h, (size_t)(n_own - h) * 4,
+                                      cudaMemcpyDeviceToDevice, Lp->cs2));
+          }
+        if (split) {
+          CP_CUDA(cudaEventRecord(Lp->ev_split[1], Lp->cs2));
+          CP_CUDA(cudaStreamWaitEvent(cs, Lp->ev_split[1], 0));
+        }
         CP_TRY(tc_time_mark(*Lp, 4, 1, cs));
         if (Lp->timing) Lp->rs_timed = 1;
       }
