@@ -46,7 +46,8 @@ struct C1Params {
   int nb, wseg, nseg, ngrp;  // B-set = nb images x 2 rows x wseg columns; nseg segments, ngrp image groups
   int nsets, mtiles;
   int nbuf, astages;     // B-set buffers (1 or 2) and A ring depth, sized to shared memory
-  int bset_bytes;        // nch * 224 rows * 128 B
+  int bset_bytes;        // nch * bstride
+  int bstride;           // bytes of one 32-wide K chunk of a B-set: N rows (max over sets, x8) * 128 B
   int pw, pimg, patch_bytes;  // patch row width (>= wseg + S - 1, x4), floats per image C*(R+1)*pw, bytes
   int relu, round;
   int off[C1_MAXK];      // im2col column kk = (r*S + s)*C + ch -> (ch*(R+1) + r)*pw + s in the patch, -1 = pad
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
             mbar_wait(&afull[stage], phase);
             tc_fence_after();
             const uint64_t ad0 = sdesc_k(smem_u32(sA + stage * C1_ABYTES), 0);
-            const uint64_t bd0 = sdesc_k(bbase + c * (C1_NMAX * 128), 0);
+            const uint64_t bd0 = sdesc_k(bbase + c * p.bstride, 0);
             const int ksteps = min(32, p.Kcol - c * 32) / 8;
             for (int k = 0; k < ksteps; ++k) {
               mma_tf32(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, accumulate);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
             const float x = (real && o >= 0) ? src[o] : 0.f;
             v[q] = tf32_round(x);
           }
-          *reinterpret_cast<float4*>(drow + c * (C1_NMAX * 128)) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(drow + c * p.bstride) = make_float4(v[0], v[1], v[2], v[3]);
         }
         rem += RSTEP;
         while (rem >= rows_per_img) {
@@ -685,11 +686,14 @@ static bool c1_plan(const Layer& L, C1Params& p, size_t* smem) {
   p.wseg = std::min(L.Wo, C1_NMAX / 2) & ~1;
   p.nseg = (L.Wo + p.wseg - 1) / p.wseg;
   p.nb = 1;
-  while (p.nb * 2 <= L.Bp && L.Bp % (p.nb * 2) == 0 && p.nb * 2 * 2 * p.wseg <= C1_NMAX) p.nb *= 2;
+  const int nb_cap = tc_env_int("CP_C1_NB", 1 << 20);   // images per B-set cap (A/B; default: as many as fit)
+  while (p.nb * 2 <= L.Bp && L.Bp % (p.nb * 2) == 0 && p.nb * 2 * 2 * p.wseg <= C1_NMAX && p.nb * 2 <= nb_cap)
+    p.nb *= 2;
   p.ngrp = L.Bp / p.nb;
   p.nsets = L.Hp * p.nseg * p.ngrp;
   p.mtiles = (L.Kc + C1_BM - 1) / C1_BM;
-  p.bset_bytes = p.nch * C1_NMAX * 128;
+  p.bstride = (p.nb * 2 * p.wseg + 7) / 8 * 8 * 128;   // the widest set's N rows
+  p.bset_bytes = p.nch * p.bstride;
   p.pw = (p.wseg + L.S - 1 + 3) / 4 * 4;
   p.pimg = L.C * (L.R + 1) * p.pw;
   p.patch_bytes = (p.nb * p.pimg * 4 + 127) / 128 * 128;
@@ -698,7 +702,7 @@ static bool c1_plan(const Layer& L, C1Params& p, size_t* smem) {
   const size_t cap = 227 * 1024;
   p.nbuf = 0;
   for (int nbuf = 2; nbuf >= 1 && !p.nbuf; --nbuf)
-    for (int st = 4; st >= 2; --st)
+    for (int st = std::min(8, std::max(2, tc_env_int("CP_C1_ASTAGES", 4))); st >= 2; --st)
       if (fixed + (size_t)nbuf * (p.bset_bytes + p.patch_bytes) + (size_t)st * C1_ABYTES <= cap) {
         p.nbuf = nbuf;
         p.astages = st;
