@@ -2029,8 +2029,18 @@ static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* 
   // operand bytes per MAC (L2-bound, ~0.5 us per K-chunk): same-box A/B at P=4 0.206 vs 0.200 ms for
   // the pair kernel, slower at P=1/2/8 as well -> off unless CP_TC_FWD_T=1 (parity-tested; the base
   // for a CTA-pair transposed kernel)
+  // default (gather input): transposed when its M tiles use the tensor core clearly better than the pair
+  // kernel's N tiles (an N <= 256 MMA costs as much as N = 256): P=4 of the paper net, 376 slots -> 0.98
+  // of 3 x 128 rows vs 0.73 of 2 x 256 columns: conv2 forward 0.200 -> 0.186 ms at N=4
+  // (profiles/r02_fwdT_auto/); P=1/2 (>= 0.98 either way) and P=8 (0.75 both) keep the pair kernel
+  int autoT = 0;
+  if (!L.images && kc == L.Kc && m_off == 0 && pl.numN > 0) {
+    const double eff_pair = (double)L.Kc / (pl.numN * (double)BN);
+    const double eff_t = (double)L.Kc / (((L.Kc + BM - 1) / BM) * (double)BM);
+    autoT = eff_t - eff_pair >= 0.15 ? 1 : 0;
+  }
   p.fwdT = (es == 4 && L.d.pool && L.Bp % 64 == 0 &&
-            (force_T >= 0 ? force_T : env_int(L.images ? "CP_TC_FWD_T_IMAGES" : "CP_TC_FWD_T", 0))) ? 1 : 0;
+            (force_T >= 0 ? force_T : env_int(L.images ? "CP_TC_FWD_T_IMAGES" : "CP_TC_FWD_T", autoT))) ? 1 : 0;
 #ifdef CP_TC_HALO_HOOK
   const bool halo_hook = true;
 #else

@@ -387,7 +387,8 @@ def test_bf16_rejects_unaligned_partition():
 VARIANTS = [{"CP_TC_WGRAD_ORDER": "1"}, {"CP_TC_WGRAD_ORDER": "1", "CP_TC_SPLIT_WGRAD": "1"},
             {"CP_TC_SPLIT_WGRAD": "1"}, {"CP_TC_ACC_TERMS": "1024"}, {"CP_TC_SPLIT_FWD": "3"},
             {"CP_TC_SPLIT_DGRAD": "2"}, {"CP_TC_CTA_GROUP": "1"}, {"CP_TC_FWD_T": "1"}, {"CP_TC_FWD_T_IMAGES": "1"},
-            {"CP_TC_FWD_T": "1", "CP_TC_FWD_MC": "1"}]   # the last: multicast clusters (P=2 here: 2 CTAs)
+            {"CP_TC_FWD_T": "1", "CP_TC_FWD_MC": "1"},   # multicast clusters (P=2 here: 2 CTAs)
+            {"CP_TC_FWD_T": "0"}]   # the pair forward also where the planner picks the transposed one
 
 
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
