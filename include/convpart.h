@@ -379,9 +379,11 @@ int cp_sgd_multi(float* const* params, const float* const* grads, const int64_t*
 /* In-place sum over all ranks of n floats on `stream`; the result is bitwise identical on every
  * rank.  Once the communicator holds symmetric memory and n <= 65536, a one-CTA peer-memory kernel:
  * each rank writes its vector into slot [rank] of every peer's scratch (double-buffered by epoch
- * parity), raises its epoch flag, waits for all peers' flags and sums the slots in ascending rank
- * order; otherwise NCCL AllReduce.  Used by the partitioned head to sum per-rank partial logits.
- * comm == NULL or a single rank: no-op. */
+ * parity) and sums the slots in ascending rank order once every peer's data is there.  For
+ * n <= 32768 (default) each value travels with the epoch in one 64-bit word and the reader polls
+ * the data itself; otherwise (or CP_AR_LL=0) the rank raises an epoch flag after a system fence and
+ * the readers wait for all flags.  Larger n: NCCL AllReduce.  Used by the partitioned head to sum
+ * per-rank partial logits.  comm == NULL or a single rank: no-op. */
 int cp_allreduce_sum(cp_comm comm, float* buf, int64_t n, void* stream);
 
 /* cp_allreduce_sum of the [B][O] partial logits followed by cp_softmax_xent on the sum, in ONE

@@ -605,6 +605,57 @@ __global__ void __launch_bounds__(512) oneshot_allreduce_kernel(float* buf, int 
   }
 }
 
+// Low-latency variant (default for n <= kArMax / 2): every value travels with its epoch in ONE 64-bit word
+// (value bits | epoch << 32, single-copy atomic), so a reader polls the data itself - no system fence, no
+// separate flag release / acquire round trip.  Slots are double-buffered by epoch parity as above; the
+// sum over source ranks runs in ascending rank order: bitwise the same result as the flagged kernel.
+constexpr int64_t kArLL = kArMax / 2;   // 64-bit slots per (parity, source rank)
+__global__ void __launch_bounds__(512) oneshot_allreduce_ll_kernel(float* buf, int n, ArPtrs peers, float* mine,
+                                                                   uint32_t* ctl, int me, int world, SoftmaxArgs sm) {
+  __shared__ uint32_t e_s;
+  __shared__ float wsum[16];
+  if (threadIdx.x == 0) e_s = ctl[kCtlArEpoch] + 1;
+  __syncthreads();
+  const uint32_t e = e_s;
+  const int par = e & 1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned long long w = (unsigned long long)__float_as_uint(buf[i]) | ((unsigned long long)e << 32);
+    for (int q = 0; q < world; ++q) {
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(peers.s[q]) + ((int64_t)par * world + me) * kArLL + i;
+      asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
+    }
+  }
+  if (threadIdx.x == 0) ctl[kCtlArEpoch] = e;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(mine) + (int64_t)par * world * kArLL;
+  const long long t0 = clock64();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float t = 0.f;
+    for (int q = 0; q < world; ++q) {
+      unsigned long long w;
+      for (;;) {
+        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(w) : "l"(src + (int64_t)q * kArLL + i) : "memory");
+        if ((uint32_t)(w >> 32) == e) break;
+        if (clock64() - t0 > (1ll << 35)) __trap();
+      }
+      const float v = __uint_as_float((uint32_t)w);
+      t = q == 0 ? v : t + v;
+    }
+    buf[i] = t;
+  }
+  if (sm.y) {
+    __syncthreads();   // every summed logit written (block-visible global stores)
+    cp::softmax_xent_block(buf, sm.y, sm.B, sm.O, sm.loss, sm.dl, wsum);
+  }
+}
+
+static bool ar_low_latency(int64_t n) {
+  static const int on = [] {
+    const char* e = getenv("CP_AR_LL");
+    return e ? atoi(e) : 1;
+  }();
+  return on && n <= kArLL;
+}
+
 // the one-shot path (scratch allocated lazily, outside graph capture), or nullptr
 static float* oneshot_scratch(cp_comm c, int64_t n, cudaStream_t s) {
   if (!c->ctl || n > kArMax) return nullptr;
@@ -631,7 +682,10 @@ extern "C" int cp_allreduce_sum(cp_comm c, float* buf, int64_t n, void* stream) 
       ap.s[q] = c->ar_peer[q];
       ap.c[q] = c->ctl_peer[q];
     }
-    oneshot_allreduce_kernel<<<1, 512, 0, s>>>(buf, (int)n, ap, c->ar, c->ctl, c->rank, c->world, SoftmaxArgs{});
+    if (ar_low_latency(n))
+      oneshot_allreduce_ll_kernel<<<1, 512, 0, s>>>(buf, (int)n, ap, c->ar, c->ctl, c->rank, c->world, SoftmaxArgs{});
+    else
+      oneshot_allreduce_kernel<<<1, 512, 0, s>>>(buf, (int)n, ap, c->ar, c->ctl, c->rank, c->world, SoftmaxArgs{});
     CP_LAUNCHED();
     return CP_OK;
   }
@@ -652,7 +706,10 @@ extern "C" int cp_allreduce_softmax_xent(cp_comm c, float* logits, const int32_t
       ap.c[q] = c->ctl_peer[q];
     }
     const SoftmaxArgs sm{labels, B, O, loss, dlogits};
-    oneshot_allreduce_kernel<<<1, 512, 0, s>>>(logits, (int)n, ap, c->ar, c->ctl, c->rank, c->world, sm);
+    if (ar_low_latency(n))
+      oneshot_allreduce_ll_kernel<<<1, 512, 0, s>>>(logits, (int)n, ap, c->ar, c->ctl, c->rank, c->world, sm);
+    else
+      oneshot_allreduce_kernel<<<1, 512, 0, s>>>(logits, (int)n, ap, c->ar, c->ctl, c->rank, c->world, sm);
     CP_LAUNCHED();
     return CP_OK;
   }
