@@ -17,6 +17,7 @@
 // w3 input-patch TMA, w4-w11 B builders, w12-w27 epilogue (four groups of four, one TMEM lane quadrant per
 // warp: the epilogue is TMEM-read and ALU bound, ~20 instructions per pooled output, and needs the warps).
 #include <algorithm>
+#include <cstdio>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -370,10 +371,13 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
 // fill different ring stages, so that many chunks' global loads are in flight at once.  Split-K: the
 // CTAs are (N tile, K range) pairs over contiguous chunk ranges; per-CTA partial dW / db go to a
 // workspace and conv1_wgrad_reduce adds them in K-range order (deterministic).
-constexpr int W1_THREADS = 768;
+#ifndef C1W_AWARPS
+#define C1W_AWARPS 12  // A builder warps: 4 -> 8 -> 12 (1024 threads): conv1 backward-filter 65.5 -> 63.5 -> 61.5 us at P=1
+#endif
 constexpr int W1_BWARP0 = 4, W1_BWARPS = 16;  // warps 4..19 build B (2 threads per kernel, 4 images each),
                                               // warps 4..7 also run the final epilogue
-constexpr int W1_AWARP0 = 20, W1_AWARPS = 4;  // warps 20..23 build A
+constexpr int W1_AWARP0 = 20, W1_AWARPS = C1W_AWARPS;  // warps 20.. build A
+constexpr int W1_THREADS = 32 * (W1_AWARP0 + W1_AWARPS);
 constexpr int W1_MAXKC = 512;
 
 struct W1Params {
@@ -389,7 +393,18 @@ struct W1Params {
   int xpw, pimg;             // patch row width (>= S + 1, x4) and floats of one image's patch C * (R+1) * xpw
   int relu, round;
   int off[C1_MAXK];          // im2col column -> (ch*(R+1) + r)*8 + s inside an image's patch
+#ifdef C1W_TRACE
+  unsigned long long* trace;   // experiment builds: CTA 0's per-chunk %globaltimer stamps [4][64]
+#endif
 };
+#ifdef C1W_TRACE
+#define C1W_STAMP(kind, c)                                                                               \
+  do {                                                                                                    \
+    if (blockIdx.x == 0 && (c) - c_begin < 64) p.trace[(kind) * 64 + ((c) - c_begin)] = globaltimer_ns(); \
+  } while (0)
+#else
+#define C1W_STAMP(kind, c) do { } while (0)
+#endif
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -469,6 +484,7 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
         // (TMA: the innermost box coordinate must be 16-byte aligned -> start at the 4-float boundary at or
         // below column 2j; the builders add the shift (2j) & 3)
         tma_load_4d(rw + p.raw_off_x, &p.xmap, &rfull[stage], (2 * j) & ~3, 2 * i, 0, b0);
+        C1W_STAMP(0, c);
         if (++stage == p.rstages) {
           stage = 0;
           phase ^= 1;
@@ -484,6 +500,7 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
       for (int c = c_begin; c < c_end; ++c) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        C1W_STAMP(1, c);
         const uint32_t a = smem_u32(smem + stage * p.tstage_bytes);
         const uint64_t ad = sdesc_k(a, 0), bd = sdesc_k(a + 128 * 128, 0);
 #pragma unroll
@@ -508,7 +525,9 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
     uint32_t rphase = 0, tphase = 0;
     for (int c = c_begin; c < c_end; ++c) {
       mbar_wait(&rfull[rstage], rphase);
+      if (threadIdx.x == W1_BWARP0 * 32) C1W_STAMP(2, c);
       mbar_wait(&empty[tstage], tphase ^ 1);          // the tile slot's previous MMAs are done
+      if (threadIdx.x == W1_BWARP0 * 32) C1W_STAMP(3, c);
       const uint8_t* rw = raws + rstage * p.rstage_bytes;
       const float* rda = reinterpret_cast<const float*>(rw);
       const float* ry = reinterpret_cast<const float*>(rw + p.raw_off_y);
@@ -575,7 +594,7 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
     }
   } else if (warp >= W1_AWARP0) {
     // ======================= A builders: item = (im2col column, image): the window's 4 input pixels
-    const int t = threadIdx.x - W1_AWARP0 * 32;        // 0..127
+    const int t = threadIdx.x - W1_AWARP0 * 32;        // 0 .. 32 * W1_AWARPS - 1
     int rstage = 0, tstage = 0;
     uint32_t rphase = 0, tphase = 0;
     int win = c_begin / p.ngrp8, bg = c_begin - win * p.ngrp8, jw = win % p.Wp;   // stepped per chunk
@@ -589,7 +608,7 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
       mbar_wait(&empty[tstage], tphase ^ 1);
       uint8_t* st = smem + tstage * p.tstage_bytes;
       const float* rx = reinterpret_cast<const float*>(raws + rstage * p.rstage_bytes + p.raw_off_x) + jsh;
-      for (int it = t; it < p.ncolr * 8; it += 128) {
+      for (int it = t; it < p.ncolr * 8; it += 32 * W1_AWARPS) {
         const int col = it >> 3, bb = it & 7;
         const float* src = rx + bb * p.pimg + off_s[col];
         float4 v = make_float4(src[0], src[1], src[p.xpw], src[p.xpw + 1]);   // (dh,dw) = (0,0),(0,1),(1,0),(1,1)
@@ -854,9 +873,28 @@ int c1_wgrad(Layer& L, const float* x, const float* da, const uint8_t* codes, co
     CP_CUDA(cudaFuncSetAttribute(conv1_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
+#ifdef C1W_TRACE
+  static unsigned long long* tbuf = nullptr;
+  if (!tbuf) CP_CUDA(cudaMalloc(&tbuf, 4 * 64 * 8));
+  CP_CUDA(cudaMemsetAsync(tbuf, 0, 4 * 64 * 8, s));
+  p.trace = tbuf;
+#endif
   CP_TRY(tc_time_mark(L, 2, 0, s));
   conv1_wgrad_kernel<<<grid, W1_THREADS, smem, s>>>(p);
   CP_LAUNCHED();
+#ifdef C1W_TRACE
+  {   // experiment build: CTA 0's per-chunk stamps (ns after the first producer issue) to stderr
+    unsigned long long h[4 * 64];
+    CP_CUDA(cudaStreamSynchronize(s));
+    CP_CUDA(cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost));
+    const int nc = std::min(64, p.nchunks / p.nkr);
+    fprintf(stderr, "[c1w_trace] Kc=%d nkr=%d chunks=%d rstages=%d: chunk producer_issued mma_start builder_raw builder_tile\n",
+            L.Kc, p.nkr, nc, p.rstages);
+    for (int c = 0; c < nc; ++c)
+      fprintf(stderr, "[c1w_trace] %2d %8.2f %8.2f %8.2f %8.2f\n", c, (h[c] - h[0]) * 1e-3, (h[64 + c] - h[0]) * 1e-3,
+              (h[128 + c] - h[0]) * 1e-3, (h[192 + c] - h[0]) * 1e-3);
+  }
+#endif
   CP_TRY(tc_time_mark(L, 2, 1, s));
   const int n = L.Kr * L.Kcol + (db ? L.Kr : 0);
   conv1_wgrad_reduce<<<(n + 31) / 32, dim3(32, 8), 0, s>>>(p.part, p.dbpart, dw, db, p.nkr, L.Kr, L.Kc, L.Kcol,
