@@ -52,7 +52,18 @@ struct C1Params {
   int pw, pimg, patch_bytes;  // patch row width (>= wseg + S - 1, x4), floats per image C*(R+1)*pw, bytes
   int relu, round;
   int off[C1_MAXK];      // im2col column kk = (r*S + s)*C + ch -> (ch*(R+1) + r)*pw + s in the patch, -1 = pad
+#ifdef C1F_TRACE
+  unsigned long long* trace;   // experiment builds: CTA 0's per-set %globaltimer stamps [5][8]
+#endif
 };
+#ifdef C1F_TRACE
+#define C1F_STAMP(kind, ls)                                                                  \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && (ls) < 8) p.trace[(kind) * 8 + (ls)] = globaltimer_ns();            \
+  } while (0)
+#else
+#define C1F_STAMP(kind, ls) do { } while (0)
+#endif
 
 struct SetGeo {
   int i, c0, ws, b0, n;  // pooled row, first output column, segment width, first image, MMA N (x8)
@@ -170,6 +181,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
         const uint32_t bph = p.nbuf == 2 ? ((ls >> 1) & 1) : (ls & 1);
         mbar_wait(&bfull[buf], bph);
         tc_fence_after();
+        C1F_STAMP(3, ls);
         const uint32_t idesc = idesc_tf32(C1_BM, g.n, 0, 0);
         const uint32_t bbase = smem_u32(sB + buf * p.bset_bytes);
         for (int mt = 0; mt < p.mtiles; ++mt, ++u) {
@@ -211,6 +223,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
         mbar_wait(&pempty[buf], bph ^ 1);
         mbar_arrive_expect_tx(&pfull[buf], p.nb * p.pimg * 4);   // exact box bytes (the buffer is rounded up)
         tma_load_4d(reinterpret_cast<uint8_t*>(sP) + buf * p.patch_bytes, &p.xmap, &pfull[buf], g.c0, 2 * g.i, 0, g.b0);
+        C1F_STAMP(0, ls);
       }
     }
   } else if (warp >= C1_BUILD_WARP0 && warp < C1_EPI_WARP0) {
@@ -232,6 +245,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
       const uint32_t bph = p.nbuf == 2 ? ((ls >> 1) & 1) : (ls & 1);
       mbar_wait(&pfull[buf], bph);
       mbar_wait(&bempty[buf], bph ^ 1);
+      if (t == 0) C1F_STAMP(1, ls);
 #if defined(C1_EXP) && C1_EXP == 3
       if (true) {   // experiment: no B build (timing only)
         asm volatile("bar.sync 1, %0;" ::"n"(C1_BUILD_THREADS) : "memory");
@@ -274,6 +288,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
       asm volatile("bar.sync 1, %0;" ::"n"(C1_BUILD_THREADS) : "memory");
       if (t == 0) {
+        C1F_STAMP(2, ls);
         mbar_arrive(&bfull[buf]);
         mbar_arrive(&pempty[buf]);
       }
@@ -345,6 +360,9 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
+#ifdef C1F_TRACE
+        if (warp == C1_EPI_WARP0 && lane == 0 && mt == p.mtiles - 1) C1F_STAMP(4, (set - (int)blockIdx.x) / (int)gridDim.x);
+#endif
       }
     }
   }
@@ -714,6 +732,10 @@ static bool c1_plan(const Layer& L, C1Params& p, size_t* smem) {
   p.bstride = (p.nb * 2 * p.wseg + 7) / 8 * 8 * 128;   // the widest set's N rows
   p.bset_bytes = p.nch * p.bstride;
   p.pw = (p.wseg + L.S - 1 + 3) / 4 * 4;
+  // patch rows (channel, tap row) start pw floats apart; an odd number of 16-byte groups spreads the
+  // builders' 8 K-column lanes over 8 bank groups (pw = 32 put them all on one bank: 8-way conflicts,
+  // the per-set build took ~3.7 us; profiles/r02_conv1_fwd_trace.txt)
+  if (((p.pw / 4) & 1) == 0 && tc_env_int("CP_C1_PAD", 1)) p.pw += 4;
   p.pimg = L.C * (L.R + 1) * p.pw;
   p.patch_bytes = (p.nb * p.pimg * 4 + 127) / 128 * 128;
   if (p.pw > 256 || L.R + 1 > 256 || L.C > 256 || p.patch_bytes > 32 * 1024) return false;
@@ -777,8 +799,27 @@ int c1_fwd(Layer& L, const float* x, const float* w, const float* b, float* y_bl
   }
   const int grid = std::min(p.nsets, tc_num_sms());
   CP_TRY(tc_time_mark(L, 0, 0, s));
+#ifdef C1F_TRACE
+  static unsigned long long* tbuf = nullptr;
+  if (!tbuf) CP_CUDA(cudaMalloc(&tbuf, 5 * 8 * 8));
+  CP_CUDA(cudaMemsetAsync(tbuf, 0, 5 * 8 * 8, s));
+  p.trace = tbuf;
+#endif
   if (p.relu) conv1_fwd_kernel<true><<<grid, C1_THREADS, smem, s>>>(p);
   else conv1_fwd_kernel<false><<<grid, C1_THREADS, smem, s>>>(p);
+#ifdef C1F_TRACE
+  {   // experiment build: CTA 0's per-set stamps (us after its first patch issue) to stderr
+    unsigned long long h[5 * 8];
+    CP_CUDA(cudaStreamSynchronize(s));
+    CP_CUDA(cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[c1f_trace] Kc=%d mtiles=%d nsets=%d grid=%d astages=%d nbuf=%d: set patch_issued build_start "
+                    "build_done mma_start epi_done\n", L.Kc, p.mtiles, p.nsets, grid, p.astages, p.nbuf);
+    for (int k = 0; k < 8; ++k)
+      if (h[k])
+        fprintf(stderr, "[c1f_trace] %d %8.2f %8.2f %8.2f %8.2f %8.2f\n", k, (h[k] - h[0]) * 1e-3, (h[8 + k] - h[0]) * 1e-3,
+                (h[16 + k] - h[0]) * 1e-3, (h[24 + k] - h[0]) * 1e-3, (h[32 + k] - h[0]) * 1e-3);
+  }
+#endif
   CP_LAUNCHED();
   CP_TRY(tc_time_mark(L, 0, 1, s));
   return CP_OK;
