@@ -46,6 +46,7 @@ struct C1Params {
   int Kr, Kc, Kcol, nch; // K chunks of 32 (the last one may be shorter)
   int nb, wseg, nseg, ngrp;  // B-set = nb images x 2 rows x wseg columns; nseg segments, ngrp image groups
   int nsets, mtiles;
+  int balance;           // 1: each CTA takes a contiguous range of the nsets x mtiles (set, M tile) units
   int nbuf, astages;     // B-set buffers (1 or 2) and A ring depth, sized to shared memory
   int bset_bytes;        // nch * bstride
   int bstride;           // bytes of one 32-wide K chunk of a B-set: N rows (max over sets, x8) * 128 B
@@ -79,6 +80,39 @@ __device__ __forceinline__ SetGeo set_geo(const C1Params& p, int set) {
   g.b0 = bg * p.nb;
   g.n = (p.nb * 2 * g.ws + 7) / 8 * 8;
   return g;
+}
+
+// This CTA's work: sets set0, set0 + step, ... (nset of them), M tiles [mt_first, mtiles) of the first
+// and [0, mt_end) of the last.  balance: a contiguous range of the (set, M tile) units, split as evenly
+// as the grid allows (448 sets x 4 M tiles on 148 SMs: 12-13 units per CTA instead of 3 or 4 whole
+// sets); otherwise whole sets strided by the grid.  A set whose tiles two CTAs share is built by both.
+struct C1Work {
+  int set0, step, nset, mt_first, mt_end;
+};
+__device__ __forceinline__ C1Work c1_work(const C1Params& p) {
+  C1Work w;
+  if (p.balance) {
+    const int U = p.nsets * p.mtiles;
+    const int lo = (int)((long long)blockIdx.x * U / gridDim.x);
+    const int hi = (int)((long long)(blockIdx.x + 1) * U / gridDim.x);
+    const int last = (hi - 1) / p.mtiles;
+    w.set0 = lo / p.mtiles;
+    w.step = 1;
+    w.nset = hi > lo ? last - w.set0 + 1 : 0;
+    w.mt_first = lo - w.set0 * p.mtiles;
+    w.mt_end = hi - last * p.mtiles;
+  } else {
+    w.set0 = blockIdx.x;
+    w.step = gridDim.x;
+    w.nset = (int)blockIdx.x < p.nsets ? (p.nsets - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    w.mt_first = 0;
+    w.mt_end = p.mtiles;
+  }
+  return w;
+}
+__device__ __forceinline__ int c1_mt_begin(const C1Work& w, int ls) { return ls == 0 ? w.mt_first : 0; }
+__device__ __forceinline__ int c1_mt_end(const C1Work& w, int ls, int mtiles) {
+  return ls == w.nset - 1 ? w.mt_end : mtiles;
 }
 
 __device__ __forceinline__ void tmem_ld_x32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
@@ -151,14 +185,15 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const C1Work wk = c1_work(p);
 
   if (warp == 0) {
     // ======================= A producer: the own kernels' weight chunks, one M tile after another
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int set = blockIdx.x; set < p.nsets; set += gridDim.x)
-        for (int mt = 0; mt < p.mtiles; ++mt)
+      for (int ls = 0; ls < wk.nset; ++ls)
+        for (int mt = c1_mt_begin(wk, ls); mt < c1_mt_end(wk, ls, p.mtiles); ++mt)
           for (int c = 0; c < p.nch; ++c) {
             mbar_wait(&aempty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&afull[stage], C1_ABYTES);
@@ -174,9 +209,9 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int u = 0, ls = 0;
-      for (int set = blockIdx.x; set < p.nsets; set += gridDim.x, ++ls) {
-        const SetGeo g = set_geo(p, set);
+      int u = 0;
+      for (int ls = 0; ls < wk.nset; ++ls) {
+        const SetGeo g = set_geo(p, wk.set0 + ls * wk.step);
         const int buf = p.nbuf == 2 ? (ls & 1) : 0;
         const uint32_t bph = p.nbuf == 2 ? ((ls >> 1) & 1) : (ls & 1);
         mbar_wait(&bfull[buf], bph);
@@ -184,7 +219,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
         C1F_STAMP(3, ls);
         const uint32_t idesc = idesc_tf32(C1_BM, g.n, 0, 0);
         const uint32_t bbase = smem_u32(sB + buf * p.bset_bytes);
-        for (int mt = 0; mt < p.mtiles; ++mt, ++u) {
+        for (int mt = c1_mt_begin(wk, ls); mt < c1_mt_end(wk, ls, p.mtiles); ++mt, ++u) {
           const int acc = u & 1;
           mbar_wait(&tempty[acc], ((u >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -215,9 +250,8 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
     // ======================= patch producer: the B-set's input pixels (nb images x C x R+1 rows x pw
     // columns, zero outside the images) in one TMA box
     if (lane == 0) {
-      int ls = 0;
-      for (int set = blockIdx.x; set < p.nsets; set += gridDim.x, ++ls) {
-        const SetGeo g = set_geo(p, set);
+      for (int ls = 0; ls < wk.nset; ++ls) {
+        const SetGeo g = set_geo(p, wk.set0 + ls * wk.step);
         const int buf = p.nbuf == 2 ? (ls & 1) : 0;
         const uint32_t bph = p.nbuf == 2 ? ((ls >> 1) & 1) : (ls & 1);
         mbar_wait(&pempty[buf], bph ^ 1);
@@ -238,9 +272,8 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
     for (int c = 0; c < C1_MAXK / 32; ++c)
 #pragma unroll
       for (int q = 0; q < 4; ++q) offr[c][q] = c < p.nch ? off_s[c * 32 + grp * 4 + q] : -1;
-    int ls = 0;
-    for (int set = blockIdx.x; set < p.nsets; set += gridDim.x, ++ls) {
-      const SetGeo g = set_geo(p, set);
+    for (int ls = 0; ls < wk.nset; ++ls) {
+      const SetGeo g = set_geo(p, wk.set0 + ls * wk.step);
       const int buf = p.nbuf == 2 ? (ls & 1) : 0;
       const uint32_t bph = p.nbuf == 2 ? ((ls >> 1) & 1) : (ls & 1);
       mbar_wait(&pfull[buf], bph);
@@ -298,10 +331,11 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
     const int quad = warp & 3, egrp = (warp - C1_EPI_WARP0) >> 2;
     const int k = quad * 32 + lane;                    // row of the M tile
     int u = 0;
-    for (int set = blockIdx.x; set < p.nsets; set += gridDim.x) {
-      const SetGeo g = set_geo(p, set);
+    for (int ls = 0; ls < wk.nset; ++ls) {
+      const SetGeo g = set_geo(p, wk.set0 + ls * wk.step);
       const int nblk = (g.ws + 15) / 16;               // 16-column blocks per row (8 pooling windows)
-      for (int mt = 0; mt < p.mtiles; ++mt, ++u) {
+      const int mt_end = c1_mt_end(wk, ls, p.mtiles);
+      for (int mt = c1_mt_begin(wk, ls); mt < mt_end; ++mt, ++u) {
         const int acc = u & 1;
         const int kk = mt * C1_BM + k;
         const float bs = (p.bias && kk < p.Kr) ? __ldg(p.bias + kk) : 0.f;
@@ -361,7 +395,7 @@ __global__ void __launch_bounds__(C1_THREADS, 1) conv1_fwd_kernel(const __grid_c
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
 #ifdef C1F_TRACE
-        if (warp == C1_EPI_WARP0 && lane == 0 && mt == p.mtiles - 1) C1F_STAMP(4, (set - (int)blockIdx.x) / (int)gridDim.x);
+        if (warp == C1_EPI_WARP0 && lane == 0 && mt == mt_end - 1) C1F_STAMP(4, ls);
 #endif
       }
     }
@@ -729,6 +763,7 @@ static bool c1_plan(const Layer& L, C1Params& p, size_t* smem) {
   p.ngrp = L.Bp / p.nb;
   p.nsets = L.Hp * p.nseg * p.ngrp;
   p.mtiles = (L.Kc + C1_BM - 1) / C1_BM;
+  p.balance = tc_env_int("CP_C1_BALANCE", p.mtiles > 1 ? 1 : 0);
   p.bstride = (p.nb * 2 * p.wseg + 7) / 8 * 8 * 128;   // the widest set's N rows
   p.bset_bytes = p.nch * p.bstride;
   p.pw = (p.wseg + L.S - 1 + 3) / 4 * 4;
@@ -797,7 +832,7 @@ int c1_fwd(Layer& L, const float* x, const float* w, const float* b, float* y_bl
     CP_CUDA(cudaFuncSetAttribute(conv1_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  const int grid = std::min(p.nsets, tc_num_sms());
+  const int grid = std::min(p.balance ? p.nsets * p.mtiles : p.nsets, tc_num_sms());
   CP_TRY(tc_time_mark(L, 0, 0, s));
 #ifdef C1F_TRACE
   static unsigned long long* tbuf = nullptr;

@@ -76,6 +76,16 @@ def test_split_forward_parity(orc, monkeypatch, split, P, B, K2):
     _forward_parity(orc, "tf32", P, B, 8, K2=K2, K1=40)
 
 
+# conv1 forward work split (CP_C1_BALANCE): with more than one 128-kernel M tile per rank the CTAs take
+# contiguous ranges of (B-set, M tile) units, so a B-set's tiles can be shared by two CTAs (each builds
+# the set).  K1 = 300: 3 / 2 M tiles at P = 1 / 2, 80 B-sets -> 240 / 160 units on the SMs.
+@pytest.mark.parametrize("balance", ["1", "0"])
+@pytest.mark.parametrize("P,B", [(1, 40), (2, 40), (1, 128)])
+def test_conv1_unit_split_parity(orc, monkeypatch, balance, P, B):
+    monkeypatch.setenv("CP_C1_BALANCE", balance)
+    _forward_parity(orc, "tf32", P, B, 8, K2=64, K1=300)
+
+
 def _forward_parity(orc, math, P, B, align, K2=300, K1=70):
     m = math_id(math)
     x, w1, b1, w2, b2 = layer_data(B=B, K1=K1, K2=K2)
