@@ -449,7 +449,8 @@ def main():
     # later loop ran on a hotter, more power-capped GPU: scripts/e2e_probe.py).
     # e2e: pinned host images/labels in, loss out to the host, per step.  Input pipeline: step k+1's
     # images/labels travel host -> device on a copy stream (pinned source, two staging buffers) while
-    # step k computes, inside step k's timed window; step 0's copy is issued inside its own window.
+    # step k computes, inside step k's timed window (its end waits for them); step 0's copy is issued
+    # inside its own window.
     # Each e2e step starts with a device copy staging -> the network's input buffer and ends with the
     # loss read back to pinned host memory, which the host then reads.  L2 flushed before every step.
     h2d = x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size()
@@ -471,12 +472,15 @@ def main():
         free[j].record(s)
     e2e_graphs = None
     if graph is not None:
-        # the e2e step as one graph per staging buffer: the D2D copies into the network's input and the
-        # step, so the host enqueues one launch per step (the GPU does not idle on host launch latency)
+        # the e2e step as one graph per staging buffer, the network reading its images / labels straight
+        # from that buffer (no device copies ahead of the step: as graph memcpy nodes they cost ~20 us of
+        # copy-engine latency per step), so the host enqueues one launch per step
         def e2e_body(j):
-            pn.x.copy_(stage[j][0])
-            pn.labels.copy_(stage[j][1])
-            step_eager()
+            prev = pn.bind_input(stage[j][0], stage[j][1])
+            try:
+                step_eager()
+            finally:
+                pn.bind_input(*prev)
         e2e_graphs = [_graph(lambda j=j: e2e_body(j), dev)[0] for j in range(2)]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -500,20 +504,25 @@ def main():
             flush.fill_(k & 0xFF)
         e2e_ev[k][0].record(s)
         if k == 0:
-            cpy.wait_stream(s)
+            cpy.wait_stream(s)   # step 0's copy starts inside its own window
             prefetch(0)
         s.wait_event(ready[j])
-        if k + 1 < args.steps:   # step k+1's inputs travel while step k computes (other staging buffer)
-            cpy.wait_stream(s)
-            prefetch(k + 1)
+        # the step is enqueued before the next input's copy, so the host's enqueue work does not sit
+        # between the window's start and the step (the L2 flush ahead of it covers the launch)
         if e2e_graphs is not None:
-            e2e_graphs[j].replay()   # staging -> input copies + the step, one graph launch
+            e2e_graphs[j].replay()   # the step on staging buffer j, one graph launch
         else:
             pn.x.copy_(stage[j][0])
             pn.labels.copy_(stage[j][1])
             step()
         free[j].record(s)
+        if k + 1 < args.steps:
+            # step k+1's inputs travel host -> device while step k computes (other staging buffer, free
+            # since step k-1's graph ended); the window closes only after they landed
+            prefetch(k + 1)
         loss_host.copy_(pn.head["loss"][:1], non_blocking=True)
+        if k + 1 < args.steps:
+            s.wait_event(ready[(k + 1) & 1])
         e2e_ev[k][1].record(s)
         e2e_ev[k][1].synchronize()
         host_losses.append(float(loss_host[0]))

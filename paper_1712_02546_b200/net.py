@@ -180,6 +180,18 @@ class PartitionedNet:
         self.x.copy_(x.reshape(-1), non_blocking=True)
         self.labels.copy_(labels.reshape(-1), non_blocking=True)
 
+    def bind_input(self, x, labels):
+        """Read the images / labels of the following steps from these device buffers (e.g. an input
+        pipeline's staging buffers, so no device copy precedes the step; a CUDA graph captured meanwhile
+        keeps the pointers).  Returns the previous pair."""
+        if x.numel() != self.x.numel() or x.device != self.x.device or x.dtype != torch.float32:
+            raise ValueError("bind_input: images must be a float32 device tensor of the batch's size")
+        if labels.numel() != self.labels.numel() or labels.dtype != torch.int32 or labels.device != self.x.device:
+            raise ValueError("bind_input: labels must be an int32 device tensor of batch size")
+        prev = (self.x, self.labels)
+        self.x, self.labels = x.reshape(-1), labels.reshape(-1)
+        return prev
+
     # ------------------------------------------------------------ one training step
     def forward(self, stream=None, comm_stream=None, head=True):
         """head=False: the conv stage only (every conv layer and its gather; no FC / loss) - bench.py's
