@@ -1161,9 +1161,13 @@ __global__ void wgrad_tail_reduce(const float* __restrict__ buf, float* __restri
   const float* src = buf + (((int64_t)ti.pbeg[tu] * ti.cg + rank) * BM + row) * BN + c;
   float a[4] = {0.f, 0.f, 0.f, 0.f};
   int pc = 0;
-  for (; pc + 4 <= np; pc += 4)
+  for (; pc + 8 <= np; pc += 8) {   // 8 loads in flight, added in the same order (piece p -> a[p & 3])
+    float v[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) a[k] += src[(pc + k) * step];
+    for (int k = 0; k < 8; ++k) v[k] = src[(pc + k) * step];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k & 3] += v[k];
+  }
   for (; pc < np; ++pc) a[pc & 3] += src[pc * step];
   const int64_t o = (int64_t)kk * ti.Ktot + ti.col0[tu] + c;
   const float d = (a[0] + a[1]) + (a[2] + a[3]);
@@ -1181,6 +1185,71 @@ struct FwdTailInfo {
   float* peer[CP_MAX_RANKS];  // fused AllGather: own block inside each peer's buffer
   int i[MAX_TAIL], j[MAX_TAIL], bc0[MAX_TAIL], n0[MAX_TAIL], ncol[MAX_TAIL];
 };
+// Sum of one accumulator value over the pieces [pc, pe) (stride pstep floats), in piece order; loads
+// batched 16 at a time (the pieces were just written: L2-latency bound, ~20-75 pieces per tail unit)
+__device__ __forceinline__ float tail_sum(const float* __restrict__ src, int np, int64_t pstep) {
+  float z = 0.f;
+  int pc = 0;
+  for (; pc + 16 <= np; pc += 16) {
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = src[(pc + u) * pstep];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) z += v[u];
+  }
+  for (; pc < np; ++pc) z += src[pc * pstep];
+  return z;
+}
+
+// blockDim (BN columns, 4 accumulator quadrants): each thread sums one pre-pool value over the pieces
+// (four times the threads of one thread per pooling window; the same order per value), the quadrants
+// meet in shared memory for the pool.  For tails of few units with many pieces each (P=1: ~20 per
+// unit, 8.1 -> 7.4 us); with many units of few pieces (P=8) the window-per-thread kernel below is
+// faster (9.1 vs 26.9 us, profiles/r02_tail_finish/)
+__global__ void __launch_bounds__(4 * BN) fwd_tail_finish_q(const float* __restrict__ buf, const float* __restrict__ bias,
+                                                           float* __restrict__ y, uint8_t* __restrict__ saved,
+                                                           const __grid_constant__ FwdTailInfo ti) {
+  __shared__ float zs[4][BN];
+  const int tu = blockIdx.z, rank = blockIdx.y, b = blockIdx.x;
+  const int c = threadIdx.x, qa = threadIdx.y;
+  const bool col = c < ti.ncol[tu];
+  if (col) {
+    const int pb = ti.pbeg[tu];
+    const float* src = buf + ((int64_t)pb * ti.cg + rank) * BM * BN + (int64_t)(qa * 32 + b) * BN + c;
+    zs[qa][c] = tail_sum(src, ti.pbeg[tu + 1] - pb, (int64_t)ti.cg * BM * BN);
+  }
+  __syncthreads();
+  if (qa != 0 || !col) return;
+  const int n = ti.n0[tu] + c;
+  const int bb = ti.bc0[tu] + rank * 32 + b;
+  const bool ok = bb < ti.B && n < ti.Kr;
+  const float bs = (bias && n < ti.Kr) ? bias[n] : 0.f;
+  float best = 0.f;
+  int code = 0;
+  for (int q = 0; q < 4; ++q) {             // q: row-major window position
+    float z = zs[win_pos(q, ti.halo)][c] + bs;
+    if (ti.relu && !(z > 0.f)) z = 0.f;
+    if (ti.pool) {
+      if (q == 0 || z > best) {
+        best = z;
+        code = q;
+      }
+    } else {
+      const int64_t o = ((int64_t)((2 * ti.i[tu] + (q >> 1)) * ti.Wo + 2 * ti.j[tu] + (q & 1)) * ti.Bp + bb) * ti.Kc + n;
+      y[o] = ok ? tf32_rna(z) : 0.f;
+      for (int k = 0; k < ti.npeers; ++k) ti.peer[k][o] = ok ? tf32_rna(z) : 0.f;
+    }
+  }
+  if (ti.pool) {
+    const int64_t o = ((int64_t)(ti.i[tu] * ti.Wp + ti.j[tu]) * ti.Bp + bb) * ti.Kc + n;
+    y[o] = ok ? tf32_rna(best) : 0.f;
+    saved[o] = ok ? (uint8_t)code : 0;
+    for (int k = 0; k < ti.npeers; ++k) ti.peer[k][o] = ok ? tf32_rna(best) : 0.f;
+  }
+  if (ti.npeers) __threadfence_system();
+}
+
+// one thread per pooling window (4 pre-pool values), 8 pieces' loads in flight
 __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __restrict__ bias, float* __restrict__ y,
                                 uint8_t* __restrict__ saved, const __grid_constant__ FwdTailInfo ti) {
   const int tu = blockIdx.z, rank = blockIdx.y, b = blockIdx.x;
@@ -1193,19 +1262,19 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
   float best = 0.f;
   int code = 0;
   float zq[4] = {0.f, 0.f, 0.f, 0.f};   // the four window positions: independent load streams
-  // pieces in K order; loads of 4 pieces batched (16 in flight), added in the same order
+  // pieces in K order; loads of 8 pieces batched (32 in flight), added in the same order
   int pc = ti.pbeg[tu];
   const int pe = ti.pbeg[tu + 1];
-  for (; pc + 4 <= pe; pc += 4) {
-    float v[4][4];
+  for (; pc + 8 <= pe; pc += 8) {   // (8 pieces: 32 loads in flight)
+    float v[8][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const float* src = buf + ((int64_t)(pc + u) * ti.cg + rank) * BM * BN + (int64_t)b * BN + c;
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[u][q] = src[q * 32 * BN];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int q = 0; q < 4; ++q) zq[q] += v[u][q];
   }
@@ -1239,8 +1308,45 @@ __global__ void fwd_tail_finish(const float* __restrict__ buf, const float* __re
 
 // stream-tail finish of the transposed forward: tile rows = own kernel slots, columns = (window
 // position, image of 64); pieces summed in K order, then bias + ReLU + first-max pool.  One block
-// per (tile row, tail unit), one thread per image.
-__global__ void fwd_tail_finish_t(const float* __restrict__ buf, const float* __restrict__ bias, float* __restrict__ y,
+// per (tile row, tail unit), one thread per (image, window position).
+__global__ void __launch_bounds__(256) fwd_tail_finish_t(const float* __restrict__ buf, const float* __restrict__ bias,
+                                                         float* __restrict__ y, uint8_t* __restrict__ saved,
+                                                         const __grid_constant__ FwdTailInfo ti) {
+  // blockIdx.z: the M tile within a multicast cluster's unit (ti.cg tiles per piece; 1 otherwise).
+  // 256 threads = 64 images x 4 window positions: one pre-pool value each, summed over the pieces in
+  // K order (~74 per tail unit at the P=4 slice), the positions meet in shared memory for the pool
+  __shared__ float zs[4][64];
+  const int tu = blockIdx.y, row = blockIdx.x, mt = blockIdx.z;
+  const int b = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int kk = ti.n0[tu] + mt * BM + row;
+  if (kk >= ti.Kc) return;
+  const int pb = ti.pbeg[tu];
+  const float* src = buf + (((int64_t)pb * ti.cg + mt) * BM + row) * BN + q * 64 + b;
+  zs[q][b] = tail_sum(src, ti.pbeg[tu + 1] - pb, (int64_t)ti.cg * BM * BN);
+  __syncthreads();
+  if (q != 0) return;
+  const int bb = ti.bc0[tu] + b;
+  const bool ok = bb < ti.B && kk < ti.Kr;
+  const float bs = (bias && kk < ti.Kr) ? bias[kk] : 0.f;
+  float best = 0.f;
+  int code = 0;
+  for (int w = 0; w < 4; ++w) {
+    float z = zs[w][b] + bs;
+    if (ti.relu && !(z > 0.f)) z = 0.f;
+    if (w == 0 || z > best) {
+      best = z;
+      code = w;
+    }
+  }
+  const int64_t o = ((int64_t)(ti.i[tu] * ti.Wp + ti.j[tu]) * ti.Bp + bb) * ti.Kc + kk;
+  y[o] = ok ? tf32_rna(best) : 0.f;
+  saved[o] = ok ? (uint8_t)code : 0;
+  for (int k = 0; k < ti.npeers; ++k) ti.peer[k][o] = ok ? tf32_rna(best) : 0.f;
+  if (ti.npeers) __threadfence_system();
+}
+
+// one thread per image (the four window positions), for tails of few pieces per unit
+__global__ void fwd_tail_finish_t1(const float* __restrict__ buf, const float* __restrict__ bias, float* __restrict__ y,
                                   uint8_t* __restrict__ saved, const __grid_constant__ FwdTailInfo ti) {
   // blockIdx.z: the M tile within a multicast cluster's unit (ti.cg tiles per piece; 1 otherwise)
   const int tu = blockIdx.y, row = blockIdx.x, b = threadIdx.x, mt = blockIdx.z;
@@ -1250,7 +1356,24 @@ __global__ void fwd_tail_finish_t(const float* __restrict__ buf, const float* __
   const bool ok = bb < ti.B && kk < ti.Kr;
   const float bs = (bias && kk < ti.Kr) ? bias[kk] : 0.f;
   float zq[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int pc = ti.pbeg[tu]; pc < ti.pbeg[tu + 1]; ++pc) {
+  // pieces in K order (~74 per tail unit at the P=4 slice): loads of 8 pieces batched (32 in flight),
+  // added in the same order as one piece at a time
+  int pc = ti.pbeg[tu];
+  const int pe = ti.pbeg[tu + 1];
+  const int64_t pstep = (int64_t)ti.cg * BM * BN;
+  for (; pc + 8 <= pe; pc += 8) {
+    const float* src = buf + (((int64_t)pc * ti.cg + mt) * BM + row) * BN + b;
+    float v[8][4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[u][q] = src[u * pstep + q * 64];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) zq[q] += v[u][q];
+  }
+  for (; pc < pe; ++pc) {
     const float* src = buf + (((int64_t)pc * ti.cg + mt) * BM + row) * BN + b;
 #pragma unroll
     for (int q = 0; q < 4; ++q) zq[q] += src[q * 64];
@@ -2205,10 +2328,22 @@ static int tc_fwd_part(Layer& L, const float* xin, const float* w, const float* 
   else CP_TRY(((pl.pair && !p.fwdT) ? launch_cg<PASS_FWD, 2>(p, s) : launch_cg<PASS_FWD, 1>(p, s)));
   if (mark1) CP_TRY(tc_time_mark(L, PASS_FWD, 1, s));
   if (p.tail_np > 0 && p.fwdT) {
-    fwd_tail_finish_t<<<dim3(BM, ti.n, p.fcl ? p.fcl : 1), 64, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
+    int max_np = 0;
+    for (int k = 0; k < ti.n; ++k) max_np = std::max(max_np, ti.pbeg[k + 1] - ti.pbeg[k]);
+    // many pieces per tail unit (P=4 slice: 2 units x ~74 pieces): one thread per pre-pool value,
+    // 22.0 -> 8.0 us (ncu, profiles/r02_tail_finish/); few: one thread per image
+    if (max_np >= 16)
+      fwd_tail_finish_t<<<dim3(BM, ti.n, p.fcl ? p.fcl : 1), 256, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
+    else
+      fwd_tail_finish_t1<<<dim3(BM, ti.n, p.fcl ? p.fcl : 1), 64, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
     CP_LAUNCHED();
   } else if (p.tail_np > 0) {
-    fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
+    int max_np = 0;
+    for (int k = 0; k < ti.n; ++k) max_np = std::max(max_np, ti.pbeg[k + 1] - ti.pbeg[k]);
+    if (max_np >= 16)
+      fwd_tail_finish_q<<<dim3(32, ti.cg, ti.n), dim3(BN, 4), 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
+    else
+      fwd_tail_finish<<<dim3(32, ti.cg, ti.n), BN, 0, s>>>(part, L.d.bias ? b : nullptr, y_block, saved, ti);
     CP_LAUNCHED();
   }
   if (pl.S > 1 && !p.fwdT) {
