@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
 }
 
 // dW[k][col] = sum over the K ranges (ascending) of the partials; db[k] = sum over K ranges and builder
-// groups.  Block = 32 outputs x 8 lanes: lane y sums K ranges y*per.. (loads batched 8 deep), the 8 lane
+// groups.  Block = 32 outputs x 8 lanes: lane y sums K ranges y*per.. (loads batched 16 deep), the 8 lane
 // sums combine in fixed order (deterministic).
 __global__ void __launch_bounds__(256) conv1_wgrad_reduce(const float* __restrict__ part, const float* __restrict__ dbpart,
                                                           float* __restrict__ dw, float* __restrict__ db, int nkr,
@@ -719,12 +719,19 @@ __global__ void __launch_bounds__(256) conv1_wgrad_reduce(const float* __restric
   float t = 0.f;
   if (is_w || is_b) {
     int g = g0;
-    for (; g + 8 <= g1; g += 8) {
-      float v[8];
+    for (; g + 16 <= g1; g += 16) {   // (148 K ranges: 19 per lane -> one 16-deep batch + 3)
+      float v[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = src[(g + u) * stride];
+      for (int u = 0; u < 16; ++u) v[u] = src[(g + u) * stride];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t += v[u];
+      for (int u = 0; u < 16; ++u) t += v[u];
+    }
+    for (; g + 4 <= g1; g += 4) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = src[(g + u) * stride];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t += v[u];
     }
     for (; g < g1; ++g) t += src[g * stride];
   }
