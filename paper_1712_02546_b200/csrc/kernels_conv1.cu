@@ -692,7 +692,8 @@ __global__ void __launch_bounds__(W1_THREADS, 1) conv1_wgrad_kernel(const __grid
 }
 
 // dW[k][col] = sum over the K ranges (ascending) of the partials; db[k] = sum over K ranges and builder
-// groups.  Block = 32 outputs x 8 lanes: lane y sums K ranges y*per.. (loads batched 16 deep), the 8 lane
+// groups.  Block = 32 outputs x 8 lanes: lane y sums K ranges y*per.. (all loads in flight when per <= 24,
+// else batched 8 deep; the same ascending order either way), the 8 lane
 // sums combine in fixed order (deterministic).
 __global__ void __launch_bounds__(256) conv1_wgrad_reduce(const float* __restrict__ part, const float* __restrict__ dbpart,
                                                           float* __restrict__ dw, float* __restrict__ db, int nkr,
@@ -719,19 +720,21 @@ __global__ void __launch_bounds__(256) conv1_wgrad_reduce(const float* __restric
   float t = 0.f;
   if (is_w || is_b) {
     int g = g0;
-    for (; g + 16 <= g1; g += 16) {   // (148 K ranges: 19 per lane -> one 16-deep batch + 3)
-      float v[16];
+    if (g1 - g0 <= 24) {   // dW: <= 148 K ranges -> <= 19 per lane, every load in flight at once
+      float v[24];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = src[(g + u) * stride];
+      for (int u = 0; u < 24; ++u) v[u] = g0 + u < g1 ? src[(g0 + u) * stride] : 0.f;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) t += v[u];
+      for (int u = 0; u < 24; ++u)
+        if (g0 + u < g1) t += v[u];
+      g = g1;
     }
-    for (; g + 4 <= g1; g += 4) {
-      float v[4];
+    for (; g + 8 <= g1; g += 8) {
+      float v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = src[(g + u) * stride];
+      for (int u = 0; u < 8; ++u) v[u] = src[(g + u) * stride];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) t += v[u];
+      for (int u = 0; u < 8; ++u) t += v[u];
     }
     for (; g < g1; ++g) t += src[g * stride];
   }
