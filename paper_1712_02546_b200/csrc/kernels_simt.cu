@@ -462,8 +462,18 @@ __global__ void __launch_bounds__(256) bias_grad_final(const float* __restrict__
   const int s0 = threadIdx.y * per, s1 = min(ns, s0 + per);
   float t = 0.f;
   if (slot < Kr) {
-    // loads batched 8 at a time (independent, in flight together), added in the same ascending order
+    // loads batched (all of a lane's when <= 32: 7 / 25 splits per lane at P=1 / 4; else 8 at a time),
+    // added in the same ascending order
     int i = s0;
+    if (s1 - s0 <= 32) {
+      float v[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] = s0 + u < s1 ? part[(int64_t)(s0 + u) * Kc + slot] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (s0 + u < s1) t += v[u];
+      i = s1;
+    }
     for (; i + 8 <= s1; i += 8) {
       float v[8];
 #pragma unroll
@@ -811,7 +821,16 @@ __global__ void __launch_bounds__(1024) fc_fwd_reduce(const float* __restrict__ 
   const int u0 = threadIdx.y * per, u1 = min(U, u0 + per);
   float t = 0.f;
   if (e < B * O) {
-    int u = u0;   // loads batched 8 at a time, added in ascending unit order
+    int u = u0;   // loads batched (all of them when <= 24 per lane: 600 units at P=1), added in ascending unit order
+    if (u1 - u0 <= 24) {
+      float v[24];
+#pragma unroll
+      for (int q = 0; q < 24; ++q) v[q] = u0 + q < u1 ? part[(int64_t)(u0 + q) * Bp * O + e] : 0.f;
+#pragma unroll
+      for (int q = 0; q < 24; ++q)
+        if (u0 + q < u1) t += v[q];
+      u = u1;
+    }
     for (; u + 8 <= u1; u += 8) {
       float v[8];
 #pragma unroll
