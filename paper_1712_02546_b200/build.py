@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                    "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o,
                    *os.environ.get("CP_NVCC_EXTRA", "").split()]   # experiment builds (-D...), use force
             if src.endswith(".cpp"):
-                cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include"),
+                cmd = [NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include"),
                        "-x", "cu", "-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:

@@ -857,110 +857,6 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
   softmax_xent_block(logits, y, B, O, loss, dl, wsum);
 }
 
-// FC backward in one launch (S:L98-115 chain rule through logits = W x + b): CTA = (rank block r,
-// position pos, 64-slot chunk); per 128-image chunk the x tile, the dlogits rows and the weight
-// slice sit in shared memory and the CTA produces both
-//   dx[(r,pos,b,slot)] = sum_o dlogits[b][o] * W[o][f]      (float4 rows, coalesced), and
-//   dW[o][f]           = sum_b dlogits[b][o] * x(b, f)      (thread = slot x row quarter, quarters
-//                                                            combined in fixed order);
-// CTA 0 also writes dbfc[o] = sum_b dlogits[b][o] (warp per class, fixed xor tree).
-__global__ void __launch_bounds__(256) fc_bwd_fused(const float* __restrict__ dl, const float* __restrict__ x,
-                                                    const float* __restrict__ wg, float* __restrict__ dx,
-                                                    float* __restrict__ dwg, float* __restrict__ dbfc, Blocks g,
-                                                    int B, int O, int PW, int nsc) {
-  constexpr int LD = kFcChunk + 4;
-  __shared__ __align__(16) float xs[128 * LD];      // reused for the quarter reduction
-  __shared__ float dls[128][kMaxO + 1];
-  __shared__ float4 ws[kMaxO][kFcChunk / 4];
-  const int u = blockIdx.x;
-  const int sc = u % nsc, rp = u / nsc;
-  const int r = rp / PW, pos = rp % PW;
-  const int kw = g.kw[r];
-  const int s0 = sc * kFcChunk;
-  const int64_t F = (int64_t)PW * g.Cg;
-  const int64_t foff = (int64_t)PW * g.coff[r] + (int64_t)pos * kw + s0;
-  const float* xb = x + g.start[r] + (int64_t)pos * g.Bp * kw + s0;
-  float* dxb = dx ? dx + g.start[r] + (int64_t)pos * g.Bp * kw + s0 : nullptr;
-  if (dbfc && u == 0) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int o = w; o < O; o += blockDim.x >> 5) {
-      float t = 0.f;
-      for (int b = lane; b < B; b += 32) t += dl[(int64_t)b * O + o];
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
-      if (lane == 0) dbfc[o] = t;
-    }
-  }
-  if (s0 >= kw) return;
-  for (int i = threadIdx.x; i < kMaxO * (kFcChunk / 4); i += blockDim.x) {
-    const int o = i / (kFcChunk / 4), q4 = (i % (kFcChunk / 4)) * 4;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (o < O && s0 + q4 < kw) v = __ldg(reinterpret_cast<const float4*>(wg + o * F + foff + q4));
-    ws[o][i % (kFcChunk / 4)] = v;
-  }
-  const int sl = threadIdx.x & 63, bq = threadIdx.x >> 6;        // dW mapping
-  const int q4 = threadIdx.x & 15, rg = threadIdx.x >> 4;        // dx mapping
-  float acc[kMaxO];
-#pragma unroll
-  for (int o = 0; o < kMaxO; ++o) acc[o] = 0.f;
-  for (int b0 = 0; b0 < g.Bp; b0 += 128) {
-    if (b0) __syncthreads();
-    {  // x tile 128 x 16 float4 and dlogits 128 x kMaxO: loads batched in registers (8 in flight)
-      float4 v[8];
-      float d[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x + k * 256, row = i >> 4, q = i & 15, b = b0 + row;
-        v[k] = (dwg && b < B && s0 + 4 * q < kw) ? __ldg(reinterpret_cast<const float4*>(xb + (int64_t)b * kw) + q)
-                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        const int drow = i / kMaxO, o = i % kMaxO;
-        d[k] = (b0 + drow < B && o < O) ? __ldg(dl + (int64_t)(b0 + drow) * O + o) : 0.f;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x + k * 256;
-        *reinterpret_cast<float4*>(xs + (i >> 4) * LD + 4 * (i & 15)) = v[k];
-        dls[i / kMaxO][i % kMaxO] = d[k];
-      }
-    }
-    __syncthreads();
-    if (dwg)
-      for (int row = bq * 32; row < bq * 32 + 32; ++row) {
-        const float xv = xs[row * LD + sl];
-#pragma unroll
-        for (int o = 0; o < kMaxO; ++o)
-          if (o < O) acc[o] = fmaf(dls[row][o], xv, acc[o]);
-      }
-    if (dxb && s0 + 4 * q4 < kw)
-      for (int row = rg; row < 128 && b0 + row < g.Bp; row += 16) {
-        float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int o = 0; o < kMaxO; ++o) {
-          if (o < O) {
-            const float d = dls[row][o];
-            const float4 w = ws[o][q4];
-            a4.x = fmaf(d, w.x, a4.x); a4.y = fmaf(d, w.y, a4.y);
-            a4.z = fmaf(d, w.z, a4.z); a4.w = fmaf(d, w.w, a4.w);
-          }
-        }
-        *reinterpret_cast<float4*>(dxb + (int64_t)(b0 + row) * kw + 4 * q4) = a4;
-      }
-  }
-  if (!dwg) return;
-  __syncthreads();
-  float* red = xs;   // [4][kMaxO][64]
-#pragma unroll
-  for (int o = 0; o < kMaxO; ++o) red[(bq * kMaxO + o) * 64 + sl] = acc[o];
-  __syncthreads();
-  for (int i = threadIdx.x; i < O * 64; i += blockDim.x) {
-    const int o = i >> 6, sx = i & 63;
-    if (s0 + sx >= kw) continue;
-    const float t = ((red[(0 * kMaxO + o) * 64 + sx] + red[(1 * kMaxO + o) * 64 + sx]) + red[(2 * kMaxO + o) * 64 + sx]) +
-                    red[(3 * kMaxO + o) * 64 + sx];
-    dwg[o * F + foff + sx] = t;
-  }
-}
-
 // FC backward, one CTA column per gather-layout feature f = (rank block r, position pos, slot) (S:L98-115,
 // chain rule through logits = W x + b):
 //   dx[b][f] = sum_o dlogits[b][o] * W[o][f]      (stored in the gathered input's layout), and

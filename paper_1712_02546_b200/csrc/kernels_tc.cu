@@ -1784,12 +1784,6 @@ int build_ntiles(TcParams& p) {
   return n;
 }
 
-int wgrad_ntiles(const Layer& L, TcParams& p) {
-  p.span = span_ok(p) ? 1 : 0;
-  (void)L;
-  return build_ntiles(p);
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- work decomposition (host)
@@ -1818,7 +1812,6 @@ static Plan fwd_plan(const Layer& L, TcParams& p, int kc = -1) {
   } else {
     const int gran = CG == 2 ? 16 : 8, groups = num_sms() / CG;
     double best = 1e300;
-    int bestT = (kc + BN - 1) / BN;
     for (int T = (kc + BN - 1) / BN; T <= (kc + BN - 1) / BN + 4; ++T) {
       const int nw = ((kc + T - 1) / T + gran - 1) / gran * gran;
       if (nw > BN || nw <= 0) continue;
@@ -1831,13 +1824,11 @@ static Plan fwd_plan(const Layer& L, TcParams& p, int kc = -1) {
       const double t = rounds * (16384.0 + 128.0 * nw / CG);
       if (t < best * 0.98) {
         best = t;
-        bestT = tiles;
         p.nw = nw;
       }
     }
     if (env_int("CP_TC_FWD_NW", 0) > 0) p.nw = env_int("CP_TC_FWD_NW", 0);
     if (p.nw <= 0) p.nw = BN;
-    (void)bestT;
     w.numN = (kc + p.nw - 1) / p.nw;
   }
   w.chunks = p.R * p.S * cpt;
